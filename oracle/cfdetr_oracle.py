@@ -1,0 +1,297 @@
+"""fp64 CPU oracle of the CF-DETR coarse-to-fine encoder hot path.
+
+TEST INFRASTRUCTURE: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline (and `bench.py --impl reference`) may import this module.  It is
+independent of the CUDA path: no shared code, headers, helpers or tables.
+
+Citations are PAPER.md line numbers (section / equation in brackets);
+"R<n>" names a reading of the paper listed in DESIGN.md §3 (taken from
+SURVEY.md §8(c)) where the paper is silent or ambiguous.
+
+Every function follows the definition written in its docstring, in fp64, with
+numpy library primitives (matmul, exp, erf, sort) as single steps and no
+blocking, fusion or reordering beyond the definition.
+
+Parity status (see tests/test_oracle_pins.py):
+  patchify ............ pinned (image bijection, coarse/fine tiling index sets)
+  embed ............... pinned (tied-mode pooling closed form, torch linear)
+  layer_norm / gelu ... pinned (torch F.layer_norm, torch F.gelu, closed forms)
+  encoder_layer ....... pinned (torch.nn.TransformerEncoderLayer, norm_first, fp64)
+  attention_probs ..... pinned (torch MHA weights, row sums, 1-token/equal-key forms)
+  criticality_score ... pinned (torch MHA head-averaged weights; sum=1; constant image)
+  select_topk/thresh .. pinned (brute force over all C(16,4) subsets; NaN/+-0 cases)
+  merge / gather ...... pinned (offset closed form; k=0 == coarse; k=Nc == fine pass)
+  batch_refine ........ pinned (== per-task refine; cu_seqlens closed form)
+"""
+from __future__ import annotations
+
+import math
+from typing import List, Sequence, Tuple
+
+import numpy as np
+from scipy.special import erf
+
+__all__ = [
+    "patchify", "patch_embed", "layer_norm", "gelu", "attention_probs",
+    "encoder_layer", "encoder", "criticality_score", "select_topk",
+    "select_threshold", "merge_tokens", "gather_layout", "coarse_encode",
+    "refine_encode", "batch_refine", "fine_pass", "as_f64_image",
+]
+
+
+# ----------------------------------------------------------------------------
+# A1: patch split and embedding
+# ----------------------------------------------------------------------------
+def as_f64_image(img_bits: np.ndarray) -> np.ndarray:
+    """bf16 bit pattern [H,W,3] (uint16) -> exact fp64 pixel values."""
+    u = np.asarray(img_bits, dtype=np.uint16).astype(np.uint32) << 16
+    return u.view(np.float32).astype(np.float64)
+
+
+def patchify(img: np.ndarray, P: int) -> np.ndarray:
+    """Image [H,W,3] -> patch matrix [(H/P)(W/P), 3P^2]  (§II-A;
+    "divided into a grid of small patches ... each patch is encoded as an
+    embedding token").  Reading R2: patch vector order (py, px, ch):
+
+        patch[c][(py*P + px)*3 + ch] = img[cy*P + py][cx*P + px][ch],
+        c = cy*(W/P) + cx.
+
+    Works on any dtype (uint16 bf16 bits give the bytes bit-exactly).
+    """
+    H, W, C = img.shape
+    assert C == 3 and H % P == 0 and W % P == 0
+    gw = W // P
+    n = (H // P) * gw
+    c = np.arange(n)[:, None]
+    kk = np.arange(3 * P * P)[None, :]
+    cy, cx = c // gw, c % gw
+    pix, ch = kk // 3, kk % 3
+    py, px = pix // P, pix % P
+    return img[cy * P + py, cx * P + px, ch]
+
+
+def patch_embed(patches: np.ndarray, W: np.ndarray, b: np.ndarray, pe_rows: np.ndarray) -> np.ndarray:
+    """token = patch . W + b + PE  (A1 "feature extraction, converting from RGB to a
+    computational vector"; linear embedding per reading R1,
+    positional table per R3)."""
+    return patches.astype(np.float64) @ W.astype(np.float64) + b.astype(np.float64) + pe_rows.astype(np.float64)
+
+
+# ----------------------------------------------------------------------------
+# Encoder block (§II-A global self-attention; reading R4:
+# pre-LN ViT block, MLP 4d, exact-erf GELU, LN eps 1e-6)
+# ----------------------------------------------------------------------------
+def layer_norm(x: np.ndarray, g: np.ndarray, b: np.ndarray, eps: float) -> np.ndarray:
+    """LN(x) = (x - mean) / sqrt(var + eps) * g + b, biased variance, per row."""
+    x = x.astype(np.float64)
+    mu = x.mean(axis=-1, keepdims=True)
+    var = ((x - mu) ** 2).mean(axis=-1, keepdims=True)
+    return (x - mu) / np.sqrt(var + eps) * g.astype(np.float64) + b.astype(np.float64)
+
+
+def gelu(z: np.ndarray) -> np.ndarray:
+    """GELU(z) = z/2 * (1 + erf(z / sqrt(2)))."""
+    return 0.5 * z * (1.0 + erf(z / math.sqrt(2.0)))
+
+
+def attention_probs(q: np.ndarray, k: np.ndarray) -> np.ndarray:
+    """P = softmax_row(q k^T / sqrt(dh)), max-subtracted, base e (reading R12).
+    "each patch attends to every other patch"."""
+    dh = q.shape[-1]
+    S = (q @ k.T) / math.sqrt(dh)
+    S = S - S.max(axis=1, keepdims=True)
+    E = np.exp(S)
+    return E / E.sum(axis=1, keepdims=True)
+
+
+def encoder_layer(x: np.ndarray, lw: dict, n_heads: int, eps: float,
+                  want_probs: bool = False) -> Tuple[np.ndarray, List[np.ndarray]]:
+    """One pre-LN block over the token set x [N, d] (fp64):
+
+        h = LN1(x);  [q|k|v] = h W_qkv + b_qkv      (head h: columns [h*dh, (h+1)*dh))
+        o = concat_h softmax(q_h k_h^T / sqrt(dh)) v_h
+        x = x + o W_o + b_o
+        x = x + GELU(LN2(x) W_1 + b_1) W_2 + b_2
+    Weight layout (in, out).  Returns (x_out, [P_h] if want_probs).
+    """
+    f = lambda a: np.asarray(a, dtype=np.float64)
+    N, d = x.shape
+    dh = d // n_heads
+    h = layer_norm(x, lw["ln1_g"], lw["ln1_b"], eps)
+    qkv = h @ f(lw["w_qkv"]) + f(lw["b_qkv"])
+    q, k, v = qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:]
+    o = np.empty((N, d))
+    probs = []
+    for hh in range(n_heads):
+        cols = slice(hh * dh, (hh + 1) * dh)
+        P = attention_probs(q[:, cols], k[:, cols])
+        o[:, cols] = P @ v[:, cols]
+        if want_probs:
+            probs.append(P)
+    x = x + o @ f(lw["w_o"]) + f(lw["b_o"])
+    h2 = layer_norm(x, lw["ln2_g"], lw["ln2_b"], eps)
+    x = x + gelu(h2 @ f(lw["w_1"]) + f(lw["b_1"])) @ f(lw["w_2"]) + f(lw["b_2"])
+    return x, probs
+
+
+def encoder(x: np.ndarray, layers: Sequence[dict], n_heads: int, eps: float,
+            probs_at: int = -1) -> Tuple[np.ndarray, List[np.ndarray], List[np.ndarray]]:
+    """Apply the L blocks in order.  Returns (y, per-layer outputs, P_h of layer
+    `probs_at` (empty list if probs_at < 0))."""
+    outs, probs = [], []
+    x = x.astype(np.float64)
+    for l, lw in enumerate(layers):
+        x, p = encoder_layer(x, lw, n_heads, eps, want_probs=(l == probs_at))
+        if l == probs_at:
+            probs = p
+        outs.append(x.copy())
+    return x, outs, probs
+
+
+# ----------------------------------------------------------------------------
+# A2: region criticality and selection
+# ----------------------------------------------------------------------------
+def criticality_score(probs: Sequence[np.ndarray]) -> np.ndarray:
+    """s_j = 1/(nh*N) * sum_h sum_i P_h[i, j]: attention mass received by coarse
+    region j at the score layer (reading R5 from the draft "attention map"
+    region proposal, PAPER.md:361/417/497 [draft]; live A2 PAPER.md:231-232)."""
+    nh = len(probs)
+    N = probs[0].shape[0]
+    return sum(P.sum(axis=0) for P in probs) / (nh * N)
+
+
+def _order_key(s: float, j: int):
+    """Total order for selection (reading R7): NaN below -inf, -0.0 == +0.0,
+    larger score first, ties to the lower index."""
+    s = float(s)
+    if math.isnan(s):
+        return (1, 0.0, j)
+    return (0, -(s + 0.0), j)
+
+
+def select_topk(scores: np.ndarray, k: int) -> np.ndarray:
+    """Top-k regions by (score desc, index asc); returned ascending (int32).
+    "only these ... regions are subsequently re-partitioned into finer patches"
+    (PAPER.md:233); explicit integer k (reading R7)."""
+    n = scores.shape[0]
+    assert 0 <= k <= n
+    order = sorted(range(n), key=lambda j: _order_key(scores[j], j))
+    return np.array(sorted(order[:k]), dtype=np.int32)
+
+
+def select_threshold(scores: np.ndarray, tau: float) -> np.ndarray:
+    """Regions with s_j > tau (strict, "exceeds"; reading R7), ascending."""
+    return np.array([j for j in range(scores.shape[0]) if scores[j] > tau], dtype=np.int32)
+
+
+# ----------------------------------------------------------------------------
+# A2: selective fine split + coarse-token reuse (merge)
+# ----------------------------------------------------------------------------
+def _fine_index(cfg, c: int, dy: int, dx: int) -> int:
+    m = cfg.m
+    cy, cx = divmod(c, cfg.gc_w)
+    return (m * cy + dy) * cfg.gf_w + (m * cx + dx)
+
+
+def merge_tokens(cfg, x0: np.ndarray, img: np.ndarray, sel: Sequence[int], w: dict):
+    """Mixed-resolution token set of one task (ROIs "re-partitioned
+    into finer patches", "non-ROI areas reuse the original coarse-stage tokens from
+    A1"; readings R6, R8, R10).  In coarse raster order:
+      - unselected c contributes x0[c] (layer-0 coarse embedding), src = c;
+      - selected c contributes its m^2 fine patches f, (dy, dx) raster, each
+        patch_f[f] W_f + b_f + PE_f[f], src = -1 - f.
+    Returns (tokens [N_t, d] fp64, mixed_src [N_t] int32)."""
+    sel_set = set(int(s) for s in sel)
+    pf = patchify(img, cfg.patch_fine)
+    rows, src = [], []
+    for c in range(cfg.n_coarse):
+        if c not in sel_set:
+            rows.append(np.asarray(x0[c], dtype=np.float64))
+            src.append(c)
+        else:
+            for dy in range(cfg.m):
+                for dx in range(cfg.m):
+                    f = _fine_index(cfg, c, dy, dx)
+                    rows.append(patch_embed(pf[f:f + 1], w["w_embed_f"], w["b_embed_f"], w["pe_f"][f:f + 1])[0])
+                    src.append(-1 - f)
+    return np.stack(rows), np.array(src, dtype=np.int32)
+
+
+def gather_layout(cfg, sels: Sequence[Sequence[int]], images_bits: Sequence[np.ndarray]):
+    """Integer / byte layout of a packed refine batch (bit-exact parity targets):
+      cu_seqlens[T+1]  prefix sums of N_t = Nc + (m^2-1) k_t,
+      mixed_src[sum N] per merge_tokens,
+      frow[R]          packed row of the r-th fine token (fine tokens in packed order),
+      fidx[R]          its fine patch index f,
+      A_f[R, 3Pf^2]    its pixel bytes (bf16 bits, patch vector order R2).
+    """
+    cu = [0]
+    msrc, frow, fidx, af = [], [], [], []
+    for t, sel in enumerate(sels):
+        sel_set = set(int(s) for s in sel)
+        pf = patchify(images_bits[t], cfg.patch_fine)
+        base = cu[-1]
+        r = 0
+        for c in range(cfg.n_coarse):
+            if c not in sel_set:
+                msrc.append(c)
+                r += 1
+            else:
+                for dy in range(cfg.m):
+                    for dx in range(cfg.m):
+                        f = _fine_index(cfg, c, dy, dx)
+                        msrc.append(-1 - f)
+                        frow.append(base + r)
+                        fidx.append(f)
+                        af.append(pf[f])
+                        r += 1
+        cu.append(base + r)
+    af_arr = np.stack(af).astype(np.uint16) if af else np.zeros((0, cfg.k_fine), np.uint16)
+    return (np.array(cu, np.int32), np.array(msrc, np.int32), np.array(frow, np.int32),
+            np.array(fidx, np.int32), af_arr)
+
+
+# ----------------------------------------------------------------------------
+# The four calls of the boundary, oracle side
+# ----------------------------------------------------------------------------
+def coarse_encode(cfg, w: dict, images_bits: Sequence[np.ndarray]):
+    """A1 coarse subtask per frame (image-level batch = independent
+    frames).  Returns per frame dict(x0, y, layers, scores)."""
+    out = []
+    for ib in images_bits:
+        img = as_f64_image(ib)
+        x0 = patch_embed(patchify(img, cfg.patch_coarse), w["w_embed_c"], w["b_embed_c"], w["pe_c"])
+        y, layers, probs = encoder(x0, w["layers"], cfg.n_heads, cfg.ln_eps, probs_at=cfg.score_layer)
+        out.append(dict(x0=x0, y=y, layers=layers, scores=criticality_score(probs)))
+    return out
+
+
+def refine_encode(cfg, w: dict, image_bits: np.ndarray, x0: np.ndarray, sel: Sequence[int]):
+    """A2 + encoder re-run on the mixed set of one task ("The
+    Transformer processes this mixed set" [draft P:363]).  Returns dict(y, layers, mixed_src)."""
+    img = as_f64_image(image_bits)
+    tokens, src = merge_tokens(cfg, x0, img, sel, w)
+    y, layers, _ = encoder(tokens, w["layers"], cfg.n_heads, cfg.ln_eps)
+    return dict(y=y, layers=layers, mixed_src=src)
+
+
+def batch_refine(cfg, w: dict, images_bits, x0s, sels):
+    """A3 patch-level batch over tasks: tasks never attend to
+    each other (reading R11), so the batch is exactly the per-task refines
+    concatenated, with cu_seqlens."""
+    per = [refine_encode(cfg, w, images_bits[t], x0s[t], sels[t]) for t in range(len(sels))]
+    cu = np.concatenate([[0], np.cumsum([p["y"].shape[0] for p in per])]).astype(np.int32)
+    y = np.concatenate([p["y"] for p in per]) if per else np.zeros((0, cfg.d_model))
+    layers = [np.concatenate([p["layers"][l] for p in per]) for l in range(cfg.n_layers)] if per else []
+    src = np.concatenate([p["mixed_src"] for p in per]) if per else np.zeros(0, np.int32)
+    return dict(y=y, layers=layers, cu_seqlens=cu, mixed_src=src)
+
+
+def fine_pass(cfg, w: dict, image_bits: np.ndarray):
+    """Full-resolution fine pass (every fine patch, fine raster order): the pass
+    A1-A3 exist to avoid ("more than 10,000 patches for equivalent full-frame fine
+    resolution").  Returns dict(y, layers)."""
+    img = as_f64_image(image_bits)
+    x = patch_embed(patchify(img, cfg.patch_fine), w["w_embed_f"], w["b_embed_f"], w["pe_f"])
+    y, layers, _ = encoder(x, w["layers"], cfg.n_heads, cfg.ln_eps)
+    return dict(y=y, layers=layers)

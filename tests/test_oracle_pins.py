@@ -1,0 +1,323 @@
+"""Pins of the fp64 oracle against things other than itself (CPU only).
+
+Each test names the oracle function it pins and what fixes the expected value:
+an independent library implementation (torch), a closed form, an invariant the
+paper implies, or brute force on tiny inputs.  See DESIGN.md §4.
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import cfd_inputs as ci
+import oracle as O
+
+TINY = ci.CONFIGS["tiny"]
+
+
+def _rng(s=0):
+    return np.random.default_rng(s)
+
+
+# --------------------------------------------------------------------------- patchify
+@pytest.mark.parametrize("P", [32, 16])
+def test_patchify_matches_reshape_formulation(P):
+    """patchify == an independent reshape/transpose formulation of the same tiling."""
+    img = ci.make_frame(128, 96, 7)
+    H, W, _ = img.shape
+    ref = img.reshape(H // P, P, W // P, P, 3).transpose(0, 2, 1, 3, 4).reshape((H // P) * (W // P), -1)
+    assert np.array_equal(O.patchify(img, P), ref)
+
+
+def test_patchify_bijection_and_fine_tiles_cover_coarse():
+    """Every pixel appears in exactly one coarse and one fine patch, and the m^2
+    fine patches of region c cover exactly coarse patch c's pixels."""
+    cfg = ci.ModelConfig(96, 160, 32, 16, 64, 2, 1, 256, 0)
+    H, W = cfg.img_h, cfg.img_w
+    coord = np.arange(H * W, dtype=np.int64).reshape(H, W)
+    cimg = np.repeat(coord[:, :, None], 3, axis=2)
+    pc = O.patchify(cimg, 32)
+    pf = O.patchify(cimg, 16)
+    assert sorted(np.unique(pc)) == list(range(H * W))
+    assert np.bincount(pc.reshape(-1)).tolist() == [3] * (H * W)
+    assert np.bincount(pf.reshape(-1)).tolist() == [3] * (H * W)
+    for c in range(cfg.n_coarse):
+        kids = [O.cfdetr_oracle._fine_index(cfg, c, dy, dx) for dy in range(2) for dx in range(2)]
+        assert set(pc[c].tolist()) == set(np.concatenate([pf[f] for f in kids]).tolist())
+
+
+def test_patch_vector_order_is_py_px_ch():
+    img = ci.make_frame(64, 64, 3)
+    p = O.patchify(img, 32)
+    c = 1 * 2 + 1  # cy=1, cx=1
+    py, px, ch = 5, 17, 2
+    assert p[c, (py * 32 + px) * 3 + ch] == img[32 + py, 32 + px, ch]
+
+
+# --------------------------------------------------------------------------- embedding
+def test_tied_embedding_is_pooling_closed_form():
+    """Tied mode (reading R1): coarse token (PE off) == mean of its m^2 fine tokens."""
+    w = ci.make_weights(TINY, seed=3, tied=True, pe=False)
+    img = O.as_f64_image(ci.make_frame(128, 128, 11))
+    xc = O.patch_embed(O.patchify(img, 32), w["w_embed_c"], w["b_embed_c"], w["pe_c"])
+    xf = O.patch_embed(O.patchify(img, 16), w["w_embed_f"], w["b_embed_f"], w["pe_f"])
+    for c in range(TINY.n_coarse):
+        kids = [O.cfdetr_oracle._fine_index(TINY, c, dy, dx) for dy in range(2) for dx in range(2)]
+        np.testing.assert_allclose(xc[c], xf[kids].mean(axis=0), rtol=0, atol=1e-12)
+
+
+def test_embed_matches_torch_linear():
+    w = ci.make_weights(TINY, seed=1)
+    img = O.as_f64_image(ci.make_frame(128, 128, 5))
+    p = O.patchify(img, 32)
+    x = O.patch_embed(p, w["w_embed_c"], w["b_embed_c"], w["pe_c"])
+    ref = torch.nn.functional.linear(torch.tensor(p), torch.tensor(w["w_embed_c"], dtype=torch.float64).T,
+                                     torch.tensor(w["b_embed_c"], dtype=torch.float64)) + torch.tensor(w["pe_c"], dtype=torch.float64)
+    np.testing.assert_allclose(x, ref.numpy(), rtol=0, atol=1e-11)
+
+
+def test_pe_table_values():
+    """PE generator check (input-side): row 0 of the coarse table, column 0 = sin(2*pi*16/640)."""
+    pe = ci.pe_table(20, 20, 32, 640, 640, 256)
+    assert abs(pe[0, 0] - math.sin(2 * math.pi * 16 / 640)) < 1e-7
+    assert abs(pe[21, 64 + 0] - math.cos(2 * math.pi * 48 / 640)) < 1e-7  # gx=1
+    assert abs(pe[21, 128 + 0] - math.sin(2 * math.pi * 48 / 640)) < 1e-7  # gy=1
+
+
+# --------------------------------------------------------------------------- LN / GELU
+def test_layer_norm_matches_torch():
+    x = _rng(1).normal(size=(7, 64)) * 3 + 1
+    g, b = _rng(2).normal(size=64), _rng(3).normal(size=64)
+    ref = torch.nn.functional.layer_norm(torch.tensor(x), (64,), torch.tensor(g), torch.tensor(b), eps=1e-6)
+    np.testing.assert_allclose(O.layer_norm(x, g, b, 1e-6), ref.numpy(), rtol=0, atol=1e-12)
+
+
+def test_gelu_matches_torch_and_closed_forms():
+    z = np.linspace(-8, 8, 1001)
+    ref = torch.nn.functional.gelu(torch.tensor(z), approximate="none").numpy()
+    np.testing.assert_allclose(O.gelu(z), ref, rtol=0, atol=1e-14)
+    assert O.gelu(np.array([0.0]))[0] == 0.0
+    np.testing.assert_allclose(O.gelu(z) - O.gelu(-z), z, atol=1e-13)  # GELU(z) - GELU(-z) = z
+    assert abs(O.gelu(np.array([1.0]))[0] - 0.8413447460685429) < 1e-15  # Phi(1)
+
+
+# --------------------------------------------------------------------------- encoder block
+def _torch_layer(lw, d, nh, F):
+    layer = torch.nn.TransformerEncoderLayer(d, nh, F, dropout=0.0, activation="gelu", layer_norm_eps=1e-6,
+                                             batch_first=True, norm_first=True, dtype=torch.float64)
+    t = lambda a: torch.tensor(np.asarray(a, dtype=np.float64))
+    with torch.no_grad():
+        layer.self_attn.in_proj_weight.copy_(t(lw["w_qkv"]).T)
+        layer.self_attn.in_proj_bias.copy_(t(lw["b_qkv"]))
+        layer.self_attn.out_proj.weight.copy_(t(lw["w_o"]).T)
+        layer.self_attn.out_proj.bias.copy_(t(lw["b_o"]))
+        layer.linear1.weight.copy_(t(lw["w_1"]).T)
+        layer.linear1.bias.copy_(t(lw["b_1"]))
+        layer.linear2.weight.copy_(t(lw["w_2"]).T)
+        layer.linear2.bias.copy_(t(lw["b_2"]))
+        layer.norm1.weight.copy_(t(lw["ln1_g"]))
+        layer.norm1.bias.copy_(t(lw["ln1_b"]))
+        layer.norm2.weight.copy_(t(lw["ln2_g"]))
+        layer.norm2.bias.copy_(t(lw["ln2_b"]))
+    return layer.eval()
+
+
+@pytest.mark.parametrize("d,nh,N", [(64, 2, 28), (256, 8, 57)])
+def test_encoder_layer_matches_torch_transformer_layer(d, nh, N):
+    """The whole pre-LN block against torch.nn.TransformerEncoderLayer(norm_first, gelu) in fp64."""
+    cfg = ci.ModelConfig(64, 64, 32, 16, d, nh, 2, 4 * d, 1)
+    w = ci.make_weights(cfg, seed=4)
+    x = _rng(5).normal(size=(N, d))
+    y = x
+    for lw in w["layers"]:
+        y, _ = O.encoder_layer(y, lw, nh, 1e-6)
+        ref = _torch_layer(lw, d, nh, 4 * d)
+    with torch.no_grad():
+        r = torch.tensor(x)[None]
+        for lw in w["layers"]:
+            r = _torch_layer(lw, d, nh, 4 * d)(r)
+    np.testing.assert_allclose(y, r[0].numpy(), rtol=0, atol=1e-10)
+
+
+def test_attention_probs_and_score_match_torch_mha():
+    """P_h and the head-averaged column mean (criticality score) against torch MHA weights."""
+    d, nh, N = 64, 2, 16
+    cfg = ci.ModelConfig(64, 64, 32, 16, d, nh, 1, 4 * d, 0)
+    lw = ci.make_weights(cfg, seed=8)["layers"][0]
+    x = _rng(9).normal(size=(N, d))
+    _, probs = O.encoder_layer(x, lw, nh, 1e-6, want_probs=True)
+    layer = _torch_layer(lw, d, nh, 4 * d)
+    with torch.no_grad():
+        h = layer.norm1(torch.tensor(x))[None]
+        _, wts = layer.self_attn(h, h, h, need_weights=True, average_attn_weights=False)
+        _, avg = layer.self_attn(h, h, h, need_weights=True, average_attn_weights=True)
+    for hh in range(nh):
+        np.testing.assert_allclose(probs[hh], wts[0, hh].numpy(), rtol=0, atol=1e-13)
+    np.testing.assert_allclose(O.criticality_score(probs), avg[0].numpy().mean(axis=0), rtol=0, atol=1e-14)
+
+
+def test_attention_closed_forms():
+    rng = _rng(10)
+    q, k = rng.normal(size=(9, 32)), rng.normal(size=(9, 32))
+    P = O.attention_probs(q, k)
+    np.testing.assert_allclose(P.sum(axis=1), 1.0, atol=1e-14)          # rows sum to 1
+    P1 = O.attention_probs(q, np.repeat(k[:1], 9, axis=0))
+    np.testing.assert_allclose(P1, 1.0 / 9, atol=1e-15)                 # identical keys -> uniform
+    assert O.attention_probs(q[:1], k[:1])[0, 0] == 1.0                 # one token -> P = 1
+
+
+def test_single_token_attention_output_is_v():
+    """N=1: attention output = v, so the block = x + (v W_o + b_o) + MLP (explicit closed form)."""
+    d, nh = 64, 2
+    cfg = ci.ModelConfig(64, 64, 32, 16, d, nh, 1, 4 * d, 0)
+    lw = ci.make_weights(cfg, seed=12)["layers"][0]
+    x = _rng(13).normal(size=(1, d))
+    y, _ = O.encoder_layer(x, lw, nh, 1e-6)
+    mu, sd = x.mean(), x.std()
+    h = (x - mu) / math.sqrt(sd * sd + 1e-6) * lw["ln1_g"] + lw["ln1_b"]
+    v = h @ lw["w_qkv"][:, 2 * d:] + lw["b_qkv"][2 * d:]
+    x1 = x + v @ lw["w_o"] + lw["b_o"]
+    mu2, sd2 = x1.mean(), x1.std()
+    h2 = (x1 - mu2) / math.sqrt(sd2 * sd2 + 1e-6) * lw["ln2_g"] + lw["ln2_b"]
+    z = h2 @ lw["w_1"] + lw["b_1"]
+    ref = x1 + (0.5 * z * (1 + torch.erf(torch.tensor(z) / math.sqrt(2)).numpy())) @ lw["w_2"] + lw["b_2"]
+    np.testing.assert_allclose(y, ref, rtol=0, atol=1e-12)
+
+
+def test_encoder_permutation_equivariance():
+    d, nh = 64, 2
+    cfg = ci.ModelConfig(64, 64, 32, 16, d, nh, 2, 4 * d, 1)
+    w = ci.make_weights(cfg, seed=14)
+    x = _rng(15).normal(size=(21, d))
+    perm = _rng(16).permutation(21)
+    y, _, _ = O.encoder(x, w["layers"], nh, 1e-6)
+    yp, _, _ = O.encoder(x[perm], w["layers"], nh, 1e-6)
+    np.testing.assert_allclose(yp, y[perm], rtol=0, atol=1e-12)
+
+
+# --------------------------------------------------------------------------- score
+def test_score_is_a_distribution():
+    w = ci.make_weights(TINY, seed=0)
+    out = O.coarse_encode(TINY, w, [ci.make_frame(128, 128, 21)])[0]
+    s = out["scores"]
+    assert (s >= 0).all()
+    assert abs(s.sum() - 1.0) < 1e-13
+
+
+def test_constant_image_gives_equal_scores_and_lowest_index_topk():
+    """Constant image, PE off -> all coarse tokens identical -> s_j = 1/Nc -> top-k = {0..k-1}."""
+    w = ci.make_weights(TINY, seed=0, pe=False)
+    img = ci.make_frame(128, 128, 0, constant=True)
+    s = O.coarse_encode(TINY, w, [img])[0]["scores"]
+    np.testing.assert_allclose(s, 1.0 / TINY.n_coarse, rtol=0, atol=1e-15)
+    s32 = np.full(16, np.float32(1.0 / 16))
+    assert O.select_topk(s32, 4).tolist() == [0, 1, 2, 3]
+
+
+# --------------------------------------------------------------------------- selection
+def _brute_topk(s, k):
+    """Smallest (lexicographic) index set among all k-subsets whose every member
+    ranks at or above every non-member (NaN ranks below everything)."""
+    rank_val = lambda x: (0, 0.0) if np.isnan(x) else (1, float(x))
+    best = None
+    for sub in itertools.combinations(range(len(s)), k):
+        inside = [rank_val(s[j]) for j in sub]
+        outside = [rank_val(s[j]) for j in range(len(s)) if j not in sub]
+        if not outside or not inside or min(inside) >= max(outside):
+            if best is None or sub < best:
+                best = sub
+    return list(best)
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_topk_brute_force(case):
+    rng = _rng(100 + case)
+    if case < 4:
+        s = rng.random(16).astype(np.float32)
+    elif case < 8:
+        s = rng.choice(np.array([0.1, 0.2, 0.3], np.float32), size=16)  # many ties
+    else:
+        s = rng.choice(np.array([0.0, -0.0, 1.0, -1.0, np.inf, -np.inf, np.nan, 0.5], np.float32), size=16)
+    for k in (0, 1, 4, 15, 16):
+        assert O.select_topk(s, k).tolist() == _brute_topk(s, k), (s, k)
+
+
+def test_topk_signed_zero_and_nan_rules():
+    s = np.array([-0.0, 0.0, np.nan, -np.inf], np.float32)
+    assert O.select_topk(s, 1).tolist() == [0]          # -0 == +0, lower index wins
+    assert O.select_topk(s, 3).tolist() == [0, 1, 3]    # NaN below -inf
+
+
+def test_threshold_count():
+    rng = _rng(7)
+    s = rng.random(400).astype(np.float32)
+    for tau in (0.0, 0.25, 0.5, 0.999, 1.0):
+        sel = O.select_threshold(s, np.float32(tau))
+        assert len(sel) == int((s > np.float32(tau)).sum())
+        assert (np.diff(sel) > 0).all()
+
+
+# --------------------------------------------------------------------------- merge / layout
+def test_gather_layout_closed_forms():
+    cfg = TINY
+    rng = _rng(3)
+    sels = [np.sort(rng.choice(16, size=k, replace=False)) for k in (0, 4, 16, 7)]
+    imgs = [ci.make_frame(128, 128, 40 + t) for t in range(4)]
+    cu, msrc, frow, fidx, af = O.gather_layout(cfg, sels, imgs)
+    m2 = cfg.m * cfg.m
+    assert np.diff(cu).tolist() == [cfg.n_coarse + (m2 - 1) * len(s) for s in sels]
+    for t, sel in enumerate(sels):
+        seq = msrc[cu[t]:cu[t + 1]]
+        for c in range(cfg.n_coarse):
+            off = c + (m2 - 1) * int((sel < c).sum())          # off[c] closed form
+            if c in sel:
+                cy, cx = divmod(c, cfg.gc_w)
+                f0 = (2 * cy) * cfg.gf_w + 2 * cx
+                assert seq[off] == -1 - f0
+            else:
+                assert seq[off] == c
+    assert len(frow) == len(fidx) == af.shape[0] == m2 * sum(len(s) for s in sels)
+    assert (msrc[frow] == -1 - fidx).all()
+
+
+def test_refine_k0_equals_coarse_pass():
+    """Refining zero regions reproduces the coarse pass exactly (PAPER.md:234 reuse; A1 easy frames)."""
+    w = ci.make_weights(TINY, seed=0)
+    img = ci.make_frame(128, 128, 50)
+    c = O.coarse_encode(TINY, w, [img])[0]
+    r = O.refine_encode(TINY, w, img, c["x0"], [])
+    assert np.array_equal(r["y"], c["y"])
+    assert r["mixed_src"].tolist() == list(range(16))
+
+
+def test_refine_all_regions_equals_fine_pass():
+    """Refining every region reproduces the full fine pass up to the region-major permutation."""
+    w = ci.make_weights(TINY, seed=0)
+    img = ci.make_frame(128, 128, 51)
+    c = O.coarse_encode(TINY, w, [img])[0]
+    r = O.refine_encode(TINY, w, img, c["x0"], list(range(16)))
+    f = O.fine_pass(TINY, w, img)
+    order = -1 - r["mixed_src"]
+    assert sorted(order.tolist()) == list(range(64))
+    np.testing.assert_allclose(r["y"], f["y"][order], rtol=0, atol=1e-11)
+
+
+def test_batch_refine_equals_per_task_refine():
+    w = ci.make_weights(TINY, seed=0)
+    imgs = [ci.make_frame(128, 128, 60 + t) for t in range(3)]
+    cs = O.coarse_encode(TINY, w, imgs)
+    sels = [O.select_topk(c["scores"].astype(np.float32), k) for c, k in zip(cs, (0, 4, 9))]
+    b = O.batch_refine(TINY, w, imgs, [c["x0"] for c in cs], sels)
+    assert np.diff(b["cu_seqlens"]).tolist() == [16, 28, 43]
+    for t in range(3):
+        r = O.refine_encode(TINY, w, imgs[t], cs[t]["x0"], sels[t])
+        assert np.array_equal(b["y"][b["cu_seqlens"][t]:b["cu_seqlens"][t + 1]], r["y"])
+
+
+def test_bf16_rounding_helper():
+    x = np.array([1.0, 1.00390625, 1.005859375, -2.5, 3.0e-3], np.float32)
+    # 1+2^-8 ties to even -> 1.0; 1+1.5*2^-8 rounds up to 1+2^-7
+    assert ci.bf16_round(x)[:4].tolist() == [1.0, 1.0, 1.0078125, -2.5]
+    assert ci.bf16_round(ci.bf16_round(x)).tolist() == ci.bf16_round(x).tolist()
