@@ -1,0 +1,158 @@
+/* cfdetr.h — C ABI of the B200 CF-DETR coarse-to-fine encoder hot path.
+ *
+ * The four calls follow the paper's statement of the problem (arXiv 2505.23317):
+ *   cfd_coarse_encode   A1 coarse-to-fine inference, coarse stage: patch split +
+ *                       embedding + encoder self-attention over the coarse tokens of
+ *                       an image-level batch of frames (PAPER.md:78 §I A3, :119-122
+ *                       §II-A, :220 §III-B A1); also emits the per-region
+ *                       criticality score (reading R5) and the layer-0 token cache.
+ *   cfd_select_regions  A2 region proposal as a per-region top-k or threshold
+ *                       selection (§III-B A2; readings R5-R7).
+ *   cfd_refine_encode   A2 selective fine split + coarse-token reuse + encoder re-run
+ *                       on the mixed-resolution set of ONE task.
+ *   cfd_batch_refine    A3 patch-level batch: the refine of T tasks with ragged token
+ *                       counts in one launch per op, varlen/cu_seqlens instead of the
+ *                       paper's zero padding (reading R11).
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer unless its name starts with h_ (host).
+ *   - `stream` is a cudaStream_t passed as void*; every call only enqueues work on
+ *     it and returns (no host synchronisation inside any call, so calls can be
+ *     captured in a CUDA graph).  A ctx is not thread-safe: one ctx per stream.
+ *   - Tensors are dense row-major.  bf16 values are passed as uint16_t bit patterns.
+ *   - Images are [.., H, W, 3] bf16 (HWC).  Patch vectors are ordered (py, px, ch)
+ *     (reading R2).  Weight matrices are given (in, out) row-major.
+ *   - The caller (e.g. torch) owns every tensor and the workspace; cfd_create copies
+ *     and repacks the weights into ctx-owned device memory, so the caller may free
+ *     its copies once the stream has synchronised after cfd_create.
+ *   - Errors: host-detectable problems return a negative cfd_status before anything
+ *     is enqueued; a CUDA launch failure returns CFD_E_CUDA; device-side input
+ *     violations (sel_count > Nc, non-ascending or out-of-range sel_idx) set a device
+ *     error word that cfd_check reports.  No C++ exception crosses the ABI.
+ *   - Numerics: bf16 GEMM operands (RNE), fp32 accumulation, fp32 residual stream,
+ *     LN statistics and softmax state, bf16 P into the PV product; fp32 outputs
+ *     (reading R13).
+ */
+#ifndef CFDETR_H_
+#define CFDETR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CFD_OK = 0,
+  CFD_E_ARG = -1,         /* null pointer, non-positive count, k > Nc, bad mode */
+  CFD_E_SHAPE = -2,       /* H or W not a multiple of Pc, Pc not a multiple of Pf, d % nh */
+  CFD_E_UNSUPPORTED = -3, /* dh != 32, d not in {64,128,256,512}, Nc > 4096, ... */
+  CFD_E_CAPACITY = -4,    /* n_tasks > max_tasks, or workspace too small */
+  CFD_E_CUDA = -5,        /* a CUDA API call or kernel launch failed */
+  CFD_E_DEVICE = -6       /* a kernel flagged invalid device-side input (cfd_check) */
+} cfd_status;
+
+/* Model geometry.  score_layer in [0, n_layers): the layer whose attention map
+ * scores the regions (default n_layers-1).  max_tasks bounds n_frames / n_tasks. */
+typedef struct {
+  int32_t img_h, img_w;
+  int32_t patch_coarse; /* Pc */
+  int32_t patch_fine;   /* Pf, Pc % Pf == 0, m = Pc/Pf */
+  int32_t d_model;      /* d */
+  int32_t n_heads;      /* nh, dh = d/nh must be 32 */
+  int32_t n_layers;     /* L */
+  int32_t d_ff;         /* F (multiple of 64) */
+  int32_t score_layer;
+  int32_t max_tasks;
+  float ln_eps;         /* 1e-6 */
+} cfd_config;
+
+/* One pre-LN encoder block (reading R4); matrices bf16 (in, out), vectors fp32. */
+typedef struct {
+  const uint16_t *w_qkv; /* [d, 3d]  columns: q | k | v, head h at [h*dh, (h+1)*dh) */
+  const uint16_t *w_o;   /* [d, d] */
+  const uint16_t *w_1;   /* [d, F] */
+  const uint16_t *w_2;   /* [F, d] */
+  const float *b_qkv, *b_o, *b_1, *b_2;          /* [3d], [d], [F], [d] */
+  const float *ln1_g, *ln1_b, *ln2_g, *ln2_b;    /* [d] each */
+} cfd_layer_weights;
+
+typedef struct {
+  const uint16_t *w_embed_c; /* [3Pc^2, d] coarse patch embedding (reading R1) */
+  const uint16_t *w_embed_f; /* [3Pf^2, d] fine patch embedding */
+  const float *b_embed_c;    /* [d] */
+  const float *b_embed_f;    /* [d] */
+  const float *pe_c;         /* [Nc, d] fixed positional table, coarse raster (reading R3) */
+  const float *pe_f;         /* [Nf, d] fine raster */
+  const cfd_layer_weights *h_layers; /* HOST array [n_layers] of device pointers */
+} cfd_weights;
+
+typedef enum { CFD_SELECT_TOPK = 0, CFD_SELECT_THRESHOLD = 1 } cfd_select_mode;
+
+typedef struct cfd_ctx cfd_ctx;
+
+/* Validate cfg, allocate ctx-owned device memory, repack weights (enqueued on stream). */
+cfd_status cfd_create(const cfd_config *cfg, const cfd_weights *w, void *stream, cfd_ctx **out);
+/* Free ctx memory (synchronises the device). NULL is a no-op. */
+cfd_status cfd_destroy(cfd_ctx *ctx);
+
+/* Geometry and the workspace a call with n_tasks frames/tasks needs:
+ *   *h_Nc = (H/Pc)(W/Pc), *h_Nf = m^2 Nc, *h_max_tokens = n_tasks * Nf (capacity of
+ *   packed refine outputs), *h_workspace_bytes = bytes for ws.  Any output may be NULL. */
+cfd_status cfd_query(const cfd_ctx *ctx, int32_t n_tasks, int32_t *h_Nc, int32_t *h_Nf, int32_t *h_max_tokens,
+                     size_t *h_workspace_bytes);
+
+/* A1 coarse pass over n_frames equal-size frames (image-level batch).
+ *   images    [B, H, W, 3] bf16
+ *   x0        [B, Nc, d] fp32 out: layer-0 coarse tokens (patch.W_c + b_c + PE_c), the
+ *             cache refine reuses for unselected regions (reading R8)
+ *   y         [B, Nc, d] fp32 out: encoder output
+ *   scores    [B, Nc] fp32 out or NULL: criticality score at cfg.score_layer
+ *   layer_out [L, B, Nc, d] fp32 out or NULL: residual stream after every layer
+ *   ws        workspace of >= cfd_query(n_frames) bytes (256-byte aligned) */
+cfd_status cfd_coarse_encode(cfd_ctx *ctx, int32_t n_frames, const uint16_t *images, float *x0, float *y,
+                             float *scores, float *layer_out, void *ws, size_t ws_bytes, void *stream);
+
+/* A2 selection over n_tasks score rows.
+ *   scores    [T, Nc] fp32
+ *   TOPK:      h_k [T] host ints, 0 <= k_t <= Nc; ties -> lower index; NaN lowest; -0 == +0
+ *   THRESHOLD: regions with score > threshold (strict)
+ *   sel_idx   [T, Nc] int32 out: selected region indices ascending in the first
+ *             sel_count[t] entries, -1 after;  sel_count [T] int32 out. */
+cfd_status cfd_select_regions(cfd_ctx *ctx, int32_t n_tasks, const float *scores, cfd_select_mode mode,
+                              const int32_t *h_k, float threshold, int32_t *sel_idx, int32_t *sel_count,
+                              void *stream);
+
+/* A2/A3 patch-level refine of n_tasks tasks, packed varlen.
+ *   images    [T, H, W, 3] bf16;  x0 [T, Nc, d] (from cfd_coarse_encode)
+ *   sel_idx/sel_count as produced by cfd_select_regions
+ *   h_token_counts [T] host hint of N_t = Nc + (m^2-1) k_t, or NULL (capacity launch)
+ *   y         [cap, d] fp32 out, cap = T*Nf: task t occupies rows [cu[t], cu[t+1])
+ *   cu_seqlens[T+1] int32 out;  mixed_src [cap] int32 out: >= 0 coarse index, < 0 is
+ *             -1 - fine index (reading R10)
+ *   layer_out [L, cap, d] or NULL.  Tasks never attend to each other; the result of
+ *   each task equals its cfd_refine_encode result bit for bit. */
+cfd_status cfd_batch_refine(cfd_ctx *ctx, int32_t n_tasks, const uint16_t *images, const float *x0,
+                            const int32_t *sel_idx, const int32_t *sel_count, const int32_t *h_token_counts,
+                            float *y, int32_t *cu_seqlens, int32_t *mixed_src, float *layer_out, void *ws,
+                            size_t ws_bytes, void *stream);
+
+/* cfd_batch_refine with T = 1 (y capacity Nf rows, cu_seqlens [2]). */
+cfd_status cfd_refine_encode(cfd_ctx *ctx, const uint16_t *image, const float *x0, const int32_t *sel_idx,
+                             const int32_t *sel_count, float *y, int32_t *mixed_src, int32_t *cu_seqlens,
+                             float *layer_out, void *ws, size_t ws_bytes, void *stream);
+
+/* Synchronise `stream`; return CFD_E_DEVICE (and clear the word) if a kernel flagged
+ * invalid device-side input since the last check, CFD_E_CUDA on a sticky CUDA error. */
+cfd_status cfd_check(cfd_ctx *ctx, void *stream);
+
+const char *cfd_status_str(cfd_status s);
+
+/* Library build identification string (static storage). */
+const char *cfd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CFDETR_H_ */

@@ -1,0 +1,56 @@
+/* cfdetr_debug.h — kernel-level entry points of libcfdetr.so for parity tests.
+ *
+ * These run ONE kernel of the hot path on caller buffers so tests can compare
+ * intermediate layouts bit for bit (gather/select) and each tensor-core kernel
+ * within tolerance, independently of the full call chain.  Same conventions as
+ * cfdetr.h: device pointers unless h_-prefixed, bf16 as uint16_t, stream as void*,
+ * enqueue-only, cfd_status results.  Not needed by normal users.
+ */
+#ifndef CFDETR_DEBUG_H_
+#define CFDETR_DEBUG_H_
+
+#include "cfdetr.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Epilogue selectors of cfdx_gemm (D = A . W^T, A [M,K] bf16, W [N,K] bf16 K-major):
+ *   0  out_bf16[M,N] = bf16(D + bias)            (QKV projection)
+ *   1  out_bf16[M,N] = bf16(GELU(D + bias))      (MLP1; GELU = z/2 (1 + erf(z/sqrt2)))
+ *   2  out_f32[M,N] += D + bias                   (O-projection / MLP2 residual)
+ * M is any positive count; N multiple of 64; K multiple of 64. */
+cfd_status cfdx_gemm(int32_t M, int32_t N, int32_t K, const uint16_t *A, const uint16_t *W, const float *bias,
+                     int32_t epi, uint16_t *out_bf16, float *out_f32, void *stream);
+
+/* Varlen multi-head attention over packed qkv [rows, 3d] (q | k | v) with
+ * cu_seqlens [T+1]; writes O [rows, d] bf16 and, if lse != NULL, the natural-log
+ * row log-sum-exp [nh, lse_ld].  rows_cap = rows allocated in qkv. */
+cfd_status cfdx_attention(int32_t n_tasks, const int32_t *cu_seqlens, int32_t max_seqlen, int32_t rows_cap,
+                          int32_t d_model, int32_t n_heads, const uint16_t *qkv, uint16_t *out, float *lse,
+                          int32_t lse_ld, void *stream);
+
+/* Row LayerNorm of fp32 x [M, d] -> bf16 y [M, d] (d in {64,128,256,512}). */
+cfd_status cfdx_layernorm(int32_t M, int32_t d, const float *x, const float *g, const float *b, float eps,
+                          uint16_t *y, void *stream);
+
+/* Criticality score from packed equal-length frames: qkv [B*Nc, 3d], lse [nh, lse_ld]
+ * -> scores [B, Nc]. */
+cfd_status cfdx_score(int32_t n_frames, int32_t n_coarse, int32_t d_model, int32_t n_heads, const uint16_t *qkv,
+                      int32_t rows_cap, const float *lse, int32_t lse_ld, float *scores, void *stream);
+
+/* The B8 gather alone (ctx geometry): writes X coarse rows, cu_seqlens [T+1],
+ * mixed_src, A_f [R, 3Pf^2] bf16, frow [R], fidx [R], meta [2] = {sum N_t, R}. */
+cfd_status cfdx_gather(cfd_ctx *ctx, int32_t n_tasks, const uint16_t *images, const float *x0,
+                       const int32_t *sel_idx, const int32_t *sel_count, float *X, int32_t *cu_seqlens,
+                       int32_t *mixed_src, uint16_t *A_f, int32_t *frow, int32_t *fidx, int32_t *meta,
+                       void *stream);
+
+/* Number of kernels the library launched since load (host counter; for bench's
+ * gpu_launches claim). */
+int64_t cfdx_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CFDETR_DEBUG_H_ */

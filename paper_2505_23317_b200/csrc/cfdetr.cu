@@ -1,0 +1,654 @@
+// cfdetr.cu — host side of libcfdetr.so: the C ABI of include/cfdetr.h and
+// include/cfdetr_debug.h.  Owns weight repacking, TMA descriptors, workspace
+// carving and the launch sequence of every call:
+//
+//   cfd_coarse_encode : im2col -> B1 embed GEMM -> L x [LN1 -> QKV GEMM -> attention
+//                       (-> score at score_layer) -> O GEMM(+res) -> LN2 -> MLP1(GELU)
+//                       -> MLP2(+res)]
+//   cfd_select_regions: B7 select
+//   cfd_batch_refine  : B8 gather -> B9 fine embed GEMM (row scatter) -> L x [same
+//                       block, varlen attention over cu_seqlens]
+// All launches go to the caller's stream; no host synchronisation.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/cfdetr.h"
+#include "../../include/cfdetr_debug.h"
+#include "attn_tc.cuh"
+#include "gemm_tc.cuh"
+#include "misc_kernels.cuh"
+#include "score_tc.cuh"
+
+using namespace cfd;
+
+namespace {
+
+std::atomic<int64_t> g_launches{0};
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode_fn() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map: inner dim `inner` elements (contiguous), `outer` rows with
+// row stride `ld` elements, box {box_inner, box_outer}.
+bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+               uint32_t box_outer, CUtensorMapSwizzle sw) {
+  PFN_encodeTiled enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ------------------------------------------------------------------ GEMM dispatch
+template <int BN>
+constexpr int gemm_stages() { return BN == 256 ? 4 : BN == 128 ? 6 : 8; }
+
+template <int BN, int EPI>
+cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows_for_grid,
+                          cudaStream_t s) {
+  constexpr int ST = gemm_stages<BN>();
+  auto kern = gemm_tc_kernel<BN, ST, EPI>;
+  constexpr int smem = GemmSmem<BN, ST>::TOTAL;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles = ((rows_for_grid + GEMM_BM - 1) / GEMM_BM) * (p.N / BN);
+  const int grid = tiles < num_sms() ? (tiles > 0 ? tiles : 1) : num_sms();
+  kern<<<grid, GEMM_THREADS, smem, s>>>(ta, tb, p);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+template <int EPI>
+cudaError_t launch_gemm_bn(int BN, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows,
+                           cudaStream_t s) {
+  switch (BN) {
+    case 256: return launch_gemm_t<256, EPI>(ta, tb, p, rows, s);
+    case 128: return launch_gemm_t<128, EPI>(ta, tb, p, rows, s);
+    default: return launch_gemm_t<64, EPI>(ta, tb, p, rows, s);
+  }
+}
+
+int pick_bn(int N) { return (N % 256 == 0) ? 256 : (N % 128 == 0) ? 128 : 64; }
+
+cudaError_t launch_gemm(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows,
+                        cudaStream_t s) {
+  const int BN = pick_bn(p.N);
+  switch (epi) {
+    case EPI_BF16_BIAS: return launch_gemm_bn<EPI_BF16_BIAS>(BN, ta, tb, p, rows, s);
+    case EPI_BF16_BIAS_GELU: return launch_gemm_bn<EPI_BF16_BIAS_GELU>(BN, ta, tb, p, rows, s);
+    case EPI_F32_RESID: return launch_gemm_bn<EPI_F32_RESID>(BN, ta, tb, p, rows, s);
+    case EPI_EMBED_COARSE: return launch_gemm_bn<EPI_EMBED_COARSE>(BN, ta, tb, p, rows, s);
+    default: return launch_gemm_bn<EPI_EMBED_FINE>(BN, ta, tb, p, rows, s);
+  }
+}
+
+// B tensor map for a K-major weight [N, K]
+bool make_wmap(CUtensorMap* m, const void* w, int N, int K) {
+  return make_tmap(m, w, K, N, K, GEMM_BK, pick_bn(N), CU_TENSOR_MAP_SWIZZLE_128B);
+}
+bool make_amap(CUtensorMap* m, const void* a, int rows, int K) {
+  return make_tmap(m, a, K, rows, K, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+bool make_qkvmap(CUtensorMap* m, const void* qkv, int rows, int d) {
+  return make_tmap(m, qkv, 3 * d, rows, 3 * d, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
+}
+
+cudaError_t launch_attention(const CUtensorMap& tq, const AttnParams& p, int max_qtiles, int nh, int T,
+                             cudaStream_t s) {
+  auto kern = attn_tc_kernel<32, 3>;
+  constexpr int smem = AttnSmem<32, 3>::TOTAL;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  kern<<<dim3(max_qtiles, nh, T), ATTN_THREADS, smem, s>>>(tq, p);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_score(const CUtensorMap& tq, const ScoreParams& p, int B, cudaStream_t s) {
+  auto kern = score_tc_kernel<32>;
+  constexpr int smem = ScoreSmem<32>::TOTAL;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  kern<<<dim3((p.n_coarse + 127) / 128, B), SCORE_THREADS, smem, s>>>(tq, p);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_layernorm(int d, const float* x, const float* g, const float* b, __nv_bfloat16* y, int M,
+                             const int* m_dev, int m_cap, float eps, int rows_for_grid, cudaStream_t s) {
+  const int rows_pad = std::min(((rows_for_grid + 127) / 128) * 128, m_cap);
+  int blocks = (rows_pad + 7) / 8;
+  blocks = std::max(1, std::min(blocks, num_sms() * 16));
+  switch (d) {
+    case 64: layernorm_kernel<2><<<blocks, 256, 0, s>>>(x, g, b, y, M, m_dev, m_cap, eps); break;
+    case 128: layernorm_kernel<4><<<blocks, 256, 0, s>>>(x, g, b, y, M, m_dev, m_cap, eps); break;
+    case 256: layernorm_kernel<8><<<blocks, 256, 0, s>>>(x, g, b, y, M, m_dev, m_cap, eps); break;
+    case 512: layernorm_kernel<16><<<blocks, 256, 0, s>>>(x, g, b, y, M, m_dev, m_cap, eps); break;
+    default: return cudaErrorInvalidValue;
+  }
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// ====================================================================== ctx
+struct LayerDev {
+  uint16_t *wqkv, *wo, *w1, *w2;  // K-major [N, K]
+  float *b_qkv, *b_o, *b_1, *b_2, *ln1_g, *ln1_b, *ln2_g, *ln2_b;
+  CUtensorMap tm_qkv, tm_o, tm_1, tm_2;
+};
+
+struct cfd_ctx {
+  cfd_config cfg;
+  int Nc, Nf, m, dh, Kc, Kf, gc_w, gf_w;
+  void* block = nullptr;  // single device allocation for all ctx-owned data
+  uint16_t *wc = nullptr, *wf = nullptr;
+  float *bc = nullptr, *bf = nullptr, *pec = nullptr, *pef = nullptr;
+  int* err = nullptr;
+  std::vector<LayerDev> layers;
+  CUtensorMap tm_wc, tm_wf;
+};
+
+namespace {
+
+struct Workspace {
+  __nv_bfloat16 *hbuf, *qkv, *obuf, *ff;
+  uint16_t* patches;
+  int32_t *frow, *fidx, *meta, *ccu;
+  float* lse;
+  int rows_cap;   // token capacity of hbuf/qkv/obuf/ff
+  int lse_ld;
+  size_t bytes;
+};
+
+// Carve the workspace for n tasks/frames.  base == nullptr -> size only.
+Workspace carve(const cfd_ctx* c, int n, void* base) {
+  Workspace w{};
+  const cfd_config& g = c->cfg;
+  const size_t rows = (size_t)n * c->Nf + 128;
+  w.rows_cap = (int)rows;
+  w.lse_ld = n * c->Nc;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 1024);
+    return base ? static_cast<char*>(base) + o : nullptr;
+  };
+  w.hbuf = (__nv_bfloat16*)take(rows * g.d_model * 2);
+  w.qkv = (__nv_bfloat16*)take(rows * 3 * g.d_model * 2);
+  w.obuf = (__nv_bfloat16*)take(rows * g.d_model * 2);
+  w.ff = (__nv_bfloat16*)take(rows * g.d_ff * 2);
+  w.patches = (uint16_t*)take(((size_t)n * g.img_h * g.img_w * 3 + 128 * (size_t)c->Kc) * 2);
+  w.frow = (int32_t*)take((size_t)n * c->Nf * 4 + 16);
+  w.fidx = (int32_t*)take((size_t)n * c->Nf * 4 + 16);
+  w.meta = (int32_t*)take(64);
+  w.ccu = (int32_t*)take((size_t)(n + 1) * 4);
+  w.lse = (float*)take((size_t)g.n_heads * n * c->Nc * 4 + 16);
+  w.bytes = off;
+  return w;
+}
+
+#define CFD_CUDA(x)                                  \
+  do {                                               \
+    cudaError_t e__ = (x);                           \
+    if (e__ != cudaSuccess) return CFD_E_CUDA;       \
+  } while (0)
+
+// One pre-LN encoder block on the packed residual stream x (fp32 [*, d]).
+cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const int* m_dev, int rows_grid,
+                     const int32_t* cu, int T, int max_qtiles, Workspace& w, bool want_lse, float* scores,
+                     int score_B, cudaStream_t s) {
+  const cfd_config& g = c->cfg;
+  const int d = g.d_model, F = g.d_ff;
+  LayerDev& L = c->layers[l];
+  CUtensorMap ta_h, ta_o, ta_f, tq;
+  if (!make_amap(&ta_h, w.hbuf, w.rows_cap, d) || !make_amap(&ta_o, w.obuf, w.rows_cap, d) ||
+      !make_amap(&ta_f, w.ff, w.rows_cap, F) || !make_qkvmap(&tq, w.qkv, w.rows_cap, d))
+    return CFD_E_CUDA;
+  // LN1
+  CFD_CUDA(launch_layernorm(d, x, L.ln1_g, L.ln1_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
+  // QKV
+  GemmParams p{};
+  p.M = M_static; p.m_dev = m_dev; p.m_cap = w.rows_cap; p.N = 3 * d; p.K = d; p.bias = L.b_qkv;
+  p.out_bf16 = w.qkv;
+  CFD_CUDA(launch_gemm(EPI_BF16_BIAS, ta_h, L.tm_qkv, p, rows_grid, s));
+  // attention
+  AttnParams ap{};
+  ap.cu_seqlens = cu; ap.d_model = d; ap.out = w.obuf; ap.lse = want_lse ? w.lse : nullptr; ap.lse_ld = w.lse_ld;
+  ap.scale_log2 = 1.4426950408889634f / std::sqrt((float)c->dh);
+  CFD_CUDA(launch_attention(tq, ap, max_qtiles, g.n_heads, T, s));
+  if (want_lse && scores) {
+    ScoreParams sp{};
+    sp.n_coarse = c->Nc; sp.n_heads = g.n_heads; sp.d_model = d; sp.lse = w.lse; sp.lse_ld = w.lse_ld;
+    sp.scale_log2 = ap.scale_log2; sp.scores = scores;
+    CFD_CUDA(launch_score(tq, sp, score_B, s));
+  }
+  // O projection + residual
+  p = GemmParams{};
+  p.M = M_static; p.m_dev = m_dev; p.m_cap = x_cap; p.N = d; p.K = d; p.bias = L.b_o; p.out_f32 = x; p.ld_out = d;
+  CFD_CUDA(launch_gemm(EPI_F32_RESID, ta_o, L.tm_o, p, rows_grid, s));
+  // LN2
+  CFD_CUDA(launch_layernorm(d, x, L.ln2_g, L.ln2_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
+  // MLP1 + GELU
+  p = GemmParams{};
+  p.M = M_static; p.m_dev = m_dev; p.m_cap = w.rows_cap; p.N = F; p.K = d; p.bias = L.b_1; p.out_bf16 = w.ff;
+  CFD_CUDA(launch_gemm(EPI_BF16_BIAS_GELU, ta_h, L.tm_1, p, rows_grid, s));
+  // MLP2 + residual
+  p = GemmParams{};
+  p.M = M_static; p.m_dev = m_dev; p.m_cap = x_cap; p.N = d; p.K = F; p.bias = L.b_2; p.out_f32 = x; p.ld_out = d;
+  CFD_CUDA(launch_gemm(EPI_F32_RESID, ta_f, L.tm_2, p, rows_grid, s));
+  return CFD_OK;
+}
+
+cfd_status validate_cfg(const cfd_config* g) {
+  if (!g) return CFD_E_ARG;
+  if (g->img_h <= 0 || g->img_w <= 0 || g->patch_coarse <= 0 || g->patch_fine <= 0 || g->d_model <= 0 ||
+      g->n_heads <= 0 || g->n_layers <= 0 || g->d_ff <= 0 || g->max_tasks <= 0)
+    return CFD_E_ARG;
+  if (g->score_layer < 0 || g->score_layer >= g->n_layers) return CFD_E_ARG;
+  if (g->img_h % g->patch_coarse || g->img_w % g->patch_coarse || g->patch_coarse % g->patch_fine ||
+      g->d_model % g->n_heads)
+    return CFD_E_SHAPE;
+  if (g->d_model / g->n_heads != 32) return CFD_E_UNSUPPORTED;
+  if (g->d_model != 64 && g->d_model != 128 && g->d_model != 256 && g->d_model != 512) return CFD_E_UNSUPPORTED;
+  if (g->d_ff % 64) return CFD_E_UNSUPPORTED;
+  if ((3 * g->patch_fine * g->patch_fine) % 64 || (g->patch_fine * 3 * 2) % 16) return CFD_E_UNSUPPORTED;
+  const int Nc = (g->img_h / g->patch_coarse) * (g->img_w / g->patch_coarse);
+  if (Nc > 4096) return CFD_E_UNSUPPORTED;
+  return CFD_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* cfd_version(void) { return "cfdetr-b200 0.1 (sm_100a, tcgen05/TMEM/TMA)"; }
+
+const char* cfd_status_str(cfd_status s) {
+  switch (s) {
+    case CFD_OK: return "ok";
+    case CFD_E_ARG: return "invalid argument";
+    case CFD_E_SHAPE: return "invalid shape";
+    case CFD_E_UNSUPPORTED: return "unsupported configuration";
+    case CFD_E_CAPACITY: return "capacity exceeded";
+    case CFD_E_CUDA: return "CUDA error";
+    case CFD_E_DEVICE: return "device-side input error";
+  }
+  return "unknown status";
+}
+
+int64_t cfdx_launch_count(void) { return g_launches.load(); }
+
+cfd_status cfd_create(const cfd_config* cfg, const cfd_weights* wts, void* stream, cfd_ctx** out) {
+  if (!out || !wts || !wts->h_layers || !wts->w_embed_c || !wts->w_embed_f || !wts->b_embed_c || !wts->b_embed_f ||
+      !wts->pe_c || !wts->pe_f)
+    return CFD_E_ARG;
+  *out = nullptr;
+  cfd_status st = validate_cfg(cfg);
+  if (st != CFD_OK) return st;
+  if (!get_encode_fn()) return CFD_E_CUDA;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cfd_ctx* c = new (std::nothrow) cfd_ctx();
+  if (!c) return CFD_E_CUDA;
+  c->cfg = *cfg;
+  const cfd_config& g = *cfg;
+  c->m = g.patch_coarse / g.patch_fine;
+  c->gc_w = g.img_w / g.patch_coarse;
+  c->gf_w = g.img_w / g.patch_fine;
+  c->Nc = (g.img_h / g.patch_coarse) * c->gc_w;
+  c->Nf = c->Nc * c->m * c->m;
+  c->dh = g.d_model / g.n_heads;
+  c->Kc = 3 * g.patch_coarse * g.patch_coarse;
+  c->Kf = 3 * g.patch_fine * g.patch_fine;
+  const int d = g.d_model, F = g.d_ff, L = g.n_layers;
+  // sizes
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+  const size_t o_wc = take((size_t)d * c->Kc * 2), o_wf = take((size_t)d * c->Kf * 2);
+  const size_t o_bc = take(d * 4), o_bf = take(d * 4), o_pec = take((size_t)c->Nc * d * 4),
+               o_pef = take((size_t)c->Nf * d * 4), o_err = take(16);
+  std::vector<size_t> o_l(L);
+  const size_t per_layer_mat = (size_t)(3 * d * d + d * d + d * F + F * d) * 2;
+  const size_t per_layer_vec = (size_t)(3 * d + d + F + d + 4 * d) * 4;
+  for (int l = 0; l < L; ++l) o_l[l] = take(per_layer_mat + per_layer_vec + 8 * 256);
+  if (cudaMalloc(&c->block, off) != cudaSuccess) { delete c; return CFD_E_CUDA; }
+  char* B = static_cast<char*>(c->block);
+  c->wc = (uint16_t*)(B + o_wc); c->wf = (uint16_t*)(B + o_wf);
+  c->bc = (float*)(B + o_bc); c->bf = (float*)(B + o_bf);
+  c->pec = (float*)(B + o_pec); c->pef = (float*)(B + o_pef);
+  c->err = (int*)(B + o_err);
+  auto fail = [&](cfd_status e) { cudaFree(c->block); delete c; return e; };
+  auto transpose = [&](const uint16_t* in, uint16_t* outp, int K, int N) {
+    dim3 grid((N + 31) / 32, (K + 31) / 32);
+    transpose_bf16_kernel<<<grid, dim3(32, 8), 0, s>>>(in, outp, K, N);
+    ++g_launches;
+    return cudaGetLastError();
+  };
+  if (transpose(wts->w_embed_c, c->wc, c->Kc, d) != cudaSuccess) return fail(CFD_E_CUDA);
+  if (transpose(wts->w_embed_f, c->wf, c->Kf, d) != cudaSuccess) return fail(CFD_E_CUDA);
+  if (cudaMemcpyAsync(c->bc, wts->b_embed_c, d * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(c->bf, wts->b_embed_f, d * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(c->pec, wts->pe_c, (size_t)c->Nc * d * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(c->pef, wts->pe_f, (size_t)c->Nf * d * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+      cudaMemsetAsync(c->err, 0, 16, s) != cudaSuccess)
+    return fail(CFD_E_CUDA);
+  if (!make_wmap(&c->tm_wc, c->wc, d, c->Kc) || !make_wmap(&c->tm_wf, c->wf, d, c->Kf)) return fail(CFD_E_CUDA);
+  c->layers.resize(L);
+  for (int l = 0; l < L; ++l) {
+    const cfd_layer_weights& hw = wts->h_layers[l];
+    if (!hw.w_qkv || !hw.w_o || !hw.w_1 || !hw.w_2 || !hw.b_qkv || !hw.b_o || !hw.b_1 || !hw.b_2 || !hw.ln1_g ||
+        !hw.ln1_b || !hw.ln2_g || !hw.ln2_b)
+      return fail(CFD_E_ARG);
+    LayerDev& ld = c->layers[l];
+    char* p = B + o_l[l];
+    size_t q = 0;
+    auto sub = [&](size_t bytes) { char* r = p + q; q = align_up(q + bytes, 256); return r; };
+    ld.wqkv = (uint16_t*)sub((size_t)3 * d * d * 2);
+    ld.wo = (uint16_t*)sub((size_t)d * d * 2);
+    ld.w1 = (uint16_t*)sub((size_t)d * F * 2);
+    ld.w2 = (uint16_t*)sub((size_t)F * d * 2);
+    ld.b_qkv = (float*)sub(3 * d * 4); ld.b_o = (float*)sub(d * 4); ld.b_1 = (float*)sub(F * 4);
+    ld.b_2 = (float*)sub(d * 4); ld.ln1_g = (float*)sub(d * 4); ld.ln1_b = (float*)sub(d * 4);
+    ld.ln2_g = (float*)sub(d * 4); ld.ln2_b = (float*)sub(d * 4);
+    if (transpose(hw.w_qkv, ld.wqkv, d, 3 * d) != cudaSuccess || transpose(hw.w_o, ld.wo, d, d) != cudaSuccess ||
+        transpose(hw.w_1, ld.w1, d, F) != cudaSuccess || transpose(hw.w_2, ld.w2, F, d) != cudaSuccess)
+      return fail(CFD_E_CUDA);
+    const std::pair<const float*, float*> vecs[] = {{hw.b_qkv, ld.b_qkv}, {hw.b_o, ld.b_o}, {hw.b_1, ld.b_1},
+                                                    {hw.b_2, ld.b_2},     {hw.ln1_g, ld.ln1_g}, {hw.ln1_b, ld.ln1_b},
+                                                    {hw.ln2_g, ld.ln2_g}, {hw.ln2_b, ld.ln2_b}};
+    const size_t lens[] = {(size_t)3 * d, (size_t)d, (size_t)F, (size_t)d, (size_t)d, (size_t)d, (size_t)d, (size_t)d};
+    for (int i = 0; i < 8; ++i)
+      if (cudaMemcpyAsync(vecs[i].second, vecs[i].first, lens[i] * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return fail(CFD_E_CUDA);
+    if (!make_wmap(&ld.tm_qkv, ld.wqkv, 3 * d, d) || !make_wmap(&ld.tm_o, ld.wo, d, d) ||
+        !make_wmap(&ld.tm_1, ld.w1, F, d) || !make_wmap(&ld.tm_2, ld.w2, d, F))
+      return fail(CFD_E_CUDA);
+  }
+  *out = c;
+  return CFD_OK;
+}
+
+cfd_status cfd_destroy(cfd_ctx* c) {
+  if (!c) return CFD_OK;
+  cudaDeviceSynchronize();
+  cudaFree(c->block);
+  delete c;
+  return CFD_OK;
+}
+
+cfd_status cfd_query(const cfd_ctx* c, int32_t n, int32_t* h_Nc, int32_t* h_Nf, int32_t* h_max_tokens,
+                     size_t* h_ws) {
+  if (!c || n < 0) return CFD_E_ARG;
+  if (h_Nc) *h_Nc = c->Nc;
+  if (h_Nf) *h_Nf = c->Nf;
+  if (h_max_tokens) *h_max_tokens = n * c->Nf;
+  if (h_ws) *h_ws = carve(c, n > 0 ? n : 1, nullptr).bytes + 1024;
+  return CFD_OK;
+}
+
+static void* align_ws(void* ws) {
+  return reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(ws), 1024));
+}
+
+cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, float* x0, float* y, float* scores,
+                             float* layer_out, void* ws, size_t ws_bytes, void* stream) {
+  if (!c) return CFD_E_ARG;
+  if (B == 0) return CFD_OK;
+  if (B < 0 || !images || !x0 || !y || !ws) return CFD_E_ARG;
+  if (B > c->cfg.max_tasks) return CFD_E_CAPACITY;
+  Workspace w = carve(c, B, align_ws(ws));
+  if (w.bytes + 1024 > ws_bytes) return CFD_E_CAPACITY;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const cfd_config& g = c->cfg;
+  const int d = g.d_model, M = B * c->Nc;
+  coarse_meta_kernel<<<1, 256, 0, s>>>(w.ccu, w.meta, B, c->Nc);
+  ++g_launches;
+  CFD_CUDA(cudaGetLastError());
+  {
+    const long long vec = (long long)B * g.img_h * (g.img_w / g.patch_coarse) * ((g.patch_coarse * 6) / 16);
+    const int blocks = (int)std::min<long long>((vec + 255) / 256, (long long)num_sms() * 8);
+    im2col_kernel<<<blocks, 256, 0, s>>>(images, w.patches, B, g.img_h, g.img_w, g.patch_coarse);
+    ++g_launches;
+    CFD_CUDA(cudaGetLastError());
+  }
+  CUtensorMap ta;
+  if (!make_amap(&ta, w.patches, M, c->Kc)) return CFD_E_CUDA;
+  GemmParams p{};
+  p.M = M; p.m_cap = M; p.N = d; p.K = c->Kc; p.bias = c->bc; p.out_f32 = y; p.out2_f32 = x0; p.ld_out = d;
+  p.pe = c->pec; p.pe_rows = c->Nc;
+  CFD_CUDA(launch_gemm(EPI_EMBED_COARSE, ta, c->tm_wc, p, M, s));
+  const int max_qtiles = (c->Nc + ATTN_BQ - 1) / ATTN_BQ;
+  for (int l = 0; l < g.n_layers; ++l) {
+    const bool sl = (l == g.score_layer);
+    cfd_status st = run_layer(c, l, y, M, M, nullptr, M, w.ccu, B, max_qtiles, w, sl && scores, scores, B, s);
+    if (st != CFD_OK) return st;
+    if (layer_out)
+      CFD_CUDA(cudaMemcpyAsync(layer_out + (size_t)l * M * d, y, (size_t)M * d * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  return CFD_OK;
+}
+
+cfd_status cfd_select_regions(cfd_ctx* c, int32_t T, const float* scores, cfd_select_mode mode, const int32_t* h_k,
+                              float threshold, int32_t* sel_idx, int32_t* sel_count, void* stream) {
+  if (!c) return CFD_E_ARG;
+  if (T == 0) return CFD_OK;
+  if (T < 0 || !scores || !sel_idx || !sel_count) return CFD_E_ARG;
+  if (mode != CFD_SELECT_TOPK && mode != CFD_SELECT_THRESHOLD) return CFD_E_ARG;
+  if (mode == CFD_SELECT_TOPK) {
+    if (!h_k) return CFD_E_ARG;
+    for (int t = 0; t < T; ++t)
+      if (h_k[t] < 0 || h_k[t] > c->Nc) return CFD_E_ARG;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int Nc = c->Nc;
+  for (int t0 = 0; t0 < T; t0 += SELECT_CHUNK) {
+    const int nt = std::min(SELECT_CHUNK, T - t0);
+    SelectK ks;
+    std::memset(&ks, 0, sizeof(ks));
+    if (mode == CFD_SELECT_TOPK) std::memcpy(ks.k, h_k + t0, nt * sizeof(int));
+    const float* sc = scores + (size_t)t0 * Nc;
+    int32_t* si = sel_idx + (size_t)t0 * Nc;
+    int32_t* cnt = sel_count + t0;
+    if (Nc <= 512) select_kernel<512><<<nt, 512, 0, s>>>(sc, Nc, (int)mode, ks, threshold, si, cnt);
+    else if (Nc <= 1024) select_kernel<1024><<<nt, 512, 0, s>>>(sc, Nc, (int)mode, ks, threshold, si, cnt);
+    else if (Nc <= 2048) select_kernel<2048><<<nt, 512, 0, s>>>(sc, Nc, (int)mode, ks, threshold, si, cnt);
+    else select_kernel<4096><<<nt, 512, 0, s>>>(sc, Nc, (int)mode, ks, threshold, si, cnt);
+    ++g_launches;
+    CFD_CUDA(cudaGetLastError());
+  }
+  return CFD_OK;
+}
+
+static cfd_status launch_gather(cfd_ctx* c, int T, const uint16_t* images, const float* x0, const int32_t* sel_idx,
+                                const int32_t* sel_count, float* X, int32_t* cu, int32_t* msrc, uint16_t* A_f,
+                                int32_t* frow, int32_t* fidx, int32_t* meta, cudaStream_t s) {
+  GatherParams gp{};
+  const cfd_config& g = c->cfg;
+  gp.T = T; gp.Nc = c->Nc; gp.gc_w = c->gc_w; gp.m = c->m; gp.gf_w = c->gf_w; gp.d = g.d_model;
+  gp.H = g.img_h; gp.W = g.img_w; gp.Pf = g.patch_fine;
+  gp.images = images; gp.x0 = x0; gp.sel_idx = sel_idx; gp.sel_count = sel_count; gp.X = X; gp.cu_seqlens = cu;
+  gp.mixed_src = msrc; gp.A_f = A_f; gp.frow = frow; gp.fidx = fidx; gp.meta = meta; gp.err = c->err;
+  const int G = std::max(1, std::min(16, (c->Nc + 63) / 64));
+  const size_t smem = (size_t)2 * c->Nc * sizeof(int32_t);
+  gather_kernel<<<dim3(T, G), 256, smem, s>>>(gp);
+  ++g_launches;
+  CFD_CUDA(cudaGetLastError());
+  return CFD_OK;
+}
+
+cfd_status cfd_batch_refine(cfd_ctx* c, int32_t T, const uint16_t* images, const float* x0, const int32_t* sel_idx,
+                            const int32_t* sel_count, const int32_t* h_token_counts, float* y, int32_t* cu,
+                            int32_t* msrc, float* layer_out, void* ws, size_t ws_bytes, void* stream) {
+  if (!c) return CFD_E_ARG;
+  if (T == 0) return CFD_OK;
+  if (T < 0 || !images || !x0 || !sel_idx || !sel_count || !y || !cu || !msrc || !ws) return CFD_E_ARG;
+  if (T > c->cfg.max_tasks) return CFD_E_CAPACITY;
+  Workspace w = carve(c, T, align_ws(ws));
+  if (w.bytes + 1024 > ws_bytes) return CFD_E_CAPACITY;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const cfd_config& g = c->cfg;
+  const int d = g.d_model;
+  const int cap = T * c->Nf;
+  // host-side sizing hints (grid sizes only; every kernel reads the true counts on device)
+  int rows_grid = cap, fine_grid = cap;
+  if (h_token_counts) {
+    long long tot = 0;
+    for (int t = 0; t < T; ++t) {
+      const int n = h_token_counts[t];
+      if (n < c->Nc || n > c->Nf || (n - c->Nc) % (c->m * c->m - 1 > 0 ? c->m * c->m - 1 : 1)) return CFD_E_ARG;
+      tot += n;
+    }
+    rows_grid = (int)tot;
+    const int m2 = c->m * c->m;
+    fine_grid = (m2 > 1) ? (int)((tot - (long long)T * c->Nc) / (m2 - 1) * m2) : 0;
+  }
+  cfd_status st = launch_gather(c, T, images, x0, sel_idx, sel_count, y, cu, msrc, w.patches, w.frow, w.fidx,
+                                w.meta, s);
+  if (st != CFD_OK) return st;
+  CUtensorMap ta;
+  if (!make_amap(&ta, w.patches, cap + 128, c->Kf)) return CFD_E_CUDA;
+  GemmParams p{};
+  p.M = 0; p.m_dev = w.meta + 1; p.m_cap = cap; p.N = d; p.K = c->Kf; p.bias = c->bf; p.out_f32 = y; p.ld_out = d;
+  p.pe = c->pef; p.pe_rows = c->Nf; p.frow = w.frow; p.fidx = w.fidx;
+  CFD_CUDA(launch_gemm(EPI_EMBED_FINE, ta, c->tm_wf, p, std::max(fine_grid, 1), s));
+  const int max_qtiles = (c->Nf + ATTN_BQ - 1) / ATTN_BQ;
+  for (int l = 0; l < g.n_layers; ++l) {
+    st = run_layer(c, l, y, cap, 0, w.meta, std::max(rows_grid, 1), cu, T, max_qtiles, w, false, nullptr, 0, s);
+    if (st != CFD_OK) return st;
+    if (layer_out)
+      CFD_CUDA(cudaMemcpyAsync(layer_out + (size_t)l * cap * d, y, (size_t)cap * d * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  return CFD_OK;
+}
+
+cfd_status cfd_refine_encode(cfd_ctx* c, const uint16_t* image, const float* x0, const int32_t* sel_idx,
+                             const int32_t* sel_count, float* y, int32_t* msrc, int32_t* cu, float* layer_out,
+                             void* ws, size_t ws_bytes, void* stream) {
+  return cfd_batch_refine(c, 1, image, x0, sel_idx, sel_count, nullptr, y, cu, msrc, layer_out, ws, ws_bytes,
+                          stream);
+}
+
+cfd_status cfd_check(cfd_ctx* c, void* stream) {
+  if (!c) return CFD_E_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return CFD_E_CUDA;
+  int e = 0;
+  if (cudaMemcpy(&e, c->err, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return CFD_E_CUDA;
+  if (e) {
+    cudaMemset(c->err, 0, sizeof(int));
+    return CFD_E_DEVICE;
+  }
+  return CFD_OK;
+}
+
+// ---------------------------------------------------------------------- debug entry points
+cfd_status cfdx_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const uint16_t* W, const float* bias,
+                     int32_t epi, uint16_t* out_bf16, float* out_f32, void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || N % 64 || K % 64 || !A || !W || !bias) return CFD_E_ARG;
+  if (epi < 0 || epi > 2 || (epi < 2 && !out_bf16) || (epi == 2 && !out_f32)) return CFD_E_ARG;
+  CUtensorMap ta, tb;
+  if (!make_amap(&ta, A, M, K) || !make_wmap(&tb, W, N, K)) return CFD_E_CUDA;
+  GemmParams p{};
+  p.M = M; p.m_cap = M; p.N = N; p.K = K; p.bias = bias; p.out_bf16 = (__nv_bfloat16*)out_bf16; p.out_f32 = out_f32;
+  p.ld_out = N;
+  CFD_CUDA(launch_gemm(epi, ta, tb, p, M, static_cast<cudaStream_t>(stream)));
+  return CFD_OK;
+}
+
+cfd_status cfdx_attention(int32_t T, const int32_t* cu, int32_t max_seqlen, int32_t rows_cap, int32_t d,
+                          int32_t nh, const uint16_t* qkv, uint16_t* out, float* lse, int32_t lse_ld,
+                          void* stream) {
+  if (T <= 0 || !cu || !qkv || !out || max_seqlen <= 0 || rows_cap <= 0 || nh <= 0 || d % nh || d / nh != 32)
+    return CFD_E_ARG;
+  CUtensorMap tq;
+  if (!make_qkvmap(&tq, qkv, rows_cap, d)) return CFD_E_CUDA;
+  AttnParams ap{};
+  ap.cu_seqlens = cu; ap.d_model = d; ap.out = (__nv_bfloat16*)out; ap.lse = lse; ap.lse_ld = lse_ld;
+  ap.scale_log2 = 1.4426950408889634f / std::sqrt(32.0f);
+  CFD_CUDA(launch_attention(tq, ap, (max_seqlen + ATTN_BQ - 1) / ATTN_BQ, nh, T, static_cast<cudaStream_t>(stream)));
+  return CFD_OK;
+}
+
+cfd_status cfdx_layernorm(int32_t M, int32_t d, const float* x, const float* g, const float* b, float eps,
+                          uint16_t* y, void* stream) {
+  if (M <= 0 || !x || !g || !b || !y) return CFD_E_ARG;
+  CFD_CUDA(launch_layernorm(d, x, g, b, (__nv_bfloat16*)y, M, nullptr, M, eps, M, static_cast<cudaStream_t>(stream)));
+  return CFD_OK;
+}
+
+cfd_status cfdx_score(int32_t B, int32_t Nc, int32_t d, int32_t nh, const uint16_t* qkv, int32_t rows_cap,
+                      const float* lse, int32_t lse_ld, float* scores, void* stream) {
+  if (B <= 0 || Nc <= 0 || !qkv || !lse || !scores || d / nh != 32) return CFD_E_ARG;
+  CUtensorMap tq;
+  if (!make_qkvmap(&tq, qkv, rows_cap, d)) return CFD_E_CUDA;
+  ScoreParams sp{};
+  sp.n_coarse = Nc; sp.n_heads = nh; sp.d_model = d; sp.lse = lse; sp.lse_ld = lse_ld;
+  sp.scale_log2 = 1.4426950408889634f / std::sqrt(32.0f); sp.scores = scores;
+  CFD_CUDA(launch_score(tq, sp, B, static_cast<cudaStream_t>(stream)));
+  return CFD_OK;
+}
+
+cfd_status cfdx_gather(cfd_ctx* c, int32_t T, const uint16_t* images, const float* x0, const int32_t* sel_idx,
+                       const int32_t* sel_count, float* X, int32_t* cu, int32_t* msrc, uint16_t* A_f, int32_t* frow,
+                       int32_t* fidx, int32_t* meta, void* stream) {
+  if (!c || T <= 0 || !images || !x0 || !sel_idx || !sel_count || !X || !cu || !msrc || !A_f || !frow || !fidx ||
+      !meta)
+    return CFD_E_ARG;
+  return launch_gather(c, T, images, x0, sel_idx, sel_count, X, cu, msrc, A_f, frow, fidx, meta,
+                       static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

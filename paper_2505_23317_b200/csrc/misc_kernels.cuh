@@ -1,0 +1,312 @@
+// misc_kernels.cuh — the non-tensor-core kernels of the hot path:
+//   layernorm_kernel    fp32 residual -> bf16 LN output (+ zeroed pad rows)
+//   im2col_kernel       coarse patch matrix from HWC bf16 frames (A1 patch split)
+//   select_kernel       B7: per-task top-k (bitonic sort on total-order keys) or threshold
+//   gather_kernel       B8: offsets, cu_seqlens, mixed_src, coarse-row reuse copy,
+//                       fine-patch pixel gather A_f, frow/fidx (A2 selective split)
+//   transpose_bf16      weight repack (in,out) -> K-major (out,in) at cfd_create
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace cfd {
+
+// error word bits (device-side input validation, reported by cfd_check)
+enum : int { ERR_SEL_COUNT = 1, ERR_SEL_ORDER = 2, ERR_TOKEN_HINT = 4 };
+
+// ------------------------------------------------------------------ LayerNorm
+// One warp per row; VPT = d/32 values per lane (d in {64,128,256,512}).
+// LN(x) = (x - mean)/sqrt(var + eps)*g + b, biased variance, fp32 statistics.
+template <int VPT>
+__global__ void layernorm_kernel(const float* __restrict__ x, const float* __restrict__ g,
+                                 const float* __restrict__ b, __nv_bfloat16* __restrict__ y, int M,
+                                 const int* __restrict__ m_dev, int m_cap, float eps) {
+  constexpr int D = VPT * 32;
+  const int rows = m_dev ? __ldg(m_dev) : M;
+  const int m_pad = min(((rows + 127) / 128) * 128, m_cap);
+  const int warps_per_block = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * warps_per_block + (threadIdx.x >> 5); row < m_pad; row += gridDim.x * warps_per_block) {
+    __nv_bfloat16* yr = y + (size_t)row * D;
+    if (row >= rows) {  // pad rows: zeros, so attention tail tiles read finite data
+      if constexpr (VPT % 8 == 0) {
+#pragma unroll
+        for (int i = 0; i < VPT / 8; ++i) reinterpret_cast<uint4*>(yr)[lane + 32 * i] = make_uint4(0, 0, 0, 0);
+      } else {
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) yr[lane * VPT + i] = __float2bfloat16(0.f);
+      }
+      continue;
+    }
+    const float* xr = x + (size_t)row * D;
+    float v[VPT];
+    // lane owns contiguous VPT values [lane*VPT, lane*VPT+VPT)
+    if constexpr (VPT % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < VPT; i += 4) {
+        float4 q = *reinterpret_cast<const float4*>(xr + lane * VPT + i);
+        v[i] = q.x; v[i + 1] = q.y; v[i + 2] = q.z; v[i + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < VPT; i += 2) {
+        float2 q = *reinterpret_cast<const float2*>(xr + lane * VPT + i);
+        v[i] = q.x; v[i + 1] = q.y;
+      }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) s += v[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mean = s * (1.0f / D);
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) { const float dlt = v[i] - mean; ss += dlt * dlt; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float rstd = rsqrtf(ss * (1.0f / D) + eps);
+    uint32_t pk[VPT / 2];
+#pragma unroll
+    for (int i = 0; i < VPT; i += 2) {
+      const int col = lane * VPT + i;
+      const float a = (v[i] - mean) * rstd * __ldg(g + col) + __ldg(b + col);
+      const float c = (v[i + 1] - mean) * rstd * __ldg(g + col + 1) + __ldg(b + col + 1);
+      __nv_bfloat162 t2 = __floats2bfloat162_rn(a, c);
+      pk[i / 2] = *reinterpret_cast<uint32_t*>(&t2);
+    }
+    if constexpr (VPT == 8) {
+      reinterpret_cast<uint4*>(yr)[lane] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < VPT / 2; ++i) reinterpret_cast<uint32_t*>(yr)[lane * (VPT / 2) + i] = pk[i];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ im2col (coarse patch split)
+// A[b*Nc + c][(py*P + px)*3 + ch] = img[b][cy*P + py][cx*P + px][ch]     (reading R2)
+// Each (frame, image row y, patch column cx) segment is P*3 contiguous bf16 in
+// both source and destination; moved as 16-byte vectors.
+__global__ void im2col_kernel(const uint16_t* __restrict__ img, uint16_t* __restrict__ A, int B, int H, int W,
+                              int P) {
+  const int seg_vec = (P * 3 * 2) / 16;  // 16B vectors per segment
+  const int gw = W / P;
+  const long long total = (long long)B * H * gw * seg_vec;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int v = (int)(i % seg_vec);
+    long long rest = i / seg_vec;
+    const int cx = (int)(rest % gw);
+    rest /= gw;
+    const int y = (int)(rest % H);
+    const int b = (int)(rest / H);
+    const int cy = y / P, py = y % P;
+    const uint4* src = reinterpret_cast<const uint4*>(img + (((size_t)b * H + y) * W + (size_t)cx * P) * 3) + v;
+    const size_t c = (size_t)b * (H / P) * gw + (size_t)cy * gw + cx;
+    uint4* dst = reinterpret_cast<uint4*>(A + c * (size_t)(3 * P * P) + (size_t)py * P * 3) + v;
+    *dst = __ldg(src);
+  }
+}
+
+// ------------------------------------------------------------------ select (B7)
+// Total-order key (reading R7): larger score first, -0 == +0, NaN below -inf,
+// ties to the lower index.  key = (ord(score) << 32) | ~idx, sorted descending.
+__device__ __forceinline__ uint32_t score_ord(float s) {
+  if (s != s) return 0u;                       // NaN: lowest
+  uint32_t u = __float_as_uint(s + 0.0f);      // -0 -> +0
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// k per task passed by value (kernel parameter), so the call needs no host->device
+// copy and is graph-capturable; launches are chunked by SELECT_CHUNK tasks.
+constexpr int SELECT_CHUNK = 1024;
+struct SelectK { int k[SELECT_CHUNK]; };
+
+// One CTA per task; SORT_N = power of two >= Nc (<= 4096); blockDim = 512.
+template <int SORT_N>
+__global__ void select_kernel(const float* __restrict__ scores, int Nc, int mode, const SelectK ks,
+                              float threshold, int32_t* __restrict__ sel_idx, int32_t* __restrict__ sel_count) {
+  __shared__ unsigned long long keys[SORT_N];
+  __shared__ uint8_t flag[SORT_N];
+  __shared__ int warp_tot[32];
+  const int t = blockIdx.x;
+  const float* s = scores + (size_t)t * Nc;
+  const int nthr = blockDim.x;
+  if (mode == 0) {
+    const int k = ks.k[t];
+    for (int i = threadIdx.x; i < SORT_N; i += nthr) {
+      keys[i] = (i < Nc) ? ((unsigned long long)score_ord(s[i]) << 32) | (unsigned long long)(~(uint32_t)i) : 0ull;
+      flag[i] = 0;
+    }
+    __syncthreads();
+    // bitonic sort, descending
+    for (int size = 2; size <= SORT_N; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = threadIdx.x; i < SORT_N / 2; i += nthr) {
+          const int lo = 2 * i - (i & (stride - 1));
+          const int hi = lo + stride;
+          const bool desc = ((lo & size) == 0);
+          const unsigned long long a = keys[lo], bb = keys[hi];
+          if ((a < bb) == desc) { keys[lo] = bb; keys[hi] = a; }
+        }
+        __syncthreads();
+      }
+    }
+    for (int i = threadIdx.x; i < k; i += nthr) flag[~(uint32_t)(keys[i] & 0xffffffffull)] = 1;
+    __syncthreads();
+  } else {
+    for (int i = threadIdx.x; i < SORT_N; i += nthr) flag[i] = (i < Nc) && (s[i] > threshold);
+    __syncthreads();
+  }
+  // ascending compaction of flagged indices (block scan over ballots)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = nthr >> 5;
+  int base = 0;
+  for (int c0 = 0; c0 < Nc; c0 += nthr) {
+    const int i = c0 + threadIdx.x;
+    const bool f = (i < Nc) && flag[i];
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) warp_tot[wid] = __popc(bal);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int w = 0; w < nw; ++w) { const int c = warp_tot[w]; before += (w < wid) ? c : 0; tot += c; }
+    if (f) sel_idx[(size_t)t * Nc + base + before + __popc(bal & ((1u << lane) - 1u))] = i;
+    base += tot;
+    __syncthreads();
+  }
+  for (int i = base + threadIdx.x; i < Nc; i += nthr) sel_idx[(size_t)t * Nc + i] = -1;
+  if (threadIdx.x == 0) sel_count[t] = base;
+}
+
+// ------------------------------------------------------------------ gather (B8)
+struct GatherParams {
+  int T, Nc, gc_w, m, gf_w, d;      // geometry
+  int H, W, Pf;
+  const uint16_t* images;           // [T, H, W, 3] bf16
+  const float* x0;                  // [T, Nc, d]
+  const int32_t* sel_idx;           // [T, Nc]
+  const int32_t* sel_count;         // [T]
+  float* X;                         // [cap, d] packed mixed tokens (coarse rows written here)
+  int32_t* cu_seqlens;              // [T+1]
+  int32_t* mixed_src;               // [cap]
+  uint16_t* A_f;                    // [Rcap, 3Pf^2]
+  int32_t* frow;                    // [Rcap]
+  int32_t* fidx;                    // [Rcap]
+  int32_t* meta;                    // [0] = total tokens, [1] = total fine rows
+  int* err;
+};
+
+// grid = (T, G); block = 256 (8 warps).  Every block of task t rebuilds the task's
+// selection flags and prefix counts in shared memory (Nc <= 4096), then handles
+// coarse cells c = g, g+G, ... one warp per cell:
+//   off[c] = c + (m^2-1) * #{selected c' < c}    (in-place expansion, reading R10)
+//   unselected: X[base+off] = x0[t][c], mixed_src = c
+//   selected:   fine f = (m*cy+dy)*gf_w + (m*cx+dx), rows off..off+m^2-1, mixed_src = -1-f,
+//               A_f row (fine_base + m^2*pos + dy*m+dx) = pixels of f, frow/fidx.
+__global__ void gather_kernel(const GatherParams p) {
+  extern __shared__ int32_t gsm[];
+  int32_t* pre = gsm;               // [Nc] number of selected cells before c
+  int32_t* pos = gsm + p.Nc;        // [Nc] position in sel list, -1 if unselected
+  __shared__ int s_tok_base, s_fine_base, s_k;
+  const int t = blockIdx.x, G = gridDim.y, g = blockIdx.y;
+  const int Nc = p.Nc, m2 = p.m * p.m;
+  if (threadIdx.x == 0) {
+    int tb = 0, fb = 0;
+    for (int u = 0; u < t; ++u) {
+      const int ku = min(max(p.sel_count[u], 0), Nc);
+      tb += Nc + (m2 - 1) * ku;
+      fb += m2 * ku;
+    }
+    int k = p.sel_count[t];
+    if (k < 0 || k > Nc) { atomicOr(p.err, ERR_SEL_COUNT); k = min(max(k, 0), Nc); }
+    s_tok_base = tb; s_fine_base = fb; s_k = k;
+    if (g == 0) {
+      if (t == 0) p.cu_seqlens[0] = 0;
+      p.cu_seqlens[t + 1] = tb + Nc + (m2 - 1) * k;
+      if (t == p.T - 1) { p.meta[0] = tb + Nc + (m2 - 1) * k; p.meta[1] = fb + m2 * k; }
+    }
+  }
+  for (int c = threadIdx.x; c < Nc; c += blockDim.x) pos[c] = -1;
+  __syncthreads();
+  const int k = s_k;
+  const int32_t* sel = p.sel_idx + (size_t)t * Nc;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const int c = sel[i];
+    if (c < 0 || c >= Nc || (i > 0 && sel[i - 1] >= c)) { atomicOr(p.err, ERR_SEL_ORDER); continue; }
+    pos[c] = i;
+  }
+  __syncthreads();
+  // pre[c] = #{selected < c}: single-warp scan over Nc (Nc <= 4096, cheap)
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int run = 0;
+    for (int c0 = 0; c0 < Nc; c0 += 32) {
+      const int c = c0 + lane;
+      const bool f = (c < Nc) && pos[c] >= 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (c < Nc) pre[c] = run + __popc(bal & ((1u << lane) - 1u));
+      run += __popc(bal);
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int tok_base = s_tok_base, fine_base = s_fine_base;
+  const int dvec = p.d / 4;  // float4 per row
+  const int seg_vec = (p.Pf * 3 * 2) / 16;  // 16B vectors per fine pixel-row segment
+  const int fvec = p.Pf * seg_vec;           // 16B vectors per fine patch
+  for (int c = g * nw + wid; c < Nc; c += G * nw) {
+    const int off = c + (m2 - 1) * pre[c];
+    const int pc = pos[c];
+    if (pc < 0) {
+      const float4* src = reinterpret_cast<const float4*>(p.x0 + ((size_t)t * Nc + c) * p.d);
+      float4* dst = reinterpret_cast<float4*>(p.X + (size_t)(tok_base + off) * p.d);
+      for (int v = lane; v < dvec; v += 32) dst[v] = __ldg(src + v);
+      if (lane == 0) p.mixed_src[tok_base + off] = c;
+    } else {
+      const int cy = c / p.gc_w, cx = c % p.gc_w;
+      for (int q = 0; q < m2; ++q) {
+        const int dy = q / p.m, dx = q % p.m;
+        const int fy = p.m * cy + dy, fx = p.m * cx + dx;
+        const int f = fy * p.gf_w + fx;
+        const int arow = fine_base + m2 * pc + q;
+        if (lane == 0) {
+          p.mixed_src[tok_base + off + q] = -1 - f;
+          p.frow[arow] = tok_base + off + q;
+          p.fidx[arow] = f;
+        }
+        uint4* dst = reinterpret_cast<uint4*>(p.A_f + (size_t)arow * (3 * p.Pf * p.Pf));
+        for (int v = lane; v < fvec; v += 32) {
+          const int py = v / seg_vec, sv = v % seg_vec;
+          const uint4* src = reinterpret_cast<const uint4*>(
+                                 p.images + (((size_t)t * p.H + (size_t)fy * p.Pf + py) * p.W + (size_t)fx * p.Pf) * 3) + sv;
+          dst[v] = __ldg(src);
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ weight repack
+// in: [K, N] row-major (in, out)  ->  out: [N, K] row-major (K-major for UMMA)
+__global__ void transpose_bf16_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int K, int N) {
+  __shared__ uint16_t tile[32][33];
+  const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int k = k0 + i, n = n0 + threadIdx.x;
+    if (k < K && n < N) tile[i][threadIdx.x] = in[(size_t)k * N + n];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int n = n0 + i, k = k0 + threadIdx.x;
+    if (k < K && n < N) out[(size_t)n * K + k] = tile[threadIdx.x][i];
+  }
+}
+
+// coarse cu_seqlens = [0, Nc, 2Nc, ...] and meta[0] = B*Nc
+__global__ void coarse_meta_kernel(int32_t* cu, int32_t* meta, int B, int Nc) {
+  for (int i = threadIdx.x; i <= B; i += blockDim.x) cu[i] = i * Nc;
+  if (threadIdx.x == 0) { meta[0] = B * Nc; meta[1] = 0; }
+}
+
+}  // namespace cfd

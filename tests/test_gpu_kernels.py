@@ -1,0 +1,256 @@
+"""Per-kernel numerics on the B200 through the C ABI (cfdetr_debug.h), each against a
+plain PyTorch fp32 reference of the same op on the same bf16 inputs, plus the
+bit-exact integer/byte kernels against the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import cfd_inputs as ci
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_2505_23317_b200 import _lib as L  # noqa: E402
+from paper_2505_23317_b200.api import CFDetrEncoder, bf16_tensor  # noqa: E402
+
+LIB = L.load()
+
+
+def _s():
+    return torch.cuda.current_stream().cuda_stream
+
+
+# ------------------------------------------------------------------ GEMM
+@pytest.mark.parametrize("M,N,K,epi", [
+    (1, 64, 64, 2), (128, 64, 64, 2), (129, 256, 256, 2), (300, 768, 256, 0), (1000, 1024, 256, 1),
+    (777, 256, 1024, 2), (400, 256, 3072, 2), (33, 128, 768, 0), (4800, 256, 768, 2), (12800, 768, 256, 0)])
+def test_gemm_matches_torch_fp32(M, N, K, epi):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g) * 0.1
+    ref = A.float() @ W.float().T + bias
+    if epi == 2:
+        base = torch.randn(M, N, device="cuda", generator=g)
+        out = base.clone()
+        assert LIB.cfdx_gemm(M, N, K, A.data_ptr(), W.data_ptr(), bias.data_ptr(), 2, None, out.data_ptr(), _s()) == 0
+        torch.cuda.synchronize()
+        torch.testing.assert_close(out, ref + base, rtol=1e-4, atol=1e-4)
+    else:
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        assert LIB.cfdx_gemm(M, N, K, A.data_ptr(), W.data_ptr(), bias.data_ptr(), epi, out.data_ptr(), None, _s()) == 0
+        torch.cuda.synchronize()
+        if epi == 1:
+            ref = torch.nn.functional.gelu(ref)
+        torch.testing.assert_close(out.float(), ref.to(torch.bfloat16).float(), rtol=1e-2, atol=1e-2)
+
+
+# ------------------------------------------------------------------ attention
+def _attn_ref(qkv, cu, d, nh):
+    out = torch.zeros(qkv.shape[0], d, device=qkv.device)
+    lse = torch.zeros(nh, qkv.shape[0], device=qkv.device)
+    q, k, v = qkv[:, :d].float(), qkv[:, d:2 * d].float(), qkv[:, 2 * d:].float()
+    for t in range(len(cu) - 1):
+        a, b = cu[t], cu[t + 1]
+        for h in range(nh):
+            c = slice(h * 32, (h + 1) * 32)
+            S = q[a:b, c] @ k[a:b, c].T / (32 ** 0.5)
+            lse[h, a:b] = torch.logsumexp(S, dim=1)
+            out[a:b, c] = torch.softmax(S, dim=1) @ v[a:b, c]
+    return out, lse
+
+
+def _run_attn(lens, d, qkv=None, seed=0):
+    nh = d // 32
+    cu_l = np.concatenate([[0], np.cumsum(lens)]).astype(int).tolist()
+    rows = cu_l[-1]
+    cap = rows + 256
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    if qkv is None:
+        qkv = torch.randn(cap, 3 * d, device="cuda", generator=g).to(torch.bfloat16)
+    cu = torch.tensor(cu_l, dtype=torch.int32, device="cuda")
+    out = torch.zeros(cap, d, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(nh, cap, device="cuda")
+    assert LIB.cfdx_attention(len(lens), cu.data_ptr(), max(lens), cap, d, nh, qkv.data_ptr(), out.data_ptr(),
+                              lse.data_ptr(), cap, _s()) == 0
+    torch.cuda.synchronize()
+    return qkv, cu_l, out, lse
+
+
+@pytest.mark.parametrize("lens,d", [([16], 64), ([28], 64), ([128], 64), ([400], 256), ([700, 1], 256),
+                                    ([400, 640, 880, 1120, 1360, 1600], 256), ([129, 255, 257], 128)])
+def test_attention_varlen_matches_torch_fp32(lens, d):
+    qkv, cu_l, out, lse = _run_attn(lens, d, seed=len(lens) + d)
+    ref, rlse = _attn_ref(qkv, cu_l, d, d // 32)
+    rows = cu_l[-1]
+    got = out.float()[:rows]
+    rel = ((got - ref[:rows]).norm() / ref[:rows].norm()).item()
+    assert rel < 1e-2, rel
+    assert (got - ref[:rows]).abs().max().item() < 3e-2
+    torch.testing.assert_close(lse[:, :rows], rlse[:, :rows], rtol=1e-4, atol=1e-4)
+
+
+def test_attention_rows_sum_to_one_v_ones_probe():
+    """V == 1 -> every output is sum_j P_ij = 1 (within bf16 rounding of P and O)."""
+    d, lens = 256, [400, 1600, 37]
+    rows = sum(lens)
+    qkv = torch.randn(rows + 256, 3 * d, device="cuda").to(torch.bfloat16)
+    qkv[:, 2 * d:] = 1.0
+    _, _, out, _ = _run_attn(lens, d, qkv=qkv)
+    err = (out[:rows].float() - 1.0).abs().max().item()
+    assert err < 8e-3, err
+
+
+def test_attention_tasks_do_not_interact():
+    """Changing task 0's tokens leaves task 1's output bit-identical (block-diagonal, R11)."""
+    d, lens = 256, [300, 500]
+    qkv, cu_l, out1, _ = _run_attn(lens, d, seed=5)
+    qkv2 = qkv.clone()
+    qkv2[:300] = torch.randn(300, 3 * d, device="cuda").to(torch.bfloat16)
+    _, _, out2, _ = _run_attn(lens, d, qkv=qkv2)
+    assert torch.equal(out1[300:800], out2[300:800])
+
+
+# ------------------------------------------------------------------ LN / score
+@pytest.mark.parametrize("M,d", [(1, 64), (5, 64), (300, 256), (1000, 128)])
+def test_layernorm_matches_torch_fp32(M, d):
+    x = torch.randn(M, d, device="cuda") * 2 + 0.5
+    g, b = torch.randn(d, device="cuda"), torch.randn(d, device="cuda")
+    y = torch.empty(M, d, device="cuda", dtype=torch.bfloat16)
+    assert LIB.cfdx_layernorm(M, d, x.data_ptr(), g.data_ptr(), b.data_ptr(), 1e-6, y.data_ptr(), _s()) == 0
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.layer_norm(x, (d,), g, b, 1e-6)
+    torch.testing.assert_close(y.float(), ref.to(torch.bfloat16).float(), rtol=1e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("B,Nc,d", [(1, 16, 64), (3, 400, 256), (2, 130, 256)])
+def test_score_matches_torch_fp32_and_is_a_distribution(B, Nc, d):
+    nh = d // 32
+    cap = B * Nc + 256
+    qkv = torch.randn(cap, 3 * d, device="cuda").to(torch.bfloat16)
+    _, rlse = _attn_ref(qkv, [i * Nc for i in range(B + 1)], d, nh)
+    scores = torch.zeros(B, Nc, device="cuda")
+    assert LIB.cfdx_score(B, Nc, d, nh, qkv.data_ptr(), cap, rlse.contiguous().data_ptr(), cap, scores.data_ptr(),
+                          _s()) == 0
+    torch.cuda.synchronize()
+    q, k = qkv[:, :d].float(), qkv[:, d:2 * d].float()
+    ref = torch.zeros(B, Nc, device="cuda")
+    for b in range(B):
+        for h in range(nh):
+            c = slice(h * 32, (h + 1) * 32)
+            S = q[b * Nc:(b + 1) * Nc, c] @ k[b * Nc:(b + 1) * Nc, c].T / (32 ** 0.5)
+            ref[b] += torch.softmax(S, dim=1).sum(0)
+        ref[b] /= nh * Nc
+    torch.testing.assert_close(scores, ref, rtol=1e-3, atol=1e-6)
+    torch.testing.assert_close(scores.sum(1), torch.ones(B, device="cuda"), rtol=0, atol=1e-4)
+
+
+# ------------------------------------------------------------------ select / gather (bit-exact)
+@pytest.fixture(scope="module")
+def enc_c640():
+    cfg = ci.CONFIGS["c640"]
+    return CFDetrEncoder(cfg, ci.make_weights(cfg, seed=0), max_tasks=64)
+
+
+def _score_cases(n, Nc, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for t in range(n):
+        kind = t % 4
+        if kind == 0:
+            s = rng.random(Nc).astype(np.float32)
+        elif kind == 1:
+            s = rng.choice(np.array([0.1, 0.2, 0.3], np.float32), size=Nc)
+        elif kind == 2:
+            s = rng.choice(np.array([0.0, -0.0, 1.0, -1.0, np.inf, -np.inf, np.nan, 0.5], np.float32), size=Nc)
+        else:
+            s = np.full(Nc, np.float32(1.0 / Nc))
+        out.append(s)
+    return np.stack(out)
+
+
+def test_select_topk_bit_exact_vs_oracle(enc_c640):
+    Nc = enc_c640.Nc
+    S = _score_cases(12, Nc, 3)
+    ks = [0, 1, 100, 160, 240, 400, 7, 399, 200, 13, 57, 100]
+    o = enc_c640.select_regions(torch.from_numpy(S).cuda(), k=ks)
+    torch.cuda.synchronize()
+    idx, cnt = o["sel_idx"].cpu().numpy(), o["sel_count"].cpu().numpy()
+    for t in range(len(ks)):
+        ref = O.select_topk(S[t], ks[t])
+        assert cnt[t] == ks[t]
+        assert np.array_equal(idx[t, :ks[t]], ref), t
+        assert (idx[t, ks[t]:] == -1).all()
+
+
+def test_select_threshold_bit_exact_vs_oracle(enc_c640):
+    Nc = enc_c640.Nc
+    S = _score_cases(8, Nc, 4)
+    for tau in (0.0, 0.25, 1.0 / Nc, 0.999):
+        o = enc_c640.select_regions(torch.from_numpy(S).cuda(), threshold=tau)
+        torch.cuda.synchronize()
+        idx, cnt = o["sel_idx"].cpu().numpy(), o["sel_count"].cpu().numpy()
+        for t in range(S.shape[0]):
+            ref = O.select_threshold(S[t], np.float32(tau))
+            assert cnt[t] == len(ref) and np.array_equal(idx[t, :cnt[t]], ref)
+
+
+def test_gather_layout_bit_exact_vs_oracle(enc_c640):
+    cfg = ci.CONFIGS["c640"]
+    ks = [0, 80, 160, 240, 320, 400, 1, 399]
+    T = len(ks)
+    rng = np.random.default_rng(9)
+    sels = [np.sort(rng.choice(400, size=k, replace=False)).astype(np.int32) for k in ks]
+    imgs = ci.make_frames(cfg, T)
+    x0 = rng.normal(size=(T, 400, 256)).astype(np.float32)
+    sel_idx = np.full((T, 400), -1, np.int32)
+    for t, s in enumerate(sels):
+        sel_idx[t, :len(s)] = s
+    dev = "cuda"
+    cap = T * 1600
+    X = torch.full((cap, 256), float("nan"), device=dev)
+    cu = torch.empty(T + 1, dtype=torch.int32, device=dev)
+    msrc = torch.empty(cap, dtype=torch.int32, device=dev)
+    A_f = torch.empty(cap, 768, dtype=torch.int16, device=dev)
+    frow = torch.empty(cap, dtype=torch.int32, device=dev)
+    fidx = torch.empty(cap, dtype=torch.int32, device=dev)
+    meta = torch.empty(4, dtype=torch.int32, device=dev)
+    dimg = bf16_tensor(imgs, dev)
+    dx0 = torch.from_numpy(x0).to(dev)
+    st = LIB.cfdx_gather(enc_c640.ctx, T, dimg.data_ptr(), dx0.data_ptr(), torch.from_numpy(sel_idx).to(dev).data_ptr(),
+                         torch.tensor(ks, dtype=torch.int32, device=dev).data_ptr(), X.data_ptr(), cu.data_ptr(),
+                         msrc.data_ptr(), A_f.data_ptr(), frow.data_ptr(), fidx.data_ptr(), meta.data_ptr(), _s())
+    assert st == 0
+    torch.cuda.synchronize()
+    r_cu, r_msrc, r_frow, r_fidx, r_af = O.gather_layout(cfg, sels, list(imgs))
+    R = len(r_frow)
+    assert np.array_equal(cu.cpu().numpy(), r_cu)
+    n = int(r_cu[-1])
+    assert meta.cpu().numpy()[:2].tolist() == [n, R]
+    assert np.array_equal(msrc[:n].cpu().numpy(), r_msrc)
+    assert np.array_equal(frow[:R].cpu().numpy(), r_frow)
+    assert np.array_equal(fidx[:R].cpu().numpy(), r_fidx)
+    assert np.array_equal(A_f[:R].cpu().numpy().view(np.uint16), r_af)
+    Xh = X[:n].cpu().numpy()
+    for t in range(T):
+        seg = slice(r_cu[t], r_cu[t + 1])
+        src = r_msrc[seg]
+        rows = Xh[seg][src >= 0]
+        assert np.array_equal(rows.view(np.uint32), x0[t][src[src >= 0]].view(np.uint32))  # bit copies
+
+
+def test_device_side_selection_errors_are_reported(enc_c640):
+    cfg = ci.CONFIGS["c640"]
+    imgs = bf16_tensor(ci.make_frames(cfg, 1), "cuda")
+    x0 = torch.zeros(1, 400, 256, device="cuda")
+    bad_idx = torch.full((1, 400), -1, dtype=torch.int32, device="cuda")
+    bad_idx[0, :3] = torch.tensor([5, 3, 9], dtype=torch.int32)  # not ascending
+    cnt = torch.tensor([3], dtype=torch.int32, device="cuda")
+    enc_c640.batch_refine(imgs, x0, bad_idx, cnt)
+    with pytest.raises(L.CfdError) as e:
+        enc_c640.check()
+    assert e.value.status == -6
+    enc_c640.check()  # cleared

@@ -1,0 +1,186 @@
+"""End-to-end parity of the CUDA path (through the C ABI) against the fp64 oracle on
+the five BASELINE.json configs.
+
+Tolerance (north_star): per layer and per task, rel-L2 <= 2e-2 and max-abs <= 5e-2.
+Selection / layouts: bit-exact under the shared-score protocol (both sides select
+from the GPU's fp32 score tensor).  At the bench's full size
+(c640, 32 frames in flight) the oracle checks a sample of frames.
+"""
+import numpy as np
+import pytest
+import torch
+
+import cfd_inputs as ci
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_2505_23317_b200.api import CFDetrEncoder, bf16_tensor  # noqa: E402
+
+REL, ABS = 2e-2, 5e-2
+_ENC = {}
+
+
+def enc_for(name):
+    cfg = ci.CONFIGS[name]
+    key = (cfg.d_model, cfg.n_layers)
+    if key not in _ENC:
+        _ENC[key] = CFDetrEncoder(cfg, ci.make_weights(cfg, seed=0), max_tasks=64)
+    return _ENC[key]
+
+
+def _tol(gpu, ref, what):
+    gpu = np.asarray(gpu, np.float64)
+    rel = np.linalg.norm(gpu - ref) / max(np.linalg.norm(ref), 1e-30)
+    mx = np.abs(gpu - ref).max() if ref.size else 0.0
+    assert rel <= REL and mx <= ABS, f"{what}: rel-L2 {rel:.3e} max-abs {mx:.3e}"
+    return rel, mx
+
+
+def run_workload(name, ks, frames=None, sample=None, task0=0):
+    """coarse_encode -> select (top-k) -> batch_refine on the GPU; oracle on sampled tasks."""
+    cfg = ci.CONFIGS[name]
+    enc = enc_for(name)
+    w = ci.make_weights(cfg, seed=0)
+    T = len(ks)
+    imgs = ci.make_frames(cfg, T, task0=task0)
+    dimg = bf16_tensor(imgs, "cuda")
+    co = enc.coarse_encode(dimg, want_layers=True)
+    sel = enc.select_regions(co["scores"], k=ks)
+    counts = [enc.Nc + (cfg.m ** 2 - 1) * k for k in ks]
+    ro = enc.batch_refine(dimg, co["x0"], sel["sel_idx"], sel["sel_count"], token_counts=counts, want_layers=True)
+    torch.cuda.synchronize()
+    enc.check()
+    cu = ro["cu_seqlens"].cpu().numpy()
+    assert np.diff(cu).tolist() == counts
+    sample = range(T) if sample is None else sample
+    for t in sample:
+        oc = O.coarse_encode(cfg, w, [imgs[t]])[0]
+        np.testing.assert_allclose(co["x0"][t].double().cpu().numpy(), oc["x0"], rtol=0, atol=2e-4)
+        for l in range(cfg.n_layers):
+            _tol(co["layer_out"][l, t].cpu().numpy(), oc["layers"][l], f"{name} task {t} coarse layer {l}")
+        s_gpu = co["scores"][t].cpu().numpy()
+        _tol(s_gpu, oc["scores"], f"{name} task {t} scores")
+        # shared-score protocol: the oracle selects from the GPU's scores, bit-exact
+        sel_o = O.select_topk(s_gpu, ks[t])
+        assert np.array_equal(sel["sel_idx"][t, :ks[t]].cpu().numpy(), sel_o)
+        rr = O.refine_encode(cfg, w, imgs[t], oc["x0"], sel_o)
+        assert np.array_equal(ro["mixed_src"][cu[t]:cu[t + 1]].cpu().numpy(), rr["mixed_src"])
+        for l in range(cfg.n_layers):
+            _tol(ro["layer_out"][l, cu[t]:cu[t + 1]].cpu().numpy(), rr["layers"][l],
+                 f"{name} task {t} refine layer {l}")
+    return enc, co, sel, ro, imgs
+
+
+def test_tiny():
+    run_workload("tiny", list(ci.WORKLOADS["tiny"].ks))
+
+
+def test_tiny_ragged_batch_edge_ks():
+    run_workload("tiny", [0, 4, 16, 1, 15])
+
+
+def test_c640_single_frame():
+    run_workload("c640", list(ci.WORKLOADS["c640"].ks))
+
+
+def test_batch6_one_varlen_launch():
+    run_workload("batch6", list(ci.WORKLOADS["batch6"].ks))
+
+
+def test_fine8_sampled():
+    run_workload("fine8", list(ci.WORKLOADS["fine8"].ks), sample=[0, 7])
+
+
+def test_multi48_group_sampled():
+    run_workload("multi48", list(ci.multi48_group_ks(3)), sample=[0, 5], task0=18)
+
+
+def test_bench_size_c640_32_frames_sampled():
+    """The bench's launch configuration (32 frames in flight, k=100), oracle on 3 sampled frames."""
+    run_workload("c640", [100] * 32, sample=[0, 17, 31])
+
+
+def test_batched_refine_equals_single_refine_bitwise():
+    """batch_refine([t...])[t] == refine(t) bit for bit: the per-task schedule is
+    independent of the other tasks (reading R11)."""
+    name = "c640"
+    enc, co, sel, ro, imgs = run_workload(name, [0, 100, 400], sample=[])
+    cu = ro["cu_seqlens"].cpu().numpy()
+    dimg = bf16_tensor(imgs, "cuda")
+    for t in range(3):
+        single = enc.refine_encode(dimg[t], co["x0"][t], sel["sel_idx"][t:t + 1], sel["sel_count"][t:t + 1])
+        torch.cuda.synchronize()
+        n = cu[t + 1] - cu[t]
+        assert torch.equal(single["y"][:n], ro["y"][cu[t]:cu[t + 1]])
+
+
+def test_refine_k0_reproduces_coarse_pass_bitwise():
+    """Refining zero regions reproduces the coarse pass exactly (PAPER.md:234 reuse of A1 tokens)."""
+    cfg = ci.CONFIGS["c640"]
+    enc = enc_for("c640")
+    imgs = bf16_tensor(ci.make_frames(cfg, 2), "cuda")
+    co = enc.coarse_encode(imgs)
+    sel = enc.select_regions(co["scores"], k=[0, 0])
+    ro = enc.batch_refine(imgs, co["x0"], sel["sel_idx"], sel["sel_count"])
+    torch.cuda.synchronize()
+    assert torch.equal(ro["y"][:800].view(2, 400, 256), co["y"])
+
+
+def test_refine_all_regions_reproduces_fine_pass():
+    """k = Nc: the refine pass is the full fine pass, checked against the
+    oracle's separately computed fine pass up to the region-major permutation."""
+    cfg = ci.CONFIGS["tiny"]
+    enc = enc_for("tiny")
+    w = ci.make_weights(cfg, seed=0)
+    imgs = ci.make_frames(cfg, 1)
+    dimg = bf16_tensor(imgs, "cuda")
+    co = enc.coarse_encode(dimg)
+    sel = enc.select_regions(co["scores"], k=[16])
+    ro = enc.refine_encode(dimg[0], co["x0"][0], sel["sel_idx"], sel["sel_count"])
+    torch.cuda.synchronize()
+    f = O.fine_pass(cfg, w, imgs[0])
+    order = -1 - ro["mixed_src"][:64].cpu().numpy()
+    _tol(ro["y"][:64].cpu().numpy(), f["y"][order], "fine pass")
+
+
+def test_constant_frame_equal_scores_pick_lowest_indices():
+    cfg = ci.CONFIGS["tiny"]
+    enc = CFDetrEncoder(cfg, ci.make_weights(cfg, seed=0, pe=False), max_tasks=4)
+    img = bf16_tensor(ci.make_frame(128, 128, 0, constant=True)[None], "cuda")
+    co = enc.coarse_encode(img)
+    sel = enc.select_regions(co["scores"], k=[4])
+    torch.cuda.synchronize()
+    s = co["scores"][0].cpu().numpy()
+    np.testing.assert_allclose(s, 1 / 16, rtol=0, atol=1e-6)
+    assert sel["sel_idx"][0, :4].cpu().tolist() == O.select_topk(s, 4).tolist()
+    enc.close()
+
+
+def test_cuda_graph_capture_replays_identically():
+    cfg = ci.CONFIGS["c640"]
+    enc = enc_for("c640")
+    T = 4
+    imgs = bf16_tensor(ci.make_frames(cfg, T), "cuda")
+    ks = [100] * T
+    counts = [400 + 3 * k for k in ks]
+    co = enc.coarse_encode(imgs)
+    sel = enc.select_regions(co["scores"], k=ks)
+    ro = enc.batch_refine(imgs, co["x0"], sel["sel_idx"], sel["sel_count"], token_counts=counts)
+    torch.cuda.synchronize()
+    ref = ro["y"].clone()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            enc.coarse_encode(imgs, out=co, stream=s)
+            enc.select_regions(co["scores"], k=ks, out=sel, stream=s)
+            enc.batch_refine(imgs, co["x0"], sel["sel_idx"], sel["sel_count"], token_counts=counts, out=ro, stream=s)
+    ro["y"].zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    n = sum(counts)
+    assert torch.equal(ro["y"][:n], ref[:n])
