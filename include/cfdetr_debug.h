@@ -46,6 +46,22 @@ cfd_status cfdx_gather(cfd_ctx *ctx, int32_t n_tasks, const uint16_t *images, co
                        int32_t *mixed_src, uint16_t *A_f, int32_t *frow, int32_t *fidx, int32_t *meta,
                        void *stream);
 
+/* Launch probes.  Kernel classes: 0 attention, 1 score, 2 QKV GEMM, 3 O-proj GEMM,
+ * 4 MLP1 GEMM, 5 MLP2 GEMM, 6 coarse-embed GEMM, 7 fine-embed GEMM, 8 layernorm,
+ * 9 select, 10 gather, 11 im2col, 12 coarse meta.  After install, the i-th launch
+ * (i < capacity) of class `kind` is bracketed by cudaEventRecordWithFlags(h_start[i] /
+ * h_end[i], stream, cudaEventRecordExternal); the caller owns the (timing-enabled)
+ * cudaEvent_t handles.  capacity 0 removes the probe.  cfdx_probe_count returns how
+ * many launches were recorded since install. */
+cfd_status cfdx_probe_install(int32_t kind, void *const *h_start, void *const *h_end, int32_t capacity);
+int32_t cfdx_probe_count(int32_t kind);
+
+/* Tuning switches (process-wide): key 0 = attention kernel variant (1: one query tile
+ * per CTA, 2: persistent two-tile ping-pong, default 2); key 1 = how many of every 16
+ * column pairs variant 2 exponentiates with the FMA-pipe polynomial instead of MUFU
+ * (0, 2, 4, 6 or 8; default 4). */
+cfd_status cfdx_set_option(int32_t key, int32_t value);
+
 /* Number of kernels the library launched since load (host counter; for bench's
  * gpu_launches claim). */
 int64_t cfdx_launch_count(void);

@@ -23,6 +23,7 @@
 #include "../../include/cfdetr.h"
 #include "../../include/cfdetr_debug.h"
 #include "attn_tc.cuh"
+#include "attn2_tc.cuh"
 #include "gemm_tc.cuh"
 #include "misc_kernels.cuh"
 #include "score_tc.cuh"
@@ -32,6 +33,35 @@ using namespace cfd;
 namespace {
 
 std::atomic<int64_t> g_launches{0};
+
+// ---------------------------------------------------------------- launch probes
+// Optional per-kernel-class CUDA event pairs (cfdx_probe_install): every launch of a
+// probed class is bracketed by cudaEventRecordWithFlags(..., External) on the
+// launching stream, so bench.py can time the dominant kernel live.
+constexpr int kProbeKinds = 16;
+struct Probe {
+  std::vector<cudaEvent_t> start, end;
+  int count = 0;
+};
+Probe g_probe[kProbeKinds];
+
+// cudaEventRecordExternal is only valid while the stream is capturing a graph.
+inline void probe_record(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else cudaEventRecord(e, s);
+}
+inline void probe_begin(int kind, cudaStream_t s) {
+  if (kind < 0 || kind >= kProbeKinds) return;
+  Probe& p = g_probe[kind];
+  if (p.count < (int)p.start.size()) probe_record(p.start[p.count], s);
+}
+inline void probe_end(int kind, cudaStream_t s) {
+  if (kind < 0 || kind >= kProbeKinds) return;
+  Probe& p = g_probe[kind];
+  if (p.count < (int)p.end.size()) probe_record(p.end[p.count++], s);
+}
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -113,8 +143,8 @@ cudaError_t launch_gemm_bn(int BN, const CUtensorMap& ta, const CUtensorMap& tb,
 
 int pick_bn(int N) { return (N % 256 == 0) ? 256 : (N % 128 == 0) ? 128 : 64; }
 
-cudaError_t launch_gemm(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows,
-                        cudaStream_t s) {
+cudaError_t launch_gemm_impl(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows,
+                             cudaStream_t s) {
   const int BN = pick_bn(p.N);
   switch (epi) {
     case EPI_BF16_BIAS: return launch_gemm_bn<EPI_BF16_BIAS>(BN, ta, tb, p, rows, s);
@@ -123,6 +153,18 @@ cudaError_t launch_gemm(int epi, const CUtensorMap& ta, const CUtensorMap& tb, c
     case EPI_EMBED_COARSE: return launch_gemm_bn<EPI_EMBED_COARSE>(BN, ta, tb, p, rows, s);
     default: return launch_gemm_bn<EPI_EMBED_FINE>(BN, ta, tb, p, rows, s);
   }
+}
+
+// probe kinds (cfdetr_debug.h)
+enum : int { PK_ATTN = 0, PK_SCORE = 1, PK_QKV = 2, PK_OPROJ = 3, PK_MLP1 = 4, PK_MLP2 = 5, PK_EMBED_C = 6,
+             PK_EMBED_F = 7, PK_LN = 8, PK_SELECT = 9, PK_GATHER = 10, PK_IM2COL = 11, PK_META = 12 };
+
+cudaError_t launch_gemm(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows,
+                        cudaStream_t s, int kind = -1) {
+  probe_begin(kind, s);
+  cudaError_t e = launch_gemm_impl(epi, ta, tb, p, rows, s);
+  probe_end(kind, s);
+  return e;
 }
 
 // B tensor map for a K-major weight [N, K]
@@ -136,19 +178,54 @@ bool make_qkvmap(CUtensorMap* m, const void* qkv, int rows, int d) {
   return make_tmap(m, qkv, 3 * d, rows, 3 * d, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
-cudaError_t launch_attention(const CUtensorMap& tq, const AttnParams& p, int max_qtiles, int nh, int T,
-                             cudaStream_t s) {
-  auto kern = attn_tc_kernel<32, 3>;
-  constexpr int smem = AttnSmem<32, 3>::TOTAL;
+// runtime options (cfdx_set_option): attention variant (1 = one q-tile per CTA,
+// 2 = persistent two-tile ping-pong) and the polynomial-exp2 share of variant 2.
+int g_attn_variant = 1;
+int g_attn_npp = 4;
+
+template <int NPP>
+cudaError_t launch_attn2_t(const CUtensorMap& tq, const AttnParams& p, int items_ub, int nh, int T, cudaStream_t s) {
+  auto kern = attn2_tc_kernel<32, 4, NPP>;
+  constexpr int smem = Attn2Smem<32, 4>::TOTAL;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kern<<<dim3(max_qtiles, nh, T), ATTN_THREADS, smem, s>>>(tq, p);
-  ++g_launches;
+  const int grid = std::max(1, std::min(items_ub, num_sms()));
+  kern<<<grid, ATTN2_THREADS, smem, s>>>(tq, p, T, nh);
   return cudaGetLastError();
+}
+
+cudaError_t launch_attention(const CUtensorMap& tq, const AttnParams& p, int max_qtiles, int nh, int T,
+                             cudaStream_t s) {
+  probe_begin(PK_ATTN, s);
+  cudaError_t e;
+  if (g_attn_variant == 2 && T <= ATTN2_MAX_T) {
+    const int items_ub = T * ((max_qtiles + 1) / 2) * nh;
+    switch (g_attn_npp) {
+      case 0: e = launch_attn2_t<0>(tq, p, items_ub, nh, T, s); break;
+      case 2: e = launch_attn2_t<2>(tq, p, items_ub, nh, T, s); break;
+      case 6: e = launch_attn2_t<6>(tq, p, items_ub, nh, T, s); break;
+      case 8: e = launch_attn2_t<8>(tq, p, items_ub, nh, T, s); break;
+      default: e = launch_attn2_t<4>(tq, p, items_ub, nh, T, s); break;
+    }
+  } else {
+    auto kern = attn_tc_kernel<32, 3>;
+    constexpr int smem = AttnSmem<32, 3>::TOTAL;
+    static bool attr = false;
+    if (!attr) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    kern<<<dim3(max_qtiles, nh, T), ATTN_THREADS, smem, s>>>(tq, p);
+    e = cudaGetLastError();
+  }
+  probe_end(PK_ATTN, s);
+  ++g_launches;
+  return e;
 }
 
 cudaError_t launch_score(const CUtensorMap& tq, const ScoreParams& p, int B, cudaStream_t s) {
@@ -160,16 +237,19 @@ cudaError_t launch_score(const CUtensorMap& tq, const ScoreParams& p, int B, cud
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  probe_begin(PK_SCORE, s);
   kern<<<dim3((p.n_coarse + 127) / 128, B), SCORE_THREADS, smem, s>>>(tq, p);
+  probe_end(PK_SCORE, s);
   ++g_launches;
   return cudaGetLastError();
 }
 
 cudaError_t launch_layernorm(int d, const float* x, const float* g, const float* b, __nv_bfloat16* y, int M,
                              const int* m_dev, int m_cap, float eps, int rows_for_grid, cudaStream_t s) {
-  const int rows_pad = std::min(((rows_for_grid + 127) / 128) * 128, m_cap);
+  const int rows_pad = pad_rows(rows_for_grid, m_cap);
   int blocks = (rows_pad + 7) / 8;
   blocks = std::max(1, std::min(blocks, num_sms() * 16));
+  probe_begin(PK_LN, s);
   switch (d) {
     case 64: layernorm_kernel<2><<<blocks, 256, 0, s>>>(x, g, b, y, M, m_dev, m_cap, eps); break;
     case 128: layernorm_kernel<4><<<blocks, 256, 0, s>>>(x, g, b, y, M, m_dev, m_cap, eps); break;
@@ -177,6 +257,7 @@ cudaError_t launch_layernorm(int d, const float* x, const float* g, const float*
     case 512: layernorm_kernel<16><<<blocks, 256, 0, s>>>(x, g, b, y, M, m_dev, m_cap, eps); break;
     default: return cudaErrorInvalidValue;
   }
+  probe_end(PK_LN, s);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -263,7 +344,7 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   GemmParams p{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = w.rows_cap; p.N = 3 * d; p.K = d; p.bias = L.b_qkv;
   p.out_bf16 = w.qkv;
-  CFD_CUDA(launch_gemm(EPI_BF16_BIAS, ta_h, L.tm_qkv, p, rows_grid, s));
+  CFD_CUDA(launch_gemm(EPI_BF16_BIAS, ta_h, L.tm_qkv, p, rows_grid, s, PK_QKV));
   // attention
   AttnParams ap{};
   ap.cu_seqlens = cu; ap.d_model = d; ap.out = w.obuf; ap.lse = want_lse ? w.lse : nullptr; ap.lse_ld = w.lse_ld;
@@ -278,17 +359,17 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   // O projection + residual
   p = GemmParams{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = x_cap; p.N = d; p.K = d; p.bias = L.b_o; p.out_f32 = x; p.ld_out = d;
-  CFD_CUDA(launch_gemm(EPI_F32_RESID, ta_o, L.tm_o, p, rows_grid, s));
+  CFD_CUDA(launch_gemm(EPI_F32_RESID, ta_o, L.tm_o, p, rows_grid, s, PK_OPROJ));
   // LN2
   CFD_CUDA(launch_layernorm(d, x, L.ln2_g, L.ln2_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
   // MLP1 + GELU
   p = GemmParams{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = w.rows_cap; p.N = F; p.K = d; p.bias = L.b_1; p.out_bf16 = w.ff;
-  CFD_CUDA(launch_gemm(EPI_BF16_BIAS_GELU, ta_h, L.tm_1, p, rows_grid, s));
+  CFD_CUDA(launch_gemm(EPI_BF16_BIAS_GELU, ta_h, L.tm_1, p, rows_grid, s, PK_MLP1));
   // MLP2 + residual
   p = GemmParams{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = x_cap; p.N = d; p.K = F; p.bias = L.b_2; p.out_f32 = x; p.ld_out = d;
-  CFD_CUDA(launch_gemm(EPI_F32_RESID, ta_f, L.tm_2, p, rows_grid, s));
+  CFD_CUDA(launch_gemm(EPI_F32_RESID, ta_f, L.tm_2, p, rows_grid, s, PK_MLP2));
   return CFD_OK;
 }
 
@@ -331,6 +412,38 @@ const char* cfd_status_str(cfd_status s) {
 }
 
 int64_t cfdx_launch_count(void) { return g_launches.load(); }
+
+cfd_status cfdx_probe_install(int32_t kind, void* const* h_start, void* const* h_end, int32_t capacity) {
+  if (kind < 0 || kind >= kProbeKinds || capacity < 0 || (capacity > 0 && (!h_start || !h_end))) return CFD_E_ARG;
+  Probe& p = g_probe[kind];
+  p.start.assign(capacity, nullptr);
+  p.end.assign(capacity, nullptr);
+  for (int i = 0; i < capacity; ++i) {
+    p.start[i] = static_cast<cudaEvent_t>(h_start[i]);
+    p.end[i] = static_cast<cudaEvent_t>(h_end[i]);
+  }
+  p.count = 0;
+  return CFD_OK;
+}
+
+cfd_status cfdx_set_option(int32_t key, int32_t value) {
+  switch (key) {
+    case 0:
+      if (value != 1 && value != 2) return CFD_E_ARG;
+      g_attn_variant = value;
+      return CFD_OK;
+    case 1:
+      if (value != 0 && value != 2 && value != 4 && value != 6 && value != 8) return CFD_E_ARG;
+      g_attn_npp = value;
+      return CFD_OK;
+  }
+  return CFD_E_ARG;
+}
+
+int32_t cfdx_probe_count(int32_t kind) {
+  if (kind < 0 || kind >= kProbeKinds) return -1;
+  return g_probe[kind].count;
+}
 
 cfd_status cfd_create(const cfd_config* cfg, const cfd_weights* wts, void* stream, cfd_ctx** out) {
   if (!out || !wts || !wts->h_layers || !wts->w_embed_c || !wts->w_embed_f || !wts->b_embed_c || !wts->b_embed_f ||
@@ -454,13 +567,17 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const cfd_config& g = c->cfg;
   const int d = g.d_model, M = B * c->Nc;
+  probe_begin(PK_META, s);
   coarse_meta_kernel<<<1, 256, 0, s>>>(w.ccu, w.meta, B, c->Nc);
+  probe_end(PK_META, s);
   ++g_launches;
   CFD_CUDA(cudaGetLastError());
   {
     const long long vec = (long long)B * g.img_h * (g.img_w / g.patch_coarse) * ((g.patch_coarse * 6) / 16);
     const int blocks = (int)std::min<long long>((vec + 255) / 256, (long long)num_sms() * 8);
+    probe_begin(PK_IM2COL, s);
     im2col_kernel<<<blocks, 256, 0, s>>>(images, w.patches, B, g.img_h, g.img_w, g.patch_coarse);
+    probe_end(PK_IM2COL, s);
     ++g_launches;
     CFD_CUDA(cudaGetLastError());
   }
@@ -469,7 +586,7 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
   GemmParams p{};
   p.M = M; p.m_cap = M; p.N = d; p.K = c->Kc; p.bias = c->bc; p.out_f32 = y; p.out2_f32 = x0; p.ld_out = d;
   p.pe = c->pec; p.pe_rows = c->Nc;
-  CFD_CUDA(launch_gemm(EPI_EMBED_COARSE, ta, c->tm_wc, p, M, s));
+  CFD_CUDA(launch_gemm(EPI_EMBED_COARSE, ta, c->tm_wc, p, M, s, PK_EMBED_C));
   const int max_qtiles = (c->Nc + ATTN_BQ - 1) / ATTN_BQ;
   for (int l = 0; l < g.n_layers; ++l) {
     const bool sl = (l == g.score_layer);
@@ -502,10 +619,12 @@ cfd_status cfd_select_regions(cfd_ctx* c, int32_t T, const float* scores, cfd_se
     const float* sc = scores + (size_t)t0 * Nc;
     int32_t* si = sel_idx + (size_t)t0 * Nc;
     int32_t* cnt = sel_count + t0;
+    probe_begin(PK_SELECT, s);
     if (Nc <= 512) select_kernel<512><<<nt, 512, 0, s>>>(sc, Nc, (int)mode, ks, threshold, si, cnt);
     else if (Nc <= 1024) select_kernel<1024><<<nt, 512, 0, s>>>(sc, Nc, (int)mode, ks, threshold, si, cnt);
     else if (Nc <= 2048) select_kernel<2048><<<nt, 512, 0, s>>>(sc, Nc, (int)mode, ks, threshold, si, cnt);
     else select_kernel<4096><<<nt, 512, 0, s>>>(sc, Nc, (int)mode, ks, threshold, si, cnt);
+    probe_end(PK_SELECT, s);
     ++g_launches;
     CFD_CUDA(cudaGetLastError());
   }
@@ -523,7 +642,9 @@ static cfd_status launch_gather(cfd_ctx* c, int T, const uint16_t* images, const
   gp.mixed_src = msrc; gp.A_f = A_f; gp.frow = frow; gp.fidx = fidx; gp.meta = meta; gp.err = c->err;
   const int G = std::max(1, std::min(16, (c->Nc + 63) / 64));
   const size_t smem = (size_t)2 * c->Nc * sizeof(int32_t);
+  probe_begin(PK_GATHER, s);
   gather_kernel<<<dim3(T, G), 256, smem, s>>>(gp);
+  probe_end(PK_GATHER, s);
   ++g_launches;
   CFD_CUDA(cudaGetLastError());
   return CFD_OK;
@@ -563,7 +684,7 @@ cfd_status cfd_batch_refine(cfd_ctx* c, int32_t T, const uint16_t* images, const
   GemmParams p{};
   p.M = 0; p.m_dev = w.meta + 1; p.m_cap = cap; p.N = d; p.K = c->Kf; p.bias = c->bf; p.out_f32 = y; p.ld_out = d;
   p.pe = c->pef; p.pe_rows = c->Nf; p.frow = w.frow; p.fidx = w.fidx;
-  CFD_CUDA(launch_gemm(EPI_EMBED_FINE, ta, c->tm_wf, p, std::max(fine_grid, 1), s));
+  CFD_CUDA(launch_gemm(EPI_EMBED_FINE, ta, c->tm_wf, p, std::max(fine_grid, 1), s, PK_EMBED_F));
   const int max_qtiles = (c->Nf + ATTN_BQ - 1) / ATTN_BQ;
   for (int l = 0; l < g.n_layers; ++l) {
     st = run_layer(c, l, y, cap, 0, w.meta, std::max(rows_grid, 1), cu, T, max_qtiles, w, false, nullptr, 0, s);

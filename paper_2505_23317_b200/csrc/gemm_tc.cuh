@@ -63,6 +63,13 @@ struct GemmSmem {
                                         : (2 * BN <= 256) ? 256 : 512;
 };
 
+// Rows a varlen attention tile may touch past the last valid row: a task's last KV
+// tile starts at (task start + 128 j) and so can overhang the packed rows by < 128.
+__host__ __device__ __forceinline__ int pad_rows(int M, int cap) {
+  const int r = ((M + 127) / 128) * 128 + 128;
+  return r < cap ? r : cap;
+}
+
 __device__ __forceinline__ float gelu_erf(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }
 
 template <int EPI>
@@ -139,13 +146,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = warp_id(), lane = lane_id();
   const int M = p.m_dev ? __ldg(p.m_dev) : p.M;
-  const int m_tiles = (M + GEMM_BM - 1) / GEMM_BM;
+  // bf16 outputs (QKV, MLP1) also cover the pad rows [M, pad_rows(M)) so attention's
+  // tail tiles (which may start at any row of the last task) read finite values
+  constexpr bool kPad = (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_GELU);
+  const int m_store = kPad ? pad_rows(M, p.m_cap) : M;
+  const int m_tiles = (m_store + GEMM_BM - 1) / GEMM_BM;
   const int n_tiles = p.N / BN;
   const int num_k = p.K / GEMM_BK;
   const int total = m_tiles * n_tiles;
-  // bf16 outputs also cover the pad rows [M, M_pad) so downstream tail tiles read finite data
-  const int m_store = (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_GELU)
-                          ? min(m_tiles * GEMM_BM, p.m_cap) : M;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);

@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include "gemm_tc.cuh"
 
 namespace cfd {
 
@@ -24,7 +25,7 @@ __global__ void layernorm_kernel(const float* __restrict__ x, const float* __res
                                  const int* __restrict__ m_dev, int m_cap, float eps) {
   constexpr int D = VPT * 32;
   const int rows = m_dev ? __ldg(m_dev) : M;
-  const int m_pad = min(((rows + 127) / 128) * 128, m_cap);
+  const int m_pad = pad_rows(rows, m_cap);  // zero the rows attention tail tiles may read
   const int warps_per_block = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int row = blockIdx.x * warps_per_block + (threadIdx.x >> 5); row < m_pad; row += gridDim.x * warps_per_block) {
@@ -227,26 +228,38 @@ __global__ void gather_kernel(const GatherParams p) {
       if (t == p.T - 1) { p.meta[0] = tb + Nc + (m2 - 1) * k; p.meta[1] = fb + m2 * k; }
     }
   }
-  for (int c = threadIdx.x; c < Nc; c += blockDim.x) pos[c] = -1;
+  for (int c = threadIdx.x; c < Nc; c += blockDim.x) pos[c] = 0;  // pos[] holds the selected flag
   __syncthreads();
   const int k = s_k;
   const int32_t* sel = p.sel_idx + (size_t)t * Nc;
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     const int c = sel[i];
-    if (c < 0 || c >= Nc || (i > 0 && sel[i - 1] >= c)) { atomicOr(p.err, ERR_SEL_ORDER); continue; }
-    pos[c] = i;
+    if (c < 0 || c >= Nc) { atomicOr(p.err, ERR_SEL_ORDER); continue; }
+    if (i > 0 && sel[i - 1] >= c) atomicOr(p.err, ERR_SEL_ORDER);
+    pos[c] = 1;
   }
   __syncthreads();
-  // pre[c] = #{selected < c}: single-warp scan over Nc (Nc <= 4096, cheap)
+  // pre[c] = #{selected < c} by a single-warp ballot scan (Nc <= 4096).  If the list was
+  // invalid (duplicates / out of range) the flagged count can fall short of k; the
+  // lowest unflagged cells are then added so every block of every task agrees on
+  // N_t = Nc + (m^2-1) k and all writes stay in bounds (the error word is already set).
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    int run = 0;
-    for (int c0 = 0; c0 < Nc; c0 += 32) {
-      const int c = c0 + lane;
-      const bool f = (c < Nc) && pos[c] >= 0;
-      const unsigned bal = __ballot_sync(0xffffffffu, f);
-      if (c < Nc) pre[c] = run + __popc(bal & ((1u << lane) - 1u));
-      run += __popc(bal);
+    for (int pass = 0; pass < 2; ++pass) {
+      int run = 0;
+      for (int c0 = 0; c0 < Nc; c0 += 32) {
+        const int c = c0 + lane;
+        const bool f = (c < Nc) && pos[c] != 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (c < Nc) pre[c] = run + __popc(bal & ((1u << lane) - 1u));
+        run += __popc(bal);
+      }
+      if (run == k) break;
+      if (lane == 0) {
+        for (int c = 0; c < Nc && run < k; ++c)
+          if (pos[c] == 0) { pos[c] = 1; ++run; }
+      }
+      __syncwarp();
     }
   }
   __syncthreads();
@@ -257,8 +270,8 @@ __global__ void gather_kernel(const GatherParams p) {
   const int fvec = p.Pf * seg_vec;           // 16B vectors per fine patch
   for (int c = g * nw + wid; c < Nc; c += G * nw) {
     const int off = c + (m2 - 1) * pre[c];
-    const int pc = pos[c];
-    if (pc < 0) {
+    const int pc = pre[c];  // rank among selected cells when pos[c] != 0
+    if (pos[c] == 0) {
       const float4* src = reinterpret_cast<const float4*>(p.x0 + ((size_t)t * Nc + c) * p.d);
       float4* dst = reinterpret_cast<float4*>(p.X + (size_t)(tok_base + off) * p.d);
       for (int v = lane; v < dvec; v += 32) dst[v] = __ldg(src + v);
