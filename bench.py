@@ -224,6 +224,7 @@ def gpu_arm(args):
     import torch
     import torch.distributed as dist
     from paper_2505_23317_b200 import _lib as L
+    from paper_2505_23317_b200 import shard
     from paper_2505_23317_b200.api import CFDetrEncoder, bf16_tensor
 
     rank, world, local = dist_env()
@@ -238,8 +239,8 @@ def gpu_arm(args):
     counts = [cfg.n_coarse + (cfg.m ** 2 - 1) * k] * B
     w = ci.make_weights(cfg, seed=0)
     enc = CFDetrEncoder(cfg, w, max_tasks=max(B, 8), device=str(dev))
-    task0 = rank * B
-    imgs_np = ci.make_frames(cfg, B, task0=task0)
+    my_tasks = shard.rank_tasks(rank, world, B)  # weak scaling: B camera frames per GPU
+    imgs_np = ci.make_frames(cfg, B, task0=my_tasks[0])
     imgs = bf16_tensor(imgs_np, dev)
     stream = torch.cuda.Stream(device=dev)
     co, sel, ro = {}, {}, {}
@@ -297,10 +298,7 @@ def gpu_arm(args):
     step_ms = [starts[i].elapsed_time(ends[i]) for i in range(args.steps)]
     total_ms = sum(step_ms)
     clk = clocks.stop()
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms_max = float(t.item())
+    total_ms_max = shard.max_over_ranks(total_ms, dev)
     frames_total = B * world * args.steps
     value = frames_total / (total_ms_max / 1e3)
 
@@ -423,11 +421,8 @@ def gpu_arm(args):
             e2e_step(stream)
         e_e.record(stream)
     stream.synchronize()
-    e2e_ms = e_s.elapsed_time(e_e)
-    t2 = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-    e2e_val = B * world * e2e_steps / (float(t2.item()) / 1e3)
+    e2e_ms = shard.max_over_ranks(e_s.elapsed_time(e_e), dev)
+    e2e_val = B * world * e2e_steps / (e2e_ms / 1e3)
     e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h_imgs.numel() * 2),
            "d2h_bytes_per_step": int(h_y.numel() * 4 + h_cu.numel() * 4),
            "note": "pinned host frames -> device, full step (eager launches), packed refined tokens -> host"}
@@ -459,19 +454,10 @@ def gpu_arm(args):
 def gather_and_check(args, world, rank, dev, cfg, w, imgs_np, co, sel, ro, k):
     """Outside timing: all-gather (NCCL) each rank's first task (cu_seqlens, selection,
     packed refined rows) and check it on rank 0 against the oracle (shared-score protocol)."""
-    import torch
-    import torch.distributed as dist
+    from paper_2505_23317_b200 import shard
     Nt = cfg.n_coarse + 3 * k
-    d = cfg.d_model
-    y0 = ro["y"][:Nt].contiguous()
-    sc0 = co["scores"][0].contiguous()
-    if world > 1:
-        ys = torch.empty(world, Nt, d, device=dev)
-        scs = torch.empty(world, cfg.n_coarse, device=dev)
-        dist.all_gather_into_tensor(ys, y0)
-        dist.all_gather_into_tensor(scs, sc0)
-    else:
-        ys, scs = y0[None], sc0[None]
+    ys = shard.gather_outputs(ro["y"][:Nt].contiguous())
+    scs = shard.gather_outputs(co["scores"][0].contiguous())
     if rank != 0:
         return None
     import oracle as O

@@ -57,7 +57,8 @@ cfd_status cfdx_probe_install(int32_t kind, void *const *h_start, void *const *h
 int32_t cfdx_probe_count(int32_t kind);
 
 /* Tuning switches (process-wide): key 0 = attention kernel variant (1: one query tile
- * per CTA, 2: persistent two-tile ping-pong, default 2); key 1 = how many of every 16
+ * per CTA, 2: persistent two-tile ping-pong with 128-key steps, 3: same with 64-key
+ * steps and double-buffered S); key 1 = how many of every 16
  * column pairs variant 2 exponentiates with the FMA-pipe polynomial instead of MUFU
  * (0, 2, 4, 6 or 8; default 4). */
 cfd_status cfdx_set_option(int32_t key, int32_t value);

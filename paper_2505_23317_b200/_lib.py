@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcfdetr.so")
+LIB_PATH = os.path.join(HERE, "libcfdetr_dbg.so" if os.environ.get("CFD_LIB_DEBUG") == "1" else "libcfdetr.so")
 
 P = C.c_void_p
 I32 = C.c_int32

@@ -13,6 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcfdetr.so")
+LIB_DBG = os.path.join(HERE, "libcfdetr_dbg.so")
 SOURCES = ["cfdetr.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -36,14 +37,18 @@ def _newest_src_mtime() -> float:
     return max(os.path.getmtime(p) for p in paths)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_src_mtime():
-        return LIB
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    """debug=True builds libcfdetr_dbg.so with -DCFD_HANG_CHECK (barrier waits trap with a
+    message instead of hanging); load it with CFD_LIB_DEBUG=1."""
+    out = LIB_DBG if debug else LIB
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= _newest_src_mtime():
+        return out
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-o", tmp, *srcs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
+    tmp = out + ".tmp"
+    extra = ["-DCFD_HANG_CHECK"] if debug else []
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-shared", "-o", tmp, *srcs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
-    log = os.path.join(HERE, "build.log")
+    log = os.path.join(HERE, "build_dbg.log" if debug else "build.log")
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
     if r.returncode != 0:
@@ -51,9 +56,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))

@@ -10,12 +10,11 @@
 //        2..5 = softmax warpgroup 0 (query tile 2*qp), 6..9 = softmax warpgroup 1
 //        (query tile 2*qp+1).  While one warpgroup computes exponentials the tensor
 //        core serves the other (ping-pong).
-// TMEM:  S_w (128 fp32 columns) per warpgroup; P_w (bf16 pairs) is written back over
-//        the first 64 columns of S_w once S_w is in registers; O_w (32 columns)
-//        accumulates P_w V_j in TMEM; the softmax warps rescale it in place (lazily,
-//        only when a row's running max grows by more than 2^8).
-//        tcgen05.mma executes in issue order, so QK_{j+1} may overwrite S_w/P_w right
-//        after PV_j is issued.
+// TMEM:  per warpgroup S_w (128 fp32 columns), P_w (64 columns of bf16 pairs) and O_w
+//        (32 columns) = 448 of 512 columns.  The warpgroup releases S_w (s_free) as soon
+//        as S_j is in registers, so QK_{j+1} runs on the tensor core during the softmax
+//        of tile j; O_w accumulates P_w V_j in TMEM and is rescaled in place by the
+//        softmax warps (lazily, only when a row's running max grows by more than 2^8).
 // Softmax per row (one thread per query row): FMNMX3 row max, FFMA2 scale/shift,
 // exp2 split between MUFU.EX2 and a degree-3 polynomial on the FMA pipe (NPP of every
 // 16 column pairs), FADD2 row sums, bf16x2 pack, tcgen05.st.  Fully masked 32-column
@@ -42,7 +41,8 @@ struct Attn2Smem {
   static constexpr int PRE_OFF = BAR_OFF + 256;
   static constexpr int TOTAL = 1024 + PRE_OFF + (ATTN2_MAX_T + 1) * 4;
   static constexpr uint32_t S_COL = 0;    // S_w at w*128
-  static constexpr uint32_t O_COL = 256;  // O_w at 256 + w*DH
+  static constexpr uint32_t P_COL = 256;  // P_w at 256 + w*64 (bf16 pairs)
+  static constexpr uint32_t O_COL = 384;  // O_w at 384 + w*DH
 };
 
 // ---------------------------------------------------------------- packed fp32 helpers
@@ -130,7 +130,8 @@ __global__ void __launch_bounds__(ATTN2_THREADS, 1)
   uint64_t* kv_full = bars + 4;             // [STAGES]
   uint64_t* kv_empty = kv_full + STAGES;    // [STAGES]
   uint64_t* s_full = kv_empty + STAGES;     // [2]
-  uint64_t* p_full = s_full + 2;            // [2]
+  uint64_t* s_free = s_full + 2;            // [2]
+  uint64_t* p_full = s_free + 2;            // [2]
   uint64_t* o_full = p_full + 2;            // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
   int* prefix = reinterpret_cast<int*>(smem + S::PRE_OFF);
@@ -145,7 +146,12 @@ __global__ void __launch_bounds__(ATTN2_THREADS, 1)
     tma_prefetch(&tmQKV);
     for (int i = 0; i < 2; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
     for (int s = 0; s < STAGES; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
-    for (int w = 0; w < 2; ++w) { mbar_init(&s_full[w], 1); mbar_init(&p_full[w], 128); mbar_init(&o_full[w], 1); }
+    for (int w = 0; w < 2; ++w) {
+      mbar_init(&s_full[w], 1);
+      mbar_init(&s_free[w], 128);
+      mbar_init(&p_full[w], 128);
+      mbar_init(&o_full[w], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -204,7 +210,7 @@ __global__ void __launch_bounds__(ATTN2_THREADS, 1)
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, 0);  // S = Q K^T
       constexpr uint32_t idesc_o = make_idesc_bf16(128, DH, 1);   // O = P V  (V MN-major)
       int it = 0, kvc = 0;
-      uint32_t p_cnt[2] = {0, 0};
+      uint32_t p_cnt[2] = {0, 0}, s_use[2] = {0, 0};
       for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
         int t, qp, h;
         decode_item(prefix, T, nh, item, t, qp, h);
@@ -214,7 +220,11 @@ __global__ void __launch_bounds__(ATTN2_THREADS, 1)
         const int nkv = (N + 127) / 128;
         const int slot = it & 1;
         mbar_wait(&q_full[slot], (it >> 1) & 1);
+        // S_w = Q_w K^T into TMEM; waits until the warpgroup has read the previous S_w
         auto issue_qk = [&](int w, int st) {
+          if (s_use[w] > 0) mbar_wait(&s_free[w], (s_use[w] - 1) & 1);
+          ++s_use[w];
+          tc_fence_after();
           const uint32_t qa = smem_u32(smem + S::Q_OFF + (slot * 2 + w) * S::TILE_BYTES);
           const uint32_t ka = smem_u32(smem + S::K_OFF + st * S::TILE_BYTES);
 #pragma unroll
@@ -233,19 +243,20 @@ __global__ void __launch_bounds__(ATTN2_THREADS, 1)
           const int st = (kvc + j) % STAGES;
           const int valid = min(128, N - j * 128);
           const int ksteps = (valid + 15) / 16;
-          const bool more = j + 1 < nkv;
-          const int st1 = (kvc + j + 1) % STAGES;
-          if (more) mbar_wait(&kv_full[st1], ((kvc + j + 1) / STAGES) & 1);
+          if (j + 1 < nkv) {  // S_{j+1} runs on the tensor core while the softmax works on S_j
+            const int st1 = (kvc + j + 1) % STAGES;
+            mbar_wait(&kv_full[st1], ((kvc + j + 1) / STAGES) & 1);
+            for (int w = 0; w < nq; ++w) issue_qk(w, st1);
+          }
           const uint32_t va = smem_u32(smem + S::V_OFF + st * S::TILE_BYTES);
           for (int w = 0; w < nq; ++w) {
             mbar_wait(&p_full[w], p_cnt[w] & 1);
             ++p_cnt[w];
             tc_fence_after();
             for (int k = 0; k < ksteps; ++k)
-              mma_ts(tmem + S::O_COL + w * DH, tmem + S::S_COL + w * 128 + k * 8,
+              mma_ts(tmem + S::O_COL + w * DH, tmem + S::P_COL + w * 64 + k * 8,
                      make_smem_desc(va + k * 16 * DH * 2, 4096, 512, kLayoutSW64), idesc_o, (j | k) != 0);
             mma_commit(&o_full[w]);
-            if (more) issue_qk(w, st1);
           }
           mma_commit(&kv_empty[st]);
         }
@@ -260,6 +271,7 @@ __global__ void __launch_bounds__(ATTN2_THREADS, 1)
     const int r = quarter * 32 + lane;              // query row in the tile
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t s_addr = tmem + lane_off + S::S_COL + wg * 128;
+    const uint32_t p_addr = tmem + lane_off + S::P_COL + wg * 64;
     const uint32_t o_addr = tmem + lane_off + S::O_COL + wg * DH;
     const float c = p.scale_log2;
     uint32_t s_cnt = 0, o_cnt = 0;
@@ -286,6 +298,8 @@ __global__ void __launch_bounds__(ATTN2_THREADS, 1)
           for (int ch = 0; ch < 4; ++ch)
             if (ch < nch) tmem_ld32(s_addr + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + ch * 32));
           tmem_wait_ld();
+          tc_fence_before();
+          mbar_arrive(&s_free[wg]);  // S_w may now be overwritten by QK_{j+1}
           if (valid < 128) {
 #pragma unroll
             for (int i = 0; i < 128; ++i)
@@ -342,14 +356,20 @@ __global__ void __launch_bounds__(ATTN2_THREADS, 1)
               tmem_st16(o_addr + 16, *reinterpret_cast<const uint32_t(*)[16]>(o + 16));
             }
           }
-          // P_j over the first 64 columns of S_w (S_j is already in registers)
+          // P_j into P_w (PV_{j-1}, its previous reader, completed: o_full waited above)
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             if (q * 32 < valid)
-              tmem_st16(s_addr + q * 16, *reinterpret_cast<const uint32_t(*)[16]>(sr + q * 32));
+              tmem_st16(p_addr + q * 16, *reinterpret_cast<const uint32_t(*)[16]>(sr + q * 32));
           tmem_wait_st();
-        } else if (j > 0) {
-          ++o_cnt;  // keep the phase count in step with the active warps
+        } else {
+          // padding-only warp: still waits for PV_{j-1} so it cannot arrive on p_full for
+          // tile j before that barrier's previous phase (tile j-1) has completed
+          mbar_arrive(&s_free[wg]);
+          if (j > 0) {
+            mbar_wait(&o_full[wg], o_cnt & 1);
+            ++o_cnt;
+          }
         }
         tc_fence_before();
         mbar_arrive(&p_full[wg]);
@@ -375,6 +395,7 @@ __global__ void __launch_bounds__(ATTN2_THREADS, 1)
         }
         tc_fence_before();  // O_w is read before the next item's first PV overwrites it
       } else {
+        mbar_wait(&o_full[wg], o_cnt & 1);
         ++o_cnt;
       }
     }

@@ -24,6 +24,7 @@
 #include "../../include/cfdetr_debug.h"
 #include "attn_tc.cuh"
 #include "attn2_tc.cuh"
+#include "attn3_tc.cuh"
 #include "gemm_tc.cuh"
 #include "misc_kernels.cuh"
 #include "score_tc.cuh"
@@ -151,6 +152,7 @@ cudaError_t launch_gemm_impl(int epi, const CUtensorMap& ta, const CUtensorMap& 
     case EPI_BF16_BIAS_GELU: return launch_gemm_bn<EPI_BF16_BIAS_GELU>(BN, ta, tb, p, rows, s);
     case EPI_F32_RESID: return launch_gemm_bn<EPI_F32_RESID>(BN, ta, tb, p, rows, s);
     case EPI_EMBED_COARSE: return launch_gemm_bn<EPI_EMBED_COARSE>(BN, ta, tb, p, rows, s);
+    case EPI_F32_RESID_LN: return launch_gemm_bn<EPI_F32_RESID_LN>(BN, ta, tb, p, rows, s);
     default: return launch_gemm_bn<EPI_EMBED_FINE>(BN, ta, tb, p, rows, s);
   }
 }
@@ -180,13 +182,13 @@ bool make_qkvmap(CUtensorMap* m, const void* qkv, int rows, int d) {
 
 // runtime options (cfdx_set_option): attention variant (1 = one q-tile per CTA,
 // 2 = persistent two-tile ping-pong) and the polynomial-exp2 share of variant 2.
-int g_attn_variant = 1;
+int g_attn_variant = 3;
 int g_attn_npp = 4;
 
-template <int NPP>
+template <int V, int NPP>
 cudaError_t launch_attn2_t(const CUtensorMap& tq, const AttnParams& p, int items_ub, int nh, int T, cudaStream_t s) {
-  auto kern = attn2_tc_kernel<32, 4, NPP>;
-  constexpr int smem = Attn2Smem<32, 4>::TOTAL;
+  auto kern = (V == 2) ? attn2_tc_kernel<32, 4, NPP> : attn3_tc_kernel<32, 4, NPP>;
+  constexpr int smem = (V == 2) ? Attn2Smem<32, 4>::TOTAL : Attn3Smem<32, 4>::TOTAL;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -194,7 +196,7 @@ cudaError_t launch_attn2_t(const CUtensorMap& tq, const AttnParams& p, int items
     attr = true;
   }
   const int grid = std::max(1, std::min(items_ub, num_sms()));
-  kern<<<grid, ATTN2_THREADS, smem, s>>>(tq, p, T, nh);
+  kern<<<grid, V == 2 ? ATTN2_THREADS : ATTN3_THREADS, smem, s>>>(tq, p, T, nh);
   return cudaGetLastError();
 }
 
@@ -202,14 +204,24 @@ cudaError_t launch_attention(const CUtensorMap& tq, const AttnParams& p, int max
                              cudaStream_t s) {
   probe_begin(PK_ATTN, s);
   cudaError_t e;
-  if (g_attn_variant == 2 && T <= ATTN2_MAX_T) {
+  if (g_attn_variant >= 2 && T <= ATTN2_MAX_T) {
     const int items_ub = T * ((max_qtiles + 1) / 2) * nh;
-    switch (g_attn_npp) {
-      case 0: e = launch_attn2_t<0>(tq, p, items_ub, nh, T, s); break;
-      case 2: e = launch_attn2_t<2>(tq, p, items_ub, nh, T, s); break;
-      case 6: e = launch_attn2_t<6>(tq, p, items_ub, nh, T, s); break;
-      case 8: e = launch_attn2_t<8>(tq, p, items_ub, nh, T, s); break;
-      default: e = launch_attn2_t<4>(tq, p, items_ub, nh, T, s); break;
+    if (g_attn_variant == 2) {
+      switch (g_attn_npp) {
+        case 0: e = launch_attn2_t<2, 0>(tq, p, items_ub, nh, T, s); break;
+        case 2: e = launch_attn2_t<2, 2>(tq, p, items_ub, nh, T, s); break;
+        case 6: e = launch_attn2_t<2, 6>(tq, p, items_ub, nh, T, s); break;
+        case 8: e = launch_attn2_t<2, 8>(tq, p, items_ub, nh, T, s); break;
+        default: e = launch_attn2_t<2, 4>(tq, p, items_ub, nh, T, s); break;
+      }
+    } else {
+      switch (g_attn_npp) {
+        case 0: e = launch_attn2_t<3, 0>(tq, p, items_ub, nh, T, s); break;
+        case 2: e = launch_attn2_t<3, 2>(tq, p, items_ub, nh, T, s); break;
+        case 6: e = launch_attn2_t<3, 6>(tq, p, items_ub, nh, T, s); break;
+        case 8: e = launch_attn2_t<3, 8>(tq, p, items_ub, nh, T, s); break;
+        default: e = launch_attn2_t<3, 4>(tq, p, items_ub, nh, T, s); break;
+      }
     }
   } else {
     auto kern = attn_tc_kernel<32, 3>;
@@ -328,18 +340,23 @@ Workspace carve(const cfd_ctx* c, int n, void* base) {
   } while (0)
 
 // One pre-LN encoder block on the packed residual stream x (fp32 [*, d]).
+// On entry w.hbuf must hold LN1(x) of this layer (bf16, pad rows zeroed): the
+// first layer's comes from a standalone LayerNorm launch, every later one from the
+// previous layer's MLP2 epilogue (EPI_F32_RESID_LN).  LN2 is fused into the
+// O-projection epilogue the same way.
 cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const int* m_dev, int rows_grid,
                      const int32_t* cu, int T, int max_qtiles, Workspace& w, bool want_lse, float* scores,
                      int score_B, cudaStream_t s) {
   const cfd_config& g = c->cfg;
   const int d = g.d_model, F = g.d_ff;
+  const bool fuse_ln = pick_bn(d) == d;  // one GEMM tile spans a whole row
   LayerDev& L = c->layers[l];
   CUtensorMap ta_h, ta_o, ta_f, tq;
   if (!make_amap(&ta_h, w.hbuf, w.rows_cap, d) || !make_amap(&ta_o, w.obuf, w.rows_cap, d) ||
       !make_amap(&ta_f, w.ff, w.rows_cap, F) || !make_qkvmap(&tq, w.qkv, w.rows_cap, d))
     return CFD_E_CUDA;
-  // LN1
-  CFD_CUDA(launch_layernorm(d, x, L.ln1_g, L.ln1_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
+  if (l == 0 || !fuse_ln)  // LN1
+    CFD_CUDA(launch_layernorm(d, x, L.ln1_g, L.ln1_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
   // QKV
   GemmParams p{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = w.rows_cap; p.N = 3 * d; p.K = d; p.bias = L.b_qkv;
@@ -356,20 +373,30 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
     sp.scale_log2 = ap.scale_log2; sp.scores = scores;
     CFD_CUDA(launch_score(tq, sp, score_B, s));
   }
-  // O projection + residual
+  // O projection + residual (+ LN2 -> hbuf)
   p = GemmParams{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = x_cap; p.N = d; p.K = d; p.bias = L.b_o; p.out_f32 = x; p.ld_out = d;
-  CFD_CUDA(launch_gemm(EPI_F32_RESID, ta_o, L.tm_o, p, rows_grid, s, PK_OPROJ));
-  // LN2
-  CFD_CUDA(launch_layernorm(d, x, L.ln2_g, L.ln2_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
+  if (fuse_ln) {
+    p.ln_g = L.ln2_g; p.ln_b = L.ln2_b; p.ln_out = w.hbuf; p.ln_cap = w.rows_cap; p.ln_eps = g.ln_eps;
+    CFD_CUDA(launch_gemm(EPI_F32_RESID_LN, ta_o, L.tm_o, p, rows_grid, s, PK_OPROJ));
+  } else {
+    CFD_CUDA(launch_gemm(EPI_F32_RESID, ta_o, L.tm_o, p, rows_grid, s, PK_OPROJ));
+    CFD_CUDA(launch_layernorm(d, x, L.ln2_g, L.ln2_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
+  }
   // MLP1 + GELU
   p = GemmParams{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = w.rows_cap; p.N = F; p.K = d; p.bias = L.b_1; p.out_bf16 = w.ff;
   CFD_CUDA(launch_gemm(EPI_BF16_BIAS_GELU, ta_h, L.tm_1, p, rows_grid, s, PK_MLP1));
-  // MLP2 + residual
+  // MLP2 + residual (+ next layer's LN1 -> hbuf)
   p = GemmParams{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = x_cap; p.N = d; p.K = F; p.bias = L.b_2; p.out_f32 = x; p.ld_out = d;
-  CFD_CUDA(launch_gemm(EPI_F32_RESID, ta_f, L.tm_2, p, rows_grid, s, PK_MLP2));
+  if (fuse_ln && l + 1 < g.n_layers) {
+    const LayerDev& Ln = c->layers[l + 1];
+    p.ln_g = Ln.ln1_g; p.ln_b = Ln.ln1_b; p.ln_out = w.hbuf; p.ln_cap = w.rows_cap; p.ln_eps = g.ln_eps;
+    CFD_CUDA(launch_gemm(EPI_F32_RESID_LN, ta_f, L.tm_2, p, rows_grid, s, PK_MLP2));
+  } else {
+    CFD_CUDA(launch_gemm(EPI_F32_RESID, ta_f, L.tm_2, p, rows_grid, s, PK_MLP2));
+  }
   return CFD_OK;
 }
 
@@ -429,7 +456,7 @@ cfd_status cfdx_probe_install(int32_t kind, void* const* h_start, void* const* h
 cfd_status cfdx_set_option(int32_t key, int32_t value) {
   switch (key) {
     case 0:
-      if (value != 1 && value != 2) return CFD_E_ARG;
+      if (value < 1 || value > 3) return CFD_E_ARG;
       g_attn_variant = value;
       return CFD_OK;
     case 1:

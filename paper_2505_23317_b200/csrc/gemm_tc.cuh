@@ -24,12 +24,23 @@
 
 namespace cfd {
 
+__device__ __forceinline__ void fma2x(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0,
+                                      float c1) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+
 enum EpiKind : int {
   EPI_BF16_BIAS = 0,       // out_bf16 = bf16(acc + bias)                      (QKV)
   EPI_BF16_BIAS_GELU = 1,  // out_bf16 = bf16(GELU(acc + bias))                (MLP1)
   EPI_F32_RESID = 2,       // out_f32 += acc + bias                            (O-proj, MLP2)
   EPI_EMBED_COARSE = 3,    // out_f32 = out2_f32 = acc + bias + pe[row % pe_rows]   (B1)
   EPI_EMBED_FINE = 4,      // out_f32[frow[row]] = acc + bias + pe[fidx[row]]        (B9)
+  EPI_F32_RESID_LN = 5,    // out_f32 += acc + bias; ln_out = bf16(LN(out_f32 row))  (O-proj/MLP2
+                           // followed by the next LayerNorm; needs BN == N, one tile per row)
 };
 
 struct GemmParams {
@@ -46,18 +57,24 @@ struct GemmParams {
   int pe_rows;
   const int* frow;
   const int* fidx;
+  const float* ln_g;         // EPI_F32_RESID_LN: next LayerNorm's gamma / beta [N]
+  const float* ln_b;
+  __nv_bfloat16* ln_out;     // [ln_cap, N]
+  int ln_cap;                // rows of ln_out (pad rows [M, pad_rows) are zeroed)
+  float ln_eps;
 };
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 192;
+constexpr int GEMM_EPI_WARPS = 8;                     // 2 per TMEM lane quarter
+constexpr int GEMM_THREADS = 64 + 32 * GEMM_EPI_WARPS;  // + TMA warp + MMA warp
 
 template <int BN, int STAGES>
 struct GemmSmem {
   static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr int B_BYTES = BN * GEMM_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_BYTES = 256;
+  static constexpr int BAR_BYTES = 128 + 2 * 128 * 8;  // barriers + RESID_LN row statistics
   static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                         : (2 * BN <= 256) ? 256 : 512;
@@ -71,6 +88,27 @@ __host__ __device__ __forceinline__ int pad_rows(int M, int cap) {
 }
 
 __device__ __forceinline__ float gelu_erf(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }
+
+// GELU(z) = z * Phi(z), Phi(z) = 1/2 + 1/2 erf(z/sqrt2), for a pair on packed FFMA2:
+// Phi(z) - 1/2 = t * q(t^2), t = clamp(z/4.5, -1, 1), q a degree-7 polynomial in t^2
+// (Chebyshev fit of degree 15, odd; |error| <= 9.1e-5 in Phi for all z, i.e. below
+// 1/20 of a bf16 ulp of the GELU output), beyond |z| >= 4.5 Phi is clamped (err 3.4e-6).
+__device__ __forceinline__ void gelu2(float& a, float& b) {
+  float t0 = fminf(fmaxf(a * (1.0f / 4.5f), -1.f), 1.f);
+  float t1 = fminf(fmaxf(b * (1.0f / 4.5f), -1.f), 1.f);
+  float u0, u1, q0, q1;
+  fma2x(u0, u1, t0, t1, t0, t1, 0.f, 0.f);
+  fma2x(q0, q1, u0, u1, -4.5690726f, -4.5690726f, 21.273092f, 21.273092f);
+  fma2x(q0, q1, q0, q1, u0, u1, -42.560215f, -42.560215f);
+  fma2x(q0, q1, q0, q1, u0, u1, 48.358903f, 48.358903f);
+  fma2x(q0, q1, q0, q1, u0, u1, -34.930427f, -34.930427f);
+  fma2x(q0, q1, q0, q1, u0, u1, 17.109918f, 17.109918f);
+  fma2x(q0, q1, q0, q1, u0, u1, -5.9759021f, -5.9759021f);
+  fma2x(q0, q1, q0, q1, u0, u1, 1.7936441f, 1.7936441f);
+  float h0, h1;
+  fma2x(h0, h1, t0, t1, q0, q1, 0.5f, 0.5f);   // Phi
+  fma2x(a, b, a, b, h0, h1, 0.f, 0.f);          // z * Phi
+}
 
 template <int EPI>
 __device__ __forceinline__ void gemm_epilogue_chunk(const GemmParams& p, int row, int col0, const uint32_t (&r)[32],
@@ -91,7 +129,7 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const GemmParams& p, int row
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       float a = v[2 * i], b = v[2 * i + 1];
-      if constexpr (EPI == EPI_BF16_BIAS_GELU) { a = gelu_erf(a); b = gelu_erf(b); }
+      if constexpr (EPI == EPI_BF16_BIAS_GELU) gelu2(a, b);
       pk[i] = pack_bf16x2(a, b);
     }
     uint4* dst = reinterpret_cast<uint4*>(p.out_bf16 + (size_t)row * p.N + col0);
@@ -129,6 +167,85 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const GemmParams& p, int row
   }
 }
 
+// Residual + LayerNorm epilogue: the tile spans the whole row (BN == N); each row is
+// split between two warps (halves of the columns) which exchange (sum, sum of squares)
+// through shared memory.  Pass 1: x += acc + bias (stored), row statistics.  Pass 2:
+// re-read the new x (L2) and write bf16 LN(x) = (x - mean) * rstd * g + b.  Rows in
+// [M, tile end) only get zeros in ln_out (pad rows for the next attention).
+template <int CH>
+__device__ __forceinline__ void resid_ln_epilogue(const GemmParams& p, uint32_t tbase, int row, int col_base, int M,
+                                                  int quarter, int half, int lane, float2* stats,
+                                                  uint64_t* tempty_bar) {
+  const bool live = row < M;
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < CH; c += 2) {
+    uint32_t r0[32], r1[32];
+    tmem_ld32(tbase + c * 32, r0);
+    if (c + 1 < CH) tmem_ld32(tbase + (c + 1) * 32, r1);
+    tmem_wait_ld();
+    if (c + 2 >= CH) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (c + q >= CH) break;
+      const uint32_t* r = q ? r1 : r0;
+      const int col0 = col_base + (c + q) * 32;
+      if (live) {
+        const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);
+        float4* dst = reinterpret_cast<float4*>(p.out_f32 + (size_t)row * p.ld_out + col0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 b = __ldg(b4 + i);
+          float4 o = dst[i];
+          o.x += __uint_as_float(r[4 * i + 0]) + b.x;
+          o.y += __uint_as_float(r[4 * i + 1]) + b.y;
+          o.z += __uint_as_float(r[4 * i + 2]) + b.z;
+          o.w += __uint_as_float(r[4 * i + 3]) + b.w;
+          dst[i] = o;
+          s1 += (o.x + o.y) + (o.z + o.w);
+          s2 += (o.x * o.x + o.y * o.y) + (o.z * o.z + o.w * o.w);
+        }
+      }
+    }
+  }
+  const int r_in_tile = quarter * 32 + lane;
+  stats[half * 128 + r_in_tile] = make_float2(s1, s2);
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");  // the two warps of this quarter
+  const float2 o = stats[(half ^ 1) * 128 + r_in_tile];
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");  // stats slot reusable
+  const float inv_n = 1.f / (float)p.N;
+  const float mean = (s1 + o.x) * inv_n;
+  const float var = fmaxf((s2 + o.y) * inv_n - mean * mean, 0.f);
+  const float rstd = rsqrtf(var + p.ln_eps);
+  if (row >= p.ln_cap) return;
+#pragma unroll 1
+  for (int c = 0; c < CH; ++c) {
+    const int col0 = col_base + c * 32;
+    uint4* hd = reinterpret_cast<uint4*>(p.ln_out + (size_t)row * p.N + col0);
+    if (!live) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) hd[i] = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    const float4* xs = reinterpret_cast<const float4*>(p.out_f32 + (size_t)row * p.ld_out + col0);
+    const float4* g4 = reinterpret_cast<const float4*>(p.ln_g + col0);
+    const float4* be4 = reinterpret_cast<const float4*>(p.ln_b + col0);
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 x = xs[i], g = __ldg(g4 + i), be = __ldg(be4 + i);
+      pk[2 * i] = pack_bf16x2((x.x - mean) * rstd * g.x + be.x, (x.y - mean) * rstd * g.y + be.y);
+      pk[2 * i + 1] = pack_bf16x2((x.z - mean) * rstd * g.z + be.z, (x.w - mean) * rstd * g.w + be.w);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) hd[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+  }
+}
+
 template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -143,6 +260,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float2* ln_stats = reinterpret_cast<float2*>(smem + STAGES * S::STAGE_BYTES + 128);  // [2][128]
 
   const int warp = warp_id(), lane = lane_id();
   const int M = p.m_dev ? __ldg(p.m_dev) : p.M;
@@ -150,7 +268,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // tail tiles (which may start at any row of the last task) read finite values
   constexpr bool kPad = (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_GELU);
   const int m_store = kPad ? pad_rows(M, p.m_cap) : M;
-  const int m_tiles = (m_store + GEMM_BM - 1) / GEMM_BM;
+  // RESID_LN also visits the tiles of the pad rows (zeroed in ln_out, x untouched)
+  const int m_tiles = ((EPI == EPI_F32_RESID_LN ? pad_rows(M, p.ln_cap) : m_store) + GEMM_BM - 1) / GEMM_BM;
   const int n_tiles = p.N / BN;
   const int num_k = p.K / GEMM_BK;
   const int total = m_tiles * n_tiles;
@@ -159,7 +278,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], GEMM_EPI_WARPS); }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<S::TMEM_COLS>(tmem_slot);
@@ -213,7 +332,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else {
-    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int quarter = warp & 3;              // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;          // which half of the tile's columns
+    constexpr int CH = BN / 64;                // 32-column chunks per epilogue warp
     const int row_in_tile = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -223,16 +344,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_after();
       const int row = m_blk * GEMM_BM + row_in_tile;
       const bool ok = row < m_store;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c * 32, r);
-        tmem_wait_ld();
-        gemm_epilogue_chunk<EPI>(p, row, n_blk * BN + c * 32, r, ok);
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + half * (BN / 2);
+      const int col_base = n_blk * BN + half * (BN / 2);
+      if constexpr (EPI == EPI_F32_RESID_LN) {
+        resid_ln_epilogue<CH>(p, tbase, row, col_base, M, quarter, half, lane, ln_stats, &tempty[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+#pragma unroll 1
+      for (int c = 0; c < CH; c += 2) {
+        uint32_t r0[32], r1[32];
+        tmem_ld32(tbase + c * 32, r0);
+        if (c + 1 < CH) tmem_ld32(tbase + (c + 1) * 32, r1);
+        tmem_wait_ld();
+        if (c + 2 >= CH) {  // last TMEM read of this accumulator: release it to the MMA warp early
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        gemm_epilogue_chunk<EPI>(p, row, col_base + c * 32, r0, ok);
+        if (c + 1 < CH) gemm_epilogue_chunk<EPI>(p, row, col_base + (c + 1) * 32, r1, ok);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }

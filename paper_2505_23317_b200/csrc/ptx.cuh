@@ -12,6 +12,7 @@
 //              | [24,29) M>>4
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_bf16.h>
 
 namespace cfd {
@@ -50,6 +51,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+#ifndef CFD_HANG_CHECK
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
@@ -60,6 +62,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#else
+// debug build (libcfdetr_dbg.so): report and trap instead of hanging forever
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  for (long long i = 0;; ++i) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (i == (1ll << 22)) {
+      printf("CFD_HANG block (%d,%d,%d) thread %d bar smem+0x%x parity %u\n", blockIdx.x, blockIdx.y, blockIdx.z,
+             threadIdx.x, addr, parity);
+      asm volatile("trap;");
+    }
+  }
+}
+#endif
 
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void tma_prefetch(const void* tmap) {

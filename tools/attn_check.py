@@ -1,0 +1,51 @@
+"""One attention correctness case: python tools/attn_check.py VARIANT NPP 400,640,1 [d]"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+from paper_2505_23317_b200 import _lib as L  # noqa: E402
+
+var, npp = int(sys.argv[1]), int(sys.argv[2])
+lens = [int(x) for x in sys.argv[3].split(",")]
+d = int(sys.argv[4]) if len(sys.argv) > 4 else 256
+nh = d // 32
+lib = L.load()
+assert lib.cfdx_set_option(0, var) == 0 and lib.cfdx_set_option(1, npp) == 0
+cu_l = [0]
+for n in lens:
+    cu_l.append(cu_l[-1] + n)
+rows = cu_l[-1]
+cap = rows + 256
+g = torch.Generator(device="cuda").manual_seed(rows)
+qkv = (torch.randn(cap, 3 * d, device="cuda", generator=g) * 1.5).to(torch.bfloat16)
+cu = torch.tensor(cu_l, dtype=torch.int32, device="cuda")
+out = torch.zeros(cap, d, device="cuda", dtype=torch.bfloat16)
+lse = torch.zeros(nh, cap, device="cuda")
+st = lib.cfdx_attention(len(lens), cu.data_ptr(), max(lens), cap, d, nh, qkv.data_ptr(), out.data_ptr(),
+                        lse.data_ptr(), cap, torch.cuda.current_stream().cuda_stream)
+torch.cuda.synchronize()
+q, k, v = qkv[:, :d].float(), qkv[:, d:2 * d].float(), qkv[:, 2 * d:].float()
+ref = torch.zeros(cap, d, device="cuda")
+rlse = torch.zeros(nh, cap, device="cuda")
+for t in range(len(lens)):
+    a, b = cu_l[t], cu_l[t + 1]
+    for h in range(nh):
+        c = slice(h * 32, (h + 1) * 32)
+        S = q[a:b, c] @ k[a:b, c].T / (32 ** 0.5)
+        rlse[h, a:b] = torch.logsumexp(S, dim=1)
+        ref[a:b, c] = torch.softmax(S, dim=1) @ v[a:b, c]
+rel = ((out.float()[:rows] - ref[:rows]).norm() / ref[:rows].norm()).item()
+le = (lse[:, :rows] - rlse[:, :rows]).abs().max().item()
+print(f"v{var} npp{npp} {sys.argv[3]}: status {st} rel {rel:.2e} lse {le:.2e} {'OK' if rel < 1e-2 and le < 1e-3 else 'BAD'}")
+if rel >= 1e-2:
+    for t in range(len(lens)):
+        a, b = cu_l[t], cu_l[t + 1]
+        for h in range(nh):
+            c = slice(h * 32, (h + 1) * 32)
+            e = ((out.float()[a:b, c] - ref[a:b, c]).norm() / ref[a:b, c].norm()).item()
+            if e > 1e-2:
+                rowerr = (out.float()[a:b, c] - ref[a:b, c]).abs().amax(dim=1)
+                bad = (rowerr > 0.05).nonzero().flatten().tolist()
+                print(f"   task {t} (N={b-a}) head {h}: rel {e:.2e} bad rows {len(bad)}: {bad[:12]}")

@@ -177,6 +177,62 @@ def probe_pipeline():
     return res
 
 
+def probe_attn_variants():
+    torch, lib = _setup()
+    res = {}
+    d, nh = 256, 8
+    cases = [[16], [128], [400], [700, 1], [400, 640, 880, 1120, 1360, 1600], [129, 255, 257, 3]]
+    for var, npp in [(1, 4), (2, 0), (3, 0), (3, 2), (3, 4), (3, 6), (3, 8)]:
+        assert lib.cfdx_set_option(0, var) == 0 and lib.cfdx_set_option(1, npp) == 0
+        key = f"v{var}_npp{npp}"
+        r = {}
+        worst = 0.0
+        for lens in cases:
+            cu_l = [0]
+            for n in lens:
+                cu_l.append(cu_l[-1] + n)
+            rows = cu_l[-1]
+            cap = rows + 256
+            g = torch.Generator(device="cuda").manual_seed(rows)
+            qkv = (torch.randn(cap, 3 * d, device="cuda", generator=g) * 1.5).to(torch.bfloat16)
+            cu = torch.tensor(cu_l, dtype=torch.int32, device="cuda")
+            out = torch.zeros(cap, d, device="cuda", dtype=torch.bfloat16)
+            lse = torch.zeros(nh, cap, device="cuda")
+            st = lib.cfdx_attention(len(lens), cu.data_ptr(), max(lens), cap, d, nh, qkv.data_ptr(), out.data_ptr(),
+                                    lse.data_ptr(), cap, torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            ref, rlse = _attn_ref(qkv, cu_l, d, nh)
+            rel = ((out.float()[:rows] - ref[:rows]).norm() / ref[:rows].norm()).item()
+            le = (lse[:, :rows] - rlse[:, :rows]).abs().max().item()
+            worst = max(worst, rel)
+            r[str(lens)] = dict(st=st, rel=rel, lse=le)
+        # timing at bench shapes
+        for lens in ([400] * 32, [700] * 32, [1600] * 8):
+            cu_l = [0]
+            for n in lens:
+                cu_l.append(cu_l[-1] + n)
+            cap = cu_l[-1] + 256
+            qkv = torch.randn(cap, 3 * d, device="cuda").to(torch.bfloat16)
+            cu = torch.tensor(cu_l, dtype=torch.int32, device="cuda")
+            out = torch.zeros(cap, d, device="cuda", dtype=torch.bfloat16)
+            s = torch.cuda.current_stream().cuda_stream
+            for _ in range(3):
+                lib.cfdx_attention(len(lens), cu.data_ptr(), max(lens), cap, d, nh, qkv.data_ptr(), out.data_ptr(), None, 0, s)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(20):
+                lib.cfdx_attention(len(lens), cu.data_ptr(), max(lens), cap, d, nh, qkv.data_ptr(), out.data_ptr(), None, 0, s)
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) / 20 * 1e3
+            fl = sum(4 * n * n * d for n in lens)
+            r[f"time_{lens[0]}x{len(lens)}"] = dict(us=us, tflops=fl / us / 1e6)
+        r["worst_rel"] = worst
+        res[key] = r
+    return res
+
+
+
 PROBES = {k[6:]: v for k, v in globals().items() if k.startswith("probe_")}
 
 if __name__ == "__main__":
@@ -199,3 +255,4 @@ if __name__ == "__main__":
         else:
             print(r.stdout[-3000:], r.stderr[-3000:])
         sys.stdout.flush()
+
