@@ -26,7 +26,7 @@ import numpy as np
 __all__ = [
     "ModelConfig", "Workload", "CONFIGS", "WORKLOADS", "bf16_round", "bf16_bits",
     "bf16_from_bits", "make_frame", "make_frames", "make_weights", "frame_seed",
-    "pe_table", "ks_for_ratios", "multi48_group_ks",
+    "pe_table", "ks_for_ratios", "multi48_group_ks", "make_queries",
 ]
 
 
@@ -277,3 +277,24 @@ def make_weights(cfg: ModelConfig, seed: int = 0, tied: bool = False, pe: bool =
         layers.append(lw)
     w["layers"] = layers
     return w
+
+
+# ----------------------------------------------------------------------------
+# coarse-stage detections (inputs of the NEXT rows f1/f2; no trained decoder here)
+# ----------------------------------------------------------------------------
+def make_queries(seed: int, n_queries: int = 128, hard: bool = True):
+    """Synthetic per-query detections (cx, cy, w, h, c), boxes normalised, shaped like
+    PAPER.md:225-227: a few high-confidence (c > 0.8) queries, intermediate ones
+    (0.05 < c <= 0.8: ~20 on a hard frame, ~3 on an easy one) and background (c <= 0.05).
+    Box sides log-uniform in [8, 192] px of a 640 px frame.  Returns (boxes [Q,4] fp32,
+    conf [Q] fp32)."""
+    rng = np.random.default_rng(seed)
+    n_hi = 5
+    n_mid = 20 if hard else 3
+    conf = np.concatenate([rng.uniform(0.8001, 1.0, n_hi), rng.uniform(0.0501, 0.8, n_mid),
+                           rng.uniform(0.0, 0.05, n_queries - n_hi - n_mid)])
+    rng.shuffle(conf)
+    side = np.exp(rng.uniform(np.log(8 / 640), np.log(192 / 640), size=(n_queries, 2)))
+    ctr = rng.uniform(0.0, 1.0, size=(n_queries, 2))
+    boxes = np.concatenate([ctr, side], axis=1)
+    return boxes.astype(np.float32), conf.astype(np.float32)

@@ -143,6 +143,24 @@ cfd_status cfd_refine_encode(cfd_ctx *ctx, const uint16_t *image, const float *x
                              const int32_t *sel_count, float *y, int32_t *mixed_src, int32_t *cu_seqlens,
                              float *layer_out, void *ws, size_t ws_bytes, void *stream);
 
+/* NEXT row f2 — A1 hardness gate: for each frame, queries with confidence
+ * c > c_hi (0.8: large, safety-critical objects) are excluded and the remaining
+ * confidences averaged; the frame is easy (hard[b] = 0: coarse result suffices, refine
+ * with k = 0) if that mean is below tau_easy (0.05), else hard (1).  No remaining query ->
+ * easy.  conf [B, Q] fp32; hard [B] int32 out.  The mean is evaluated as an fp64
+ * sequential sum in query order compared with tau_easy * n (bit-exact decision). */
+cfd_status cfd_hardness(cfd_ctx *ctx, int32_t n_frames, int32_t n_queries, const float *conf, float c_hi,
+                        float tau_easy, int32_t *hard, void *stream);
+
+/* NEXT row f1 — box-driven region proposal: ROIs from the boxes of
+ * intermediate-confidence queries (c_lo < c <= c_hi; 0.05 / 0.8).
+ * boxes [B, Q, 4] fp32 (cx, cy, w, h) normalised to the image; conf [B, Q] fp32;
+ * scores [B, Nc] fp32 out = number of (query, pixel) pairs inside each coarse cell (an
+ * exact integer).  cfd_select_regions(THRESHOLD, 0) then selects every cell an
+ * intermediate box touches; TOPK ranks them by coverage.  n_queries <= 4096. */
+cfd_status cfd_box_scores(cfd_ctx *ctx, int32_t n_frames, int32_t n_queries, const float *boxes, const float *conf,
+                          float c_lo, float c_hi, float *scores, void *stream);
+
 /* Synchronise `stream`; return CFD_E_DEVICE (and clear the word) if a kernel flagged
  * invalid device-side input since the last check, CFD_E_CUDA on a sticky CUDA error. */
 cfd_status cfd_check(cfd_ctx *ctx, void *stream);

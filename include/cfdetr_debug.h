@@ -58,9 +58,9 @@ int32_t cfdx_probe_count(int32_t kind);
 
 /* Tuning switches (process-wide): key 0 = attention kernel variant (1: one query tile
  * per CTA, 2: persistent two-tile ping-pong with 128-key steps, 3: same with 64-key
- * steps and double-buffered S); key 1 = how many of every 16
+ * steps and double-buffered S, 4: three query tiles / warpgroups per CTA); key 1 = how many of every 16
  * column pairs variant 2 exponentiates with the FMA-pipe polynomial instead of MUFU
- * (0, 2, 4, 6 or 8; default 4). */
+ * (0, 2, 4, 6 or 8; default 4); key 2 = fused MLP kernel on (1, default) / off (0). */
 cfd_status cfdx_set_option(int32_t key, int32_t value);
 
 /* Number of kernels the library launched since load (host counter; for bench's

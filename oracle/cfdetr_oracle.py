@@ -22,6 +22,8 @@ Parity status (see tests/test_oracle_pins.py):
   select_topk/thresh .. pinned (brute force over all C(16,4) subsets; NaN/+-0 cases)
   merge / gather ...... pinned (offset closed form; k=0 == coarse; k=Nc == fine pass)
   batch_refine ........ pinned (== per-task refine; cu_seqlens closed form)
+  hardness_gate ....... pinned (vectorised fp64 mean; all-critical / single-query cases)
+  box_cell_scores ..... pinned (brute-force pixel-mask rasterisation; full-image box)
 """
 from __future__ import annotations
 
@@ -35,7 +37,8 @@ __all__ = [
     "patchify", "patch_embed", "layer_norm", "gelu", "attention_probs",
     "encoder_layer", "encoder", "criticality_score", "select_topk",
     "select_threshold", "merge_tokens", "gather_layout", "coarse_encode",
-    "refine_encode", "batch_refine", "fine_pass", "as_f64_image",
+    "refine_encode", "batch_refine", "fine_pass", "as_f64_image", "hardness_gate", "box_pixel_rect",
+    "box_cell_scores",
 ]
 
 
@@ -295,3 +298,64 @@ def fine_pass(cfg, w: dict, image_bits: np.ndarray):
     x = patch_embed(patchify(img, cfg.patch_fine), w["w_embed_f"], w["b_embed_f"], w["pe_f"])
     y, layers, _ = encoder(x, w["layers"], cfg.n_heads, cfg.ln_eps)
     return dict(y=y, layers=layers)
+
+
+# ----------------------------------------------------------------------------
+# NEXT rows: A1 hardness gate and box-driven region proposal
+# ----------------------------------------------------------------------------
+def hardness_gate(conf: np.ndarray, c_hi: float = 0.8, tau: float = 0.05) -> int:
+    """A1 frame difficulty (§III-B): exclude queries with c > c_hi ("high
+    confidence ... large and safety-critical"), average the remaining confidences; the
+    frame is easy (0) if that mean is below tau, else hard (1).  No remaining query ->
+    easy.  Reading R22: the mean is compared as  sum_i c_i < tau * n  with the sum taken
+    sequentially in query order in fp64 of the fp32 inputs and tau the fp32 value."""
+    c32 = np.asarray(conf, dtype=np.float32)
+    hi = float(np.float32(c_hi))
+    s, n = 0.0, 0
+    for c in c32:
+        if float(c) <= hi:
+            s += float(c)
+            n += 1
+    if n == 0:
+        return 0
+    return 0 if s < float(np.float32(tau)) * n else 1
+
+
+def box_pixel_rect(box, H: int, W: int):
+    """Pixel rectangle [x0, x1) x [y0, y1) of a query box (cx, cy, w, h) normalised to the
+    image (DETR convention, reading R21), edges rounded outward: x0 = floor((cx - w/2) W),
+    x1 = ceil((cx + w/2) W), clamped to the image.  Evaluated in fp32, one rounding per
+    operation, in this order (the GPU follows the same arithmetic)."""
+    f = np.float32
+    cx, cy, w, h = (f(v) for v in box)
+    half = f(0.5)
+    xa = f(f(cx - f(w * half)) * f(W))
+    xb = f(f(cx + f(w * half)) * f(W))
+    ya = f(f(cy - f(h * half)) * f(H))
+    yb = f(f(cy + f(h * half)) * f(H))
+    x0 = min(max(int(math.floor(xa)), 0), W)
+    x1 = min(max(int(math.ceil(xb)), 0), W)
+    y0 = min(max(int(math.floor(ya)), 0), H)
+    y1 = min(max(int(math.ceil(yb)), 0), H)
+    return x0, x1, y0, y1
+
+
+def box_cell_scores(cfg, boxes: np.ndarray, conf: np.ndarray, c_lo: float = 0.05, c_hi: float = 0.8) -> np.ndarray:
+    """A2 region proposal: "ROIs are proposed based on the locations
+    (x, y) and sizes (w, h) of intermediate-confidence queries" (0.05 < c <= 0.8, bands of
+    PAPER.md:225).  Per coarse cell: score = number of (query, pixel) pairs with the pixel
+    inside both the query's box and the cell (integer, returned as float64).  A cell is a
+    region proposal when its score > 0 (select_threshold with tau = 0)."""
+    H, W, P = cfg.img_h, cfg.img_w, cfg.patch_coarse
+    lo, hi = float(np.float32(c_lo)), float(np.float32(c_hi))
+    s = np.zeros(cfg.n_coarse, dtype=np.int64)
+    for b, c in zip(boxes, np.asarray(conf, np.float32)):
+        if not (lo < float(c) <= hi):
+            continue
+        x0, x1, y0, y1 = box_pixel_rect(b, H, W)
+        for cell in range(cfg.n_coarse):
+            gy, gx = divmod(cell, cfg.gc_w)
+            ox = max(0, min(x1, (gx + 1) * P) - max(x0, gx * P))
+            oy = max(0, min(y1, (gy + 1) * P) - max(y0, gy * P))
+            s[cell] += ox * oy
+    return s.astype(np.float64)

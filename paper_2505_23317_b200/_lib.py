@@ -22,7 +22,8 @@ STATUS = {0: "CFD_OK", -1: "CFD_E_ARG", -2: "CFD_E_SHAPE", -3: "CFD_E_UNSUPPORTE
 
 # public symbols of include/cfdetr.h and include/cfdetr_debug.h
 PUBLIC_SYMBOLS = ["cfd_create", "cfd_destroy", "cfd_query", "cfd_coarse_encode", "cfd_select_regions",
-                  "cfd_refine_encode", "cfd_batch_refine", "cfd_check", "cfd_status_str", "cfd_version"]
+                  "cfd_refine_encode", "cfd_batch_refine", "cfd_check", "cfd_status_str", "cfd_version",
+                  "cfd_hardness", "cfd_box_scores"]
 DEBUG_SYMBOLS = ["cfdx_gemm", "cfdx_attention", "cfdx_layernorm", "cfdx_score", "cfdx_gather",
                  "cfdx_launch_count", "cfdx_probe_install", "cfdx_probe_count", "cfdx_set_option"]
 PROBE_KINDS = {"attention": 0, "score": 1, "gemm_qkv": 2, "gemm_oproj": 3, "gemm_mlp1": 4, "gemm_mlp2": 5,
@@ -73,6 +74,8 @@ def load() -> C.CDLL:
         "cfd_refine_encode": [P, P, P, P, P, P, P, P, P, P, SZ, P],
         "cfd_batch_refine": [P, I32, P, P, P, P, C.POINTER(I32), P, P, P, P, P, SZ, P],
         "cfd_check": [P, P],
+        "cfd_hardness": [P, I32, I32, P, F32, F32, P, P],
+        "cfd_box_scores": [P, I32, I32, P, P, F32, F32, P, P],
         "cfd_status_str": [I32],
         "cfd_version": [],
         "cfdx_gemm": [I32, I32, I32, P, P, P, I32, P, P, P],

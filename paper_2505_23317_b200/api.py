@@ -180,5 +180,28 @@ class CFDetrEncoder:
         return o
 
 
+def _hardness(self, conf: torch.Tensor, c_hi: float = 0.8, tau_easy: float = 0.05, stream=None) -> torch.Tensor:
+    """A1 hardness gate (NEXT f2): conf [B, Q] fp32 -> hard [B] int32 (1 = refine, 0 = easy)."""
+    B, Q = conf.shape
+    hard = torch.empty(B, dtype=torch.int32, device=self.device)
+    L.check("cfd_hardness", self.lib.cfd_hardness(self.ctx, B, Q, conf.data_ptr(), c_hi, tau_easy, hard.data_ptr(),
+                                                  _stream(stream)))
+    return hard
+
+
+def _box_scores(self, boxes: torch.Tensor, conf: torch.Tensor, c_lo: float = 0.05, c_hi: float = 0.8,
+                stream=None) -> torch.Tensor:
+    """Box-driven region scores (NEXT f1): boxes [B, Q, 4], conf [B, Q] -> scores [B, Nc]."""
+    B, Q = conf.shape
+    scores = torch.empty(B, self.Nc, dtype=torch.float32, device=self.device)
+    L.check("cfd_box_scores", self.lib.cfd_box_scores(self.ctx, B, Q, boxes.data_ptr(), conf.data_ptr(), c_lo, c_hi,
+                                                      scores.data_ptr(), _stream(stream)))
+    return scores
+
+
+CFDetrEncoder.hardness = _hardness
+CFDetrEncoder.box_scores = _box_scores
+
+
 def launch_count() -> int:
     return int(L.load().cfdx_launch_count())

@@ -1,20 +1,15 @@
-// attn3_tc.cuh — persistent varlen multi-head attention on tcgen05, 64-key softmax steps
-// (PAPER.md:121 global self-attention, block-diagonal per task for the
-// patch-level batch PAPER.md:261-265 / reading R11).
+// attn4_tc.cuh — attention v4: like attn3 (persistent, 64-key softmax steps, per-warpgroup
+// MMA issuers, lazy rescale, MUFU/polynomial exp2) but with THREE softmax warpgroups per
+// CTA, so an item is (task, triple of 128-row query tiles, head) and every K/V tile the
+// TMA warp streams serves three query tiles.
 //
-// Same work decomposition as attn2 (item = task x pair of 128-row query tiles x head,
-// round-robin over one persistent CTA per SM, both query tiles share the streamed K/V),
-// but the softmax advances in 64-key sub-tiles u (K/V still arrive as 128-row TMA tiles):
-//
-//   TMEM per warpgroup w:  S_w[2] (2 x 64 fp32 cols, double-buffered), P_w (32 cols of
-//   bf16 pairs), O_w (32 cols)  ->  2 x 192 = 384 of 512 columns.
-//
-//   MMA warp, per sub-tile u:  QK_{u+1}(w) as soon as S_w[(u+1)&1] is released, then
-//   PV_u(w) when P_u is stored.  So S_{u+1} is computed while the softmax works on S_u.
-//   Softmax warp (one thread per query row): ld 64 S values, release S buffer, row max,
-//   lazy rescale (only when the max grows by > 2^8), 64 exp2 (MUFU / FMA polynomial
-//   split), rescale O in TMEM if needed, st P, release to the MMA warp.
-// 64-value rows keep the softmax warps at ~100 registers (no spills at 320 threads).
+//   TMEM per warpgroup w (128 columns, 3 x 128 = 384 of 512):
+//     S_w  64 fp32 cols  — single-buffered: the warpgroup moves S_u into registers at the
+//                          start of sub-tile u and releases it (s_free), so QK_{u+1} still
+//                          runs on the tensor core during the exponentials of S_u
+//     P_w  32 cols (bf16 pairs), O_w 32 cols (accumulated, rescaled in place)
+//   Warps: 0 TMA, 1..3 MMA issuers (one per warpgroup), 4..15 softmax (3 x 4); 512 threads,
+//   <= 128 registers per thread.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -22,31 +17,32 @@
 #include "ptx.cuh"
 #include "attn_tc.cuh"
 #include "attn2_tc.cuh"
+#include "attn3_tc.cuh"
 
 namespace cfd {
 
 template <int DH, int STAGES>
-struct Attn3Smem {
+struct Attn4Smem {
   static constexpr int TILE_BYTES = 128 * DH * 2;
-  static constexpr int Q_OFF = 0;                              // [2 slots][2 tiles]
-  static constexpr int K_OFF = Q_OFF + 4 * TILE_BYTES;         // [STAGES]
+  static constexpr int Q_OFF = 0;                              // [2 slots][3 tiles]
+  static constexpr int K_OFF = Q_OFF + 6 * TILE_BYTES;         // [STAGES]
   static constexpr int V_OFF = K_OFF + STAGES * TILE_BYTES;    // [STAGES]
   static constexpr int BAR_OFF = V_OFF + STAGES * TILE_BYTES;
   static constexpr int PRE_OFF = BAR_OFF + 512;
   static constexpr int TOTAL = 1024 + PRE_OFF + (ATTN2_MAX_T + 1) * 4;
-  static constexpr uint32_t S_COL = 0;    // S_w[b] at w*128 + b*64
-  static constexpr uint32_t P_COL = 256;  // P_w at 256 + w*32
-  static constexpr uint32_t O_COL = 320;  // O_w at 320 + w*32
+  static constexpr uint32_t S_COL = 0;    // S_w at w*128
+  static constexpr uint32_t P_COL = 64;   // P_w at w*128 + 64
+  static constexpr uint32_t O_COL = 96;   // O_w at w*128 + 96
 };
 
-constexpr int ATTN3_THREADS = 352;    // TMA warp, MMA warp (WG0), 8 softmax warps, MMA warp (WG1)
-constexpr int ATTN3_MMA1_WARP = 10;
+constexpr int ATTN4_THREADS = 512;    // TMA warp, 3 MMA warps, 12 softmax warps
+constexpr int ATTN4_NWG = 3;
 
 template <int DH, int STAGES, int NPP>
-__global__ void __launch_bounds__(ATTN3_THREADS, 1)
-    attn3_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const AttnParams p, const int T, const int nh) {
+__global__ void __launch_bounds__(ATTN4_THREADS, 1)
+    attn4_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const AttnParams p, const int T, const int nh) {
   static_assert(DH == 32, "specialised for dh = 32 (64-byte rows, SW64)");
-  using S = Attn3Smem<DH, STAGES>;
+  using S = Attn4Smem<DH, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
@@ -54,25 +50,29 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
   uint64_t* q_empty = bars + 2;             // [2]
   uint64_t* kv_full = bars + 4;             // [STAGES]
   uint64_t* kv_empty = kv_full + STAGES;    // [STAGES]
-  uint64_t* s_full = kv_empty + STAGES;     // [2 w][2 b]
-  uint64_t* s_free = s_full + 4;            // [2 w][2 b]
-  uint64_t* p_full = s_free + 4;            // [2 w]
-  uint64_t* o_full = p_full + 2;            // [2 w]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+  uint64_t* s_full = kv_empty + STAGES;     // [3 w]
+  uint64_t* s_free = s_full + 3;            // [3 w]
+  uint64_t* p_full = s_free + 3;            // [3 w]
+  uint64_t* o_full = p_full + 3;            // [3 w]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 3);
   int* prefix = reinterpret_cast<int*>(smem + S::PRE_OFF);
 
   const int warp = warp_id(), lane = lane_id();
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     const int n = __ldg(p.cu_seqlens + t + 1) - __ldg(p.cu_seqlens + t);
-    prefix[t + 1] = ((n + 255) / 256) * nh;
+    prefix[t + 1] = ((n + 383) / 384) * nh;
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQKV);
-    // Q slots and K/V stages are released by both MMA threads (one per warpgroup)
-    for (int i = 0; i < 2; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 2); }
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 2); }
-    for (int i = 0; i < 4; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_free[i], 128); }
-    for (int w = 0; w < 2; ++w) { mbar_init(&p_full[w], 128); mbar_init(&o_full[w], 1); }
+    // Q slots and K/V stages are released by all three MMA threads (one per warpgroup)
+    for (int i = 0; i < 2; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], ATTN4_NWG); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], ATTN4_NWG); }
+    for (int w = 0; w < ATTN4_NWG; ++w) {
+      mbar_init(&s_full[w], 1);
+      mbar_init(&s_free[w], 128);
+      mbar_init(&p_full[w], 128);
+      mbar_init(&o_full[w], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -108,14 +108,14 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
         decode_item(prefix, T, nh, item, t, qp, h);
         const int seq0 = __ldg(p.cu_seqlens + t);
         const int N = __ldg(p.cu_seqlens + t + 1) - seq0;
-        const int nq = ((2 * qp + 1) * 128 < N) ? 2 : 1;
+        const int nq = min(ATTN4_NWG, (N - 3 * qp * 128 + 127) / 128);
         const int nkv = (N + 127) / 128;
         const int slot = it & 1;
         mbar_wait(&q_empty[slot], ((it >> 1) & 1) ^ 1);
         mbar_expect_tx(&q_full[slot], nq * S::TILE_BYTES);
         for (int w = 0; w < nq; ++w)
-          tma_load_2d(smem + S::Q_OFF + (slot * 2 + w) * S::TILE_BYTES, &tmQKV, &q_full[slot], h * DH,
-                      seq0 + (2 * qp + w) * 128);
+          tma_load_2d(smem + S::Q_OFF + (slot * 3 + w) * S::TILE_BYTES, &tmQKV, &q_full[slot], h * DH,
+                      seq0 + (3 * qp + w) * 128);
         for (int j = 0; j < nkv; ++j, ++kvc) {
           const int st = kvc % STAGES;
           mbar_wait(&kv_empty[st], ((kvc / STAGES) & 1) ^ 1);
@@ -125,18 +125,18 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
         }
       }
     }
-  } else if (warp == 1 || warp == ATTN3_MMA1_WARP) {
+  } else if (warp >= 1 && warp <= ATTN4_NWG) {
     // ================================================================ MMA issuers
     // warp 1 issues for warpgroup 0, the last warp for warpgroup 1: each warpgroup's
     // S/P/O pipeline advances independently (tcgen05.commit tracks the issuing thread's
     // MMAs).  A K/V stage or Q slot is released once both issuers are done with it.
     if (lane == 0) {
-      const int w = (warp == 1) ? 0 : 1;
+      const int w = warp - 1;
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, 0);  // S_u = Q K_u^T (64 keys)
       constexpr uint32_t idesc_o = make_idesc_bf16(128, DH, 1);  // O += P_u V_u (V MN-major)
       int it = 0, kvc = 0;
       uint32_t p_cnt = 0;
-      uint32_t s_use[2] = {0, 0};   // QKs issued into S_w[b]
+      uint32_t s_use = 0;   // QKs issued into S_w
       for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
         int t, qp, h;
         decode_item(prefix, T, nh, item, t, qp, h);
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
         const int nkv = (N + 127) / 128;
         const int slot = it & 1;
         mbar_wait(&q_full[slot], (it >> 1) & 1);
-        if ((2 * qp + w) * 128 >= N) {
+        if ((3 * qp + w) * 128 >= N) {
           // no query tile for this warpgroup: release the item's stages in step
           for (int j = 0; j < nkv; ++j) {
             const int st = (kvc + j) % STAGES;
@@ -157,21 +157,20 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
           continue;
         }
         const int nsub = (N + 63) / 64;
-        const uint32_t qa = smem_u32(smem + S::Q_OFF + (slot * 2 + w) * S::TILE_BYTES);
+        const uint32_t qa = smem_u32(smem + S::Q_OFF + (slot * 3 + w) * S::TILE_BYTES);
         auto issue_qk = [&](int u) {
           const int j = u >> 1;
           const int st = (kvc + j) % STAGES;
           if ((u & 1) == 0) mbar_wait(&kv_full[st], ((kvc + j) / STAGES) & 1);
           const uint32_t ka = smem_u32(smem + S::K_OFF + st * S::TILE_BYTES) + (u & 1) * 64 * DH * 2;
-          const int b = u & 1;
-          if (s_use[b] > 0) mbar_wait(&s_free[w * 2 + b], (s_use[b] - 1) & 1);
-          ++s_use[b];
+          if (s_use > 0) mbar_wait(&s_free[w], (s_use - 1) & 1);
+          ++s_use;
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < DH / 16; ++k)
-            mma_ss(tmem + S::S_COL + (w * 2 + b) * 64, make_smem_desc(qa + k * 32, 16, 512, kLayoutSW64),
+            mma_ss(tmem + w * 128 + S::S_COL, make_smem_desc(qa + k * 32, 16, 512, kLayoutSW64),
                    make_smem_desc(ka + k * 32, 16, 512, kLayoutSW64), idesc_s, k);
-          mma_commit(&s_full[w * 2 + b]);
+          mma_commit(&s_full[w]);
         };
         issue_qk(0);
         for (int u = 0; u < nsub; ++u) {
@@ -185,7 +184,7 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
           ++p_cnt;
           tc_fence_after();
           for (int k = 0; k < ksteps; ++k)
-            mma_ts(tmem + S::O_COL + w * DH, tmem + S::P_COL + w * 32 + k * 8,
+            mma_ts(tmem + w * 128 + S::O_COL, tmem + w * 128 + S::P_COL + k * 8,
                    make_smem_desc(va + k * 16 * DH * 2, 4096, 512, kLayoutSW64), idesc_o, (u | k) != 0);
           mma_commit(&o_full[w]);
           if ((u & 1) || u + 1 == nsub) mma_commit(&kv_empty[st]);
@@ -195,40 +194,39 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
       }
     }
   } else {
-    // ================================================================ softmax warpgroups (warps 2..9)
-    const int wg = (warp - 2) >> 2;
+    // ================================================================ softmax warpgroups (warps 4..15)
+    const int wg = (warp - 4) >> 2;
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t s_base = tmem + lane_off + S::S_COL + wg * 128;
-    const uint32_t p_addr = tmem + lane_off + S::P_COL + wg * 32;
-    const uint32_t o_addr = tmem + lane_off + S::O_COL + wg * DH;
+    const uint32_t s_base = tmem + lane_off + wg * 128 + S::S_COL;
+    const uint32_t p_addr = tmem + lane_off + wg * 128 + S::P_COL;
+    const uint32_t o_addr = tmem + lane_off + wg * 128 + S::O_COL;
     const float c = p.scale_log2;
-    uint32_t s_cnt[2] = {0, 0}, o_cnt = 0;
+    uint32_t s_cnt = 0, o_cnt = 0;
     for (int item = blockIdx.x; item < total; item += gridDim.x) {
       int t, qp, h;
       decode_item(prefix, T, nh, item, t, qp, h);
       const int seq0 = __ldg(p.cu_seqlens + t);
       const int N = __ldg(p.cu_seqlens + t + 1) - seq0;
-      const int qt = 2 * qp + wg;
+      const int qt = 3 * qp + wg;
       if (qt * 128 >= N) continue;
       const int nsub = (N + 63) / 64;
       const int q_valid = N - qt * 128;
       const bool active = quarter * 32 < q_valid;
       float m_run = -INFINITY, l_run = 0.f;
       for (int u = 0; u < nsub; ++u) {
-        const int b = u & 1;
-        mbar_wait(&s_full[wg * 2 + b], s_cnt[b] & 1);
-        ++s_cnt[b];
+        mbar_wait(&s_full[wg], s_cnt & 1);
+        ++s_cnt;
         tc_fence_after();
         if (active) {
           const int valid = min(64, N - u * 64);
           uint32_t sr[64];
-          tmem_ld32(s_base + b * 64, *reinterpret_cast<uint32_t(*)[32]>(sr));
-          if (valid > 32) tmem_ld32(s_base + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+          tmem_ld32(s_base, *reinterpret_cast<uint32_t(*)[32]>(sr));
+          if (valid > 32) tmem_ld32(s_base + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
           tmem_wait_ld();
           tc_fence_before();
-          mbar_arrive(&s_free[wg * 2 + b]);  // S_w[b] may be overwritten by QK_{u+2}
+          mbar_arrive(&s_free[wg]);  // S_w may now be overwritten by QK_{u+1}
           if (valid < 64) {
 #pragma unroll
             for (int i = 0; i < 64; ++i)
@@ -282,7 +280,7 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
         } else {
           // padding-only warp: still waits for PV_{u-1} so it cannot arrive on p_full for
           // sub-tile u before that barrier's previous phase (sub-tile u-1) has completed
-          mbar_arrive(&s_free[wg * 2 + b]);
+          mbar_arrive(&s_free[wg]);
           if (u > 0) {
             mbar_wait(&o_full[wg], o_cnt & 1);
             ++o_cnt;

@@ -25,8 +25,10 @@
 #include "attn_tc.cuh"
 #include "attn2_tc.cuh"
 #include "attn3_tc.cuh"
+#include "attn4_tc.cuh"
 #include "gemm_tc.cuh"
 #include "misc_kernels.cuh"
+#include "mlp_tc.cuh"
 #include "score_tc.cuh"
 
 using namespace cfd;
@@ -113,12 +115,16 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 template <int BN>
 constexpr int gemm_stages() { return BN == 256 ? 4 : BN == 128 ? 6 : 8; }
 
-template <int BN, int EPI>
+// mode 0: 1 CTA/SM, 8 epilogue warps, double-buffered accumulator (many tiles)
+// mode 1: 2 CTAs/SM, 4 epilogue warps, single accumulator, 2-stage ring (N = d GEMMs)
+template <int BN, int EPI, int MODE>
 cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows_for_grid,
                           cudaStream_t s) {
-  constexpr int ST = gemm_stages<BN>();
-  auto kern = gemm_tc_kernel<BN, ST, EPI>;
-  constexpr int smem = GemmSmem<BN, ST>::TOTAL;
+  constexpr int EW = MODE ? 4 : 8;
+  constexpr int NACC = MODE ? 1 : 2;
+  constexpr int ST = MODE ? 2 : gemm_stages<BN>();
+  auto kern = gemm_tc_kernel<BN, ST, EPI, EW, NACC>;
+  constexpr int smem = GemmSmem<BN, ST, NACC>::TOTAL;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -126,8 +132,9 @@ cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
     attr = true;
   }
   const int tiles = ((rows_for_grid + GEMM_BM - 1) / GEMM_BM) * (p.N / BN);
-  const int grid = tiles < num_sms() ? (tiles > 0 ? tiles : 1) : num_sms();
-  kern<<<grid, GEMM_THREADS, smem, s>>>(ta, tb, p);
+  const int slots = num_sms() * (MODE ? 2 : 1);
+  const int grid = tiles < slots ? (tiles > 0 ? tiles : 1) : slots;
+  kern<<<grid, 64 + 32 * EW, smem, s>>>(ta, tb, p);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -135,10 +142,18 @@ cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
 template <int EPI>
 cudaError_t launch_gemm_bn(int BN, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows,
                            cudaStream_t s) {
+  // N = BN: a single column tile per row block -> the 2-CTA/SM configuration
+  if (p.N == BN) {
+    switch (BN) {
+      case 256: return launch_gemm_t<256, EPI, 1>(ta, tb, p, rows, s);
+      case 128: return launch_gemm_t<128, EPI, 1>(ta, tb, p, rows, s);
+      default: return launch_gemm_t<64, EPI, 1>(ta, tb, p, rows, s);
+    }
+  }
   switch (BN) {
-    case 256: return launch_gemm_t<256, EPI>(ta, tb, p, rows, s);
-    case 128: return launch_gemm_t<128, EPI>(ta, tb, p, rows, s);
-    default: return launch_gemm_t<64, EPI>(ta, tb, p, rows, s);
+    case 256: return launch_gemm_t<256, EPI, 0>(ta, tb, p, rows, s);
+    case 128: return launch_gemm_t<128, EPI, 0>(ta, tb, p, rows, s);
+    default: return launch_gemm_t<64, EPI, 0>(ta, tb, p, rows, s);
   }
 }
 
@@ -182,13 +197,31 @@ bool make_qkvmap(CUtensorMap* m, const void* qkv, int rows, int d) {
 
 // runtime options (cfdx_set_option): attention variant (1 = one q-tile per CTA,
 // 2 = persistent two-tile ping-pong) and the polynomial-exp2 share of variant 2.
-int g_attn_variant = 3;
+int g_attn_variant = 4;
 int g_attn_npp = 4;
+int g_fused_mlp = 1;  // fused MLP kernel (d == 256) instead of two GEMM launches
+
+cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUtensorMap& tw2, const MlpParams& p,
+                       int rows_for_grid, cudaStream_t s) {
+  auto kern = mlp_tc_kernel<256>;
+  constexpr int smem = MlpSmem<256>::TOTAL;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles = (pad_rows(rows_for_grid, p.ln_cap > 0 ? p.ln_cap : rows_for_grid + 256) + 127) / 128;
+  const int grid = std::max(1, std::min(tiles, num_sms()));
+  kern<<<grid, MLP_THREADS, smem, s>>>(th, tw1, tw2, p);
+  ++g_launches;
+  return cudaGetLastError();
+}
 
 template <int V, int NPP>
 cudaError_t launch_attn2_t(const CUtensorMap& tq, const AttnParams& p, int items_ub, int nh, int T, cudaStream_t s) {
-  auto kern = (V == 2) ? attn2_tc_kernel<32, 4, NPP> : attn3_tc_kernel<32, 4, NPP>;
-  constexpr int smem = (V == 2) ? Attn2Smem<32, 4>::TOTAL : Attn3Smem<32, 4>::TOTAL;
+  auto kern = (V == 2) ? attn2_tc_kernel<32, 4, NPP> : (V == 3) ? attn3_tc_kernel<32, 4, NPP> : attn4_tc_kernel<32, 4, NPP>;
+  constexpr int smem = (V == 2) ? Attn2Smem<32, 4>::TOTAL : (V == 3) ? Attn3Smem<32, 4>::TOTAL : Attn4Smem<32, 4>::TOTAL;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -196,7 +229,7 @@ cudaError_t launch_attn2_t(const CUtensorMap& tq, const AttnParams& p, int items
     attr = true;
   }
   const int grid = std::max(1, std::min(items_ub, num_sms()));
-  kern<<<grid, V == 2 ? ATTN2_THREADS : ATTN3_THREADS, smem, s>>>(tq, p, T, nh);
+  kern<<<grid, V == 2 ? ATTN2_THREADS : V == 3 ? ATTN3_THREADS : ATTN4_THREADS, smem, s>>>(tq, p, T, nh);
   return cudaGetLastError();
 }
 
@@ -214,13 +247,21 @@ cudaError_t launch_attention(const CUtensorMap& tq, const AttnParams& p, int max
         case 8: e = launch_attn2_t<2, 8>(tq, p, items_ub, nh, T, s); break;
         default: e = launch_attn2_t<2, 4>(tq, p, items_ub, nh, T, s); break;
       }
-    } else {
+    } else if (g_attn_variant == 3) {
       switch (g_attn_npp) {
         case 0: e = launch_attn2_t<3, 0>(tq, p, items_ub, nh, T, s); break;
         case 2: e = launch_attn2_t<3, 2>(tq, p, items_ub, nh, T, s); break;
         case 6: e = launch_attn2_t<3, 6>(tq, p, items_ub, nh, T, s); break;
         case 8: e = launch_attn2_t<3, 8>(tq, p, items_ub, nh, T, s); break;
         default: e = launch_attn2_t<3, 4>(tq, p, items_ub, nh, T, s); break;
+      }
+    } else {
+      switch (g_attn_npp) {
+        case 0: e = launch_attn2_t<4, 0>(tq, p, items_ub, nh, T, s); break;
+        case 2: e = launch_attn2_t<4, 2>(tq, p, items_ub, nh, T, s); break;
+        case 6: e = launch_attn2_t<4, 6>(tq, p, items_ub, nh, T, s); break;
+        case 8: e = launch_attn2_t<4, 8>(tq, p, items_ub, nh, T, s); break;
+        default: e = launch_attn2_t<4, 4>(tq, p, items_ub, nh, T, s); break;
       }
     }
   } else {
@@ -281,6 +322,7 @@ struct LayerDev {
   uint16_t *wqkv, *wo, *w1, *w2;  // K-major [N, K]
   float *b_qkv, *b_o, *b_1, *b_2, *ln1_g, *ln1_b, *ln2_g, *ln2_b;
   CUtensorMap tm_qkv, tm_o, tm_1, tm_2;
+  CUtensorMap tm_1c;  // W1^T with 128-row boxes (fused MLP chunks)
 };
 
 struct cfd_ctx {
@@ -383,6 +425,19 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
     CFD_CUDA(launch_gemm(EPI_F32_RESID, ta_o, L.tm_o, p, rows_grid, s, PK_OPROJ));
     CFD_CUDA(launch_layernorm(d, x, L.ln2_g, L.ln2_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
   }
+  if (g_fused_mlp && fuse_ln && d == 256 && F % 128 == 0) {
+    // fused MLP1 + GELU + MLP2 + residual (+ next LN1): the hidden activations stay on chip
+    MlpParams mp{};
+    mp.M = M_static; mp.m_dev = m_dev; mp.F = F; mp.b1 = L.b_1; mp.b2 = L.b_2; mp.x = x; mp.ln_eps = g.ln_eps;
+    if (l + 1 < g.n_layers) {
+      const LayerDev& Ln = c->layers[l + 1];
+      mp.ln_g = Ln.ln1_g; mp.ln_b = Ln.ln1_b; mp.ln_out = w.hbuf; mp.ln_cap = w.rows_cap;
+    }
+    probe_begin(PK_MLP1, s);
+    CFD_CUDA(launch_mlp(ta_h, L.tm_1c, L.tm_2, mp, rows_grid, s));
+    probe_end(PK_MLP1, s);
+    return CFD_OK;
+  }
   // MLP1 + GELU
   p = GemmParams{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = w.rows_cap; p.N = F; p.K = d; p.bias = L.b_1; p.out_bf16 = w.ff;
@@ -411,7 +466,7 @@ cfd_status validate_cfg(const cfd_config* g) {
     return CFD_E_SHAPE;
   if (g->d_model / g->n_heads != 32) return CFD_E_UNSUPPORTED;
   if (g->d_model != 64 && g->d_model != 128 && g->d_model != 256 && g->d_model != 512) return CFD_E_UNSUPPORTED;
-  if (g->d_ff % 64) return CFD_E_UNSUPPORTED;
+  if (g->d_ff % 64 || g->d_ff > GEMM_MAX_N) return CFD_E_UNSUPPORTED;
   if ((3 * g->patch_fine * g->patch_fine) % 64 || (g->patch_fine * 3 * 2) % 16) return CFD_E_UNSUPPORTED;
   const int Nc = (g->img_h / g->patch_coarse) * (g->img_w / g->patch_coarse);
   if (Nc > 4096) return CFD_E_UNSUPPORTED;
@@ -456,12 +511,15 @@ cfd_status cfdx_probe_install(int32_t kind, void* const* h_start, void* const* h
 cfd_status cfdx_set_option(int32_t key, int32_t value) {
   switch (key) {
     case 0:
-      if (value < 1 || value > 3) return CFD_E_ARG;
+      if (value < 1 || value > 4) return CFD_E_ARG;
       g_attn_variant = value;
       return CFD_OK;
     case 1:
       if (value != 0 && value != 2 && value != 4 && value != 6 && value != 8) return CFD_E_ARG;
       g_attn_npp = value;
+      return CFD_OK;
+    case 2:
+      g_fused_mlp = value ? 1 : 0;
       return CFD_OK;
   }
   return CFD_E_ARG;
@@ -554,7 +612,8 @@ cfd_status cfd_create(const cfd_config* cfg, const cfd_weights* wts, void* strea
       if (cudaMemcpyAsync(vecs[i].second, vecs[i].first, lens[i] * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
         return fail(CFD_E_CUDA);
     if (!make_wmap(&ld.tm_qkv, ld.wqkv, 3 * d, d) || !make_wmap(&ld.tm_o, ld.wo, d, d) ||
-        !make_wmap(&ld.tm_1, ld.w1, F, d) || !make_wmap(&ld.tm_2, ld.w2, d, F))
+        !make_wmap(&ld.tm_1, ld.w1, F, d) || !make_wmap(&ld.tm_2, ld.w2, d, F) ||
+        !make_tmap(&ld.tm_1c, ld.w1, d, F, d, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B))
       return fail(CFD_E_CUDA);
   }
   *out = c;
@@ -729,6 +788,32 @@ cfd_status cfd_refine_encode(cfd_ctx* c, const uint16_t* image, const float* x0,
                           stream);
 }
 
+cfd_status cfd_hardness(cfd_ctx* c, int32_t B, int32_t Q, const float* conf, float c_hi, float tau,
+                        int32_t* hard, void* stream) {
+  if (!c) return CFD_E_ARG;
+  if (B == 0) return CFD_OK;
+  if (B < 0 || Q < 0 || !conf || !hard) return CFD_E_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  hardness_kernel<<<(B + 127) / 128, 128, 0, s>>>(conf, B, Q, c_hi, tau, hard);
+  ++g_launches;
+  CFD_CUDA(cudaGetLastError());
+  return CFD_OK;
+}
+
+cfd_status cfd_box_scores(cfd_ctx* c, int32_t B, int32_t Q, const float* boxes, const float* conf, float c_lo,
+                          float c_hi, float* scores, void* stream) {
+  if (!c) return CFD_E_ARG;
+  if (B == 0) return CFD_OK;
+  if (B < 0 || Q < 0 || Q > 4096 || !boxes || !conf || !scores) return CFD_E_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const cfd_config& g = c->cfg;
+  box_scores_kernel<<<B, 256, (size_t)std::max(Q, 1) * sizeof(int4), s>>>(
+      boxes, conf, Q, g.img_h, g.img_w, g.patch_coarse, c->gc_w, c->Nc, c_lo, c_hi, scores);
+  ++g_launches;
+  CFD_CUDA(cudaGetLastError());
+  return CFD_OK;
+}
+
 cfd_status cfd_check(cfd_ctx* c, void* stream) {
   if (!c) return CFD_E_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -745,7 +830,7 @@ cfd_status cfd_check(cfd_ctx* c, void* stream) {
 // ---------------------------------------------------------------------- debug entry points
 cfd_status cfdx_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const uint16_t* W, const float* bias,
                      int32_t epi, uint16_t* out_bf16, float* out_f32, void* stream) {
-  if (M <= 0 || N <= 0 || K <= 0 || N % 64 || K % 64 || !A || !W || !bias) return CFD_E_ARG;
+  if (M <= 0 || N <= 0 || K <= 0 || N % 64 || K % 64 || N > GEMM_MAX_N || !A || !W || !bias) return CFD_E_ARG;
   if (epi < 0 || epi > 2 || (epi < 2 && !out_bf16) || (epi == 2 && !out_f32)) return CFD_E_ARG;
   CUtensorMap ta, tb;
   if (!make_amap(&ta, A, M, K) || !make_wmap(&tb, W, N, K)) return CFD_E_CUDA;

@@ -66,18 +66,27 @@ struct GemmParams {
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_EPI_WARPS = 8;                     // 2 per TMEM lane quarter
+// Two configurations (template EW = epilogue warps, NACC = TMEM accumulator buffers):
+//   EW=8, NACC=2: one CTA per SM, 2 warps per TMEM lane quarter (column halves), the
+//                 epilogue of tile i overlaps the MMAs of tile i+1   (many-tile GEMMs)
+//   EW=4, NACC=1: two CTAs per SM (256 TMEM columns, 2-stage ring each), one thread per
+//                 full row, the two co-resident CTAs overlap each other (N = d GEMMs whose
+//                 ~M/128 tiles would otherwise leave a badly quantised second wave)
+constexpr int GEMM_EPI_WARPS = 8;                     // maximum
 constexpr int GEMM_THREADS = 64 + 32 * GEMM_EPI_WARPS;  // + TMA warp + MMA warp
+constexpr int GEMM_MAX_N = 2048;   // bias columns staged in shared memory
+constexpr int GEMM_MAX_LN = 512;   // LayerNorm width for EPI_F32_RESID_LN
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int NACC = 2>
 struct GemmSmem {
   static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr int B_BYTES = BN * GEMM_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_BYTES = 128 + 2 * 128 * 8;  // barriers + RESID_LN row statistics
-  static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES;
-  static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
-                                        : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int PAR_FLOATS = GEMM_MAX_N + 2 * GEMM_MAX_LN;  // bias | ln gamma | ln beta
+  static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES + PAR_FLOATS * 4;
+  static constexpr uint32_t TMEM_COLS = (NACC * BN <= 32) ? 32 : (NACC * BN <= 64) ? 64 : (NACC * BN <= 128) ? 128
+                                        : (NACC * BN <= 256) ? 256 : 512;
 };
 
 // Rows a varlen attention tile may touch past the last valid row: a task's last KV
@@ -110,21 +119,15 @@ __device__ __forceinline__ void gelu2(float& a, float& b) {
   fma2x(a, b, a, b, h0, h1, 0.f, 0.f);          // z * Phi
 }
 
+// ---------------------------------------------------------------------------- epilogue
+// Each epilogue warp owns 32 rows (its TMEM lane quarter) x BN/2 columns of a tile, one
+// row per thread, in 32-column chunks: tcgen05.ld -> + bias (shared-memory broadcast) ->
+// fused op -> 16-byte vector stores of the thread's row segment.
 template <int EPI>
-__device__ __forceinline__ void gemm_epilogue_chunk(const GemmParams& p, int row, int col0, const uint32_t (&r)[32],
-                                                    bool store_ok) {
-  float v[32];
-  const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    float4 b = __ldg(b4 + i);
-    v[4 * i + 0] = __uint_as_float(r[4 * i + 0]) + b.x;
-    v[4 * i + 1] = __uint_as_float(r[4 * i + 1]) + b.y;
-    v[4 * i + 2] = __uint_as_float(r[4 * i + 2]) + b.z;
-    v[4 * i + 3] = __uint_as_float(r[4 * i + 3]) + b.w;
-  }
-  if (!store_ok) return;
+__device__ __forceinline__ void direct_chunk(const GemmParams& p, float (&v)[32], int row, int col0, int m_store,
+                                             int M, float& s1, float& s2) {
   if constexpr (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_GELU) {
+    if (row >= m_store) return;
     uint32_t pk[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -135,122 +138,53 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const GemmParams& p, int row
     uint4* dst = reinterpret_cast<uint4*>(p.out_bf16 + (size_t)row * p.N + col0);
 #pragma unroll
     for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-  } else if constexpr (EPI == EPI_F32_RESID) {
+  } else if constexpr (EPI == EPI_F32_RESID || EPI == EPI_F32_RESID_LN) {
+    if (row >= M) return;
     float4* dst = reinterpret_cast<float4*>(p.out_f32 + (size_t)row * p.ld_out + col0);
+    float4 x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = dst[i];  // all 8 loads in flight before the adds
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      float4 o = dst[i];
-      o.x += v[4 * i + 0]; o.y += v[4 * i + 1]; o.z += v[4 * i + 2]; o.w += v[4 * i + 3];
-      dst[i] = o;
+      x[i].x += v[4 * i + 0]; x[i].y += v[4 * i + 1]; x[i].z += v[4 * i + 2]; x[i].w += v[4 * i + 3];
+      dst[i] = x[i];
+      if constexpr (EPI == EPI_F32_RESID_LN) {
+        s1 += (x[i].x + x[i].y) + (x[i].z + x[i].w);
+        s2 += (x[i].x * x[i].x + x[i].y * x[i].y) + (x[i].z * x[i].z + x[i].w * x[i].w);
+      }
     }
   } else if constexpr (EPI == EPI_EMBED_COARSE) {
+    if (row >= m_store) return;
     const float4* pe4 = reinterpret_cast<const float4*>(p.pe + (size_t)(row % p.pe_rows) * p.N + col0);
     float4* d1 = reinterpret_cast<float4*>(p.out_f32 + (size_t)row * p.ld_out + col0);
     float4* d2 = reinterpret_cast<float4*>(p.out2_f32 + (size_t)row * p.ld_out + col0);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      float4 e = __ldg(pe4 + i);
-      float4 o = make_float4(v[4 * i] + e.x, v[4 * i + 1] + e.y, v[4 * i + 2] + e.z, v[4 * i + 3] + e.w);
+      const float4 e = __ldg(pe4 + i);
+      const float4 o = make_float4(v[4 * i] + e.x, v[4 * i + 1] + e.y, v[4 * i + 2] + e.z, v[4 * i + 3] + e.w);
       d1[i] = o;
       d2[i] = o;
     }
   } else if constexpr (EPI == EPI_EMBED_FINE) {
+    if (row >= m_store) return;
     const int orow = __ldg(p.frow + row);
     const int prow = __ldg(p.fidx + row);
     const float4* pe4 = reinterpret_cast<const float4*>(p.pe + (size_t)prow * p.N + col0);
     float4* d1 = reinterpret_cast<float4*>(p.out_f32 + (size_t)orow * p.ld_out + col0);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      float4 e = __ldg(pe4 + i);
+      const float4 e = __ldg(pe4 + i);
       d1[i] = make_float4(v[4 * i] + e.x, v[4 * i + 1] + e.y, v[4 * i + 2] + e.z, v[4 * i + 3] + e.w);
     }
   }
 }
 
-// Residual + LayerNorm epilogue: the tile spans the whole row (BN == N); each row is
-// split between two warps (halves of the columns) which exchange (sum, sum of squares)
-// through shared memory.  Pass 1: x += acc + bias (stored), row statistics.  Pass 2:
-// re-read the new x (L2) and write bf16 LN(x) = (x - mean) * rstd * g + b.  Rows in
-// [M, tile end) only get zeros in ln_out (pad rows for the next attention).
-template <int CH>
-__device__ __forceinline__ void resid_ln_epilogue(const GemmParams& p, uint32_t tbase, int row, int col_base, int M,
-                                                  int quarter, int half, int lane, float2* stats,
-                                                  uint64_t* tempty_bar) {
-  const bool live = row < M;
-  float s1 = 0.f, s2 = 0.f;
-#pragma unroll 1
-  for (int c = 0; c < CH; c += 2) {
-    uint32_t r0[32], r1[32];
-    tmem_ld32(tbase + c * 32, r0);
-    if (c + 1 < CH) tmem_ld32(tbase + (c + 1) * 32, r1);
-    tmem_wait_ld();
-    if (c + 2 >= CH) {
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_bar);
-    }
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      if (c + q >= CH) break;
-      const uint32_t* r = q ? r1 : r0;
-      const int col0 = col_base + (c + q) * 32;
-      if (live) {
-        const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);
-        float4* dst = reinterpret_cast<float4*>(p.out_f32 + (size_t)row * p.ld_out + col0);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float4 b = __ldg(b4 + i);
-          float4 o = dst[i];
-          o.x += __uint_as_float(r[4 * i + 0]) + b.x;
-          o.y += __uint_as_float(r[4 * i + 1]) + b.y;
-          o.z += __uint_as_float(r[4 * i + 2]) + b.z;
-          o.w += __uint_as_float(r[4 * i + 3]) + b.w;
-          dst[i] = o;
-          s1 += (o.x + o.y) + (o.z + o.w);
-          s2 += (o.x * o.x + o.y * o.y) + (o.z * o.z + o.w * o.w);
-        }
-      }
-    }
-  }
-  const int r_in_tile = quarter * 32 + lane;
-  stats[half * 128 + r_in_tile] = make_float2(s1, s2);
-  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");  // the two warps of this quarter
-  const float2 o = stats[(half ^ 1) * 128 + r_in_tile];
-  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");  // stats slot reusable
-  const float inv_n = 1.f / (float)p.N;
-  const float mean = (s1 + o.x) * inv_n;
-  const float var = fmaxf((s2 + o.y) * inv_n - mean * mean, 0.f);
-  const float rstd = rsqrtf(var + p.ln_eps);
-  if (row >= p.ln_cap) return;
-#pragma unroll 1
-  for (int c = 0; c < CH; ++c) {
-    const int col0 = col_base + c * 32;
-    uint4* hd = reinterpret_cast<uint4*>(p.ln_out + (size_t)row * p.N + col0);
-    if (!live) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) hd[i] = make_uint4(0, 0, 0, 0);
-      continue;
-    }
-    const float4* xs = reinterpret_cast<const float4*>(p.out_f32 + (size_t)row * p.ld_out + col0);
-    const float4* g4 = reinterpret_cast<const float4*>(p.ln_g + col0);
-    const float4* be4 = reinterpret_cast<const float4*>(p.ln_b + col0);
-    uint32_t pk[16];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float4 x = xs[i], g = __ldg(g4 + i), be = __ldg(be4 + i);
-      pk[2 * i] = pack_bf16x2((x.x - mean) * rstd * g.x + be.x, (x.y - mean) * rstd * g.y + be.y);
-      pk[2 * i + 1] = pack_bf16x2((x.z - mean) * rstd * g.z + be.z, (x.w - mean) * rstd * g.w + be.w);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) hd[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-  }
-}
-
-template <int BN, int STAGES, int EPI>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+template <int BN, int STAGES, int EPI, int EW, int NACC>
+__global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmParams p) {
-  using S = GemmSmem<BN, STAGES>;
+  static_assert((EW == 8 && NACC == 2) || (EW == 4 && NACC == 1), "supported epilogue configurations");
+  using S = GemmSmem<BN, STAGES, NACC>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -261,6 +195,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float2* ln_stats = reinterpret_cast<float2*>(smem + STAGES * S::STAGE_BYTES + 128);  // [2][128]
+  float* par = reinterpret_cast<float*>(smem + STAGES * S::STAGE_BYTES + S::BAR_BYTES);
+  float* bias_s = par;                       // [N]
+  float* lng_s = par + GEMM_MAX_N;           // [N] (RESID_LN)
+  float* lnb_s = lng_s + GEMM_MAX_LN;        // [N] (RESID_LN)
 
   const int warp = warp_id(), lane = lane_id();
   const int M = p.m_dev ? __ldg(p.m_dev) : p.M;
@@ -278,7 +216,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], GEMM_EPI_WARPS); }
+    for (int a = 0; a < NACC; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], EW); }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<S::TMEM_COLS>(tmem_slot);
@@ -328,29 +266,78 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         mma_commit(&tfull[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else {
     const int quarter = warp & 3;              // TMEM lane quarter this warp may access
-    const int half = (warp - 2) >> 2;          // which half of the tile's columns
-    constexpr int CH = BN / 64;                // 32-column chunks per epilogue warp
-    const int row_in_tile = quarter * 32 + lane;
+    const int half = (EW == 8) ? (warp - 2) >> 2 : 0;  // which column half (EW=8) of the tile
+    constexpr int CH = BN / (32 * (EW / 4));            // 32-column chunks per epilogue warp
+    constexpr int WCOLS = BN / (EW / 4);                // columns per epilogue warp
+    const int et = threadIdx.x - 64;                    // index among the epilogue threads
+    for (int i = et; i < p.N; i += 32 * EW) bias_s[i] = __ldg(p.bias + i);
+    if constexpr (EPI == EPI_F32_RESID_LN)
+      for (int i = et; i < p.N; i += 32 * EW) { lng_s[i] = __ldg(p.ln_g + i); lnb_s[i] = __ldg(p.ln_b + i); }
+    asm volatile("bar.sync 5, %0;" ::"n"(32 * EW) : "memory");  // epilogue warps only
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       const int m_blk = tile / n_tiles, n_blk = tile % n_tiles;
+      const int row0 = m_blk * GEMM_BM + quarter * 32;
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + half * WCOLS;
+      const int col_base = n_blk * BN + half * WCOLS;
+      float s1 = 0.f, s2 = 0.f;  // RESID_LN row statistics (lane = row)
+      if constexpr (EPI == EPI_F32_RESID || EPI == EPI_F32_RESID_LN) {
+        // Residual epilogue, software-pipelined over the 32-column chunks: the residual
+        // row segment of chunk c+1 is loaded while chunk c is added and stored, and chunk
+        // 0's is requested before the accumulator is even ready.
+        const int row = row0 + lane;
+        const bool live = row < M;
+        float* xrow = p.out_f32 + (size_t)row * p.ld_out + col_base;
+        float4 xn[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xn[i] = live ? reinterpret_cast<const float4*>(xrow)[i] : make_float4(0, 0, 0, 0);
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < CH; ++c) {
+          float4 xc[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xc[i] = xn[i];
+          if (c + 1 < CH && live) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xn[i] = reinterpret_cast<const float4*>(xrow + (c + 1) * 32)[i];
+          }
+          uint32_t r[32];
+          tmem_ld32(tbase + c * 32, r);
+          tmem_wait_ld();
+          if (c + 1 == CH) {  // last TMEM read of this accumulator: release it early
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          if (live) {
+            const int col0 = col_base + c * 32;
+            float4* dst = reinterpret_cast<float4*>(xrow + c * 32);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + 4 * i);
+              float4 x = xc[i];
+              x.x += __uint_as_float(r[4 * i + 0]) + bb.x;
+              x.y += __uint_as_float(r[4 * i + 1]) + bb.y;
+              x.z += __uint_as_float(r[4 * i + 2]) + bb.z;
+              x.w += __uint_as_float(r[4 * i + 3]) + bb.w;
+              dst[i] = x;
+              if constexpr (EPI == EPI_F32_RESID_LN) {
+                s1 += (x.x + x.y) + (x.z + x.w);
+                s2 += (x.x * x.x + x.y * x.y) + (x.z * x.z + x.w * x.w);
+              }
+            }
+          }
+        }
+      } else {
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = m_blk * GEMM_BM + row_in_tile;
-      const bool ok = row < m_store;
-      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + half * (BN / 2);
-      const int col_base = n_blk * BN + half * (BN / 2);
-      if constexpr (EPI == EPI_F32_RESID_LN) {
-        resid_ln_epilogue<CH>(p, tbase, row, col_base, M, quarter, half, lane, ln_stats, &tempty[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        continue;
-      }
 #pragma unroll 1
       for (int c = 0; c < CH; c += 2) {
         uint32_t r0[32], r1[32];
@@ -362,10 +349,77 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        gemm_epilogue_chunk<EPI>(p, row, col_base + c * 32, r0, ok);
-        if (c + 1 < CH) gemm_epilogue_chunk<EPI>(p, row, col_base + (c + 1) * 32, r1, ok);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (c + q >= CH) break;
+          const uint32_t* r = q ? r1 : r0;
+          const int col0 = col_base + (c + q) * 32;
+          const int row = row0 + lane;
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + j);  // smem broadcast
+            v[j] = __uint_as_float(r[j]) + bb.x;
+            v[j + 1] = __uint_as_float(r[j + 1]) + bb.y;
+            v[j + 2] = __uint_as_float(r[j + 2]) + bb.z;
+            v[j + 3] = __uint_as_float(r[j + 3]) + bb.w;
+          }
+          direct_chunk<EPI>(p, v, row, col0, m_store, M, s1, s2);
+        }
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+      if constexpr (EPI == EPI_F32_RESID_LN) {
+        // row statistics; with EW=8 the two warps sharing these rows exchange halves
+        float2 o = make_float2(0.f, 0.f);
+        if constexpr (EW == 8) {
+          const int r_in_tile = quarter * 32 + lane;
+          ln_stats[half * 128 + r_in_tile] = make_float2(s1, s2);
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+          o = ln_stats[(half ^ 1) * 128 + r_in_tile];
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+        }
+        const float inv_n = 1.f / (float)p.N;
+        const float mean = (s1 + o.x) * inv_n;
+        const float rstd = rsqrtf(fmaxf((s2 + o.y) * inv_n - mean * mean, 0.f) + p.ln_eps);
+        // LN(x) -> bf16 from the x just written (same thread, row = lane)
+        const int row = row0 + lane;
+        if (row < p.ln_cap) {
+          const bool live = row < M;
+          const float4* xrow = reinterpret_cast<const float4*>(p.out_f32 + (size_t)row * p.ld_out + col_base);
+          float4 xn[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xn[i] = live ? xrow[i] : make_float4(0, 0, 0, 0);
+#pragma unroll 1
+          for (int c = 0; c < CH; ++c) {
+            const int col0 = col_base + c * 32;
+            uint4* hd = reinterpret_cast<uint4*>(p.ln_out + (size_t)row * p.N + col0);
+            if (!live) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) hd[i] = make_uint4(0, 0, 0, 0);
+              continue;
+            }
+            float4 xc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xc[i] = xn[i];
+            if (c + 1 < CH) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) xn[i] = xrow[(c + 1) * 8 + i];
+            }
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 x = xc[i];
+              const float4 g = *reinterpret_cast<const float4*>(lng_s + col0 + 4 * i);
+              const float4 be = *reinterpret_cast<const float4*>(lnb_s + col0 + 4 * i);
+              pk[2 * i] = pack_bf16x2((x.x - mean) * rstd * g.x + be.x, (x.y - mean) * rstd * g.y + be.y);
+              pk[2 * i + 1] = pack_bf16x2((x.z - mean) * rstd * g.z + be.z, (x.w - mean) * rstd * g.w + be.w);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) hd[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          }
+        }
+      }
+      if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
     }
   }
   tc_fence_before();

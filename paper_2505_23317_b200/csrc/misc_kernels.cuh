@@ -323,3 +323,68 @@ __global__ void coarse_meta_kernel(int32_t* cu, int32_t* meta, int B, int Nc) {
 }
 
 }  // namespace cfd
+
+namespace cfd {
+
+// ------------------------------------------------------------------ NEXT f2: A1 hardness gate
+// drop queries with c > c_hi, mean of the rest < tau -> easy (0), else hard (1).
+// One thread per frame; fp64 sequential sum in query order, decision sum < tau*n (reading R22),
+// so the integer result is bit-identical to the oracle's.
+__global__ void hardness_kernel(const float* __restrict__ conf, int B, int Q, float c_hi, float tau,
+                                int32_t* __restrict__ hard) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const float* c = conf + (size_t)b * Q;
+  double s = 0.0;
+  int n = 0;
+  for (int q = 0; q < Q; ++q) {
+    const float v = c[q];
+    if (v <= c_hi) { s += (double)v; ++n; }
+  }
+  hard[b] = (n == 0) ? 0 : (s < (double)tau * (double)n ? 0 : 1);
+}
+
+// ------------------------------------------------------------------ NEXT f1: box-driven region scores
+// regions from the boxes of intermediate-confidence queries (c_lo < c <= c_hi).
+// score[cell] = #(query, pixel) pairs with the pixel in both the box and the coarse cell.  Box
+// (cx, cy, w, h) normalised; pixel rect edges floor((cx - w/2) W) / ceil((cx + w/2) W) computed
+// with explicitly rounded fp32 operations (no FMA contraction) so the integer edges match the
+// oracle exactly (reading R21).  grid = frames, block = 256: rects to smem, then one thread per cell.
+__global__ void box_scores_kernel(const float* __restrict__ boxes, const float* __restrict__ conf, int Q, int H,
+                                  int W, int P, int gc_w, int Nc, float c_lo, float c_hi,
+                                  float* __restrict__ scores) {
+  extern __shared__ int4 rects[];  // [Q]
+  const int b = blockIdx.x;
+  for (int q = threadIdx.x; q < Q; q += blockDim.x) {
+    const float c = conf[(size_t)b * Q + q];
+    const float* bx = boxes + ((size_t)b * Q + q) * 4;
+    int4 r = make_int4(0, 0, 0, 0);
+    if (c > c_lo && c <= c_hi) {
+      const float hw = __fmul_rn(bx[2], 0.5f), hh = __fmul_rn(bx[3], 0.5f);
+      const float xa = __fmul_rn(__fsub_rn(bx[0], hw), (float)W);
+      const float xb = __fmul_rn(__fadd_rn(bx[0], hw), (float)W);
+      const float ya = __fmul_rn(__fsub_rn(bx[1], hh), (float)H);
+      const float yb = __fmul_rn(__fadd_rn(bx[1], hh), (float)H);
+      r.x = min(max((int)floorf(xa), 0), W);
+      r.y = min(max((int)ceilf(xb), 0), W);
+      r.z = min(max((int)floorf(ya), 0), H);
+      r.w = min(max((int)ceilf(yb), 0), H);
+    }
+    rects[q] = r;
+  }
+  __syncthreads();
+  for (int cell = threadIdx.x; cell < Nc; cell += blockDim.x) {
+    const int gy = cell / gc_w, gx = cell % gc_w;
+    const int cx0 = gx * P, cx1 = cx0 + P, cy0 = gy * P, cy1 = cy0 + P;
+    int sum = 0;
+    for (int q = 0; q < Q; ++q) {
+      const int4 r = rects[q];
+      const int ox = max(0, min(r.y, cx1) - max(r.x, cx0));
+      const int oy = max(0, min(r.w, cy1) - max(r.z, cy0));
+      sum += ox * oy;
+    }
+    scores[(size_t)b * Nc + cell] = (float)sum;
+  }
+}
+
+}  // namespace cfd

@@ -1,0 +1,379 @@
+// mlp_tc.cuh — fused encoder MLP block on tcgen05 (reading R4):
+//
+//   x += GELU(h W_1^T + b_1) W_2^T + b_2,     h = LN2(x) (bf16, from the O-projection epilogue)
+//   (+ optionally hn = LN1_next(x) for the next layer, as EPI_F32_RESID_LN does)
+//
+// One persistent CTA per SM walks 128-row tiles.  Per tile the A operand h (128 x d bf16) is
+// loaded once by TMA and the hidden dimension F is processed in 128-column chunks j:
+//   MMA1(j):  acc1[j&1] (TMEM, 128 cols) = h . W1[j]^T            (K = d)
+//   GELU(j):  8 epilogue warps: acc1 + b1 -> polynomial-erf GELU -> bf16 -> shared memory H[j&1]
+//             written directly in the 128B-swizzled K-major layout the tensor core reads
+//   MMA2(j):  acc2 (TMEM, 256 cols) += H[j&1] . W2[:, j]^T          (K = 128)
+// issued as MMA1(j+1) before MMA2(j) so GELU(j) overlaps the tensor core.  The hidden
+// activations never leave the SM.  TMEM: acc1 x2 (256) + acc2 (256) = 512 columns.
+// Weights stream through a ring of 32 KB slots (W1 chunk = 2 slots of two 64-wide k-blocks,
+// W2 chunk = 2 slots of one 256-row k-block) in exactly the order the MMA warp consumes them.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include "ptx.cuh"
+#include "gemm_tc.cuh"
+
+namespace cfd {
+
+struct MlpParams {
+  int M;                 // rows when m_dev == nullptr
+  const int* m_dev;
+  int F;                 // hidden width (multiple of 128, <= GEMM_MAX_N)
+  const float* b1;       // [F]
+  const float* b2;       // [D]
+  float* x;              // residual [*, D] fp32 (in / out)
+  const float* ln_g;     // next LayerNorm (nullptr: none)
+  const float* ln_b;
+  __nv_bfloat16* ln_out; // [ln_cap, D]
+  int ln_cap;
+  float ln_eps;
+};
+
+constexpr int MLP_THREADS = 320;  // TMA warp, MMA warp, 8 epilogue warps
+constexpr int MLP_SLOTS = 2;
+
+template <int D>
+struct MlpSmem {
+  static_assert(D == 256, "fused MLP is laid out for d = 256 (acc2 = 256 TMEM columns)");
+  static constexpr int A_BYTES = 128 * D * 2;             // 64 KB: h tile, D/64 k-blocks of 16 KB
+  static constexpr int H_BYTES = 128 * 128 * 2;           // 32 KB: GELU chunk, 2 k-blocks
+  static constexpr int SLOT_BYTES = 32768;
+  static constexpr int A_OFF = 0;
+  static constexpr int H_OFF = A_OFF + A_BYTES;           // [2]
+  static constexpr int W_OFF = H_OFF + 2 * H_BYTES;       // [MLP_SLOTS]
+  static constexpr int BAR_OFF = W_OFF + MLP_SLOTS * SLOT_BYTES;
+  static constexpr int STATS_OFF = BAR_OFF + 256;         // float2 [2][128]
+  static constexpr int PAR_OFF = STATS_OFF + 2 * 128 * 8; // b1 [F] | b2 [D] | g [D] | b [D]
+  static constexpr int TOTAL = 1024 + PAR_OFF + (GEMM_MAX_N + 3 * D) * 4;
+};
+
+template <int D>
+__global__ void __launch_bounds__(MLP_THREADS, 1)
+    mlp_tc_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW1,
+                  const __grid_constant__ CUtensorMap tmW2, const MlpParams p) {
+  using S = MlpSmem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+  uint64_t* a_full = bars + 0;
+  uint64_t* a_empty = bars + 1;
+  uint64_t* w_full = bars + 2;               // [MLP_SLOTS]
+  uint64_t* w_empty = w_full + MLP_SLOTS;    // [MLP_SLOTS]
+  uint64_t* a1_full = w_empty + MLP_SLOTS;   // [2]
+  uint64_t* a1_empty = a1_full + 2;          // [2]
+  uint64_t* h_full = a1_empty + 2;           // [2]
+  uint64_t* h_empty = h_full + 2;            // [2]
+  uint64_t* a2_full = h_empty + 2;
+  uint64_t* a2_empty = a2_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a2_empty + 1);
+  float2* ln_stats = reinterpret_cast<float2*>(smem + S::STATS_OFF);
+  float* b1_s = reinterpret_cast<float*>(smem + S::PAR_OFF);
+  float* b2_s = b1_s + GEMM_MAX_N;
+  float* lng_s = b2_s + D;
+  float* lnb_s = lng_s + D;
+
+  const int warp = warp_id(), lane = lane_id();
+  const int M = p.m_dev ? __ldg(p.m_dev) : p.M;
+  const bool do_ln = p.ln_g != nullptr;
+  const int m_tiles = ((do_ln ? pad_rows(M, p.ln_cap) : M) + 127) / 128;
+  const int n_chunks = p.F / 128;
+  constexpr int KB = D / 64;  // k-blocks of the h tile
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmH);
+    tma_prefetch(&tmW1);
+    tma_prefetch(&tmW2);
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    for (int i = 0; i < MLP_SLOTS; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&a1_full[i], 1);
+      mbar_init(&a1_empty[i], 8);
+      mbar_init(&h_full[i], 8);
+      mbar_init(&h_empty[i], 1);
+    }
+    mbar_init(a2_full, 1);
+    mbar_init(a2_empty, 8);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t ACC1 = 0, ACC2 = 256;
+
+  if (warp == 0) {
+    // ============================================================ TMA producer
+    if (lane == 0) {
+      int slot = 0;
+      uint32_t sph = 0;
+      int it = 0;
+      auto next_slot = [&](int bytes) -> uint8_t* {
+        mbar_wait(&w_empty[slot], sph ^ 1);
+        mbar_expect_tx(&w_full[slot], bytes);
+        return smem + S::W_OFF + slot * S::SLOT_BYTES;
+      };
+      auto adv = [&]() { if (++slot == MLP_SLOTS) { slot = 0; sph ^= 1; } };
+      auto load_w1 = [&](int j) {  // W1^T rows [128j, 128j+128), k-blocks (0,1) then (2,3)
+        for (int hb = 0; hb < KB / 2; ++hb) {
+          uint8_t* dst = next_slot(2 * 16384);
+          tma_load_2d(dst, &tmW1, &w_full[slot], (2 * hb) * 64, 128 * j);
+          tma_load_2d(dst + 16384, &tmW1, &w_full[slot], (2 * hb + 1) * 64, 128 * j);
+          adv();
+        }
+      };
+      auto load_w2 = [&](int j) {  // W2^T all D rows, k columns [128j, 128j+128) as two k-blocks
+        for (int kb = 0; kb < 2; ++kb) {
+          uint8_t* dst = next_slot(32768);
+          tma_load_2d(dst, &tmW2, &w_full[slot], 128 * j + 64 * kb, 0);
+          adv();
+        }
+      };
+      for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
+        mbar_wait(a_empty, (it & 1) ^ 1);
+        mbar_expect_tx(a_full, S::A_BYTES);
+        for (int kb = 0; kb < KB; ++kb)
+          tma_load_2d(smem + S::A_OFF + kb * 16384, &tmH, a_full, kb * 64, tile * 128);
+        load_w1(0);
+        for (int j = 1; j < n_chunks; ++j) {
+          load_w1(j);
+          load_w2(j - 1);
+        }
+        load_w2(n_chunks - 1);
+      }
+    }
+  } else if (warp == 1) {
+    // ============================================================ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc1 = make_idesc_bf16(128, 128, 0);
+      constexpr uint32_t idesc2 = make_idesc_bf16(128, D, 0);
+      int slot = 0;
+      uint32_t sph = 0;
+      int it = 0;
+      uint32_t a1_cnt[2] = {0, 0}, h_cnt[2] = {0, 0}, a2_cnt = 0;
+      auto take = [&]() -> uint32_t {
+        mbar_wait(&w_full[slot], sph);
+        tc_fence_after();
+        return smem_u32(smem + S::W_OFF + slot * S::SLOT_BYTES);
+      };
+      auto give = [&]() {
+        mma_commit(&w_empty[slot]);
+        if (++slot == MLP_SLOTS) { slot = 0; sph ^= 1; }
+      };
+      const uint32_t a_base = smem_u32(smem + S::A_OFF);
+      auto mma1 = [&](int j) {
+        const int b = j & 1;
+        mbar_wait(&a1_empty[b], (a1_cnt[b] & 1) ^ 1);
+        ++a1_cnt[b];
+        tc_fence_after();
+        for (int hb = 0; hb < KB / 2; ++hb) {
+          const uint32_t w = take();
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int kb = 2 * hb + q;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_ss(tmem + ACC1 + b * 128, make_smem_desc(a_base + kb * 16384 + k * 32, 16, 1024, kLayoutSW128),
+                     make_smem_desc(w + q * 16384 + k * 32, 16, 1024, kLayoutSW128), idesc1, (kb | k) != 0);
+          }
+          give();
+        }
+        mma_commit(&a1_full[b]);
+      };
+      auto mma2 = [&](int j) {
+        const int b = j & 1;
+        mbar_wait(&h_full[b], h_cnt[b] & 1);
+        ++h_cnt[b];
+        if (j == 0) {  // acc2 must have been drained by the previous tile's epilogue
+          mbar_wait(a2_empty, (a2_cnt & 1) ^ 1);
+          ++a2_cnt;
+        }
+        tc_fence_after();
+        const uint32_t h_base = smem_u32(smem + S::H_OFF + b * S::H_BYTES);
+        for (int kb = 0; kb < 2; ++kb) {
+          const uint32_t w = take();
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_ss(tmem + ACC2, make_smem_desc(h_base + kb * 16384 + k * 32, 16, 1024, kLayoutSW128),
+                   make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128), idesc2, (j | kb | k) != 0);
+          give();
+        }
+        mma_commit(&h_empty[b]);
+      };
+      for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
+        mbar_wait(a_full, it & 1);
+        tc_fence_after();
+        mma1(0);
+        if (n_chunks == 1) mma_commit(a_empty);
+        for (int j = 1; j < n_chunks; ++j) {
+          mma1(j);
+          if (j == n_chunks - 1) mma_commit(a_empty);  // h tile no longer read: next tile's TMA may start
+          mma2(j - 1);
+        }
+        mma2(n_chunks - 1);
+        mma_commit(a2_full);
+      }
+    }
+  } else {
+    // ============================================================ epilogue warps (2..9)
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int et = threadIdx.x - 64;
+    for (int i = et; i < p.F; i += 256) b1_s[i] = __ldg(p.b1 + i);
+    for (int i = et; i < D; i += 256) {
+      b2_s[i] = __ldg(p.b2 + i);
+      if (do_ln) { lng_s[i] = __ldg(p.ln_g + i); lnb_s[i] = __ldg(p.ln_b + i); }
+    }
+    asm volatile("bar.sync 5, 256;" ::: "memory");
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    const int r_in_tile = quarter * 32 + lane;
+    uint32_t a1_cnt[2] = {0, 0}, h_cnt[2] = {0, 0};
+    int it = 0;
+    for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
+      const int row = tile * 128 + r_in_tile;
+      // ---- hidden chunks: GELU(acc1 + b1) -> bf16 -> H[j&1] (SW128 K-major, k-block = half)
+      for (int j = 0; j < n_chunks; ++j) {
+        const int b = j & 1;
+        mbar_wait(&a1_full[b], a1_cnt[b] & 1);
+        ++a1_cnt[b];
+        tc_fence_after();
+        uint32_t r0[32], r1[32];
+        const uint32_t ta = tmem + lane_off + ACC1 + b * 128 + half * 64;
+        tmem_ld32(ta, r0);
+        tmem_ld32(ta + 32, r1);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a1_empty[b]);
+        // H[b] may still be read by MMA2(j-2): wait for its commit
+        if (j >= 2) {
+          mbar_wait(&h_empty[b], h_cnt[b] & 1);
+          ++h_cnt[b];
+        }
+        uint8_t* hrow = smem + S::H_OFF + b * S::H_BYTES + half * 16384 + r_in_tile * 128;
+        const int col0 = 128 * j + half * 64;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {  // 16-byte chunk q = columns [8q, 8q+8)
+          const uint32_t* r = (q < 4) ? r0 : r1;
+          const int o = (q & 3) * 8;
+          uint32_t pk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float a = __uint_as_float(r[o + 2 * e]) + b1_s[col0 + 8 * q + 2 * e];
+            float c = __uint_as_float(r[o + 2 * e + 1]) + b1_s[col0 + 8 * q + 2 * e + 1];
+            gelu2(a, c);
+            pk[e] = pack_bf16x2(a, c);
+          }
+          *reinterpret_cast<uint4*>(hrow + ((q ^ (r_in_tile & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+        fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&h_full[b]);
+      }
+      // the last two H buffers' MMA2 commits (consumed so the phase counts stay in step)
+      for (int j = (n_chunks >= 2 ? n_chunks - 2 : 0); j < n_chunks; ++j) {
+        const int b = j & 1;
+        mbar_wait(&h_empty[b], h_cnt[b] & 1);
+        ++h_cnt[b];
+      }
+      // ---- x += acc2 + b2  (+ next LayerNorm)
+      mbar_wait(a2_full, it & 1);
+      tc_fence_after();
+      const bool live = row < M;
+      float* xrow = p.x + (size_t)row * D + half * 128;
+      float s1 = 0.f, s2 = 0.f;
+      float4 xn[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xn[i] = live ? reinterpret_cast<const float4*>(xrow)[i] : make_float4(0, 0, 0, 0);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float4 xc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xc[i] = xn[i];
+        if (c + 1 < 4 && live) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xn[i] = reinterpret_cast<const float4*>(xrow + (c + 1) * 32)[i];
+        }
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_off + ACC2 + half * 128 + c * 32, r);
+        tmem_wait_ld();
+        if (c == 3) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(a2_empty);
+        }
+        if (live) {
+          const int col0 = half * 128 + c * 32;
+          float4* dst = reinterpret_cast<float4*>(xrow + c * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 bb = *reinterpret_cast<const float4*>(b2_s + col0 + 4 * i);
+            float4 x = xc[i];
+            x.x += __uint_as_float(r[4 * i + 0]) + bb.x;
+            x.y += __uint_as_float(r[4 * i + 1]) + bb.y;
+            x.z += __uint_as_float(r[4 * i + 2]) + bb.z;
+            x.w += __uint_as_float(r[4 * i + 3]) + bb.w;
+            dst[i] = x;
+            s1 += (x.x + x.y) + (x.z + x.w);
+            s2 += (x.x * x.x + x.y * x.y) + (x.z * x.z + x.w * x.w);
+          }
+        }
+      }
+      if (do_ln) {
+        ln_stats[half * 128 + r_in_tile] = make_float2(s1, s2);
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+        const float2 o = ln_stats[(half ^ 1) * 128 + r_in_tile];
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+        const float mean = (s1 + o.x) * (1.f / D);
+        const float rstd = rsqrtf(fmaxf((s2 + o.y) * (1.f / D) - mean * mean, 0.f) + p.ln_eps);
+        if (row < p.ln_cap) {
+          const float4* xr = reinterpret_cast<const float4*>(xrow);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xn[i] = live ? xr[i] : make_float4(0, 0, 0, 0);
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            const int col0 = half * 128 + c * 32;
+            uint4* hd = reinterpret_cast<uint4*>(p.ln_out + (size_t)row * D + col0);
+            if (!live) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) hd[i] = make_uint4(0, 0, 0, 0);
+              continue;
+            }
+            float4 xc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xc[i] = xn[i];
+            if (c + 1 < 4) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) xn[i] = xr[(c + 1) * 8 + i];
+            }
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 x = xc[i];
+              const float4 g = *reinterpret_cast<const float4*>(lng_s + col0 + 4 * i);
+              const float4 be = *reinterpret_cast<const float4*>(lnb_s + col0 + 4 * i);
+              pk[2 * i] = pack_bf16x2((x.x - mean) * rstd * g.x + be.x, (x.y - mean) * rstd * g.y + be.y);
+              pk[2 * i + 1] = pack_bf16x2((x.z - mean) * rstd * g.z + be.z, (x.w - mean) * rstd * g.w + be.w);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) hd[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace cfd

@@ -184,3 +184,31 @@ def test_cuda_graph_capture_replays_identically():
     torch.cuda.synchronize()
     n = sum(counts)
     assert torch.equal(ro["y"][:n], ref[:n])
+
+
+def test_fused_mlp_matches_two_gemm_path():
+    """The fused MLP kernel (default) against the MLP1 + MLP2 GEMM launches it replaces
+    (same selection for both runs: near-tie scores may otherwise pick different regions)."""
+    from paper_2505_23317_b200 import _lib as L
+    lib = L.load()
+    cfg = ci.CONFIGS["c640"]
+    enc = enc_for("c640")
+    imgs = bf16_tensor(ci.make_frames(cfg, 3, task0=7), "cuda")
+    ks = [0, 100, 400]
+    co = enc.coarse_encode(imgs)
+    sel = enc.select_regions(co["scores"], k=ks)
+    x0 = co["x0"].clone()
+    outs = []
+    try:
+        for fused in (1, 0):
+            assert lib.cfdx_set_option(2, fused) == 0
+            c2 = enc.coarse_encode(imgs)
+            ro = enc.batch_refine(imgs, x0, sel["sel_idx"], sel["sel_count"])
+            torch.cuda.synchronize()
+            n = int(ro["cu_seqlens"][-1])
+            outs.append((c2["y"].clone(), ro["y"][:n].clone()))
+    finally:
+        lib.cfdx_set_option(2, 1)
+    for a, b in zip(outs[0], outs[1]):
+        rel = ((a - b).norm() / b.norm()).item()
+        assert rel < 3e-3, rel

@@ -321,3 +321,43 @@ def test_bf16_rounding_helper():
     # 1+2^-8 ties to even -> 1.0; 1+1.5*2^-8 rounds up to 1+2^-7
     assert ci.bf16_round(x)[:4].tolist() == [1.0, 1.0, 1.0078125, -2.5]
     assert ci.bf16_round(ci.bf16_round(x)).tolist() == ci.bf16_round(x).tolist()
+
+
+# --------------------------------------------------------------------------- NEXT rows f1 / f2
+def test_hardness_gate_against_vectorised_mean_and_special_cases():
+    rng = _rng(31)
+    for t in range(50):
+        conf = rng.random(128).astype(np.float32) * (0.2 if t % 2 else 1.0)
+        keep = conf[conf <= np.float32(0.8)].astype(np.float64)
+        ref = 0 if keep.size == 0 else int(keep.mean() >= 0.05)
+        if keep.size and abs(keep.mean() - 0.05) < 1e-12:
+            continue
+        assert O.hardness_gate(conf) == ref
+    assert O.hardness_gate(np.full(10, 0.9, np.float32)) == 0          # only critical objects -> easy
+    assert O.hardness_gate(np.array([0.95, 0.3], np.float32)) == 1      # one ambiguous query -> hard
+    assert O.hardness_gate(np.array([0.01, 0.02, 0.9], np.float32)) == 0  # background only -> easy
+
+
+def test_box_cell_scores_against_pixel_mask_rasterisation():
+    cfg = ci.ModelConfig(128, 160, 32, 16, 64, 2, 1, 256, 0)
+    boxes, conf = ci.make_queries(7, 40, hard=True)
+    s = O.box_cell_scores(cfg, boxes, conf)
+    mask_count = np.zeros((cfg.img_h, cfg.img_w), np.int64)
+    for b, c in zip(boxes, conf):
+        if 0.05 < float(c) <= 0.8:
+            x0, x1, y0, y1 = O.box_pixel_rect(b, cfg.img_h, cfg.img_w)
+            m = np.zeros_like(mask_count)
+            m[y0:y1, x0:x1] = 1
+            mask_count += m
+    ref = mask_count.reshape(cfg.gc_h, 32, cfg.gc_w, 32).sum(axis=(1, 3)).reshape(-1)
+    assert np.array_equal(s.astype(np.int64), ref)
+
+
+def test_box_cell_scores_closed_forms():
+    cfg = ci.ModelConfig(128, 128, 32, 16, 64, 2, 1, 256, 0)
+    full = np.array([[0.5, 0.5, 1.0, 1.0]], np.float32)
+    assert (O.box_cell_scores(cfg, full, np.array([0.5], np.float32)) == 32 * 32).all()
+    assert (O.box_cell_scores(cfg, full, np.array([0.9], np.float32)) == 0).all()    # critical: not refined
+    inner = np.array([[40 / 128, 40 / 128, 8 / 128, 8 / 128]], np.float32)           # pixels [36,44)^2 in cell (1,1)
+    s = O.box_cell_scores(cfg, inner, np.array([0.3], np.float32))
+    assert s[1 * 4 + 1] == 64 and s.sum() == 64
