@@ -207,7 +207,8 @@ def algorithmic_bytes(cfg, B, k):
         "select": B * (4 * Nc + 4 * Nc + 4),
         "gather": B * ((Nc - k) * d * 4 * 2 + m2 * k * cfg.k_fine * 2 * 2 + 4 * Nt + m2 * k * 8),
         "im2col": B * cfg.img_h * cfg.img_w * 3 * 2 * 2,
-        "layernorm": cfg.n_layers * 2 * B * (Nc + Nt) * d * (4 + 2),
+        # standalone LN only for layer 0 of each pass; later LN1/LN2 are fused into GEMM epilogues
+        "layernorm": B * (Nc + Nt) * d * (4 + 2),
     }
 
 
@@ -386,46 +387,76 @@ def gpu_arm(args):
     attn_roof = roofline_for("attention")
 
     # ---------------------------------------------------------------- e2e through the public API, host buffers
+    # Serving-style loop: frames arrive in pinned host memory, results return to pinned host
+    # memory.  Two buffer sets: while batch i computes (graph replay on the compute stream),
+    # the copy stream uploads batch i+1 and downloads batch i-1's refined tokens.
     h_imgs = torch.from_numpy(imgs_np.view(np.int16)).pin_memory()
-    d_imgs = torch.empty_like(imgs)
     n_out = sum(counts)
-    h_y = torch.empty(n_out, cfg.d_model, dtype=torch.float32).pin_memory()
-    h_cu = torch.empty(B + 1, dtype=torch.int32).pin_memory()
-    e2e_steps = max(3, min(args.steps, 10))
-    co2, sel2, ro2 = {}, {}, {}
+    copy_s = torch.cuda.Stream(device=dev)
+    sets = []
+    for bset in range(2):
+        d_im = torch.empty_like(imgs)
+        o_co, o_sel, o_ro = {}, {}, {}
+        with torch.cuda.stream(stream):
+            d_im.view(torch.int16).copy_(h_imgs)
+            o_co.update(enc.coarse_encode(d_im, stream=stream))
+            o_sel.update(enc.select_regions(o_co["scores"], k=ks, stream=stream))
+            o_ro.update(enc.batch_refine(d_im, o_co["x0"], o_sel["sel_idx"], o_sel["sel_count"], token_counts=counts,
+                                         stream=stream))
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            with torch.cuda.graph(g, stream=stream):
+                enc.coarse_encode(d_im, out=o_co, stream=stream)
+                enc.select_regions(o_co["scores"], k=ks, out=o_sel, stream=stream)
+                enc.batch_refine(d_im, o_co["x0"], o_sel["sel_idx"], o_sel["sel_count"], token_counts=counts,
+                                 out=o_ro, stream=stream)
+        stream.synchronize()
+        sets.append(dict(img=d_im, ro=o_ro, graph=g,
+                         h_y=torch.empty(n_out, cfg.d_model, dtype=torch.float32).pin_memory(),
+                         h_cu=torch.empty(B + 1, dtype=torch.int32).pin_memory(),
+                         up=torch.cuda.Event(), done=torch.cuda.Event(), down=torch.cuda.Event()))
+    e2e_steps = max(4, min(args.steps, 16))
 
-    def e2e_step(s):
-        d_imgs.view(torch.int16).copy_(h_imgs, non_blocking=True)
-        enc.coarse_encode(d_imgs.view(torch.bfloat16), out=co2 if co2 else None, stream=s)
-        enc.select_regions(co2["scores"], k=ks, out=sel2 if sel2 else None, stream=s)
-        enc.batch_refine(d_imgs.view(torch.bfloat16), co2["x0"], sel2["sel_idx"], sel2["sel_count"],
-                         token_counts=counts, out=ro2 if ro2 else None, stream=s)
-        h_y.copy_(ro2["y"][:n_out], non_blocking=True)
-        h_cu.copy_(ro2["cu_seqlens"], non_blocking=True)
+    def e2e_run(n_steps):
+        with torch.cuda.stream(copy_s):
+            sets[0]["img"].view(torch.int16).copy_(h_imgs, non_blocking=True)
+            sets[0]["up"].record(copy_s)
+        for i in range(n_steps):
+            cur, nxt = sets[i % 2], sets[(i + 1) % 2]
+            stream.wait_event(cur["up"])
+            if i >= 2:
+                stream.wait_event(cur["down"])       # results of step i-2 read out of this set
+            cur["graph"].replay()
+            cur["done"].record(stream)
+            with torch.cuda.stream(copy_s):
+                if i + 1 < n_steps:
+                    if i >= 1:
+                        copy_s.wait_event(nxt["done"])  # step i-1 finished with the other set
+                    nxt["img"].view(torch.int16).copy_(h_imgs, non_blocking=True)
+                    nxt["up"].record(copy_s)
+                copy_s.wait_event(cur["done"])
+                cur["h_y"].copy_(cur["ro"]["y"][:n_out], non_blocking=True)
+                cur["h_cu"].copy_(cur["ro"]["cu_seqlens"], non_blocking=True)
+                cur["down"].record(copy_s)
 
-    with torch.cuda.stream(stream):
-        d_imgs.view(torch.int16).copy_(h_imgs)
-        co2.update(enc.coarse_encode(d_imgs, stream=stream))
-        sel2.update(enc.select_regions(co2["scores"], k=ks, stream=stream))
-        ro2.update(enc.batch_refine(d_imgs, co2["x0"], sel2["sel_idx"], sel2["sel_count"], token_counts=counts,
-                                    stream=stream))
-        e2e_step(stream)
-    stream.synchronize()
+    e2e_run(2)
+    torch.cuda.synchronize()
     e_s = torch.cuda.Event(enable_timing=True)
     e_e = torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
-    with torch.cuda.stream(stream):
-        e_s.record(stream)
-        for _ in range(e2e_steps):
-            e2e_step(stream)
-        e_e.record(stream)
-    stream.synchronize()
+    e_s.record(stream)
+    e2e_run(e2e_steps)
+    copy_s.wait_stream(stream)
+    e_e.record(copy_s)
+    torch.cuda.synchronize()
     e2e_ms = shard.max_over_ranks(e_s.elapsed_time(e_e), dev)
     e2e_val = B * world * e2e_steps / (e2e_ms / 1e3)
     e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h_imgs.numel() * 2),
-           "d2h_bytes_per_step": int(h_y.numel() * 4 + h_cu.numel() * 4),
-           "note": "pinned host frames -> device, full step (eager launches), packed refined tokens -> host"}
+           "d2h_bytes_per_step": int(sets[0]["h_y"].numel() * 4 + sets[0]["h_cu"].numel() * 4),
+           "note": "pinned host frames -> device and packed refined tokens -> host every step, copies on a "
+                   "second stream overlapped with the previous/next batch's compute (graph replay)"}
 
     # ---------------------------------------------------------------- NCCL gather of outputs for checking
     check = None

@@ -23,6 +23,14 @@ extern "C" {
 cfd_status cfdx_gemm(int32_t M, int32_t N, int32_t K, const uint16_t *A, const uint16_t *W, const float *bias,
                      int32_t epi, uint16_t *out_bf16, float *out_f32, void *stream);
 
+/* Residual + LayerNorm epilogue GEMM (EPI_F32_RESID_LN; N must be a single column tile,
+ * N in {64, 128, 256}):  x[M,N] += A . W^T + bias;  ln_out[r] = bf16(LN(x[r]) * g + b) for
+ * r < M and 0 for M <= r < ln_cap (pad rows).  staged = 1 selects the TMA-staged
+ * epilogue (1 CTA/SM), 0 the direct-store one (2 CTAs/SM). */
+cfd_status cfdx_gemm_resid_ln(int32_t M, int32_t N, int32_t K, const uint16_t *A, const uint16_t *W,
+                              const float *bias, float *x, const float *ln_g, const float *ln_b, float eps,
+                              uint16_t *ln_out, int32_t ln_cap, int32_t staged, void *stream);
+
 /* Varlen multi-head attention over packed qkv [rows, 3d] (q | k | v) with
  * cu_seqlens [T+1]; writes O [rows, d] bf16 and, if lse != NULL, the natural-log
  * row log-sum-exp [nh, lse_ld].  rows_cap = rows allocated in qkv. */
@@ -60,7 +68,8 @@ int32_t cfdx_probe_count(int32_t kind);
  * per CTA, 2: persistent two-tile ping-pong with 128-key steps, 3: same with 64-key
  * steps and double-buffered S, 4: three query tiles / warpgroups per CTA); key 1 = how many of every 16
  * column pairs variant 2 exponentiates with the FMA-pipe polynomial instead of MUFU
- * (0, 2, 4, 6 or 8; default 4); key 2 = fused MLP kernel on (1, default) / off (0). */
+ * (0, 2, 4, 6 or 8; default 4); key 2 = fused MLP kernel on (1, default) / off (0); key 3 = TMA-staged
+ * residual + LayerNorm epilogue of the O-projection on (1, default) / off (0). */
 cfd_status cfdx_set_option(int32_t key, int32_t value);
 
 /* Number of kernels the library launched since load (host counter; for bench's

@@ -24,7 +24,7 @@ STATUS = {0: "CFD_OK", -1: "CFD_E_ARG", -2: "CFD_E_SHAPE", -3: "CFD_E_UNSUPPORTE
 PUBLIC_SYMBOLS = ["cfd_create", "cfd_destroy", "cfd_query", "cfd_coarse_encode", "cfd_select_regions",
                   "cfd_refine_encode", "cfd_batch_refine", "cfd_check", "cfd_status_str", "cfd_version",
                   "cfd_hardness", "cfd_box_scores"]
-DEBUG_SYMBOLS = ["cfdx_gemm", "cfdx_attention", "cfdx_layernorm", "cfdx_score", "cfdx_gather",
+DEBUG_SYMBOLS = ["cfdx_gemm", "cfdx_gemm_resid_ln", "cfdx_attention", "cfdx_layernorm", "cfdx_score", "cfdx_gather",
                  "cfdx_launch_count", "cfdx_probe_install", "cfdx_probe_count", "cfdx_set_option"]
 PROBE_KINDS = {"attention": 0, "score": 1, "gemm_qkv": 2, "gemm_oproj": 3, "gemm_mlp1": 4, "gemm_mlp2": 5,
                "gemm_embed_c": 6, "gemm_embed_f": 7, "layernorm": 8, "select": 9, "gather": 10, "im2col": 11,
@@ -79,6 +79,7 @@ def load() -> C.CDLL:
         "cfd_status_str": [I32],
         "cfd_version": [],
         "cfdx_gemm": [I32, I32, I32, P, P, P, I32, P, P, P],
+        "cfdx_gemm_resid_ln": [I32, I32, I32, P, P, P, P, P, P, F32, P, I32, I32, P],
         "cfdx_attention": [I32, P, I32, I32, I32, I32, P, P, P, I32, P],
         "cfdx_layernorm": [I32, I32, P, P, P, F32, P, P],
         "cfdx_score": [I32, I32, I32, I32, P, I32, P, I32, P, P],

@@ -85,14 +85,15 @@ PFN_encodeTiled get_encode_fn() {
 // 2-D bf16 tensor map: inner dim `inner` elements (contiguous), `outer` rows with
 // row stride `ld` elements, box {box_inner, box_outer}.
 bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
-               uint32_t box_outer, CUtensorMapSwizzle sw) {
+               uint32_t box_outer, CUtensorMapSwizzle sw, bool fp32 = false) {
   PFN_encodeTiled enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * 2};
+  cuuint64_t strides[1] = {ld * (fp32 ? 4 : 2)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+  CUresult r = enc(m, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(base), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -115,16 +116,18 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 template <int BN>
 constexpr int gemm_stages() { return BN == 256 ? 4 : BN == 128 ? 6 : 8; }
 
-// mode 0: 1 CTA/SM, 8 epilogue warps, double-buffered accumulator (many tiles)
+// mode 0: 1 CTA/SM, 8 epilogue warps, double-buffered accumulator (many tiles);
+//         for EPI_F32_RESID_LN a 2-stage ring and the TMA-staged residual epilogue
 // mode 1: 2 CTAs/SM, 4 epilogue warps, single accumulator, 2-stage ring (N = d GEMMs)
 template <int BN, int EPI, int MODE>
 cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows_for_grid,
-                          cudaStream_t s) {
+                          cudaStream_t s, const CUtensorMap* tx, const CUtensorMap* tln) {
+  constexpr bool kTmaEpi = (EPI == EPI_F32_RESID_LN && MODE == 0);
   constexpr int EW = MODE ? 4 : 8;
   constexpr int NACC = MODE ? 1 : 2;
-  constexpr int ST = MODE ? 2 : gemm_stages<BN>();
+  constexpr int ST = (MODE || kTmaEpi) ? 2 : gemm_stages<BN>();
   auto kern = gemm_tc_kernel<BN, ST, EPI, EW, NACC>;
-  constexpr int smem = GemmSmem<BN, ST, NACC>::TOTAL;
+  constexpr int smem = kTmaEpi ? GemmSmem<BN, ST, NACC>::TOTAL_TMA_EPI : GemmSmem<BN, ST, NACC>::TOTAL;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -134,41 +137,42 @@ cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
   const int tiles = ((rows_for_grid + GEMM_BM - 1) / GEMM_BM) * (p.N / BN);
   const int slots = num_sms() * (MODE ? 2 : 1);
   const int grid = tiles < slots ? (tiles > 0 ? tiles : 1) : slots;
-  kern<<<grid, 64 + 32 * EW, smem, s>>>(ta, tb, p);
+  kern<<<grid, 64 + 32 * EW, smem, s>>>(ta, tb, p, tx ? *tx : ta, tln ? *tln : ta);
   ++g_launches;
   return cudaGetLastError();
 }
 
 template <int EPI>
 cudaError_t launch_gemm_bn(int BN, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows,
-                           cudaStream_t s) {
-  // N = BN: a single column tile per row block -> the 2-CTA/SM configuration
-  if (p.N == BN) {
+                           cudaStream_t s, const CUtensorMap* tx, const CUtensorMap* tln) {
+  // N = BN: a single column tile per row block -> the 2-CTA/SM configuration, except the
+  // residual+LN epilogue with staging maps, which runs 1 CTA/SM with TMA-staged I/O
+  if (p.N == BN && !(EPI == EPI_F32_RESID_LN && tx && tln)) {
     switch (BN) {
-      case 256: return launch_gemm_t<256, EPI, 1>(ta, tb, p, rows, s);
-      case 128: return launch_gemm_t<128, EPI, 1>(ta, tb, p, rows, s);
-      default: return launch_gemm_t<64, EPI, 1>(ta, tb, p, rows, s);
+      case 256: return launch_gemm_t<256, EPI, 1>(ta, tb, p, rows, s, tx, tln);
+      case 128: return launch_gemm_t<128, EPI, 1>(ta, tb, p, rows, s, tx, tln);
+      default: return launch_gemm_t<64, EPI, 1>(ta, tb, p, rows, s, tx, tln);
     }
   }
   switch (BN) {
-    case 256: return launch_gemm_t<256, EPI, 0>(ta, tb, p, rows, s);
-    case 128: return launch_gemm_t<128, EPI, 0>(ta, tb, p, rows, s);
-    default: return launch_gemm_t<64, EPI, 0>(ta, tb, p, rows, s);
+    case 256: return launch_gemm_t<256, EPI, 0>(ta, tb, p, rows, s, tx, tln);
+    case 128: return launch_gemm_t<128, EPI, 0>(ta, tb, p, rows, s, tx, tln);
+    default: return launch_gemm_t<64, EPI, 0>(ta, tb, p, rows, s, tx, tln);
   }
 }
 
 int pick_bn(int N) { return (N % 256 == 0) ? 256 : (N % 128 == 0) ? 128 : 64; }
 
 cudaError_t launch_gemm_impl(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows,
-                             cudaStream_t s) {
+                             cudaStream_t s, const CUtensorMap* tx, const CUtensorMap* tln) {
   const int BN = pick_bn(p.N);
   switch (epi) {
-    case EPI_BF16_BIAS: return launch_gemm_bn<EPI_BF16_BIAS>(BN, ta, tb, p, rows, s);
-    case EPI_BF16_BIAS_GELU: return launch_gemm_bn<EPI_BF16_BIAS_GELU>(BN, ta, tb, p, rows, s);
-    case EPI_F32_RESID: return launch_gemm_bn<EPI_F32_RESID>(BN, ta, tb, p, rows, s);
-    case EPI_EMBED_COARSE: return launch_gemm_bn<EPI_EMBED_COARSE>(BN, ta, tb, p, rows, s);
-    case EPI_F32_RESID_LN: return launch_gemm_bn<EPI_F32_RESID_LN>(BN, ta, tb, p, rows, s);
-    default: return launch_gemm_bn<EPI_EMBED_FINE>(BN, ta, tb, p, rows, s);
+    case EPI_BF16_BIAS: return launch_gemm_bn<EPI_BF16_BIAS>(BN, ta, tb, p, rows, s, nullptr, nullptr);
+    case EPI_BF16_BIAS_GELU: return launch_gemm_bn<EPI_BF16_BIAS_GELU>(BN, ta, tb, p, rows, s, nullptr, nullptr);
+    case EPI_F32_RESID: return launch_gemm_bn<EPI_F32_RESID>(BN, ta, tb, p, rows, s, nullptr, nullptr);
+    case EPI_EMBED_COARSE: return launch_gemm_bn<EPI_EMBED_COARSE>(BN, ta, tb, p, rows, s, nullptr, nullptr);
+    case EPI_F32_RESID_LN: return launch_gemm_bn<EPI_F32_RESID_LN>(BN, ta, tb, p, rows, s, tx, tln);
+    default: return launch_gemm_bn<EPI_EMBED_FINE>(BN, ta, tb, p, rows, s, nullptr, nullptr);
   }
 }
 
@@ -177,9 +181,10 @@ enum : int { PK_ATTN = 0, PK_SCORE = 1, PK_QKV = 2, PK_OPROJ = 3, PK_MLP1 = 4, P
              PK_EMBED_F = 7, PK_LN = 8, PK_SELECT = 9, PK_GATHER = 10, PK_IM2COL = 11, PK_META = 12 };
 
 cudaError_t launch_gemm(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows,
-                        cudaStream_t s, int kind = -1) {
+                        cudaStream_t s, int kind = -1, const CUtensorMap* tx = nullptr,
+                        const CUtensorMap* tln = nullptr) {
   probe_begin(kind, s);
-  cudaError_t e = launch_gemm_impl(epi, ta, tb, p, rows, s);
+  cudaError_t e = launch_gemm_impl(epi, ta, tb, p, rows, s, tx, tln);
   probe_end(kind, s);
   return e;
 }
@@ -200,6 +205,7 @@ bool make_qkvmap(CUtensorMap* m, const void* qkv, int rows, int d) {
 int g_attn_variant = 4;
 int g_attn_npp = 4;
 int g_fused_mlp = 1;  // fused MLP kernel (d == 256) instead of two GEMM launches
+int g_staged_epi = 1; // TMA-staged residual + LayerNorm epilogue for the O-projection
 
 cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUtensorMap& tw2, const MlpParams& p,
                        int rows_for_grid, cudaStream_t s) {
@@ -420,7 +426,12 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   p.M = M_static; p.m_dev = m_dev; p.m_cap = x_cap; p.N = d; p.K = d; p.bias = L.b_o; p.out_f32 = x; p.ld_out = d;
   if (fuse_ln) {
     p.ln_g = L.ln2_g; p.ln_b = L.ln2_b; p.ln_out = w.hbuf; p.ln_cap = w.rows_cap; p.ln_eps = g.ln_eps;
-    CFD_CUDA(launch_gemm(EPI_F32_RESID_LN, ta_o, L.tm_o, p, rows_grid, s, PK_OPROJ));
+    CUtensorMap tx, tln;  // staging maps: fp32 x [x_cap, d] and bf16 LN out, 32 x 32 boxes
+    const bool staged = g_staged_epi && (d % 64 == 0) &&
+                        make_tmap(&tx, x, d, x_cap, d, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, true) &&
+                        make_tmap(&tln, w.hbuf, d, w.rows_cap, d, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    CFD_CUDA(launch_gemm(EPI_F32_RESID_LN, ta_o, L.tm_o, p, rows_grid, s, PK_OPROJ, staged ? &tx : nullptr,
+                         staged ? &tln : nullptr));
   } else {
     CFD_CUDA(launch_gemm(EPI_F32_RESID, ta_o, L.tm_o, p, rows_grid, s, PK_OPROJ));
     CFD_CUDA(launch_layernorm(d, x, L.ln2_g, L.ln2_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
@@ -520,6 +531,9 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
       return CFD_OK;
     case 2:
       g_fused_mlp = value ? 1 : 0;
+      return CFD_OK;
+    case 3:
+      g_staged_epi = value ? 1 : 0;
       return CFD_OK;
   }
   return CFD_E_ARG;
@@ -838,6 +852,25 @@ cfd_status cfdx_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const u
   p.M = M; p.m_cap = M; p.N = N; p.K = K; p.bias = bias; p.out_bf16 = (__nv_bfloat16*)out_bf16; p.out_f32 = out_f32;
   p.ld_out = N;
   CFD_CUDA(launch_gemm(epi, ta, tb, p, M, static_cast<cudaStream_t>(stream)));
+  return CFD_OK;
+}
+
+cfd_status cfdx_gemm_resid_ln(int32_t M, int32_t N, int32_t K, const uint16_t* A, const uint16_t* W,
+                              const float* bias, float* x, const float* ln_g, const float* ln_b, float eps,
+                              uint16_t* ln_out, int32_t ln_cap, int32_t staged, void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || N % 64 || K % 64 || N > GEMM_MAX_LN || !A || !W || !bias || !x || !ln_g ||
+      !ln_b || !ln_out || ln_cap < M || pick_bn(N) != N)
+    return CFD_E_ARG;
+  CUtensorMap ta, tb, tx, tln;
+  if (!make_amap(&ta, A, M, K) || !make_wmap(&tb, W, N, K) ||
+      !make_tmap(&tx, x, N, M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, true) ||
+      !make_tmap(&tln, ln_out, N, ln_cap, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+    return CFD_E_CUDA;
+  GemmParams p{};
+  p.M = M; p.m_cap = M; p.N = N; p.K = K; p.bias = bias; p.out_f32 = x; p.ld_out = N;
+  p.ln_g = ln_g; p.ln_b = ln_b; p.ln_out = (__nv_bfloat16*)ln_out; p.ln_cap = ln_cap; p.ln_eps = eps;
+  CFD_CUDA(launch_gemm(EPI_F32_RESID_LN, ta, tb, p, M, static_cast<cudaStream_t>(stream), -1, staged ? &tx : nullptr,
+                       staged ? &tln : nullptr));
   return CFD_OK;
 }
 

@@ -82,9 +82,13 @@ struct GemmSmem {
   static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr int B_BYTES = BN * GEMM_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_BYTES = 128 + 2 * 128 * 8;  // barriers + RESID_LN row statistics
+  static constexpr int BAR_BYTES = 256 + 2 * 128 * 8;  // barriers + RESID_LN row statistics
   static constexpr int PAR_FLOATS = GEMM_MAX_N + 2 * GEMM_MAX_LN;  // bias | ln gamma | ln beta
-  static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES + PAR_FLOATS * 4;
+  static constexpr int PAR_BYTES = ((PAR_FLOATS * 4 + 1023) / 1024) * 1024;
+  static constexpr int STG_BYTES = 12288;  // per epilogue warp: x chunks [2] 4 KB + LN chunks [2] 2 KB
+  static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES + PAR_BYTES;
+  static constexpr int STG_OFF = STAGES * STAGE_BYTES + ((BAR_BYTES + PAR_BYTES + 1023) / 1024) * 1024;
+  static constexpr int TOTAL_TMA_EPI = 1024 + STG_OFF + GEMM_EPI_WARPS * STG_BYTES;
   static constexpr uint32_t TMEM_COLS = (NACC * BN <= 32) ? 32 : (NACC * BN <= 64) ? 64 : (NACC * BN <= 128) ? 128
                                         : (NACC * BN <= 256) ? 256 : 512;
 };
@@ -179,10 +183,139 @@ __device__ __forceinline__ void direct_chunk(const GemmParams& p, float (&v)[32]
   }
 }
 
+// ---------------------------------------------------------------------------- staged residual + LN
+// Residual + LayerNorm epilogue of one warp (32 rows x CH 32-column chunks of a row half)
+// through shared memory with TMA: x chunks [32 rows x 32 fp32] are TMA-loaded into a
+// 128B-swizzled buffer, each thread reads / writes its row with conflict-free 16-byte
+// accesses, and the results leave by TMA store, so no per-row global access is issued.
+//   pass A: x_old + acc + bias -> row statistics (the two column-half warps exchange)
+//   pass B: reload x_old, x_new = x_old + acc + bias -> x (TMA store) and LN(x_new) -> bf16
+//           (SW64 buffer, TMA store).  Rows >= M keep x and get zeros in ln_out.
+// The accumulator stays in TMEM until pass B's last read.
+template <int CH>
+__device__ __forceinline__ void resid_ln_tma(const GemmParams& p, const CUtensorMap& tmX, const CUtensorMap& tmLN,
+                                             uint8_t* stg, uint64_t* bar, uint32_t& xph, uint32_t tbase, int row0,
+                                             int col_base, int M, const float* bias_s, const float* lng_s,
+                                             const float* lnb_s, float2* stats, int quarter, int half, int lane,
+                                             uint64_t* tfull_bar, uint32_t tfull_parity, uint64_t* tempty_bar) {
+  uint8_t* xb[2] = {stg, stg + 4096};
+  uint8_t* hb[2] = {stg + 8192, stg + 10240};
+  const int r = lane;
+  const bool live = row0 + r < M;
+  auto load = [&](int c, int b) {
+    if (lane == 0) {
+      mbar_expect_tx(&bar[b], 4096);
+      tma_load_2d(xb[b], &tmX, &bar[b], col_base + c * 32, row0);
+    }
+  };
+  auto wait = [&](int b) {
+    mbar_wait(&bar[b], (xph >> b) & 1);
+    xph ^= 1u << b;
+  };
+  auto row_ptr = [&](int b, int q) { return reinterpret_cast<float4*>(xb[b] + r * 128 + ((q ^ (r & 7)) << 4)); };
+  float s1 = 0.f, s2 = 0.f;
+  // ---- pass A (the first residual chunks are requested before the accumulator is ready)
+  load(0, 0);
+  if (CH > 1) load(1, 1);
+  mbar_wait(tfull_bar, tfull_parity);
+  tc_fence_after();
+#pragma unroll 1
+  for (int c = 0; c < CH; ++c) {
+    const int b = c & 1;
+    uint32_t a[32];
+    tmem_ld32(tbase + c * 32, a);
+    wait(b);
+    tmem_wait_ld();
+    const int col0 = col_base + c * 32;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 x = *row_ptr(b, q);
+      const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + 4 * q);
+      const float v0 = x.x + (__uint_as_float(a[4 * q]) + bb.x), v1 = x.y + (__uint_as_float(a[4 * q + 1]) + bb.y);
+      const float v2 = x.z + (__uint_as_float(a[4 * q + 2]) + bb.z), v3 = x.w + (__uint_as_float(a[4 * q + 3]) + bb.w);
+      s1 += (v0 + v1) + (v2 + v3);
+      s2 += (v0 * v0 + v1 * v1) + (v2 * v2 + v3 * v3);
+    }
+    __syncwarp();
+    if (c + 2 < CH) load(c + 2, b);
+  }
+  // ---- statistics of the full row (two warps, one per column half)
+  const int r_in_tile = quarter * 32 + lane;
+  stats[half * 128 + r_in_tile] = make_float2(s1, s2);
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+  const float2 o = stats[(half ^ 1) * 128 + r_in_tile];
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+  const float inv_n = 1.f / (float)p.N;
+  const float mean = (s1 + o.x) * inv_n;
+  const float rstd = rsqrtf(fmaxf((s2 + o.y) * inv_n - mean * mean, 0.f) + p.ln_eps);
+  // ---- pass B
+  load(0, 0);
+  if (CH > 1) load(1, 1);
+#pragma unroll 1
+  for (int c = 0; c < CH; ++c) {
+    const int b = c & 1;
+    uint32_t a[32];
+    tmem_ld32(tbase + c * 32, a);
+    wait(b);
+    tmem_wait_ld();
+    if (c + 1 == CH) {  // accumulator fully read: hand TMEM back to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar);
+    }
+    const int col0 = col_base + c * 32;
+    uint32_t pk[16];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4* px = row_ptr(b, q);
+      float4 x = *px;
+      const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + 4 * q);
+      if (live) {
+        x.x += __uint_as_float(a[4 * q]) + bb.x;
+        x.y += __uint_as_float(a[4 * q + 1]) + bb.y;
+        x.z += __uint_as_float(a[4 * q + 2]) + bb.z;
+        x.w += __uint_as_float(a[4 * q + 3]) + bb.w;
+        *px = x;
+        const float4 g = *reinterpret_cast<const float4*>(lng_s + col0 + 4 * q);
+        const float4 be = *reinterpret_cast<const float4*>(lnb_s + col0 + 4 * q);
+        pk[2 * q] = pack_bf16x2((x.x - mean) * rstd * g.x + be.x, (x.y - mean) * rstd * g.y + be.y);
+        pk[2 * q + 1] = pack_bf16x2((x.z - mean) * rstd * g.z + be.z, (x.w - mean) * rstd * g.w + be.w);
+      } else {
+        pk[2 * q] = 0u;
+        pk[2 * q + 1] = 0u;
+      }
+    }
+    // LN chunk: 32 rows x 64 B, SW64 layout (16-byte chunk q of row r at q ^ ((r >> 1) & 3))
+    if (c >= 2) {  // the TMA store that last read hb[b] / xb[b] must be done reading
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<uint4*>(hb[b] + r * 64 + ((q ^ ((r >> 1) & 3)) << 4)) =
+          make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(&tmX, xb[b], col0, row0);
+      if (row0 < p.ln_cap) tma_store_2d(&tmLN, hb[b], col0, row0);
+      bulk_commit();
+    }
+    if (c + 2 < CH) {
+      if (lane == 0) bulk_wait_read0();  // xb[b] is reloaded next
+      __syncwarp();
+      load(c + 2, b);
+    }
+  }
+  if (lane == 0) bulk_wait_read0();  // staging buffers reusable by the next tile
+  __syncwarp();
+}
+
 template <int BN, int STAGES, int EPI, int EW, int NACC>
 __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const GemmParams p) {
+                   const GemmParams p, const __grid_constant__ CUtensorMap tmX,
+                   const __grid_constant__ CUtensorMap tmLN) {
   static_assert((EW == 8 && NACC == 2) || (EW == 4 && NACC == 1), "supported epilogue configurations");
   using S = GemmSmem<BN, STAGES, NACC>;
   extern __shared__ uint8_t smem_raw[];
@@ -193,8 +326,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float2* ln_stats = reinterpret_cast<float2*>(smem + STAGES * S::STAGE_BYTES + 128);  // [2][128]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2 + 16);
+  float2* ln_stats = reinterpret_cast<float2*>(smem + STAGES * S::STAGE_BYTES + 256);  // [2][128]
+  uint64_t* xbar = tempty + 2;  // [8 warps][2] TMA-load barriers of the staged residual epilogue
   float* par = reinterpret_cast<float*>(smem + STAGES * S::STAGE_BYTES + S::BAR_BYTES);
   float* bias_s = par;                       // [N]
   float* lng_s = par + GEMM_MAX_N;           // [N] (RESID_LN)
@@ -217,6 +351,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
     tma_prefetch(&tmB);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < NACC; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], EW); }
+    for (int i = 0; i < 16; ++i) mbar_init(&xbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<S::TMEM_COLS>(tmem_slot);
@@ -281,13 +416,18 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
     asm volatile("bar.sync 5, %0;" ::"n"(32 * EW) : "memory");  // epilogue warps only
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t xph = 0;  // bit b: phase of this warp's staging barrier b
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       const int m_blk = tile / n_tiles, n_blk = tile % n_tiles;
       const int row0 = m_blk * GEMM_BM + quarter * 32;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + half * WCOLS;
       const int col_base = n_blk * BN + half * WCOLS;
       float s1 = 0.f, s2 = 0.f;  // RESID_LN row statistics (lane = row)
-      if constexpr (EPI == EPI_F32_RESID || EPI == EPI_F32_RESID_LN) {
+      if constexpr (EPI == EPI_F32_RESID_LN && EW == 8) {
+        resid_ln_tma<CH>(p, tmX, tmLN, smem + S::STG_OFF + (warp - 2) * S::STG_BYTES, xbar + (warp - 2) * 2,
+                         xph, tbase, row0, col_base, M, bias_s, lng_s, lnb_s, ln_stats, quarter, half, lane,
+                         &tfull[acc], acc_phase, &tempty[acc]);
+      } else if constexpr (EPI == EPI_F32_RESID || EPI == EPI_F32_RESID_LN) {
         // Residual epilogue, software-pipelined over the 32-column chunks: the residual
         // row segment of chunk c+1 is loaded while chunk c is added and stored, and chunk
         // 0's is requested before the accumulator is even ready.
@@ -368,7 +508,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
         }
       }
       }
-      if constexpr (EPI == EPI_F32_RESID_LN) {
+      if constexpr (EPI == EPI_F32_RESID_LN && EW != 8) {
         // row statistics; with EW=8 the two warps sharing these rows exchange halves
         float2 o = make_float2(0.f, 0.f);
         if constexpr (EW == 8) {
@@ -421,6 +561,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
       }
       if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
     }
+  }
+  if constexpr (EPI == EPI_F32_RESID_LN && EW == 8) {
+    if (warp >= 2 && lane == 0) bulk_wait0();  // staged TMA stores fully written before exit
   }
   tc_fence_before();
   __syncthreads();

@@ -254,3 +254,29 @@ def test_device_side_selection_errors_are_reported(enc_c640):
         enc_c640.check()
     assert e.value.status == -6
     enc_c640.check()  # cleared
+
+
+@pytest.mark.parametrize("staged", [1, 0])
+@pytest.mark.parametrize("M,N,K", [(16, 64, 64), (80, 64, 256), (128, 256, 256), (300, 256, 1024), (1000, 256, 256),
+                                   (22400, 256, 256)])
+def test_gemm_residual_layernorm_epilogue(M, N, K, staged):
+    """x += A W^T + b and LN(x) -> bf16 with zeroed pad rows, against torch fp32."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + K + staged)
+    A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g) * 0.1
+    x = torch.randn(M, N, device="cuda", generator=g)
+    lg = 1 + 0.1 * torch.randn(N, device="cuda", generator=g)
+    lb = 0.1 * torch.randn(N, device="cuda", generator=g)
+    cap = M + 200
+    ln = torch.full((cap, N), 7.0, device="cuda").to(torch.bfloat16)
+    ref_x = x + A.float() @ W.float().T + bias
+    ref_ln = torch.nn.functional.layer_norm(ref_x, (N,), lg, lb, 1e-6)
+    xx = x.clone()
+    assert LIB.cfdx_gemm_resid_ln(M, N, K, A.data_ptr(), W.data_ptr(), bias.data_ptr(), xx.data_ptr(), lg.data_ptr(),
+                                  lb.data_ptr(), 1e-6, ln.data_ptr(), cap, staged, _s()) == 0
+    torch.cuda.synchronize()
+    torch.testing.assert_close(xx, ref_x, rtol=1e-4, atol=1e-4)
+    torch.testing.assert_close(ln[:M].float(), ref_ln.to(torch.bfloat16).float(), rtol=1e-2, atol=2e-2)
+    pad = min(cap, ((M + 127) // 128) * 128 + 128)
+    assert (ln[M:pad].float() == 0).all()
