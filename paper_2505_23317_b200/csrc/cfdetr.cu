@@ -208,7 +208,8 @@ int g_fused_mlp = 1;  // fused MLP kernel (d == 256) instead of two GEMM launche
 int g_staged_epi = 1; // TMA-staged residual + LayerNorm epilogue for the O-projection
 
 cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUtensorMap& tw2, const MlpParams& p,
-                       int rows_for_grid, cudaStream_t s) {
+                       int rows_for_grid, cudaStream_t s, const CUtensorMap* tx = nullptr,
+                       const CUtensorMap* tln = nullptr) {
   auto kern = mlp_tc_kernel<256>;
   constexpr int smem = MlpSmem<256>::TOTAL;
   static bool attr = false;
@@ -219,7 +220,9 @@ cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUte
   }
   const int tiles = (pad_rows(rows_for_grid, p.ln_cap > 0 ? p.ln_cap : rows_for_grid + 256) + 127) / 128;
   const int grid = std::max(1, std::min(tiles, num_sms()));
-  kern<<<grid, MLP_THREADS, smem, s>>>(th, tw1, tw2, p);
+  MlpParams q = p;
+  q.staged = (tx != nullptr && (tln != nullptr || p.ln_g == nullptr)) ? 1 : 0;
+  kern<<<grid, MLP_THREADS, smem, s>>>(th, tw1, tw2, q, tx ? *tx : th, tln ? *tln : th);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -424,12 +427,12 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   // O projection + residual (+ LN2 -> hbuf)
   p = GemmParams{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = x_cap; p.N = d; p.K = d; p.bias = L.b_o; p.out_f32 = x; p.ld_out = d;
+  CUtensorMap tx, tln;  // staging maps: fp32 x [x_cap, d] and bf16 LN out, 32 x 32 boxes
+  const bool staged = fuse_ln && g_staged_epi && (d % 64 == 0) &&
+                      make_tmap(&tx, x, d, x_cap, d, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, true) &&
+                      make_tmap(&tln, w.hbuf, d, w.rows_cap, d, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (fuse_ln) {
     p.ln_g = L.ln2_g; p.ln_b = L.ln2_b; p.ln_out = w.hbuf; p.ln_cap = w.rows_cap; p.ln_eps = g.ln_eps;
-    CUtensorMap tx, tln;  // staging maps: fp32 x [x_cap, d] and bf16 LN out, 32 x 32 boxes
-    const bool staged = g_staged_epi && (d % 64 == 0) &&
-                        make_tmap(&tx, x, d, x_cap, d, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, true) &&
-                        make_tmap(&tln, w.hbuf, d, w.rows_cap, d, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
     CFD_CUDA(launch_gemm(EPI_F32_RESID_LN, ta_o, L.tm_o, p, rows_grid, s, PK_OPROJ, staged ? &tx : nullptr,
                          staged ? &tln : nullptr));
   } else {
@@ -445,7 +448,7 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
       mp.ln_g = Ln.ln1_g; mp.ln_b = Ln.ln1_b; mp.ln_out = w.hbuf; mp.ln_cap = w.rows_cap;
     }
     probe_begin(PK_MLP1, s);
-    CFD_CUDA(launch_mlp(ta_h, L.tm_1c, L.tm_2, mp, rows_grid, s));
+    CFD_CUDA(launch_mlp(ta_h, L.tm_1c, L.tm_2, mp, rows_grid, s, staged ? &tx : nullptr, staged ? &tln : nullptr));
     probe_end(PK_MLP1, s);
     return CFD_OK;
   }

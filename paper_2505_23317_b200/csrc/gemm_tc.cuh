@@ -184,73 +184,93 @@ __device__ __forceinline__ void direct_chunk(const GemmParams& p, float (&v)[32]
 }
 
 // ---------------------------------------------------------------------------- staged residual + LN
-// Residual + LayerNorm epilogue of one warp (32 rows x CH 32-column chunks of a row half)
+// Residual (+ LayerNorm) epilogue of one warp (32 rows x CH 32-column chunks of a row half)
 // through shared memory with TMA: x chunks [32 rows x 32 fp32] are TMA-loaded into a
 // 128B-swizzled buffer, each thread reads / writes its row with conflict-free 16-byte
 // accesses, and the results leave by TMA store, so no per-row global access is issued.
-//   pass A: x_old + acc + bias -> row statistics (the two column-half warps exchange)
-//   pass B: reload x_old, x_new = x_old + acc + bias -> x (TMA store) and LN(x_new) -> bf16
-//           (SW64 buffer, TMA store).  Rows >= M keep x and get zeros in ln_out.
-// The accumulator stays in TMEM until pass B's last read.
-template <int CH>
-__device__ __forceinline__ void resid_ln_tma(const GemmParams& p, const CUtensorMap& tmX, const CUtensorMap& tmLN,
-                                             uint8_t* stg, uint64_t* bar, uint32_t& xph, uint32_t tbase, int row0,
-                                             int col_base, int M, const float* bias_s, const float* lng_s,
-                                             const float* lnb_s, float2* stats, int quarter, int half, int lane,
-                                             uint64_t* tfull_bar, uint32_t tfull_parity, uint64_t* tempty_bar) {
-  uint8_t* xb[2] = {stg, stg + 4096};
-  uint8_t* hb[2] = {stg + 8192, stg + 10240};
+//   LN:   pass A: x_old + acc + bias -> row statistics (the two column-half warps exchange)
+//         pass B: reload x_old, x_new = x_old + acc + bias -> x (TMA store) and LN(x_new) -> bf16
+//                 (SW64 buffer, TMA store).  Rows >= M keep x and get zeros in ln_out.
+//   !LN:  one pass: x_new = x_old + acc + bias -> x (TMA store).
+// The accumulator stays in TMEM until the last read.  Staging: two 4 KB x buffers (1024-B
+// aligned) at xb + b * xb_stride; LN buffers of 2 KB at hb + b * hb_stride (hb_stride 0: one
+// buffer, the store of chunk c-1 is then drained before chunk c is written).
+struct ResidStage {
+  uint8_t* xb;
+  int xb_stride;
+  uint8_t* hb;
+  int hb_stride;
+  uint64_t* bar;   // [2] this warp's TMA-load barriers
+  uint32_t* xph;   // bit b: phase of bar[b]
+};
+
+struct ResidLnArgs {
+  int n_total;     // LayerNorm width (row length)
+  int ln_cap;      // rows of ln_out
+  float ln_eps;
+};
+
+template <int CH, bool LN>
+__device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtensorMap& tmX, const CUtensorMap& tmLN,
+                                             const ResidStage& st, uint32_t tbase, int row0, int col_base, int M,
+                                             const float* bias_s, const float* lng_s, const float* lnb_s,
+                                             float2* stats, int quarter, int half, int lane, uint64_t* tfull_bar,
+                                             uint32_t tfull_parity, uint64_t* tempty_bar) {
   const int r = lane;
   const bool live = row0 + r < M;
+  const bool one_hb = st.hb_stride == 0;
   auto load = [&](int c, int b) {
     if (lane == 0) {
-      mbar_expect_tx(&bar[b], 4096);
-      tma_load_2d(xb[b], &tmX, &bar[b], col_base + c * 32, row0);
+      mbar_expect_tx(&st.bar[b], 4096);
+      tma_load_2d(st.xb + b * st.xb_stride, &tmX, &st.bar[b], col_base + c * 32, row0);
     }
   };
   auto wait = [&](int b) {
-    mbar_wait(&bar[b], (xph >> b) & 1);
-    xph ^= 1u << b;
+    mbar_wait(&st.bar[b], (*st.xph >> b) & 1);
+    *st.xph ^= 1u << b;
   };
-  auto row_ptr = [&](int b, int q) { return reinterpret_cast<float4*>(xb[b] + r * 128 + ((q ^ (r & 7)) << 4)); };
-  float s1 = 0.f, s2 = 0.f;
-  // ---- pass A (the first residual chunks are requested before the accumulator is ready)
+  auto row_ptr = [&](int b, int q) { return reinterpret_cast<float4*>(st.xb + b * st.xb_stride + r * 128 + ((q ^ (r & 7)) << 4)); };
+  float mean = 0.f, rstd = 0.f;
   load(0, 0);
   if (CH > 1) load(1, 1);
   mbar_wait(tfull_bar, tfull_parity);
   tc_fence_after();
+  if constexpr (LN) {
+    // ---- pass A (the first residual chunks were requested before the accumulator was ready)
+    float s1 = 0.f, s2 = 0.f;
 #pragma unroll 1
-  for (int c = 0; c < CH; ++c) {
-    const int b = c & 1;
-    uint32_t a[32];
-    tmem_ld32(tbase + c * 32, a);
-    wait(b);
-    tmem_wait_ld();
-    const int col0 = col_base + c * 32;
+    for (int c = 0; c < CH; ++c) {
+      const int b = c & 1;
+      uint32_t a[32];
+      tmem_ld32(tbase + c * 32, a);
+      wait(b);
+      tmem_wait_ld();
+      const int col0 = col_base + c * 32;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float4 x = *row_ptr(b, q);
-      const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + 4 * q);
-      const float v0 = x.x + (__uint_as_float(a[4 * q]) + bb.x), v1 = x.y + (__uint_as_float(a[4 * q + 1]) + bb.y);
-      const float v2 = x.z + (__uint_as_float(a[4 * q + 2]) + bb.z), v3 = x.w + (__uint_as_float(a[4 * q + 3]) + bb.w);
-      s1 += (v0 + v1) + (v2 + v3);
-      s2 += (v0 * v0 + v1 * v1) + (v2 * v2 + v3 * v3);
+      for (int q = 0; q < 8; ++q) {
+        const float4 x = *row_ptr(b, q);
+        const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + 4 * q);
+        const float v0 = x.x + (__uint_as_float(a[4 * q]) + bb.x), v1 = x.y + (__uint_as_float(a[4 * q + 1]) + bb.y);
+        const float v2 = x.z + (__uint_as_float(a[4 * q + 2]) + bb.z), v3 = x.w + (__uint_as_float(a[4 * q + 3]) + bb.w);
+        s1 += (v0 + v1) + (v2 + v3);
+        s2 += (v0 * v0 + v1 * v1) + (v2 * v2 + v3 * v3);
+      }
+      __syncwarp();
+      if (c + 2 < CH) load(c + 2, b);
     }
-    __syncwarp();
-    if (c + 2 < CH) load(c + 2, b);
+    // ---- statistics of the full row (two warps, one per column half)
+    const int r_in_tile = quarter * 32 + lane;
+    stats[half * 128 + r_in_tile] = make_float2(s1, s2);
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+    const float2 o = stats[(half ^ 1) * 128 + r_in_tile];
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+    const float inv_n = 1.f / (float)la.n_total;
+    mean = (s1 + o.x) * inv_n;
+    rstd = rsqrtf(fmaxf((s2 + o.y) * inv_n - mean * mean, 0.f) + la.ln_eps);
+    // ---- pass B
+    load(0, 0);
+    if (CH > 1) load(1, 1);
   }
-  // ---- statistics of the full row (two warps, one per column half)
-  const int r_in_tile = quarter * 32 + lane;
-  stats[half * 128 + r_in_tile] = make_float2(s1, s2);
-  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
-  const float2 o = stats[(half ^ 1) * 128 + r_in_tile];
-  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
-  const float inv_n = 1.f / (float)p.N;
-  const float mean = (s1 + o.x) * inv_n;
-  const float rstd = rsqrtf(fmaxf((s2 + o.y) * inv_n - mean * mean, 0.f) + p.ln_eps);
-  // ---- pass B
-  load(0, 0);
-  if (CH > 1) load(1, 1);
 #pragma unroll 1
   for (int c = 0; c < CH; ++c) {
     const int b = c & 1;
@@ -276,29 +296,36 @@ __device__ __forceinline__ void resid_ln_tma(const GemmParams& p, const CUtensor
         x.z += __uint_as_float(a[4 * q + 2]) + bb.z;
         x.w += __uint_as_float(a[4 * q + 3]) + bb.w;
         *px = x;
-        const float4 g = *reinterpret_cast<const float4*>(lng_s + col0 + 4 * q);
-        const float4 be = *reinterpret_cast<const float4*>(lnb_s + col0 + 4 * q);
-        pk[2 * q] = pack_bf16x2((x.x - mean) * rstd * g.x + be.x, (x.y - mean) * rstd * g.y + be.y);
-        pk[2 * q + 1] = pack_bf16x2((x.z - mean) * rstd * g.z + be.z, (x.w - mean) * rstd * g.w + be.w);
-      } else {
-        pk[2 * q] = 0u;
-        pk[2 * q + 1] = 0u;
+      }
+      if constexpr (LN) {
+        if (live) {
+          const float4 g = *reinterpret_cast<const float4*>(lng_s + col0 + 4 * q);
+          const float4 be = *reinterpret_cast<const float4*>(lnb_s + col0 + 4 * q);
+          pk[2 * q] = pack_bf16x2((x.x - mean) * rstd * g.x + be.x, (x.y - mean) * rstd * g.y + be.y);
+          pk[2 * q + 1] = pack_bf16x2((x.z - mean) * rstd * g.z + be.z, (x.w - mean) * rstd * g.w + be.w);
+        } else {
+          pk[2 * q] = 0u;
+          pk[2 * q + 1] = 0u;
+        }
       }
     }
-    // LN chunk: 32 rows x 64 B, SW64 layout (16-byte chunk q of row r at q ^ ((r >> 1) & 3))
-    if (c >= 2) {  // the TMA store that last read hb[b] / xb[b] must be done reading
-      if (lane == 0) bulk_wait_read0();
-      __syncwarp();
-    }
+    if constexpr (LN) {
+      // LN chunk: 32 rows x 64 B, SW64 layout (16-byte chunk q of row r at q ^ ((r >> 1) & 3))
+      if (c >= (one_hb ? 1 : 2)) {  // the TMA store that last read this hb must be done reading
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+      }
+      uint8_t* hb = st.hb + b * st.hb_stride;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      *reinterpret_cast<uint4*>(hb[b] + r * 64 + ((q ^ ((r >> 1) & 3)) << 4)) =
-          make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<uint4*>(hb + r * 64 + ((q ^ ((r >> 1) & 3)) << 4)) =
+            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    }
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
-      tma_store_2d(&tmX, xb[b], col0, row0);
-      if (row0 < p.ln_cap) tma_store_2d(&tmLN, hb[b], col0, row0);
+      tma_store_2d(&tmX, st.xb + b * st.xb_stride, col0, row0);
+      if (LN && row0 < la.ln_cap) tma_store_2d(&tmLN, st.hb + b * st.hb_stride, col0, row0);
       bulk_commit();
     }
     if (c + 2 < CH) {
@@ -424,9 +451,11 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
       const int col_base = n_blk * BN + half * WCOLS;
       float s1 = 0.f, s2 = 0.f;  // RESID_LN row statistics (lane = row)
       if constexpr (EPI == EPI_F32_RESID_LN && EW == 8) {
-        resid_ln_tma<CH>(p, tmX, tmLN, smem + S::STG_OFF + (warp - 2) * S::STG_BYTES, xbar + (warp - 2) * 2,
-                         xph, tbase, row0, col_base, M, bias_s, lng_s, lnb_s, ln_stats, quarter, half, lane,
-                         &tfull[acc], acc_phase, &tempty[acc]);
+        uint8_t* stg = smem + S::STG_OFF + (warp - 2) * S::STG_BYTES;
+        const ResidStage st{stg, 4096, stg + 8192, 2048, xbar + (warp - 2) * 2, &xph};
+        const ResidLnArgs la{p.N, p.ln_cap, p.ln_eps};
+        resid_ln_tma<CH, true>(la, tmX, tmLN, st, tbase, row0, col_base, M, bias_s, lng_s, lnb_s, ln_stats, quarter,
+                               half, lane, &tfull[acc], acc_phase, &tempty[acc]);
       } else if constexpr (EPI == EPI_F32_RESID || EPI == EPI_F32_RESID_LN) {
         // Residual epilogue, software-pipelined over the 32-column chunks: the residual
         // row segment of chunk c+1 is loaded while chunk c is added and stored, and chunk

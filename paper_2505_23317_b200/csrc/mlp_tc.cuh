@@ -34,6 +34,7 @@ struct MlpParams {
   __nv_bfloat16* ln_out; // [ln_cap, D]
   int ln_cap;
   float ln_eps;
+  int staged;            // 1: residual (+LN) epilogue staged through smem with TMA (tmX / tmLN valid)
 };
 
 constexpr int MLP_THREADS = 320;  // TMA warp, MMA warp, 8 epilogue warps
@@ -49,15 +50,20 @@ struct MlpSmem {
   static constexpr int H_OFF = A_OFF + A_BYTES;           // [2]
   static constexpr int W_OFF = H_OFF + 2 * H_BYTES;       // [MLP_SLOTS]
   static constexpr int BAR_OFF = W_OFF + MLP_SLOTS * SLOT_BYTES;
-  static constexpr int STATS_OFF = BAR_OFF + 256;         // float2 [2][128]
+  static constexpr int STATS_OFF = BAR_OFF + 512;         // float2 [2][128]
   static constexpr int PAR_OFF = STATS_OFF + 2 * 128 * 8; // b1 [F] | b2 [D] | g [D] | b [D]
-  static constexpr int TOTAL = 1024 + PAR_OFF + (GEMM_MAX_N + 3 * D) * 4;
+  // staged final epilogue: each epilogue warp's x staging buffers are its own 4 KB slices of
+  // H[0] / H[1] (the slices it writes during GELU, free once the last MMA2 has committed);
+  // one 2 KB LN output buffer per warp lives here
+  static constexpr int LNSTG_OFF = ((PAR_OFF + (GEMM_MAX_N + 3 * D) * 4 + 1023) / 1024) * 1024;
+  static constexpr int TOTAL = 1024 + LNSTG_OFF + 8 * 2048;
 };
 
 template <int D>
 __global__ void __launch_bounds__(MLP_THREADS, 1)
     mlp_tc_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW1,
-                  const __grid_constant__ CUtensorMap tmW2, const MlpParams p) {
+                  const __grid_constant__ CUtensorMap tmW2, const MlpParams p,
+                  const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmLN) {
   using S = MlpSmem<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -72,7 +78,8 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   uint64_t* h_empty = h_full + 2;            // [2]
   uint64_t* a2_full = h_empty + 2;
   uint64_t* a2_empty = a2_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a2_empty + 1);
+  uint64_t* xbar = a2_empty + 1;             // [8 warps][2] staged-epilogue TMA loads
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + 16);
   float2* ln_stats = reinterpret_cast<float2*>(smem + S::STATS_OFF);
   float* b1_s = reinterpret_cast<float*>(smem + S::PAR_OFF);
   float* b2_s = b1_s + GEMM_MAX_N;
@@ -101,6 +108,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     }
     mbar_init(a2_full, 1);
     mbar_init(a2_empty, 8);
+    for (int i = 0; i < 16; ++i) mbar_init(&xbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -236,6 +244,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const int r_in_tile = quarter * 32 + lane;
     uint32_t a1_cnt[2] = {0, 0}, h_cnt[2] = {0, 0};
+    uint32_t xph = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
       const int row = tile * 128 + r_in_tile;
@@ -285,6 +294,21 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         ++h_cnt[b];
       }
       // ---- x += acc2 + b2  (+ next LayerNorm)
+      if (p.staged) {
+        const int e = warp - 2;
+        uint8_t* hslice = smem + S::H_OFF + half * 16384 + quarter * 4096;
+        uint8_t* lnb = smem + S::LNSTG_OFF + e * 2048;
+        const ResidStage st{hslice, S::H_BYTES, lnb, 0, xbar + 2 * e, &xph};
+        const ResidLnArgs la{D, p.ln_cap, p.ln_eps};
+        const uint32_t tb = tmem + lane_off + ACC2 + half * 128;
+        if (do_ln)
+          resid_ln_tma<4, true>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M, b2_s, lng_s, lnb_s,
+                                ln_stats, quarter, half, lane, a2_full, it & 1, a2_empty);
+        else
+          resid_ln_tma<4, false>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M, b2_s, lng_s,
+                                 lnb_s, ln_stats, quarter, half, lane, a2_full, it & 1, a2_empty);
+        continue;
+      }
       mbar_wait(a2_full, it & 1);
       tc_fence_after();
       const bool live = row < M;

@@ -212,3 +212,33 @@ def test_fused_mlp_matches_two_gemm_path():
     for a, b in zip(outs[0], outs[1]):
         rel = ((a - b).norm() / b.norm()).item()
         assert rel < 3e-3, rel
+
+
+def test_staged_epilogues_match_direct_epilogues():
+    """The TMA-staged residual(+LN) epilogues (O-projection and fused-MLP tails, default) against
+    the per-row direct-store epilogues on a ragged batch.  Not bitwise: with staging off the
+    O-projection runs the two-CTA/SM configuration whose LayerNorm row sums are taken by one
+    warp over all 256 columns instead of two 128-column halves (different rounding order)."""
+    from paper_2505_23317_b200 import _lib as L
+    lib = L.load()
+    cfg = ci.CONFIGS["c640"]
+    enc = enc_for("c640")
+    imgs = bf16_tensor(ci.make_frames(cfg, 3, task0=11), "cuda")
+    ks = [0, 37, 400]
+    co = enc.coarse_encode(imgs)
+    sel = enc.select_regions(co["scores"], k=ks)
+    x0 = co["x0"].clone()
+    outs = []
+    try:
+        for staged in (1, 0):
+            assert lib.cfdx_set_option(3, staged) == 0
+            c2 = enc.coarse_encode(imgs)
+            ro = enc.batch_refine(imgs, x0, sel["sel_idx"], sel["sel_count"])
+            torch.cuda.synchronize()
+            n = int(ro["cu_seqlens"][-1])
+            outs.append((c2["y"].clone(), c2["scores"].clone(), ro["y"][:n].clone()))
+    finally:
+        lib.cfdx_set_option(3, 1)
+    for a, b in zip(outs[0], outs[1]):
+        rel = ((a - b).norm() / b.norm()).item()
+        assert rel < 3e-3, rel
