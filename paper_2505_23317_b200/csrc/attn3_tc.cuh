@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(ATTN3_THREADS, 1)
   static_assert(DH == 32, "specialised for dh = 32 (64-byte rows, SW64)");
   using S = Attn3Smem<DH, STAGES>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
   uint64_t* q_full = bars;                  // [2]
   uint64_t* q_empty = bars + 2;             // [2]

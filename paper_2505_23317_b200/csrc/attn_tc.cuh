@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   const int q_row0 = seq0 + qt * ATTN_BQ;
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + S::Q_BYTES;
   uint8_t* sV = sK + STAGES * S::K_BYTES;

@@ -115,6 +115,8 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // ------------------------------------------------------------------ GEMM dispatch
 template <int BN>
 constexpr int gemm_stages() { return BN == 256 ? 4 : BN == 128 ? 6 : 8; }
+template <int BN>  // with the 32 KB bf16 output staging area
+constexpr int gemm_stages_stg() { return BN == 256 ? 3 : BN == 128 ? 5 : 7; }
 
 // mode 0: 1 CTA/SM, 8 epilogue warps, double-buffered accumulator (many tiles);
 //         for EPI_F32_RESID_LN a 2-stage ring and the TMA-staged residual epilogue
@@ -123,11 +125,20 @@ template <int BN, int EPI, int MODE>
 cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows_for_grid,
                           cudaStream_t s, const CUtensorMap* tx, const CUtensorMap* tln) {
   constexpr bool kTmaEpi = (EPI == EPI_F32_RESID_LN && MODE == 0);
+  constexpr bool kStgOut = (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_GELU) && MODE == 0;
   constexpr int EW = MODE ? 4 : 8;
   constexpr int NACC = MODE ? 1 : 2;
-  constexpr int ST = (MODE || kTmaEpi) ? 2 : gemm_stages<BN>();
+  constexpr int ST = (MODE || kTmaEpi) ? 2 : kStgOut ? gemm_stages_stg<BN>() : gemm_stages<BN>();
   auto kern = gemm_tc_kernel<BN, ST, EPI, EW, NACC>;
-  constexpr int smem = kTmaEpi ? GemmSmem<BN, ST, NACC>::TOTAL_TMA_EPI : GemmSmem<BN, ST, NACC>::TOTAL;
+  constexpr int smem = kTmaEpi ? GemmSmem<BN, ST, NACC>::TOTAL_TMA_EPI
+                       : kStgOut ? GemmSmem<BN, ST, NACC>::TOTAL_STG_OUT : GemmSmem<BN, ST, NACC>::TOTAL;
+  static_assert(smem <= 232448, "shared memory budget");
+  CUtensorMap tout;
+  if constexpr (kStgOut) {  // bf16 output [m_cap, N], 32 x 32 boxes
+    if (!make_tmap(&tout, p.out_bf16, p.N, p.m_cap, p.N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+      return cudaErrorInvalidValue;
+    tx = &tout;
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -331,7 +342,7 @@ struct LayerDev {
   uint16_t *wqkv, *wo, *w1, *w2;  // K-major [N, K]
   float *b_qkv, *b_o, *b_1, *b_2, *ln1_g, *ln1_b, *ln2_g, *ln2_b;
   CUtensorMap tm_qkv, tm_o, tm_1, tm_2;
-  CUtensorMap tm_1c;  // W1^T with 128-row boxes (fused MLP chunks)
+  CUtensorMap tm_1c, tm_2c;  // W1 / W2 with 128-row x 64-k boxes (fused MLP ring slots)
 };
 
 struct cfd_ctx {
@@ -448,7 +459,7 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
       mp.ln_g = Ln.ln1_g; mp.ln_b = Ln.ln1_b; mp.ln_out = w.hbuf; mp.ln_cap = w.rows_cap;
     }
     probe_begin(PK_MLP1, s);
-    CFD_CUDA(launch_mlp(ta_h, L.tm_1c, L.tm_2, mp, rows_grid, s, staged ? &tx : nullptr, staged ? &tln : nullptr));
+    CFD_CUDA(launch_mlp(ta_h, L.tm_1c, L.tm_2c, mp, rows_grid, s, staged ? &tx : nullptr, staged ? &tln : nullptr));
     probe_end(PK_MLP1, s);
     return CFD_OK;
   }
@@ -630,7 +641,8 @@ cfd_status cfd_create(const cfd_config* cfg, const cfd_weights* wts, void* strea
         return fail(CFD_E_CUDA);
     if (!make_wmap(&ld.tm_qkv, ld.wqkv, 3 * d, d) || !make_wmap(&ld.tm_o, ld.wo, d, d) ||
         !make_wmap(&ld.tm_1, ld.w1, F, d) || !make_wmap(&ld.tm_2, ld.w2, d, F) ||
-        !make_tmap(&ld.tm_1c, ld.w1, d, F, d, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+        !make_tmap(&ld.tm_1c, ld.w1, d, F, d, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap(&ld.tm_2c, ld.w2, F, d, F, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B))
       return fail(CFD_E_CUDA);
   }
   *out = c;

@@ -89,6 +89,7 @@ struct GemmSmem {
   static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES + PAR_BYTES;
   static constexpr int STG_OFF = STAGES * STAGE_BYTES + ((BAR_BYTES + PAR_BYTES + 1023) / 1024) * 1024;
   static constexpr int TOTAL_TMA_EPI = 1024 + STG_OFF + GEMM_EPI_WARPS * STG_BYTES;
+  static constexpr int TOTAL_STG_OUT = 1024 + STG_OFF + GEMM_EPI_WARPS * 4096;  // bf16 out: 2 x 2 KB per warp
   static constexpr uint32_t TMEM_COLS = (NACC * BN <= 32) ? 32 : (NACC * BN <= 64) ? 64 : (NACC * BN <= 128) ? 128
                                         : (NACC * BN <= 256) ? 256 : 512;
 };
@@ -102,25 +103,26 @@ __host__ __device__ __forceinline__ int pad_rows(int M, int cap) {
 
 __device__ __forceinline__ float gelu_erf(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }
 
-// GELU(z) = z * Phi(z), Phi(z) = 1/2 + 1/2 erf(z/sqrt2), for a pair on packed FFMA2:
-// Phi(z) - 1/2 = t * q(t^2), t = clamp(z/4.5, -1, 1), q a degree-7 polynomial in t^2
-// (Chebyshev fit of degree 15, odd; |error| <= 9.1e-5 in Phi for all z, i.e. below
-// 1/20 of a bf16 ulp of the GELU output), beyond |z| >= 4.5 Phi is clamped (err 3.4e-6).
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// GELU(z) = z * Phi(z), Phi(z) = 1/2 + 1/2 erf(z/sqrt2) (reading R4), for a pair:
+//   Phi(z) ~= 1/2 + 1/2 tanh(z (A + B z^2)),  A, B minimax-fitted to the exact-erf Phi
+// (|dPhi| <= 1.4e-4 for all z; <= 3.9e-4 including tanh.approx.f32's error, i.e. the GELU
+// error stays below 1/5 of a bf16 ulp of the output).  3 FFMA2 + 2 MUFU.TANH + 1 FFMA2 per
+// pair: the tanh runs on the otherwise idle MUFU pipe.
 __device__ __forceinline__ void gelu2(float& a, float& b) {
-  float t0 = fminf(fmaxf(a * (1.0f / 4.5f), -1.f), 1.f);
-  float t1 = fminf(fmaxf(b * (1.0f / 4.5f), -1.f), 1.f);
-  float u0, u1, q0, q1;
-  fma2x(u0, u1, t0, t1, t0, t1, 0.f, 0.f);
-  fma2x(q0, q1, u0, u1, -4.5690726f, -4.5690726f, 21.273092f, 21.273092f);
-  fma2x(q0, q1, q0, q1, u0, u1, -42.560215f, -42.560215f);
-  fma2x(q0, q1, q0, q1, u0, u1, 48.358903f, 48.358903f);
-  fma2x(q0, q1, q0, q1, u0, u1, -34.930427f, -34.930427f);
-  fma2x(q0, q1, q0, q1, u0, u1, 17.109918f, 17.109918f);
-  fma2x(q0, q1, q0, q1, u0, u1, -5.9759021f, -5.9759021f);
-  fma2x(q0, q1, q0, q1, u0, u1, 1.7936441f, 1.7936441f);
-  float h0, h1;
-  fma2x(h0, h1, t0, t1, q0, q1, 0.5f, 0.5f);   // Phi
-  fma2x(a, b, a, b, h0, h1, 0.f, 0.f);          // z * Phi
+  constexpr float A = 0.79880144f, B = 0.03528205f;
+  float u0, u1, w0, w1, v0, v1, h0, h1;
+  fma2x(u0, u1, a, b, a, b, 0.f, 0.f);         // z^2
+  fma2x(w0, w1, u0, u1, B, B, A, A);           // A + B z^2
+  fma2x(v0, v1, a, b, w0, w1, 0.f, 0.f);       // z (A + B z^2)
+  fma2x(h0, h1, a, b, 0.5f, 0.5f, 0.f, 0.f);   // z / 2
+  const float t0 = tanh_approx(v0), t1 = tanh_approx(v1);
+  fma2x(a, b, h0, h1, t0, t1, h0, h1);         // z/2 (1 + tanh)
 }
 
 // ---------------------------------------------------------------------------- epilogue
@@ -188,9 +190,10 @@ __device__ __forceinline__ void direct_chunk(const GemmParams& p, float (&v)[32]
 // through shared memory with TMA: x chunks [32 rows x 32 fp32] are TMA-loaded into a
 // 128B-swizzled buffer, each thread reads / writes its row with conflict-free 16-byte
 // accesses, and the results leave by TMA store, so no per-row global access is issued.
-//   LN:   pass A: x_old + acc + bias -> row statistics (the two column-half warps exchange)
-//         pass B: reload x_old, x_new = x_old + acc + bias -> x (TMA store) and LN(x_new) -> bf16
-//                 (SW64 buffer, TMA store).  Rows >= M keep x and get zeros in ln_out.
+//   LN:   pass A: x_new = x_old + acc + bias -> x (TMA store) and back into the accumulator's
+//                 TMEM columns; row statistics (the two column-half warps exchange)
+//         pass B: LN(x_new) read back from TMEM -> bf16 (SW64 buffer, TMA store); x is read
+//                 from memory once.  Rows >= M keep x and get zeros in ln_out.
 //   !LN:  one pass: x_new = x_old + acc + bias -> x (TMA store).
 // The accumulator stays in TMEM until the last read.  Staging: two 4 KB x buffers (1024-B
 // aligned) at xb + b * xb_stride; LN buffers of 2 KB at hb + b * hb_stride (hb_stride 0: one
@@ -236,7 +239,9 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
   mbar_wait(tfull_bar, tfull_parity);
   tc_fence_after();
   if constexpr (LN) {
-    // ---- pass A (the first residual chunks were requested before the accumulator was ready)
+    // ---- pass A: x_new = x_old + acc + bias -> x (TMA store) and back into the accumulator's
+    //      TMEM columns; row statistics.  (The first residual chunks were requested before the
+    //      accumulator was ready.)
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll 1
     for (int c = 0; c < CH; ++c) {
@@ -248,16 +253,34 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
       const int col0 = col_base + c * 32;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const float4 x = *row_ptr(b, q);
+        float4* px = row_ptr(b, q);
+        float4 x = *px;
         const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + 4 * q);
         const float v0 = x.x + (__uint_as_float(a[4 * q]) + bb.x), v1 = x.y + (__uint_as_float(a[4 * q + 1]) + bb.y);
         const float v2 = x.z + (__uint_as_float(a[4 * q + 2]) + bb.z), v3 = x.w + (__uint_as_float(a[4 * q + 3]) + bb.w);
+        if (live) *px = make_float4(v0, v1, v2, v3);
         s1 += (v0 + v1) + (v2 + v3);
         s2 += (v0 * v0 + v1 * v1) + (v2 * v2 + v3 * v3);
+        a[4 * q] = __float_as_uint(v0);
+        a[4 * q + 1] = __float_as_uint(v1);
+        a[4 * q + 2] = __float_as_uint(v2);
+        a[4 * q + 3] = __float_as_uint(v3);
       }
+      tmem_st16(tbase + c * 32, *reinterpret_cast<const uint32_t(*)[16]>(a));
+      tmem_st16(tbase + c * 32 + 16, *reinterpret_cast<const uint32_t(*)[16]>(a + 16));
+      fence_proxy_async();
       __syncwarp();
-      if (c + 2 < CH) load(c + 2, b);
+      if (lane == 0) {
+        tma_store_2d(&tmX, st.xb + b * st.xb_stride, col0, row0);
+        bulk_commit();
+      }
+      if (c + 2 < CH) {
+        if (lane == 0) bulk_wait_read0();  // xb[b] is reloaded next
+        __syncwarp();
+        load(c + 2, b);
+      }
     }
+    tmem_wait_st();
     // ---- statistics of the full row (two warps, one per column half)
     const int r_in_tile = quarter * 32 + lane;
     stats[half * 128 + r_in_tile] = make_float2(s1, s2);
@@ -267,16 +290,111 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
     const float inv_n = 1.f / (float)la.n_total;
     mean = (s1 + o.x) * inv_n;
     rstd = rsqrtf(fmaxf((s2 + o.y) * inv_n - mean * mean, 0.f) + la.ln_eps);
-    // ---- pass B
-    load(0, 0);
-    if (CH > 1) load(1, 1);
+    // ---- pass B: LN(x_new) from TMEM -> bf16 (SW64 buffer) -> TMA store
+#pragma unroll 1
+    for (int c = 0; c < CH; ++c) {
+      uint32_t a[32];
+      tmem_ld32(tbase + c * 32, a);
+      tmem_wait_ld();
+      if (c + 1 == CH) {  // accumulator fully read: hand TMEM back to the MMA warp
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty_bar);
+      }
+      const int col0 = col_base + c * 32;
+      uint32_t pk[16];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (live) {
+          const float4 g = *reinterpret_cast<const float4*>(lng_s + col0 + 4 * q);
+          const float4 be = *reinterpret_cast<const float4*>(lnb_s + col0 + 4 * q);
+          const float x0 = __uint_as_float(a[4 * q]), x1 = __uint_as_float(a[4 * q + 1]);
+          const float x2 = __uint_as_float(a[4 * q + 2]), x3 = __uint_as_float(a[4 * q + 3]);
+          pk[2 * q] = pack_bf16x2((x0 - mean) * rstd * g.x + be.x, (x1 - mean) * rstd * g.y + be.y);
+          pk[2 * q + 1] = pack_bf16x2((x2 - mean) * rstd * g.z + be.z, (x3 - mean) * rstd * g.w + be.w);
+        } else {
+          pk[2 * q] = 0u;
+          pk[2 * q + 1] = 0u;
+        }
+      }
+      const int b = c & 1;
+      if (c >= (one_hb ? 1 : 2)) {  // the TMA store that last read this hb must be done reading
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+      }
+      uint8_t* hb = st.hb + b * st.hb_stride;
+      // LN chunk: 32 rows x 64 B, SW64 layout (16-byte chunk q of row r at q ^ ((r >> 1) & 3))
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<uint4*>(hb + r * 64 + ((q ^ ((r >> 1) & 3)) << 4)) =
+            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        if (row0 < la.ln_cap) tma_store_2d(&tmLN, hb, col0, row0);
+        bulk_commit();
+      }
+    }
+  } else {
+    // ---- single pass: x_new = x_old + acc + bias -> x (TMA store)
+#pragma unroll 1
+    for (int c = 0; c < CH; ++c) {
+      const int b = c & 1;
+      uint32_t a[32];
+      tmem_ld32(tbase + c * 32, a);
+      wait(b);
+      tmem_wait_ld();
+      if (c + 1 == CH) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty_bar);
+      }
+      const int col0 = col_base + c * 32;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4* px = row_ptr(b, q);
+        float4 x = *px;
+        const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + 4 * q);
+        if (live) {
+          x.x += __uint_as_float(a[4 * q]) + bb.x;
+          x.y += __uint_as_float(a[4 * q + 1]) + bb.y;
+          x.z += __uint_as_float(a[4 * q + 2]) + bb.z;
+          x.w += __uint_as_float(a[4 * q + 3]) + bb.w;
+          *px = x;
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(&tmX, st.xb + b * st.xb_stride, col0, row0);
+        bulk_commit();
+      }
+      if (c + 2 < CH) {
+        if (lane == 0) bulk_wait_read0();  // xb[b] is reloaded next
+        __syncwarp();
+        load(c + 2, b);
+      }
+    }
   }
+  if (lane == 0) bulk_wait_read0();  // staging buffers reusable by the next tile
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------- staged bf16 store
+// bf16 output epilogue of one warp (32 rows x CH 32-column chunks) through shared memory:
+// acc + bias (+GELU) -> bf16 -> a 2 KB SW64 buffer (conflict-free 16-byte writes, one row per
+// thread) -> TMA store of the 32 x 32 box.  Two buffers alternate; a buffer is rewritten once
+// the store issued from it two chunks earlier has finished reading.
+template <int CH, int EPI>
+__device__ __forceinline__ void store_bf16_tma(const CUtensorMap& tmO, uint8_t* stg, uint32_t tbase, int row0,
+                                               int col_base, const float* bias_s, int lane, uint64_t* tfull_bar,
+                                               uint32_t tfull_parity, uint64_t* tempty_bar) {
+  mbar_wait(tfull_bar, tfull_parity);
+  tc_fence_after();
 #pragma unroll 1
   for (int c = 0; c < CH; ++c) {
-    const int b = c & 1;
     uint32_t a[32];
     tmem_ld32(tbase + c * 32, a);
-    wait(b);
     tmem_wait_ld();
     if (c + 1 == CH) {  // accumulator fully read: hand TMEM back to the MMA warp
       tc_fence_before();
@@ -286,56 +404,26 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
     const int col0 = col_base + c * 32;
     uint32_t pk[16];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      float4* px = row_ptr(b, q);
-      float4 x = *px;
-      const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + 4 * q);
-      if (live) {
-        x.x += __uint_as_float(a[4 * q]) + bb.x;
-        x.y += __uint_as_float(a[4 * q + 1]) + bb.y;
-        x.z += __uint_as_float(a[4 * q + 2]) + bb.z;
-        x.w += __uint_as_float(a[4 * q + 3]) + bb.w;
-        *px = x;
-      }
-      if constexpr (LN) {
-        if (live) {
-          const float4 g = *reinterpret_cast<const float4*>(lng_s + col0 + 4 * q);
-          const float4 be = *reinterpret_cast<const float4*>(lnb_s + col0 + 4 * q);
-          pk[2 * q] = pack_bf16x2((x.x - mean) * rstd * g.x + be.x, (x.y - mean) * rstd * g.y + be.y);
-          pk[2 * q + 1] = pack_bf16x2((x.z - mean) * rstd * g.z + be.z, (x.w - mean) * rstd * g.w + be.w);
-        } else {
-          pk[2 * q] = 0u;
-          pk[2 * q + 1] = 0u;
-        }
-      }
+    for (int i = 0; i < 16; ++i) {
+      const float2 bb = *reinterpret_cast<const float2*>(bias_s + col0 + 2 * i);
+      float x0 = __uint_as_float(a[2 * i]) + bb.x, x1 = __uint_as_float(a[2 * i + 1]) + bb.y;
+      if constexpr (EPI == EPI_BF16_BIAS_GELU) gelu2(x0, x1);
+      pk[i] = pack_bf16x2(x0, x1);
     }
-    if constexpr (LN) {
-      // LN chunk: 32 rows x 64 B, SW64 layout (16-byte chunk q of row r at q ^ ((r >> 1) & 3))
-      if (c >= (one_hb ? 1 : 2)) {  // the TMA store that last read this hb must be done reading
-        if (lane == 0) bulk_wait_read0();
-        __syncwarp();
-      }
-      uint8_t* hb = st.hb + b * st.hb_stride;
+    if (lane == 0) bulk_wait_read1();  // the store that last read this buffer is done reading
+    __syncwarp();
+    uint8_t* buf = stg + (c & 1) * 2048;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<uint4*>(hb + r * 64 + ((q ^ ((r >> 1) & 3)) << 4)) =
-            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-    }
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
+          make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
-      tma_store_2d(&tmX, st.xb + b * st.xb_stride, col0, row0);
-      if (LN && row0 < la.ln_cap) tma_store_2d(&tmLN, st.hb + b * st.hb_stride, col0, row0);
+      tma_store_2d(&tmO, buf, col0, row0);
       bulk_commit();
     }
-    if (c + 2 < CH) {
-      if (lane == 0) bulk_wait_read0();  // xb[b] is reloaded next
-      __syncwarp();
-      load(c + 2, b);
-    }
   }
-  if (lane == 0) bulk_wait_read0();  // staging buffers reusable by the next tile
-  __syncwarp();
 }
 
 template <int BN, int STAGES, int EPI, int EW, int NACC>
@@ -346,7 +434,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
   static_assert((EW == 8 && NACC == 2) || (EW == 4 && NACC == 1), "supported epilogue configurations");
   using S = GemmSmem<BN, STAGES, NACC>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * S::A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES);
@@ -366,6 +454,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
   // bf16 outputs (QKV, MLP1) also cover the pad rows [M, pad_rows(M)) so attention's
   // tail tiles (which may start at any row of the last task) read finite values
   constexpr bool kPad = (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_GELU);
+  // bf16 outputs of the one-CTA/SM configuration leave through smem + TMA store (tmX = out map)
+  constexpr bool kStgOut = kPad && EW == 8;
   const int m_store = kPad ? pad_rows(M, p.m_cap) : M;
   // RESID_LN also visits the tiles of the pad rows (zeroed in ln_out, x untouched)
   const int m_tiles = ((EPI == EPI_F32_RESID_LN ? pad_rows(M, p.ln_cap) : m_store) + GEMM_BM - 1) / GEMM_BM;
@@ -456,6 +546,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
         const ResidLnArgs la{p.N, p.ln_cap, p.ln_eps};
         resid_ln_tma<CH, true>(la, tmX, tmLN, st, tbase, row0, col_base, M, bias_s, lng_s, lnb_s, ln_stats, quarter,
                                half, lane, &tfull[acc], acc_phase, &tempty[acc]);
+      } else if constexpr (kStgOut) {
+        store_bf16_tma<CH, EPI>(tmX, smem + S::STG_OFF + (warp - 2) * 4096, tbase, row0, col_base, bias_s, lane,
+                                &tfull[acc], acc_phase, &tempty[acc]);
       } else if constexpr (EPI == EPI_F32_RESID || EPI == EPI_F32_RESID_LN) {
         // Residual epilogue, software-pipelined over the 32-column chunks: the residual
         // row segment of chunk c+1 is loaded while chunk c is added and stored, and chunk
@@ -591,7 +684,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
       if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
     }
   }
-  if constexpr (EPI == EPI_F32_RESID_LN && EW == 8) {
+  if constexpr ((EPI == EPI_F32_RESID_LN || kStgOut) && EW == 8) {
     if (warp >= 2 && lane == 0) bulk_wait0();  // staged TMA stores fully written before exit
   }
   tc_fence_before();

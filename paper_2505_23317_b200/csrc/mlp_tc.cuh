@@ -11,8 +11,10 @@
 //   MMA2(j):  acc2 (TMEM, 256 cols) += H[j&1] . W2[:, j]^T          (K = 128)
 // issued as MMA1(j+1) before MMA2(j) so GELU(j) overlaps the tensor core.  The hidden
 // activations never leave the SM.  TMEM: acc1 x2 (256) + acc2 (256) = 512 columns.
-// Weights stream through a ring of 32 KB slots (W1 chunk = 2 slots of two 64-wide k-blocks,
-// W2 chunk = 2 slots of one 256-row k-block) in exactly the order the MMA warp consumes them.
+// Weights stream through a ring of four 16 KB slots (128 rows x one 64-wide k-block each:
+// W1 chunk = D/64 slots, W2 chunk = 2 k-blocks x 2 row halves) in exactly the order the MMA
+// warp consumes them; small slots keep 3-4 loads in flight so the L2 latency is hidden
+// (with two 32 KB slots only one load could overlap an MMA and the ring was latency-bound).
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -38,14 +40,14 @@ struct MlpParams {
 };
 
 constexpr int MLP_THREADS = 320;  // TMA warp, MMA warp, 8 epilogue warps
-constexpr int MLP_SLOTS = 2;
+constexpr int MLP_SLOTS = 4;
 
 template <int D>
 struct MlpSmem {
   static_assert(D == 256, "fused MLP is laid out for d = 256 (acc2 = 256 TMEM columns)");
   static constexpr int A_BYTES = 128 * D * 2;             // 64 KB: h tile, D/64 k-blocks of 16 KB
   static constexpr int H_BYTES = 128 * 128 * 2;           // 32 KB: GELU chunk, 2 k-blocks
-  static constexpr int SLOT_BYTES = 32768;
+  static constexpr int SLOT_BYTES = 16384;
   static constexpr int A_OFF = 0;
   static constexpr int H_OFF = A_OFF + A_BYTES;           // [2]
   static constexpr int W_OFF = H_OFF + 2 * H_BYTES;       // [MLP_SLOTS]
@@ -66,7 +68,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
                   const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmLN) {
   using S = MlpSmem<D>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
   uint64_t* a_full = bars + 0;
   uint64_t* a_empty = bars + 1;
@@ -130,20 +132,20 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         return smem + S::W_OFF + slot * S::SLOT_BYTES;
       };
       auto adv = [&]() { if (++slot == MLP_SLOTS) { slot = 0; sph ^= 1; } };
-      auto load_w1 = [&](int j) {  // W1^T rows [128j, 128j+128), k-blocks (0,1) then (2,3)
-        for (int hb = 0; hb < KB / 2; ++hb) {
-          uint8_t* dst = next_slot(2 * 16384);
-          tma_load_2d(dst, &tmW1, &w_full[slot], (2 * hb) * 64, 128 * j);
-          tma_load_2d(dst + 16384, &tmW1, &w_full[slot], (2 * hb + 1) * 64, 128 * j);
+      auto load_w1 = [&](int j) {  // W1 rows [128j, 128j+128), one slot per k-block
+        for (int kb = 0; kb < KB; ++kb) {
+          uint8_t* dst = next_slot(16384);
+          tma_load_2d(dst, &tmW1, &w_full[slot], kb * 64, 128 * j);
           adv();
         }
       };
-      auto load_w2 = [&](int j) {  // W2^T all D rows, k columns [128j, 128j+128) as two k-blocks
-        for (int kb = 0; kb < 2; ++kb) {
-          uint8_t* dst = next_slot(32768);
-          tma_load_2d(dst, &tmW2, &w_full[slot], 128 * j + 64 * kb, 0);
-          adv();
-        }
+      auto load_w2 = [&](int j) {  // W2 (K-major [D, F]) k columns [128j, 128j+128): (k-block, row half)
+        for (int kb = 0; kb < 2; ++kb)
+          for (int nh = 0; nh < D / 128; ++nh) {
+            uint8_t* dst = next_slot(16384);
+            tma_load_2d(dst, &tmW2, &w_full[slot], 128 * j + 64 * kb, 128 * nh);
+            adv();
+          }
       };
       for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
         mbar_wait(a_empty, (it & 1) ^ 1);
@@ -162,11 +164,10 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     // ============================================================ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc1 = make_idesc_bf16(128, 128, 0);
-      constexpr uint32_t idesc2 = make_idesc_bf16(128, D, 0);
       int slot = 0;
       uint32_t sph = 0;
       int it = 0;
-      uint32_t a1_cnt[2] = {0, 0}, h_cnt[2] = {0, 0}, a2_cnt = 0;
+      uint32_t a1_ph = 0, h_ph = 0, a2_cnt = 0;  // bit b: phase of barrier [b]
       auto take = [&]() -> uint32_t {
         mbar_wait(&w_full[slot], sph);
         tc_fence_after();
@@ -179,41 +180,38 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
       const uint32_t a_base = smem_u32(smem + S::A_OFF);
       auto mma1 = [&](int j) {
         const int b = j & 1;
-        mbar_wait(&a1_empty[b], (a1_cnt[b] & 1) ^ 1);
-        ++a1_cnt[b];
+        mbar_wait(&a1_empty[b], ((a1_ph >> b) & 1) ^ 1);
+        a1_ph ^= 1u << b;
         tc_fence_after();
-        for (int hb = 0; hb < KB / 2; ++hb) {
+        for (int kb = 0; kb < KB; ++kb) {
           const uint32_t w = take();
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int kb = 2 * hb + q;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_ss(tmem + ACC1 + b * 128, make_smem_desc(a_base + kb * 16384 + k * 32, 16, 1024, kLayoutSW128),
-                     make_smem_desc(w + q * 16384 + k * 32, 16, 1024, kLayoutSW128), idesc1, (kb | k) != 0);
-          }
+          for (int k = 0; k < 4; ++k)
+            mma_ss(tmem + ACC1 + b * 128, make_smem_desc(a_base + kb * 16384 + k * 32, 16, 1024, kLayoutSW128),
+                   make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128), idesc1, (kb | k) != 0);
           give();
         }
         mma_commit(&a1_full[b]);
       };
       auto mma2 = [&](int j) {
         const int b = j & 1;
-        mbar_wait(&h_full[b], h_cnt[b] & 1);
-        ++h_cnt[b];
+        mbar_wait(&h_full[b], (h_ph >> b) & 1);
+        h_ph ^= 1u << b;
         if (j == 0) {  // acc2 must have been drained by the previous tile's epilogue
           mbar_wait(a2_empty, (a2_cnt & 1) ^ 1);
           ++a2_cnt;
         }
         tc_fence_after();
         const uint32_t h_base = smem_u32(smem + S::H_OFF + b * S::H_BYTES);
-        for (int kb = 0; kb < 2; ++kb) {
-          const uint32_t w = take();
+        for (int kb = 0; kb < 2; ++kb)
+          for (int nh = 0; nh < D / 128; ++nh) {  // acc2 columns [128 nh, 128 nh + 128)
+            const uint32_t w = take();
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            mma_ss(tmem + ACC2, make_smem_desc(h_base + kb * 16384 + k * 32, 16, 1024, kLayoutSW128),
-                   make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128), idesc2, (j | kb | k) != 0);
-          give();
-        }
+            for (int k = 0; k < 4; ++k)
+              mma_ss(tmem + ACC2 + nh * 128, make_smem_desc(h_base + kb * 16384 + k * 32, 16, 1024, kLayoutSW128),
+                     make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128), idesc1, (j | kb | k) != 0);
+            give();
+          }
         mma_commit(&h_empty[b]);
       };
       for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
@@ -243,7 +241,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     asm volatile("bar.sync 5, 256;" ::: "memory");
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const int r_in_tile = quarter * 32 + lane;
-    uint32_t a1_cnt[2] = {0, 0}, h_cnt[2] = {0, 0};
+    uint32_t a1_ph = 0, h_ph = 0;  // bit b: phase of barrier [b]
     uint32_t xph = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
@@ -251,8 +249,8 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
       // ---- hidden chunks: GELU(acc1 + b1) -> bf16 -> H[j&1] (SW128 K-major, k-block = half)
       for (int j = 0; j < n_chunks; ++j) {
         const int b = j & 1;
-        mbar_wait(&a1_full[b], a1_cnt[b] & 1);
-        ++a1_cnt[b];
+        mbar_wait(&a1_full[b], (a1_ph >> b) & 1);
+        a1_ph ^= 1u << b;
         tc_fence_after();
         uint32_t r0[32], r1[32];
         const uint32_t ta = tmem + lane_off + ACC1 + b * 128 + half * 64;
@@ -264,8 +262,8 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         if (lane == 0) mbar_arrive(&a1_empty[b]);
         // H[b] may still be read by MMA2(j-2): wait for its commit
         if (j >= 2) {
-          mbar_wait(&h_empty[b], h_cnt[b] & 1);
-          ++h_cnt[b];
+          mbar_wait(&h_empty[b], (h_ph >> b) & 1);
+          h_ph ^= 1u << b;
         }
         uint8_t* hrow = smem + S::H_OFF + b * S::H_BYTES + half * 16384 + r_in_tile * 128;
         const int col0 = 128 * j + half * 64;
@@ -274,10 +272,14 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
           const uint32_t* r = (q < 4) ? r0 : r1;
           const int o = (q & 3) * 8;
           uint32_t pk[4];
+          const float4 bl = *reinterpret_cast<const float4*>(b1_s + col0 + 8 * q);      // smem broadcast
+          const float4 bh = *reinterpret_cast<const float4*>(b1_s + col0 + 8 * q + 4);
+          const float bv[8] = {bl.x, bl.y, bl.z, bl.w, bh.x, bh.y, bh.z, bh.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            float a = __uint_as_float(r[o + 2 * e]) + b1_s[col0 + 8 * q + 2 * e];
-            float c = __uint_as_float(r[o + 2 * e + 1]) + b1_s[col0 + 8 * q + 2 * e + 1];
+            float a, c;
+            fma2x(a, c, __uint_as_float(r[o + 2 * e]), __uint_as_float(r[o + 2 * e + 1]), 1.f, 1.f, bv[2 * e],
+                  bv[2 * e + 1]);
             gelu2(a, c);
             pk[e] = pack_bf16x2(a, c);
           }
@@ -290,8 +292,8 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
       // the last two H buffers' MMA2 commits (consumed so the phase counts stay in step)
       for (int j = (n_chunks >= 2 ? n_chunks - 2 : 0); j < n_chunks; ++j) {
         const int b = j & 1;
-        mbar_wait(&h_empty[b], h_cnt[b] & 1);
-        ++h_cnt[b];
+        mbar_wait(&h_empty[b], (h_ph >> b) & 1);
+        h_ph ^= 1u << b;
       }
       // ---- x += acc2 + b2  (+ next LayerNorm)
       if (p.staged) {

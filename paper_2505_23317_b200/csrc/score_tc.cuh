@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(SCORE_THREADS, 1)
   const int row0 = b * Nc;
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
   uint8_t* sK = smem;
   uint8_t* sQ = smem + S::T_BYTES;  // [2]
   float* lse_s = reinterpret_cast<float*>(sQ + 2 * S::T_BYTES);  // [2][128]

@@ -48,6 +48,32 @@ def test_gemm_matches_torch_fp32(M, N, K, epi):
         torch.testing.assert_close(out.float(), ref.to(torch.bfloat16).float(), rtol=1e-2, atol=1e-2)
 
 
+def test_gemm_gelu_epilogue_error_bound():
+    """The bias+GELU epilogue against exact-erf GELU (reading R4) over every bf16 z in
+    [-12, 12]: |out - GELU(z)| <= half a bf16 ulp of the output (final rounding) +
+    |z| * 3.9e-4 (the tanh-form Phi approximation incl. tanh.approx)."""
+    from scipy.special import erf
+    z = np.arange(-12.0, 12.0, 1.0 / 64.0)
+    M, N, K = len(z), 64, 64
+    A = torch.zeros(M, K, dtype=torch.bfloat16)
+    A[:, 0] = torch.from_numpy(z).to(torch.bfloat16)
+    zb = A[:, 0].double().numpy()
+    W = torch.zeros(N, K, dtype=torch.bfloat16)
+    W[:, 0] = 1.0
+    bias = torch.zeros(N, device="cuda")
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    A, W = A.cuda(), W.cuda()
+    assert LIB.cfdx_gemm(M, N, K, A.data_ptr(), W.data_ptr(), bias.data_ptr(), 1, out.data_ptr(), None, _s()) == 0
+    torch.cuda.synchronize()
+    got = out.double().cpu().numpy()
+    assert (got == got[:, :1]).all()
+    exact = zb * 0.5 * (1.0 + erf(zb / np.sqrt(2.0)))
+    ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(exact), 1e-30))) - 7)
+    bound = 0.5 * ulp + np.abs(zb) * 3.9e-4 + 1e-30
+    err = np.abs(got[:, 0] - exact)
+    assert (err <= bound).all(), (zb[np.argmax(err / bound)], err.max())
+
+
 # ------------------------------------------------------------------ attention
 def _attn_ref(qkv, cu, d, nh):
     out = torch.zeros(qkv.shape[0], d, device=qkv.device)

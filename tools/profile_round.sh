@@ -15,14 +15,15 @@ fi
 if [ "$WHAT" != list ]; then
   # name  demangled-name regex  launches to skip (warm-up first)
   while read -r name rx skip; do
+    if [ -n "${ONLY:-}" ] && ! echo " $ONLY " | grep -q " $name "; then continue; fi
     timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
       -k "regex:$rx" --launch-skip "$skip" -c 1 -o "$OUT/full_${TAG}_$name" -f $BENCH \
       > "$OUT/full_${TAG}_$name.log" 2>&1
   done <<LIST
 mlp mlp_tc_kernel 20
 attn attn4_tc_kernel 20
-oproj gemm_tc_kernel<256,.2,.5 20
-qkv gemm_tc_kernel<256,.4,.0 20
+oproj gemm_tc_kernel<.int.256,..int.2,..int.5 20
+qkv gemm_tc_kernel<.int.256,..int.[34],..int.0 20
 score score_tc_kernel 2
 gather gather_kernel 2
 LIST

@@ -1,0 +1,137 @@
+// tc_micro.cu — microbenchmarks of the sm_100a resources the hot kernels lean on:
+//   1. TMEM read bandwidth (tcgen05.ld 32x32b.x32) vs number of reading warps per SM
+//   2. tcgen05.mma (kind::f16, SS) issue/completion rate for M=128, N in {64,128,256}
+//   3. both at once (one MMA thread + 8 TMEM-reading warps), to expose contention
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2505_23317_b200/csrc tools/tc_micro.cu -o tc_micro
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "ptx.cuh"
+
+using namespace cfd;
+
+__global__ void tmem_ld_bw(int iters, int nwarps, unsigned long long* cyc, uint32_t* sink) {
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = slot + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+  uint32_t acc = 0;
+  const unsigned long long t0 = clock64();
+  if (warp < nwarps) {
+    for (int i = 0; i < iters; ++i) {
+      uint32_t r[32];
+      tmem_ld32(tm + ((i * 32 + warp * 64) & 511), r);
+      tmem_wait_ld();
+#pragma unroll
+      for (int k = 0; k < 32; ++k) acc ^= r[k];
+    }
+  }
+  __syncthreads();
+  const unsigned long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  if (acc == 0x12345678u) sink[threadIdx.x] = acc;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(slot);
+}
+
+template <int N>
+__global__ void mma_rate(int iters, int ld_warps, unsigned long long* cyc, uint32_t* sink) {
+  extern __shared__ uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < (128 + 256) * 64 * 2 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (warp == 0) tmem_alloc<512>(&slot);
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = slot;
+  const unsigned long long t0 = clock64();
+  uint32_t acc = 0;
+  if (warp == 0) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(128, N, 0);
+      const uint32_t a = smem_u32(sm), b = smem_u32(sm + 128 * 64 * 2);
+      for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_ss(tm, make_smem_desc(a + k * 32, 16, 1024, kLayoutSW128), make_smem_desc(b + k * 32, 16, 1024, kLayoutSW128),
+                 idesc, 1);
+      }
+      mma_commit(&bar);
+      mbar_wait(&bar, 0);
+    }
+    __syncwarp();
+  } else if (warp - 1 < ld_warps) {
+    // TMEM readers on the columns the MMA does not write (256..511)
+    const uint32_t t = tm + (static_cast<uint32_t>((warp & 3) * 32) << 16) + 256;
+    for (int i = 0; i < iters; ++i) {
+      uint32_t r[32];
+      tmem_ld32(t + ((i * 32) & 255), r);
+      tmem_wait_ld();
+#pragma unroll
+      for (int k = 0; k < 32; ++k) acc ^= r[k];
+    }
+  }
+  const unsigned long long t1 = clock64();
+  __syncthreads();
+  if (warp == 0 && lane == 0) cyc[blockIdx.x] = t1 - t0;
+  if (warp > 0 && lane == 0) cyc[gridDim.x * warp + blockIdx.x] = t1 - t0;
+  if (acc == 0x12345678u) sink[threadIdx.x] = acc;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(slot);
+}
+
+int main() {
+  unsigned long long* cyc;
+  uint32_t* sink;
+  const int grid = 148;
+  cudaMalloc(&cyc, sizeof(unsigned long long) * grid * 32);
+  cudaMalloc(&sink, 4096);
+  unsigned long long h[148 * 32];
+  // 1. TMEM read bandwidth
+  for (int nw : {1, 2, 4, 8, 12, 16}) {
+    const int iters = 4096;
+    tmem_ld_bw<<<grid, 512>>>(iters, nw, cyc, sink);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h, cyc, sizeof(unsigned long long) * grid, cudaMemcpyDeviceToHost);
+    double c = 0;
+    for (int i = 0; i < grid; ++i) c += h[i];
+    c /= grid;
+    const double bytes = (double)nw * iters * 32 * 32 * 4;
+    printf("tmem_ld  warps=%2d  cycles=%.0f  bytes/clk/SM=%.1f\n", nw, c, bytes / c);
+  }
+  // 2./3. MMA rate alone and with TMEM readers
+  const int smem = (128 + 256) * 64 * 2 + 1024;
+  cudaFuncSetAttribute(mma_rate<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_rate<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_rate<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  for (int ldw : {0, 4, 8}) {
+    for (int n : {64, 128, 256}) {
+      const int iters = 2048;
+      if (n == 64) mma_rate<64><<<grid, 32 * 9, smem>>>(iters, ldw, cyc, sink);
+      if (n == 128) mma_rate<128><<<grid, 32 * 9, smem>>>(iters, ldw, cyc, sink);
+      if (n == 256) mma_rate<256><<<grid, 32 * 9, smem>>>(iters, ldw, cyc, sink);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
+      cudaMemcpy(h, cyc, sizeof(unsigned long long) * grid * 9, cudaMemcpyDeviceToHost);
+      double c = 0, cl = 0;
+      for (int i = 0; i < grid; ++i) { c += h[i]; if (ldw) cl += h[grid + i]; }
+      c /= grid; cl /= grid;
+      const double flop = 2.0 * 128 * n * 16 * 4 * iters;
+      printf("mma N=%3d ld_warps=%d  mma cycles=%.0f  FLOP/clk/SM=%.0f (peak ~8192)  cyc/instr=%.1f", n, ldw, c,
+             flop / c, c / (4.0 * iters));
+      if (ldw) printf("  | ld warp cycles=%.0f  ld bytes/clk/SM=%.1f", cl, (double)ldw * iters * 4096 / cl);
+      printf("\n");
+    }
+  }
+  return 0;
+}
