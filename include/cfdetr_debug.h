@@ -67,14 +67,21 @@ int32_t cfdx_probe_count(int32_t kind);
 /* Tuning switches (process-wide): key 0 = attention kernel variant (1: one query tile
  * per CTA, 2: persistent two-tile ping-pong with 128-key steps, 3: same with 64-key
  * steps and double-buffered S, 4: three query tiles / warpgroups per CTA); key 1 = how many of every 16
- * column pairs variant 2 exponentiates with the FMA-pipe polynomial instead of MUFU
- * (0, 2, 4, 6 or 8; default 4); key 2 = fused MLP kernel on (1, default) / off (0); key 3 = TMA-staged
- * residual + LayerNorm epilogue of the O-projection on (1, default) / off (0). */
+ * column pairs variants 2-4 exponentiate with the FMA-pipe polynomial instead of MUFU
+ * (0, 2, 4, 6, 8; 10 and 12 for variant 4 only; default 4); key 2 = fused MLP kernel on
+ * (1, default) / off (0); key 3 = TMA-staged residual(+LayerNorm) epilogues of the
+ * O-projection and the fused MLP on (1, default) / off (0).  Other values: CFD_E_ARG. */
 cfd_status cfdx_set_option(int32_t key, int32_t value);
 
 /* Number of kernels the library launched since load (host counter; for bench's
  * gpu_launches claim). */
 int64_t cfdx_launch_count(void);
+
+/* Pipeline event trace of the fused MLP kernel (debug library only, built with
+ * -DCFD_TRACE): copies the SM clock64() stamps the last fused-MLP launch recorded for the
+ * first two tiles of every CTA, 148 x 96 uint64 (layout in csrc/mlp_tc.cuh), into the host
+ * buffer dst (n_words >= 148 * 96).  CFD_E_ARG when the library was built without tracing. */
+cfd_status cfdx_mlp_trace(uint64_t* dst, int32_t n_words);
 
 #ifdef __cplusplus
 }

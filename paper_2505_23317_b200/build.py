@@ -38,14 +38,14 @@ def _newest_src_mtime() -> float:
 
 
 def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
-    """debug=True builds libcfdetr_dbg.so with -DCFD_HANG_CHECK (barrier waits trap with a
+    """debug=True builds libcfdetr_dbg.so with -DCFD_HANG_CHECK -DCFD_TRACE (barrier waits trap with a
     message instead of hanging); load it with CFD_LIB_DEBUG=1."""
     out = LIB_DBG if debug else LIB
     if not force and os.path.exists(out) and os.path.getmtime(out) >= _newest_src_mtime():
         return out
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     tmp = out + ".tmp"
-    extra = ["-DCFD_HANG_CHECK"] if debug else []
+    extra = ["-DCFD_HANG_CHECK", "-DCFD_TRACE"] if debug else []
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-shared", "-o", tmp, *srcs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     log = os.path.join(HERE, "build_dbg.log" if debug else "build.log")

@@ -281,6 +281,8 @@ cudaError_t launch_attention(const CUtensorMap& tq, const AttnParams& p, int max
         case 2: e = launch_attn2_t<4, 2>(tq, p, items_ub, nh, T, s); break;
         case 6: e = launch_attn2_t<4, 6>(tq, p, items_ub, nh, T, s); break;
         case 8: e = launch_attn2_t<4, 8>(tq, p, items_ub, nh, T, s); break;
+        case 10: e = launch_attn2_t<4, 10>(tq, p, items_ub, nh, T, s); break;
+        case 12: e = launch_attn2_t<4, 12>(tq, p, items_ub, nh, T, s); break;
         default: e = launch_attn2_t<4, 4>(tq, p, items_ub, nh, T, s); break;
       }
     }
@@ -520,6 +522,18 @@ const char* cfd_status_str(cfd_status s) {
 
 int64_t cfdx_launch_count(void) { return g_launches.load(); }
 
+cfd_status cfdx_mlp_trace(uint64_t* dst, int32_t n_words) {
+#ifdef CFD_TRACE
+  if (!dst || n_words < MLP_TRACE_WORDS) return CFD_E_ARG;
+  CFD_CUDA(cudaMemcpyFromSymbol(dst, g_mlp_trace, sizeof(unsigned long long) * MLP_TRACE_WORDS));
+  return CFD_OK;
+#else
+  (void)dst;
+  (void)n_words;
+  return CFD_E_ARG;
+#endif
+}
+
 cfd_status cfdx_probe_install(int32_t kind, void* const* h_start, void* const* h_end, int32_t capacity) {
   if (kind < 0 || kind >= kProbeKinds || capacity < 0 || (capacity > 0 && (!h_start || !h_end))) return CFD_E_ARG;
   Probe& p = g_probe[kind];
@@ -540,7 +554,7 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
       g_attn_variant = value;
       return CFD_OK;
     case 1:
-      if (value != 0 && value != 2 && value != 4 && value != 6 && value != 8) return CFD_E_ARG;
+      if (value < 0 || value > 12 || (value & 1)) return CFD_E_ARG;  // 10, 12: variant 4 only
       g_attn_npp = value;
       return CFD_OK;
     case 2:

@@ -3,18 +3,27 @@
 //   x += GELU(h W_1^T + b_1) W_2^T + b_2,     h = LN2(x) (bf16, from the O-projection epilogue)
 //   (+ optionally hn = LN1_next(x) for the next layer, as EPI_F32_RESID_LN does)
 //
-// One persistent CTA per SM walks 128-row tiles.  Per tile the A operand h (128 x d bf16) is
-// loaded once by TMA and the hidden dimension F is processed in 128-column chunks j:
-//   MMA1(j):  acc1[j&1] (TMEM, 128 cols) = h . W1[j]^T            (K = d)
-//   GELU(j):  8 epilogue warps: acc1 + b1 -> polynomial-erf GELU -> bf16 -> shared memory H[j&1]
-//             written directly in the 128B-swizzled K-major layout the tensor core reads
-//   MMA2(j):  acc2 (TMEM, 256 cols) += H[j&1] . W2[:, j]^T          (K = 128)
-// issued as MMA1(j+1) before MMA2(j) so GELU(j) overlaps the tensor core.  The hidden
-// activations never leave the SM.  TMEM: acc1 x2 (256) + acc2 (256) = 512 columns.
-// Weights stream through a ring of four 16 KB slots (128 rows x one 64-wide k-block each:
-// W1 chunk = D/64 slots, W2 chunk = 2 k-blocks x 2 row halves) in exactly the order the MMA
-// warp consumes them; small slots keep 3-4 loads in flight so the L2 latency is hidden
-// (with two 32 KB slots only one load could overlap an MMA and the ring was latency-bound).
+// One persistent CTA per SM walks 128-row tiles; the hidden dimension F is processed in
+// 128-column chunks j:
+//   MMA1(j):  acc1 (TMEM, 128 cols) = h . W1[j]^T     (K = d; A = h from TMEM: "TS" form)
+//   GELU(j):  8 epilogue warps: acc1 + b1 -> GELU -> bf16 -> shared memory H[j&1], written
+//             directly in the 128B-swizzled K-major layout the tensor core reads
+//   MMA2(j):  acc2 (TMEM, 256 cols) += H[j&1] . W2[:, j]^T  (K = 128, N = 256)
+// issued as MMA1(j+1) before MMA2(j) so GELU(j) overlaps the tensor core (acc1 is released
+// as soon as the epilogue has moved it into registers).  The hidden activations never leave
+// the SM.
+//
+// Resource plan (measured, profiles/r1_tc_micro.txt): the tensor core reads shared memory at
+// 128 B/clk/SM, which an SS-form M=128 N=128 MMA alone saturates.  Keeping the h tile in
+// TMEM (A operand of MMA1) and issuing MMA2 as one N=256 MMA cuts the per-chunk smem reads
+// to W1 64 KB + H 32 KB + W2 64 KB.  TMEM: h tile [0,128) (bf16 pairs), acc1 [128,256),
+// acc2 [256,512).  Everything that arrives by TMA — the h tile (4 pieces) and the weights —
+// streams through ONE ring of eight 16 KB slots in consumption order: per tile
+//   h k-blocks 0..3 | W1(0) k-blocks 0..3 | { W1(j) k-blocks 0..3, W2(j-1) } j=1..n-1 | W2(n-1)
+// with W2(j) = (k-block 0: rows 0-127, 128-255), (k-block 1: rows 0-127, 128-255), so every
+// group is 4 slots and a W2 k-block always occupies two adjacent slots (one 256-row operand).
+// The 128 KB ring keeps ~2 operands of loads in flight ahead of the MMAs.  The epilogue warps
+// consume the h pieces (smem -> TMEM copy), the MMA warp everything else.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -40,16 +49,33 @@ struct MlpParams {
 };
 
 constexpr int MLP_THREADS = 320;  // TMA warp, MMA warp, 8 epilogue warps
-constexpr int MLP_SLOTS = 4;
+
+// Debug-library pipeline trace (-DCFD_TRACE, read by cfdx_mlp_trace): per CTA 96 words,
+// tiles it = 0, 1 at word it * 48 + event, clock64() of
+//   0 producer issues the tile's first h piece     1 epilogue: last h piece landed
+//   2 epilogue: h tile in TMEM (ht_full arrive)     3 MMA: ht_full observed
+//   4+j MMA: MMA1(j) issue start (a1_empty passed)  12+j MMA: MMA2(j) issue start (h_full passed)
+//   20+j epilogue: a1_full(j) observed              28+j epilogue: GELU(j) written (h_full arrive)
+//   36 epilogue: final epilogue starts (before its a2_full wait)   37 epilogue: tile done
+// (j < 8; epilogue events from epilogue thread 0), word 47 of tile 0 = kernel start.
+constexpr int MLP_TRACE_WORDS = 148 * 96;
+#ifdef CFD_TRACE
+__device__ unsigned long long g_mlp_trace[MLP_TRACE_WORDS];
+#define MLP_TR(it_, ev_)                                                                   \
+  do {                                                                                    \
+    if ((it_) < 2 && blockIdx.x < 148) g_mlp_trace[blockIdx.x * 96 + (it_) * 48 + (ev_)] = clock64(); \
+  } while (0)
+#else
+#define MLP_TR(it_, ev_) do { } while (0)
+#endif
+constexpr int MLP_SLOTS = 8;
 
 template <int D>
 struct MlpSmem {
   static_assert(D == 256, "fused MLP is laid out for d = 256 (acc2 = 256 TMEM columns)");
-  static constexpr int A_BYTES = 128 * D * 2;             // 64 KB: h tile, D/64 k-blocks of 16 KB
   static constexpr int H_BYTES = 128 * 128 * 2;           // 32 KB: GELU chunk, 2 k-blocks
-  static constexpr int SLOT_BYTES = 16384;
-  static constexpr int A_OFF = 0;
-  static constexpr int H_OFF = A_OFF + A_BYTES;           // [2]
+  static constexpr int SLOT_BYTES = 16384;                // 128 rows x 64 bf16 (one SW128 k-block)
+  static constexpr int H_OFF = 0;                         // [2]
   static constexpr int W_OFF = H_OFF + 2 * H_BYTES;       // [MLP_SLOTS]
   static constexpr int BAR_OFF = W_OFF + MLP_SLOTS * SLOT_BYTES;
   static constexpr int STATS_OFF = BAR_OFF + 512;         // float2 [2][128]
@@ -70,13 +96,12 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
-  uint64_t* a_full = bars + 0;
-  uint64_t* a_empty = bars + 1;
-  uint64_t* w_full = bars + 2;               // [MLP_SLOTS]
+  uint64_t* w_full = bars;                   // [MLP_SLOTS]
   uint64_t* w_empty = w_full + MLP_SLOTS;    // [MLP_SLOTS]
-  uint64_t* a1_full = w_empty + MLP_SLOTS;   // [2]
-  uint64_t* a1_empty = a1_full + 2;          // [2]
-  uint64_t* h_full = a1_empty + 2;           // [2]
+  uint64_t* ht_full = w_empty + MLP_SLOTS;   // h tile copied into TMEM
+  uint64_t* a1_full = ht_full + 1;
+  uint64_t* a1_empty = a1_full + 1;
+  uint64_t* h_full = a1_empty + 1;           // [2]
   uint64_t* h_empty = h_full + 2;            // [2]
   uint64_t* a2_full = h_empty + 2;
   uint64_t* a2_empty = a2_full + 1;
@@ -93,65 +118,56 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   const bool do_ln = p.ln_g != nullptr;
   const int m_tiles = ((do_ln ? pad_rows(M, p.ln_cap) : M) + 127) / 128;
   const int n_chunks = p.F / 128;
-  constexpr int KB = D / 64;  // k-blocks of the h tile
+  constexpr int KB = D / 64;                 // k-blocks of the h tile (= its ring pieces)
+  const int slots_per_tile = KB + 8 * n_chunks;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmH);
     tma_prefetch(&tmW1);
     tma_prefetch(&tmW2);
-    mbar_init(a_full, 1);
-    mbar_init(a_empty, 1);
     for (int i = 0; i < MLP_SLOTS; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&a1_full[i], 1);
-      mbar_init(&a1_empty[i], 8);
-      mbar_init(&h_full[i], 8);
-      mbar_init(&h_empty[i], 1);
-    }
+    mbar_init(ht_full, 1);
+    mbar_init(a1_full, 1);
+    mbar_init(a1_empty, 8);
+    for (int i = 0; i < 2; ++i) { mbar_init(&h_full[i], 8); mbar_init(&h_empty[i], 1); }
     mbar_init(a2_full, 1);
     mbar_init(a2_empty, 8);
     for (int i = 0; i < 16; ++i) mbar_init(&xbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
+#ifdef CFD_TRACE
+  if (threadIdx.x < 96 && blockIdx.x < 148) g_mlp_trace[blockIdx.x * 96 + threadIdx.x] = 0;
+#endif
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t ACC1 = 0, ACC2 = 256;
+  constexpr uint32_t HT = 0, ACC1 = 128, ACC2 = 256;
+  if (threadIdx.x == 0) MLP_TR(0, 47);
 
   if (warp == 0) {
     // ============================================================ TMA producer
     if (lane == 0) {
-      int slot = 0;
-      uint32_t sph = 0;
-      int it = 0;
-      auto next_slot = [&](int bytes) -> uint8_t* {
-        mbar_wait(&w_empty[slot], sph ^ 1);
-        mbar_expect_tx(&w_full[slot], bytes);
-        return smem + S::W_OFF + slot * S::SLOT_BYTES;
+      uint32_t pos = 0;  // ring position (slot = pos % MLP_SLOTS, phase = (pos / MLP_SLOTS) & 1)
+      auto load = [&](const CUtensorMap* tm, int x, int y) {
+        const int slot = pos % MLP_SLOTS;
+        mbar_wait(&w_empty[slot], ((pos / MLP_SLOTS) & 1) ^ 1);
+        mbar_expect_tx(&w_full[slot], S::SLOT_BYTES);
+        tma_load_2d(smem + S::W_OFF + slot * S::SLOT_BYTES, tm, &w_full[slot], x, y);
+        ++pos;
       };
-      auto adv = [&]() { if (++slot == MLP_SLOTS) { slot = 0; sph ^= 1; } };
-      auto load_w1 = [&](int j) {  // W1 rows [128j, 128j+128), one slot per k-block
-        for (int kb = 0; kb < KB; ++kb) {
-          uint8_t* dst = next_slot(16384);
-          tma_load_2d(dst, &tmW1, &w_full[slot], kb * 64, 128 * j);
-          adv();
-        }
+      auto load_w1 = [&](int j) {
+        for (int kb = 0; kb < KB; ++kb) load(&tmW1, kb * 64, 128 * j);
       };
-      auto load_w2 = [&](int j) {  // W2 (K-major [D, F]) k columns [128j, 128j+128): (k-block, row half)
+      auto load_w2 = [&](int j) {  // W2 (K-major [D, F]) k columns [128j, 128j+128)
         for (int kb = 0; kb < 2; ++kb)
-          for (int nh = 0; nh < D / 128; ++nh) {
-            uint8_t* dst = next_slot(16384);
-            tma_load_2d(dst, &tmW2, &w_full[slot], 128 * j + 64 * kb, 128 * nh);
-            adv();
-          }
+          for (int nh = 0; nh < D / 128; ++nh) load(&tmW2, 128 * j + 64 * kb, 128 * nh);
       };
-      for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
-        mbar_wait(a_empty, (it & 1) ^ 1);
-        mbar_expect_tx(a_full, S::A_BYTES);
-        for (int kb = 0; kb < KB; ++kb)
-          tma_load_2d(smem + S::A_OFF + kb * 16384, &tmH, a_full, kb * 64, tile * 128);
+      int pit = 0;
+      for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++pit) {
+        MLP_TR(pit, 0);
+        for (int kb = 0; kb < KB; ++kb) load(&tmH, kb * 64, tile * 128);
         load_w1(0);
         for (int j = 1; j < n_chunks; ++j) {
           load_w1(j);
@@ -164,64 +180,67 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     // ============================================================ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc1 = make_idesc_bf16(128, 128, 0);
-      int slot = 0;
-      uint32_t sph = 0;
+      constexpr uint32_t idesc2 = make_idesc_bf16(128, D, 0);
       int it = 0;
+      uint32_t pos = 0;
       uint32_t a1_ph = 0, h_ph = 0, a2_cnt = 0;  // bit b: phase of barrier [b]
       auto take = [&]() -> uint32_t {
-        mbar_wait(&w_full[slot], sph);
-        tc_fence_after();
+        const int slot = pos % MLP_SLOTS;
+        mbar_wait(&w_full[slot], (pos / MLP_SLOTS) & 1);
         return smem_u32(smem + S::W_OFF + slot * S::SLOT_BYTES);
       };
       auto give = [&]() {
-        mma_commit(&w_empty[slot]);
-        if (++slot == MLP_SLOTS) { slot = 0; sph ^= 1; }
+        mma_commit(&w_empty[pos % MLP_SLOTS]);
+        ++pos;
       };
-      const uint32_t a_base = smem_u32(smem + S::A_OFF);
       auto mma1 = [&](int j) {
-        const int b = j & 1;
-        mbar_wait(&a1_empty[b], ((a1_ph >> b) & 1) ^ 1);
-        a1_ph ^= 1u << b;
-        tc_fence_after();
+        mbar_wait(a1_empty, a1_ph ^ 1);
+        a1_ph ^= 1;
+        if (j < 8) MLP_TR(it, 4 + j);
         for (int kb = 0; kb < KB; ++kb) {
           const uint32_t w = take();
+          tc_fence_after();
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_ss(tmem + ACC1 + b * 128, make_smem_desc(a_base + kb * 16384 + k * 32, 16, 1024, kLayoutSW128),
-                   make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128), idesc1, (kb | k) != 0);
+            mma_ts(tmem + ACC1, tmem + HT + kb * 32 + k * 8, make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128),
+                   idesc1, (kb | k) != 0);
           give();
         }
-        mma_commit(&a1_full[b]);
+        mma_commit(a1_full);
       };
       auto mma2 = [&](int j) {
         const int b = j & 1;
         mbar_wait(&h_full[b], (h_ph >> b) & 1);
         h_ph ^= 1u << b;
+        if (j < 8) MLP_TR(it, 12 + j);
         if (j == 0) {  // acc2 must have been drained by the previous tile's epilogue
           mbar_wait(a2_empty, (a2_cnt & 1) ^ 1);
           ++a2_cnt;
         }
-        tc_fence_after();
         const uint32_t h_base = smem_u32(smem + S::H_OFF + b * S::H_BYTES);
-        for (int kb = 0; kb < 2; ++kb)
-          for (int nh = 0; nh < D / 128; ++nh) {  // acc2 columns [128 nh, 128 nh + 128)
-            const uint32_t w = take();
+        for (int kb = 0; kb < 2; ++kb) {
+          const uint32_t w = take();  // rows 0-127 of the k-block; rows 128-255 in the next slot
+          ++pos;
+          take();
+          --pos;
+          tc_fence_after();
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_ss(tmem + ACC2 + nh * 128, make_smem_desc(h_base + kb * 16384 + k * 32, 16, 1024, kLayoutSW128),
-                     make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128), idesc1, (j | kb | k) != 0);
-            give();
-          }
+          for (int k = 0; k < 4; ++k)
+            mma_ss(tmem + ACC2, make_smem_desc(h_base + kb * 16384 + k * 32, 16, 1024, kLayoutSW128),
+                   make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128), idesc2, (j | kb | k) != 0);
+          give();
+          give();
+        }
         mma_commit(&h_empty[b]);
       };
       for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
-        mbar_wait(a_full, it & 1);
+        pos = static_cast<uint32_t>(it) * slots_per_tile + KB;  // the h pieces belong to the epilogue
+        mbar_wait(ht_full, it & 1);
+        MLP_TR(it, 3);
         tc_fence_after();
         mma1(0);
-        if (n_chunks == 1) mma_commit(a_empty);
         for (int j = 1; j < n_chunks; ++j) {
           mma1(j);
-          if (j == n_chunks - 1) mma_commit(a_empty);  // h tile no longer read: next tile's TMA may start
           mma2(j - 1);
         }
         mma2(n_chunks - 1);
@@ -246,20 +265,52 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     int it = 0;
     for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
       const int row = tile * 128 + r_in_tile;
+      // ---- h tile -> TMEM (A operand of MMA1): piece kb = k-block kb -> columns [32 kb, 32 kb + 32);
+      //      this warp moves its 32 rows x 32 k (16 columns) of each piece.  The previous
+      //      tile's MMA1s are complete (its acc2 epilogue below waited for them).
+      {
+        const uint32_t pos0 = static_cast<uint32_t>(it) * slots_per_tile;
+#pragma unroll 1
+        for (int kb = 0; kb < KB; ++kb) {
+          const uint32_t pos = pos0 + kb;
+          const int slot = pos % MLP_SLOTS;
+          mbar_wait(&w_full[slot], (pos / MLP_SLOTS) & 1);
+          const uint8_t* prow = smem + S::W_OFF + slot * S::SLOT_BYTES + r_in_tile * 128;
+          uint32_t v[16];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int qq = 4 * half + q;  // logical 16-byte chunk (8 k-values)
+            const uint4 c = *reinterpret_cast<const uint4*>(prow + ((qq ^ (r_in_tile & 7)) << 4));
+            v[4 * q] = c.x; v[4 * q + 1] = c.y; v[4 * q + 2] = c.z; v[4 * q + 3] = c.w;
+          }
+          if (et == 0 && kb == KB - 1) MLP_TR(it, 1);
+          tmem_st16(tmem + lane_off + HT + kb * 32 + half * 16, v);
+          asm volatile("bar.sync 5, 256;" ::: "memory");  // all 8 warps done reading the piece
+          if (et == 0) mbar_arrive(&w_empty[slot]);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        asm volatile("bar.sync 5, 256;" ::: "memory");
+        if (et == 0) {
+          MLP_TR(it, 2);
+          mbar_arrive(ht_full);
+        }
+      }
       // ---- hidden chunks: GELU(acc1 + b1) -> bf16 -> H[j&1] (SW128 K-major, k-block = half)
       for (int j = 0; j < n_chunks; ++j) {
         const int b = j & 1;
-        mbar_wait(&a1_full[b], (a1_ph >> b) & 1);
-        a1_ph ^= 1u << b;
+        mbar_wait(a1_full, a1_ph);
+        a1_ph ^= 1;
+        if (et == 0 && j < 8) MLP_TR(it, 20 + j);
         tc_fence_after();
         uint32_t r0[32], r1[32];
-        const uint32_t ta = tmem + lane_off + ACC1 + b * 128 + half * 64;
+        const uint32_t ta = tmem + lane_off + ACC1 + half * 64;
         tmem_ld32(ta, r0);
         tmem_ld32(ta + 32, r1);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&a1_empty[b]);
+        if (lane == 0) mbar_arrive(a1_empty);
         // H[b] may still be read by MMA2(j-2): wait for its commit
         if (j >= 2) {
           mbar_wait(&h_empty[b], (h_ph >> b) & 1);
@@ -288,6 +339,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
         __syncwarp();
         if (lane == 0) mbar_arrive(&h_full[b]);
+        if (et == 0 && j < 8) MLP_TR(it, 28 + j);
       }
       // the last two H buffers' MMA2 commits (consumed so the phase counts stay in step)
       for (int j = (n_chunks >= 2 ? n_chunks - 2 : 0); j < n_chunks; ++j) {
@@ -296,6 +348,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         h_ph ^= 1u << b;
       }
       // ---- x += acc2 + b2  (+ next LayerNorm)
+      if (et == 0) MLP_TR(it, 36);
       if (p.staged) {
         const int e = warp - 2;
         uint8_t* hslice = smem + S::H_OFF + half * 16384 + quarter * 4096;
@@ -309,6 +362,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         else
           resid_ln_tma<4, false>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M, b2_s, lng_s,
                                  lnb_s, ln_stats, quarter, half, lane, a2_full, it & 1, a2_empty);
+        if (et == 0) MLP_TR(it, 37);
         continue;
       }
       mbar_wait(a2_full, it & 1);

@@ -50,6 +50,17 @@ def test_host_side_argument_errors_without_gpu(lib):
     assert lib.cfdx_gemm(10, 60, 64, 1, 1, 1, 0, 1, None, None) == -1
 
 
+def test_tuning_option_validation_without_gpu(lib):
+    """cfdx_set_option accepts the documented keys/values (cfdetr_debug.h) and rejects others."""
+    assert lib.cfdx_set_option(0, 5) == -1 and lib.cfdx_set_option(0, 0) == -1
+    assert lib.cfdx_set_option(1, 3) == -1 and lib.cfdx_set_option(1, 14) == -1 and lib.cfdx_set_option(1, -2) == -1
+    assert lib.cfdx_set_option(9, 0) == -1
+    for key, val in ((0, 3), (1, 12), (2, 0), (3, 0)):
+        assert lib.cfdx_set_option(key, val) == 0
+    for key, val in ((0, 4), (1, 4), (2, 1), (3, 1)):  # restore the defaults
+        assert lib.cfdx_set_option(key, val) == 0
+
+
 def test_config_validation_without_gpu(lib):
     cfg = L.cfd_config(640, 640, 32, 16, 256, 8, 6, 1024, 5, 8, 1e-6)
     w = L.cfd_weights()
