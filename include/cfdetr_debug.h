@@ -70,7 +70,9 @@ int32_t cfdx_probe_count(int32_t kind);
  * column pairs variants 2-4 exponentiate with the FMA-pipe polynomial instead of MUFU
  * (0, 2, 4, 6, 8; 10 and 12 for variant 4 only; default 4); key 2 = fused MLP kernel on
  * (1, default) / off (0); key 3 = TMA-staged residual(+LayerNorm) epilogues of the
- * O-projection and the fused MLP on (1, default) / off (0).  Other values: CFD_E_ARG. */
+ * O-projection and the fused MLP on (1, default) / off (0); key 4 = fused MLP as 2-CTA
+ * clusters sharing the weight stream by TMA multicast on (1) / off (0, default).  Other
+ * keys / values: CFD_E_ARG. */
 cfd_status cfdx_set_option(int32_t key, int32_t value);
 
 /* Number of kernels the library launched since load (host counter; for bench's

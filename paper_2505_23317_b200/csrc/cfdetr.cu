@@ -217,23 +217,47 @@ int g_attn_variant = 4;
 int g_attn_npp = 4;
 int g_fused_mlp = 1;  // fused MLP kernel (d == 256) instead of two GEMM launches
 int g_staged_epi = 1; // TMA-staged residual + LayerNorm epilogue for the O-projection
+int g_mlp_cluster = 0; // fused MLP as 2-CTA clusters sharing the weight stream (measured slower: off)
 
 cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUtensorMap& tw2, const MlpParams& p,
                        int rows_for_grid, cudaStream_t s, const CUtensorMap* tx = nullptr,
                        const CUtensorMap* tln = nullptr) {
-  auto kern = mlp_tc_kernel<256>;
   constexpr int smem = MlpSmem<256>::TOTAL;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(mlp_tc_kernel<256, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mlp_tc_kernel<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int tiles = (pad_rows(rows_for_grid, p.ln_cap > 0 ? p.ln_cap : rows_for_grid + 256) + 127) / 128;
-  const int grid = std::max(1, std::min(tiles, num_sms()));
   MlpParams q = p;
   q.staged = (tx != nullptr && (tln != nullptr || p.ln_g == nullptr)) ? 1 : 0;
-  kern<<<grid, MLP_THREADS, smem, s>>>(th, tw1, tw2, q, tx ? *tx : th, tln ? *tln : th);
+  const CUtensorMap& mx = tx ? *tx : th;
+  const CUtensorMap& ml = tln ? *tln : th;
+  if (g_mlp_cluster && num_sms() >= 2) {
+    // 2-CTA clusters sharing the weight stream (TMA multicast), one tile pair per cluster step
+    const int pairs = (tiles + 1) / 2;
+    const int clusters = std::max(1, std::min(pairs, num_sms() / 2));
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(2 * clusters);
+    lc.blockDim = dim3(MLP_THREADS);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = 2;
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    lc.attrs = la;
+    lc.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&lc, mlp_tc_kernel<256, 2>, th, tw1, tw2, q, mx, ml);
+    ++g_launches;
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
+  const int grid = std::max(1, std::min(tiles, num_sms()));
+  mlp_tc_kernel<256, 1><<<grid, MLP_THREADS, smem, s>>>(th, tw1, tw2, q, mx, ml);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -559,6 +583,9 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
       return CFD_OK;
     case 2:
       g_fused_mlp = value ? 1 : 0;
+      return CFD_OK;
+    case 4:
+      g_mlp_cluster = value ? 1 : 0;
       return CFD_OK;
     case 3:
       g_staged_epi = value ? 1 : 0;

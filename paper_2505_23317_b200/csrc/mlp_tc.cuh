@@ -87,7 +87,14 @@ struct MlpSmem {
   static constexpr int TOTAL = 1024 + LNSTG_OFF + 8 * 2048;
 };
 
-template <int D>
+// CL = 2: the kernel runs as 2-CTA clusters.  Each CTA still computes its own 128-row tile
+// with cta_group::1 MMAs, but the weight pieces are fetched once per pair: the two producers
+// alternate pieces and multicast each into both CTAs' ring slot, so every SM pulls half of
+// the 1 MB per tile of weights from L2 (the fused MLP is bound by that stream, profiles/
+// r1_mlp_trace.txt).  A slot is refilled once both CTAs released it (w_empty counts 2: the
+// MMA commit is multicast, the h-piece release arrives remotely).  The pair walks tile pairs
+// in lockstep; an odd last tile leaves the second CTA a masked "ghost" tile.
+template <int D, int CL>
 __global__ void __launch_bounds__(MLP_THREADS, 1)
     mlp_tc_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW1,
                   const __grid_constant__ CUtensorMap tmW2, const MlpParams p,
@@ -120,12 +127,17 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   const int n_chunks = p.F / 128;
   constexpr int KB = D / 64;                 // k-blocks of the h tile (= its ring pieces)
   const int slots_per_tile = KB + 8 * n_chunks;
+  const int rank = (CL == 2) ? static_cast<int>(cluster_ctarank()) : 0;
+  const int t_first = (CL == 2) ? 2 * static_cast<int>(cluster_id_x()) + rank : static_cast<int>(blockIdx.x);
+  const int t_step = (CL == 2) ? 2 * static_cast<int>(nclusters_x()) : static_cast<int>(gridDim.x);
+  // tile loop: CL == 2 keeps both CTAs of a pair in step (tile >= m_tiles: ghost tile)
+#define MLP_TILES(tile_) for (int tile_ = t_first; (tile_) - rank < m_tiles; tile_ += t_step)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmH);
     tma_prefetch(&tmW1);
     tma_prefetch(&tmW2);
-    for (int i = 0; i < MLP_SLOTS; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 1); }
+    for (int i = 0; i < MLP_SLOTS; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], CL); }
     mbar_init(ht_full, 1);
     mbar_init(a1_full, 1);
     mbar_init(a1_empty, 8);
@@ -140,7 +152,8 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   if (threadIdx.x < 96 && blockIdx.x < 148) g_mlp_trace[blockIdx.x * 96 + threadIdx.x] = 0;
 #endif
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL == 2) cluster_sync();  // peer barriers initialised before any multicast / remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   constexpr uint32_t HT = 0, ACC1 = 128, ACC2 = 256;
@@ -150,24 +163,29 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     // ============================================================ TMA producer
     if (lane == 0) {
       uint32_t pos = 0;  // ring position (slot = pos % MLP_SLOTS, phase = (pos / MLP_SLOTS) & 1)
-      auto load = [&](const CUtensorMap* tm, int x, int y) {
+      // every piece is expected in this CTA's slot; a weight piece is issued by one CTA of
+      // the pair (alternating) and multicast into both
+      auto load = [&](const CUtensorMap* tm, int x, int y, bool weight) {
         const int slot = pos % MLP_SLOTS;
         mbar_wait(&w_empty[slot], ((pos / MLP_SLOTS) & 1) ^ 1);
         mbar_expect_tx(&w_full[slot], S::SLOT_BYTES);
-        tma_load_2d(smem + S::W_OFF + slot * S::SLOT_BYTES, tm, &w_full[slot], x, y);
+        uint8_t* dst = smem + S::W_OFF + slot * S::SLOT_BYTES;
+        if (CL == 1 || !weight) tma_load_2d(dst, tm, &w_full[slot], x, y);
+        else if (static_cast<int>(pos & 1) == rank) tma_load_2d_mc(dst, tm, &w_full[slot], x, y, 0x3);
         ++pos;
       };
       auto load_w1 = [&](int j) {
-        for (int kb = 0; kb < KB; ++kb) load(&tmW1, kb * 64, 128 * j);
+        for (int kb = 0; kb < KB; ++kb) load(&tmW1, kb * 64, 128 * j, true);
       };
       auto load_w2 = [&](int j) {  // W2 (K-major [D, F]) k columns [128j, 128j+128)
         for (int kb = 0; kb < 2; ++kb)
-          for (int nh = 0; nh < D / 128; ++nh) load(&tmW2, 128 * j + 64 * kb, 128 * nh);
+          for (int nh = 0; nh < D / 128; ++nh) load(&tmW2, 128 * j + 64 * kb, 128 * nh, true);
       };
       int pit = 0;
-      for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++pit) {
+      MLP_TILES(tile) {
         MLP_TR(pit, 0);
-        for (int kb = 0; kb < KB; ++kb) load(&tmH, kb * 64, tile * 128);
+        ++pit;
+        for (int kb = 0; kb < KB; ++kb) load(&tmH, kb * 64, tile * 128, false);
         load_w1(0);
         for (int j = 1; j < n_chunks; ++j) {
           load_w1(j);
@@ -190,7 +208,8 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         return smem_u32(smem + S::W_OFF + slot * S::SLOT_BYTES);
       };
       auto give = [&]() {
-        mma_commit(&w_empty[pos % MLP_SLOTS]);
+        if constexpr (CL == 2) mma_commit_mc(&w_empty[pos % MLP_SLOTS], 0x3);
+        else mma_commit(&w_empty[pos % MLP_SLOTS]);
         ++pos;
       };
       auto mma1 = [&](int j) {
@@ -233,7 +252,8 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         }
         mma_commit(&h_empty[b]);
       };
-      for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
+      MLP_TILES(tile) {
+        (void)tile;
         pos = static_cast<uint32_t>(it) * slots_per_tile + KB;  // the h pieces belong to the epilogue
         mbar_wait(ht_full, it & 1);
         MLP_TR(it, 3);
@@ -245,6 +265,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         }
         mma2(n_chunks - 1);
         mma_commit(a2_full);
+        ++it;
       }
     }
   } else {
@@ -262,8 +283,8 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     const int r_in_tile = quarter * 32 + lane;
     uint32_t a1_ph = 0, h_ph = 0;  // bit b: phase of barrier [b]
     uint32_t xph = 0;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
+    MLP_TILES(tile) {
+      const int it = (tile - t_first) / t_step;
       const int row = tile * 128 + r_in_tile;
       // ---- h tile -> TMEM (A operand of MMA1): piece kb = k-block kb -> columns [32 kb, 32 kb + 32);
       //      this warp moves its 32 rows x 32 k (16 columns) of each piece.  The previous
@@ -286,7 +307,10 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
           if (et == 0 && kb == KB - 1) MLP_TR(it, 1);
           tmem_st16(tmem + lane_off + HT + kb * 32 + half * 16, v);
           asm volatile("bar.sync 5, 256;" ::: "memory");  // all 8 warps done reading the piece
-          if (et == 0) mbar_arrive(&w_empty[slot]);
+          if (et == 0) {
+            mbar_arrive(&w_empty[slot]);
+            if constexpr (CL == 2) mbar_arrive_cluster(&w_empty[slot], rank ^ 1);
+          }
         }
         tmem_wait_st();
         tc_fence_before();
@@ -451,9 +475,11 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL == 2) cluster_sync();  // the peer may still arrive on / multicast into this CTA
+  else __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
+#undef MLP_TILES
 
 }  // namespace cfd

@@ -55,9 +55,9 @@ def test_tuning_option_validation_without_gpu(lib):
     assert lib.cfdx_set_option(0, 5) == -1 and lib.cfdx_set_option(0, 0) == -1
     assert lib.cfdx_set_option(1, 3) == -1 and lib.cfdx_set_option(1, 14) == -1 and lib.cfdx_set_option(1, -2) == -1
     assert lib.cfdx_set_option(9, 0) == -1
-    for key, val in ((0, 3), (1, 12), (2, 0), (3, 0)):
+    for key, val in ((0, 3), (1, 12), (2, 0), (3, 0), (4, 1)):
         assert lib.cfdx_set_option(key, val) == 0
-    for key, val in ((0, 4), (1, 4), (2, 1), (3, 1)):  # restore the defaults
+    for key, val in ((0, 4), (1, 4), (2, 1), (3, 1), (4, 0)):  # restore the defaults
         assert lib.cfdx_set_option(key, val) == 0
 
 

@@ -242,3 +242,31 @@ def test_staged_epilogues_match_direct_epilogues():
     for a, b in zip(outs[0], outs[1]):
         rel = ((a - b).norm() / b.norm()).item()
         assert rel < 3e-3, rel
+
+
+def test_mlp_cluster_multicast_variant_matches_default_bitwise():
+    """The 2-CTA-cluster fused MLP (weights multicast to both CTAs, cfdx_set_option(4, 1)) does
+    the same per-tile arithmetic as the default single-CTA kernel: outputs agree bit for bit,
+    including an odd tile count (ghost tile in the last pair)."""
+    from paper_2505_23317_b200 import _lib as L
+    lib = L.load()
+    cfg = ci.CONFIGS["c640"]
+    enc = enc_for("c640")
+    imgs = bf16_tensor(ci.make_frames(cfg, 3, task0=5), "cuda")
+    ks = [0, 100, 37]
+    co = enc.coarse_encode(imgs)
+    sel = enc.select_regions(co["scores"], k=ks)
+    x0 = co["x0"].clone()
+    outs = []
+    try:
+        for cl in (0, 1):
+            assert lib.cfdx_set_option(4, cl) == 0
+            c2 = enc.coarse_encode(imgs)
+            ro = enc.batch_refine(imgs, x0, sel["sel_idx"], sel["sel_count"])
+            torch.cuda.synchronize()
+            n = int(ro["cu_seqlens"][-1])
+            outs.append((c2["y"].clone(), ro["y"][:n].clone()))
+    finally:
+        lib.cfdx_set_option(4, 0)
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
