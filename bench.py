@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--option", action="append", default=[],
+                    help="library tuning switch KEY=VAL (cfdx_set_option, include/cfdetr_debug.h); repeatable")
     return ap.parse_args()
 
 
@@ -64,7 +66,8 @@ def workload_config(args, n_gpus, l2_note):
             "patch_coarse": cfg.patch_coarse, "patch_fine": cfg.patch_fine, "refine_ratio_pct": args.ratio,
             "k_per_frame": k, "tokens_per_frame": cfg.n_coarse + 3 * k, "encoder": "d256/h8/L6",
             "parallelism": f"task-sharded x{n_gpus} (no collective on the hot path)", "l2": l2_note,
-            "global_batch_frames": args.frames * n_gpus}
+            "global_batch_frames": args.frames * n_gpus,
+            **({"options": list(args.option)} if getattr(args, "option", None) else {})}
 
 
 # ============================================================================ CPU oracle
@@ -239,6 +242,10 @@ def gpu_arm(args):
     ks = [k] * B
     counts = [cfg.n_coarse + (cfg.m ** 2 - 1) * k] * B
     w = ci.make_weights(cfg, seed=0)
+    for kv in args.option:
+        k_, v_ = (int(t) for t in kv.split("="))
+        if L.load().cfdx_set_option(k_, v_) != 0:
+            raise SystemExit(f"bench: invalid --option {kv}")
     enc = CFDetrEncoder(cfg, w, max_tasks=max(B, 8), device=str(dev))
     my_tasks = shard.rank_tasks(rank, world, B)  # weak scaling: B camera frames per GPU
     imgs_np = ci.make_frames(cfg, B, task0=my_tasks[0])

@@ -217,10 +217,11 @@ int g_attn_variant = 4;
 int g_attn_npp = 4;
 int g_fused_mlp = 1;  // fused MLP kernel (d == 256) instead of two GEMM launches
 int g_staged_epi = 1; // TMA-staged residual + LayerNorm epilogue for the O-projection
-int g_mlp_cluster = 0; // fused MLP as 2-CTA clusters sharing the weight stream (measured slower: off)
+int g_mlp_cluster = 0; // fused MLP as CTA pairs (cta_group::2)
 
-cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUtensorMap& tw2, const MlpParams& p,
-                       int rows_for_grid, cudaStream_t s, const CUtensorMap* tx = nullptr,
+// tw1: W1 with 128-row boxes (single-CTA kernel); tw1h: 64-row boxes (CTA-pair kernel)
+cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUtensorMap& tw1h, const CUtensorMap& tw2,
+                       const MlpParams& p, int rows_for_grid, cudaStream_t s, const CUtensorMap* tx = nullptr,
                        const CUtensorMap* tln = nullptr) {
   constexpr int smem = MlpSmem<256>::TOTAL;
   static bool attr = false;
@@ -237,7 +238,7 @@ cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUte
   const CUtensorMap& mx = tx ? *tx : th;
   const CUtensorMap& ml = tln ? *tln : th;
   if (g_mlp_cluster && num_sms() >= 2) {
-    // 2-CTA clusters sharing the weight stream (TMA multicast), one tile pair per cluster step
+    // CTA pairs (cta_group::2 MMAs, each SM holding half of every weight operand)
     const int pairs = (tiles + 1) / 2;
     const int clusters = std::max(1, std::min(pairs, num_sms() / 2));
     cudaLaunchConfig_t lc = {};
@@ -252,7 +253,7 @@ cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUte
     la[0].val.clusterDim.z = 1;
     lc.attrs = la;
     lc.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&lc, mlp_tc_kernel<256, 2>, th, tw1, tw2, q, mx, ml);
+    cudaError_t e = cudaLaunchKernelEx(&lc, mlp_tc_kernel<256, 2>, th, tw1h, tw2, q, mx, ml);
     ++g_launches;
     return e != cudaSuccess ? e : cudaGetLastError();
   }
@@ -369,6 +370,7 @@ struct LayerDev {
   float *b_qkv, *b_o, *b_1, *b_2, *ln1_g, *ln1_b, *ln2_g, *ln2_b;
   CUtensorMap tm_qkv, tm_o, tm_1, tm_2;
   CUtensorMap tm_1c, tm_2c;  // W1 / W2 with 128-row x 64-k boxes (fused MLP ring slots)
+  CUtensorMap tm_1h;         // W1 with 64-row x 64-k boxes (CTA-pair fused MLP)
 };
 
 struct cfd_ctx {
@@ -485,7 +487,7 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
       mp.ln_g = Ln.ln1_g; mp.ln_b = Ln.ln1_b; mp.ln_out = w.hbuf; mp.ln_cap = w.rows_cap;
     }
     probe_begin(PK_MLP1, s);
-    CFD_CUDA(launch_mlp(ta_h, L.tm_1c, L.tm_2c, mp, rows_grid, s, staged ? &tx : nullptr, staged ? &tln : nullptr));
+    CFD_CUDA(launch_mlp(ta_h, L.tm_1c, L.tm_1h, L.tm_2c, mp, rows_grid, s, staged ? &tx : nullptr, staged ? &tln : nullptr));
     probe_end(PK_MLP1, s);
     return CFD_OK;
   }
@@ -683,7 +685,8 @@ cfd_status cfd_create(const cfd_config* cfg, const cfd_weights* wts, void* strea
     if (!make_wmap(&ld.tm_qkv, ld.wqkv, 3 * d, d) || !make_wmap(&ld.tm_o, ld.wo, d, d) ||
         !make_wmap(&ld.tm_1, ld.w1, F, d) || !make_wmap(&ld.tm_2, ld.w2, d, F) ||
         !make_tmap(&ld.tm_1c, ld.w1, d, F, d, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_tmap(&ld.tm_2c, ld.w2, F, d, F, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+        !make_tmap(&ld.tm_2c, ld.w2, F, d, F, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap(&ld.tm_1h, ld.w1, d, F, d, GEMM_BK, 64, CU_TENSOR_MAP_SWIZZLE_128B))
       return fail(CFD_E_CUDA);
   }
   *out = c;

@@ -218,7 +218,12 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
                                              const ResidStage& st, uint32_t tbase, int row0, int col_base, int M,
                                              const float* bias_s, const float* lng_s, const float* lnb_s,
                                              float2* stats, int quarter, int half, int lane, uint64_t* tfull_bar,
-                                             uint32_t tfull_parity, uint64_t* tempty_bar) {
+                                             uint32_t tfull_parity, uint64_t* tempty_bar, int tempty_cta = -1) {
+  // tempty_cta >= 0: the accumulator-empty barrier lives in that cluster CTA (CTA-pair MMA)
+  auto release_acc = [&]() {
+    if (tempty_cta >= 0) mbar_arrive_cluster(tempty_bar, static_cast<uint32_t>(tempty_cta));
+    else mbar_arrive(tempty_bar);
+  };
   const int r = lane;
   const bool live = row0 + r < M;
   const bool one_hb = st.hb_stride == 0;
@@ -299,7 +304,7 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
       if (c + 1 == CH) {  // accumulator fully read: hand TMEM back to the MMA warp
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty_bar);
+        if (lane == 0) release_acc();
       }
       const int col0 = col_base + c * 32;
       uint32_t pk[16];
@@ -347,7 +352,7 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
       if (c + 1 == CH) {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty_bar);
+        if (lane == 0) release_acc();
       }
       const int col0 = col_base + c * 32;
 #pragma unroll

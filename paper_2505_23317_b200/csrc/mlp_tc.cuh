@@ -87,13 +87,18 @@ struct MlpSmem {
   static constexpr int TOTAL = 1024 + LNSTG_OFF + 8 * 2048;
 };
 
-// CL = 2: the kernel runs as 2-CTA clusters.  Each CTA still computes its own 128-row tile
-// with cta_group::1 MMAs, but the weight pieces are fetched once per pair: the two producers
-// alternate pieces and multicast each into both CTAs' ring slot, so every SM pulls half of
-// the 1 MB per tile of weights from L2 (the fused MLP is bound by that stream, profiles/
-// r1_mlp_trace.txt).  A slot is refilled once both CTAs released it (w_empty counts 2: the
-// MMA commit is multicast, the h-piece release arrives remotely).  The pair walks tile pairs
-// in lockstep; an odd last tile leaves the second CTA a masked "ghost" tile.
+// CL = 2: CTA-pair kernel (2-CTA clusters, tcgen05 cta_group::2).  The single-CTA kernel is
+// bound by shared-memory ingress of the weight stream (~40 B/clk/SM for 1 MB per 128-row
+// tile, profiles/r1_mlp_trace.txt; multicasting the same bytes into both CTAs did not help).
+// Here the leader CTA issues M = 256 MMAs for the pair's two tiles: each CTA keeps its own
+// 128 rows (h in its TMEM, H in its smem, acc1/acc2 in its TMEM) and holds HALF of each
+// weight operand — W1 chunk rows [64 r, 64 r + 64), W2 output rows [128 r, 128 r + 128) for
+// rank r — so per-SM weight ingress halves.  Ring: per tile h(4 local) | W1(0)(2) |
+// {W1(j)(2), W2(j-1)(2)} | W2(n-1)(2), each W1 slot = two 64-row k-blocks.  Weight halves are
+// pair-TMA loads completing on the leader's w_full (expecting both halves); the leader's
+// commits are multicast to both CTAs (w_empty, a1_full, h_empty, a2_full); the epilogues of
+// both CTAs arrive on the leader's ht_full / a1_empty / h_full / a2_empty.  The pair walks
+// tile pairs in lockstep; an odd last tile leaves CTA 1 a masked "ghost" tile.
 template <int D, int CL>
 __global__ void __launch_bounds__(MLP_THREADS, 1)
     mlp_tc_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW1,
@@ -126,7 +131,8 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   const int m_tiles = ((do_ln ? pad_rows(M, p.ln_cap) : M) + 127) / 128;
   const int n_chunks = p.F / 128;
   constexpr int KB = D / 64;                 // k-blocks of the h tile (= its ring pieces)
-  const int slots_per_tile = KB + 8 * n_chunks;
+  constexpr bool PAIR = (CL == 2);
+  const int slots_per_tile = KB + (PAIR ? 4 : 8) * n_chunks;
   const int rank = (CL == 2) ? static_cast<int>(cluster_ctarank()) : 0;
   const int t_first = (CL == 2) ? 2 * static_cast<int>(cluster_id_x()) + rank : static_cast<int>(blockIdx.x);
   const int t_step = (CL == 2) ? 2 * static_cast<int>(nclusters_x()) : static_cast<int>(gridDim.x);
@@ -137,17 +143,20 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     tma_prefetch(&tmH);
     tma_prefetch(&tmW1);
     tma_prefetch(&tmW2);
-    for (int i = 0; i < MLP_SLOTS; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], CL); }
-    mbar_init(ht_full, 1);
+    for (int i = 0; i < MLP_SLOTS; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 1); }
+    mbar_init(ht_full, CL);
     mbar_init(a1_full, 1);
-    mbar_init(a1_empty, 8);
-    for (int i = 0; i < 2; ++i) { mbar_init(&h_full[i], 8); mbar_init(&h_empty[i], 1); }
+    mbar_init(a1_empty, 8 * CL);
+    for (int i = 0; i < 2; ++i) { mbar_init(&h_full[i], 8 * CL); mbar_init(&h_empty[i], 1); }
     mbar_init(a2_full, 1);
-    mbar_init(a2_empty, 8);
+    mbar_init(a2_empty, 8 * CL);
     for (int i = 0; i < 16; ++i) mbar_init(&xbar[i], 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_alloc_2sm<512>(tmem_slot);
+    else tmem_alloc<512>(tmem_slot);
+  }
 #ifdef CFD_TRACE
   if (threadIdx.x < 96 && blockIdx.x < 148) g_mlp_trace[blockIdx.x * 96 + threadIdx.x] = 0;
 #endif
@@ -158,34 +167,56 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   constexpr uint32_t HT = 0, ACC1 = 128, ACC2 = 256;
   if (threadIdx.x == 0) MLP_TR(0, 47);
+  // arrive on a barrier the leader CTA waits on (pair epilogue -> leader MMA warp)
+  auto arrive_leader = [&](uint64_t* bar) {
+    if (PAIR && rank != 0) mbar_arrive_cluster(bar, 0);
+    else mbar_arrive(bar);
+  };
 
   if (warp == 0) {
     // ============================================================ TMA producer
     if (lane == 0) {
       uint32_t pos = 0;  // ring position (slot = pos % MLP_SLOTS, phase = (pos / MLP_SLOTS) & 1)
-      // every piece is expected in this CTA's slot; a weight piece is issued by one CTA of
-      // the pair (alternating) and multicast into both
-      auto load = [&](const CUtensorMap* tm, int x, int y, bool weight) {
+      auto load = [&](const CUtensorMap* tm, int x, int y) {  // local piece (h; all pieces if !PAIR)
         const int slot = pos % MLP_SLOTS;
         mbar_wait(&w_empty[slot], ((pos / MLP_SLOTS) & 1) ^ 1);
         mbar_expect_tx(&w_full[slot], S::SLOT_BYTES);
+        tma_load_2d(smem + S::W_OFF + slot * S::SLOT_BYTES, tm, &w_full[slot], x, y);
+        ++pos;
+      };
+      // PAIR: this CTA's half of a weight slot (nbox boxes of 16 KB / nbox), completing on the
+      // leader's w_full, which expects both halves
+      auto load_half = [&](const CUtensorMap* tm, int x0, int y0, int x1, int y1, int nbox) {
+        const int slot = pos % MLP_SLOTS;
+        mbar_wait(&w_empty[slot], ((pos / MLP_SLOTS) & 1) ^ 1);
+        if (rank == 0) mbar_expect_tx(&w_full[slot], 2 * S::SLOT_BYTES);
+        const uint32_t lb = mapa_u32(&w_full[slot], 0);
         uint8_t* dst = smem + S::W_OFF + slot * S::SLOT_BYTES;
-        if (CL == 1 || !weight) tma_load_2d(dst, tm, &w_full[slot], x, y);
-        else if (static_cast<int>(pos & 1) == rank) tma_load_2d_mc(dst, tm, &w_full[slot], x, y, 0x3);
+        tma_load_2d_2sm(dst, tm, lb, x0, y0);
+        if (nbox == 2) tma_load_2d_2sm(dst + S::SLOT_BYTES / 2, tm, lb, x1, y1);
         ++pos;
       };
       auto load_w1 = [&](int j) {
-        for (int kb = 0; kb < KB; ++kb) load(&tmW1, kb * 64, 128 * j, true);
+        if constexpr (PAIR) {  // rows [128 j + 64 rank, +64), k-blocks (0,1) and (2,3): tmW1 box = 64 rows
+          for (int q = 0; q < KB / 2; ++q)
+            load_half(&tmW1, (2 * q) * 64, 128 * j + 64 * rank, (2 * q + 1) * 64, 128 * j + 64 * rank, 2);
+        } else {
+          for (int kb = 0; kb < KB; ++kb) load(&tmW1, kb * 64, 128 * j);
+        }
       };
       auto load_w2 = [&](int j) {  // W2 (K-major [D, F]) k columns [128j, 128j+128)
-        for (int kb = 0; kb < 2; ++kb)
-          for (int nh = 0; nh < D / 128; ++nh) load(&tmW2, 128 * j + 64 * kb, 128 * nh, true);
+        if constexpr (PAIR) {  // output rows [128 rank, +128)
+          for (int kb = 0; kb < 2; ++kb) load_half(&tmW2, 128 * j + 64 * kb, 128 * rank, 0, 0, 1);
+        } else {
+          for (int kb = 0; kb < 2; ++kb)
+            for (int nh = 0; nh < D / 128; ++nh) load(&tmW2, 128 * j + 64 * kb, 128 * nh);
+        }
       };
       int pit = 0;
       MLP_TILES(tile) {
         MLP_TR(pit, 0);
         ++pit;
-        for (int kb = 0; kb < KB; ++kb) load(&tmH, kb * 64, tile * 128, false);
+        for (int kb = 0; kb < KB; ++kb) load(&tmH, kb * 64, tile * 128);
         load_w1(0);
         for (int j = 1; j < n_chunks; ++j) {
           load_w1(j);
@@ -195,10 +226,14 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ============================================================ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc1 = make_idesc_bf16(128, 128, 0);
-      constexpr uint32_t idesc2 = make_idesc_bf16(128, D, 0);
+    // ============================================================ MMA issuer (PAIR: leader only)
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc1 = make_idesc_bf16(128 * CL, 128, 0);
+      constexpr uint32_t idesc2 = make_idesc_bf16(128 * CL, D, 0);
+      auto commit = [&](uint64_t* bar) {  // PAIR: arrive in both CTAs
+        if constexpr (PAIR) mma_commit_2sm(bar, 0x3);
+        else mma_commit(bar);
+      };
       int it = 0;
       uint32_t pos = 0;
       uint32_t a1_ph = 0, h_ph = 0, a2_cnt = 0;  // bit b: phase of barrier [b]
@@ -208,24 +243,38 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         return smem_u32(smem + S::W_OFF + slot * S::SLOT_BYTES);
       };
       auto give = [&]() {
-        if constexpr (CL == 2) mma_commit_mc(&w_empty[pos % MLP_SLOTS], 0x3);
-        else mma_commit(&w_empty[pos % MLP_SLOTS]);
+        commit(&w_empty[pos % MLP_SLOTS]);
         ++pos;
       };
       auto mma1 = [&](int j) {
         mbar_wait(a1_empty, a1_ph ^ 1);
         a1_ph ^= 1;
         if (j < 8) MLP_TR(it, 4 + j);
-        for (int kb = 0; kb < KB; ++kb) {
-          const uint32_t w = take();
-          tc_fence_after();
+        if constexpr (PAIR) {
+          for (int q = 0; q < KB / 2; ++q) {
+            const uint32_t w = take();  // k-blocks 2q, 2q+1 of this CTA's 64 rows (8 KB each)
+            tc_fence_after();
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            mma_ts(tmem + ACC1, tmem + HT + kb * 32 + k * 8, make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128),
-                   idesc1, (kb | k) != 0);
-          give();
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_ts_2sm(tmem + ACC1, tmem + HT + (2 * q + i) * 32 + k * 8,
+                           make_smem_desc(w + i * (S::SLOT_BYTES / 2) + k * 32, 16, 1024, kLayoutSW128), idesc1,
+                           (q | i | k) != 0);
+            give();
+          }
+        } else {
+          for (int kb = 0; kb < KB; ++kb) {
+            const uint32_t w = take();
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_ts(tmem + ACC1, tmem + HT + kb * 32 + k * 8, make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128),
+                     idesc1, (kb | k) != 0);
+            give();
+          }
         }
-        mma_commit(a1_full);
+        commit(a1_full);
       };
       auto mma2 = [&](int j) {
         const int b = j & 1;
@@ -238,19 +287,24 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         }
         const uint32_t h_base = smem_u32(smem + S::H_OFF + b * S::H_BYTES);
         for (int kb = 0; kb < 2; ++kb) {
-          const uint32_t w = take();  // rows 0-127 of the k-block; rows 128-255 in the next slot
-          ++pos;
-          take();
-          --pos;
+          const uint32_t w = take();  // !PAIR: rows 0-127 of the k-block, rows 128-255 in the next slot
+          if constexpr (!PAIR) {
+            ++pos;
+            take();
+            --pos;
+          }
           tc_fence_after();
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            mma_ss(tmem + ACC2, make_smem_desc(h_base + kb * 16384 + k * 32, 16, 1024, kLayoutSW128),
-                   make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128), idesc2, (j | kb | k) != 0);
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = make_smem_desc(h_base + kb * 16384 + k * 32, 16, 1024, kLayoutSW128);
+            const uint64_t bd = make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128);
+            if constexpr (PAIR) mma_ss_2sm(tmem + ACC2, ad, bd, idesc2, (j | kb | k) != 0);
+            else mma_ss(tmem + ACC2, ad, bd, idesc2, (j | kb | k) != 0);
+          }
           give();
-          give();
+          if constexpr (!PAIR) give();
         }
-        mma_commit(&h_empty[b]);
+        commit(&h_empty[b]);
       };
       MLP_TILES(tile) {
         (void)tile;
@@ -264,7 +318,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
           mma2(j - 1);
         }
         mma2(n_chunks - 1);
-        mma_commit(a2_full);
+        commit(a2_full);
         ++it;
       }
     }
@@ -307,17 +361,14 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
           if (et == 0 && kb == KB - 1) MLP_TR(it, 1);
           tmem_st16(tmem + lane_off + HT + kb * 32 + half * 16, v);
           asm volatile("bar.sync 5, 256;" ::: "memory");  // all 8 warps done reading the piece
-          if (et == 0) {
-            mbar_arrive(&w_empty[slot]);
-            if constexpr (CL == 2) mbar_arrive_cluster(&w_empty[slot], rank ^ 1);
-          }
+          if (et == 0) mbar_arrive(&w_empty[slot]);
         }
         tmem_wait_st();
         tc_fence_before();
         asm volatile("bar.sync 5, 256;" ::: "memory");
         if (et == 0) {
           MLP_TR(it, 2);
-          mbar_arrive(ht_full);
+          arrive_leader(ht_full);
         }
       }
       // ---- hidden chunks: GELU(acc1 + b1) -> bf16 -> H[j&1] (SW128 K-major, k-block = half)
@@ -334,7 +385,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(a1_empty);
+        if (lane == 0) arrive_leader(a1_empty);
         // H[b] may still be read by MMA2(j-2): wait for its commit
         if (j >= 2) {
           mbar_wait(&h_empty[b], (h_ph >> b) & 1);
@@ -362,7 +413,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         }
         fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
         __syncwarp();
-        if (lane == 0) mbar_arrive(&h_full[b]);
+        if (lane == 0) arrive_leader(&h_full[b]);
         if (et == 0 && j < 8) MLP_TR(it, 28 + j);
       }
       // the last two H buffers' MMA2 commits (consumed so the phase counts stay in step)
@@ -382,10 +433,11 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         const uint32_t tb = tmem + lane_off + ACC2 + half * 128;
         if (do_ln)
           resid_ln_tma<4, true>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M, b2_s, lng_s, lnb_s,
-                                ln_stats, quarter, half, lane, a2_full, it & 1, a2_empty);
+                                ln_stats, quarter, half, lane, a2_full, it & 1, a2_empty, PAIR && rank ? 0 : -1);
         else
           resid_ln_tma<4, false>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M, b2_s, lng_s,
-                                 lnb_s, ln_stats, quarter, half, lane, a2_full, it & 1, a2_empty);
+                                 lnb_s, ln_stats, quarter, half, lane, a2_full, it & 1, a2_empty,
+                                 PAIR && rank ? 0 : -1);
         if (et == 0) MLP_TR(it, 37);
         continue;
       }
@@ -412,7 +464,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         if (c == 3) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(a2_empty);
+          if (lane == 0) arrive_leader(a2_empty);
         }
         if (live) {
           const int col0 = half * 128 + c * 32;
@@ -478,7 +530,10 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   if constexpr (CL == 2) cluster_sync();  // the peer may still arrive on / multicast into this CTA
   else __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc<512>(tmem);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_dealloc_2sm<512>(tmem);
+    else tmem_dealloc<512>(tmem);
+  }
 }
 #undef MLP_TILES
 

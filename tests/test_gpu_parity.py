@@ -244,10 +244,11 @@ def test_staged_epilogues_match_direct_epilogues():
         assert rel < 3e-3, rel
 
 
-def test_mlp_cluster_multicast_variant_matches_default_bitwise():
-    """The 2-CTA-cluster fused MLP (weights multicast to both CTAs, cfdx_set_option(4, 1)) does
-    the same per-tile arithmetic as the default single-CTA kernel: outputs agree bit for bit,
-    including an odd tile count (ghost tile in the last pair)."""
+def test_mlp_cta_pair_variant_matches_single_cta_bitwise():
+    """The CTA-pair fused MLP (cta_group::2 M=256 MMAs, each SM holding half of every weight
+    operand; cfdx_set_option(4, 1)) accumulates the same products in the same k order as the
+    single-CTA kernel: outputs agree bit for bit, including an odd tile count (ghost tile in
+    the last pair)."""
     from paper_2505_23317_b200 import _lib as L
     lib = L.load()
     cfg = ci.CONFIGS["c640"]
