@@ -25,7 +25,7 @@ PUBLIC_SYMBOLS = ["cfd_create", "cfd_destroy", "cfd_query", "cfd_coarse_encode",
                   "cfd_refine_encode", "cfd_batch_refine", "cfd_check", "cfd_status_str", "cfd_version",
                   "cfd_hardness", "cfd_box_scores"]
 DEBUG_SYMBOLS = ["cfdx_gemm", "cfdx_gemm_resid_ln", "cfdx_attention", "cfdx_layernorm", "cfdx_score", "cfdx_gather",
-                 "cfdx_launch_count", "cfdx_mlp_trace", "cfdx_probe_install", "cfdx_probe_count", "cfdx_set_option"]
+                 "cfdx_launch_count", "cfdx_mlp_trace", "cfdx_attn_trace", "cfdx_probe_install", "cfdx_probe_count", "cfdx_set_option"]
 PROBE_KINDS = {"attention": 0, "score": 1, "gemm_qkv": 2, "gemm_oproj": 3, "gemm_mlp1": 4, "gemm_mlp2": 5,
                "gemm_embed_c": 6, "gemm_embed_f": 7, "layernorm": 8, "select": 9, "gather": 10, "im2col": 11,
                "meta": 12}
@@ -86,6 +86,7 @@ def load() -> C.CDLL:
         "cfdx_gather": [P, I32, P, P, P, P, P, P, P, P, P, P, P, P],
         "cfdx_launch_count": [],
         "cfdx_mlp_trace": [P, I32],
+        "cfdx_attn_trace": [P, I32],
         "cfdx_probe_install": [I32, C.POINTER(P), C.POINTER(P), I32],
         "cfdx_probe_count": [I32],
         "cfdx_set_option": [I32, I32],

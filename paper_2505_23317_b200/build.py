@@ -37,15 +37,17 @@ def _newest_src_mtime() -> float:
     return max(os.path.getmtime(p) for p in paths)
 
 
-def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug: bool = False, trace_only: bool = False) -> str:
     """debug=True builds libcfdetr_dbg.so with -DCFD_HANG_CHECK -DCFD_TRACE (barrier waits trap with a
-    message instead of hanging); load it with CFD_LIB_DEBUG=1."""
+    message instead of hanging); trace_only=True builds it with -DCFD_TRACE alone (release barrier
+    waits, so pipeline traces keep release timing).  Load it with CFD_LIB_DEBUG=1."""
+    debug = debug or trace_only
     out = LIB_DBG if debug else LIB
     if not force and os.path.exists(out) and os.path.getmtime(out) >= _newest_src_mtime():
         return out
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     tmp = out + ".tmp"
-    extra = ["-DCFD_HANG_CHECK", "-DCFD_TRACE"] if debug else []
+    extra = (["-DCFD_TRACE"] if trace_only else ["-DCFD_HANG_CHECK", "-DCFD_TRACE"]) if debug else []
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-shared", "-o", tmp, *srcs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     log = os.path.join(HERE, "build_dbg.log" if debug else "build.log")
@@ -61,4 +63,5 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv,
+                trace_only="--trace" in sys.argv))

@@ -32,6 +32,7 @@ struct AttnParams {
   float* lse;              // [nh, lse_ld] or nullptr
   int lse_ld;
   float scale_log2;        // log2(e) / sqrt(dh)
+  int stagger = 0;         // v4: softmax warpgroup w starts w * stagger cycles late (0 = off)
 };
 
 constexpr int ATTN_THREADS = 192;

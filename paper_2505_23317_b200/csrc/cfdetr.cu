@@ -16,6 +16,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -26,6 +27,7 @@
 #include "attn2_tc.cuh"
 #include "attn3_tc.cuh"
 #include "attn4_tc.cuh"
+#include "attn5_tc.cuh"
 #include "gemm_tc.cuh"
 #include "misc_kernels.cuh"
 #include "mlp_tc.cuh"
@@ -215,6 +217,7 @@ bool make_qkvmap(CUtensorMap* m, const void* qkv, int rows, int d) {
 // 2 = persistent two-tile ping-pong) and the polynomial-exp2 share of variant 2.
 int g_attn_variant = 4;
 int g_attn_npp = 4;
+int g_attn_stagger = 0;
 int g_fused_mlp = 1;  // fused MLP kernel (d == 256) instead of two GEMM launches
 int g_staged_epi = 1; // TMA-staged residual + LayerNorm epilogue for the O-projection
 int g_mlp_cluster = 0; // fused MLP as CTA pairs (cta_group::2)
@@ -265,17 +268,32 @@ cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUte
 
 template <int V, int NPP>
 cudaError_t launch_attn2_t(const CUtensorMap& tq, const AttnParams& p, int items_ub, int nh, int T, cudaStream_t s) {
-  auto kern = (V == 2) ? attn2_tc_kernel<32, 4, NPP> : (V == 3) ? attn3_tc_kernel<32, 4, NPP> : attn4_tc_kernel<32, 4, NPP>;
-  constexpr int smem = (V == 2) ? Attn2Smem<32, 4>::TOTAL : (V == 3) ? Attn3Smem<32, 4>::TOTAL : Attn4Smem<32, 4>::TOTAL;
+  auto kern = (V == 2)   ? attn2_tc_kernel<32, 4, NPP>
+              : (V == 3) ? attn3_tc_kernel<32, 4, NPP>
+              : (V == 4) ? attn4_tc_kernel<32, 4, NPP>
+                         : attn5_tc_kernel<32, 4, NPP>;
+  constexpr int smem = (V == 2)   ? Attn2Smem<32, 4>::TOTAL
+                       : (V == 3) ? Attn3Smem<32, 4>::TOTAL
+                       : (V == 4) ? Attn4Smem<32, 4>::TOTAL
+                                  : Attn5Smem<32, 4>::TOTAL;
+  constexpr int threads = V == 2 ? ATTN2_THREADS : V == 3 ? ATTN3_THREADS : V == 4 ? ATTN4_THREADS : ATTN5_THREADS;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int grid = std::max(1, std::min(items_ub, num_sms()));
-  kern<<<grid, V == 2 ? ATTN2_THREADS : V == 3 ? ATTN3_THREADS : ATTN4_THREADS, smem, s>>>(tq, p, T, nh);
-  return cudaGetLastError();
+  // v5: two items (pairs) in flight per CTA
+  const int grid = std::max(1, std::min(V == 5 ? (items_ub + 1) / 2 : items_ub, num_sms()));
+  kern<<<grid, threads, smem, s>>>(tq, p, T, nh);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && getenv("CFD_VERBOSE")) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kern);
+    fprintf(stderr, "attention v%d launch (grid %d, %d threads, %d B smem; kernel: %d regs, max %d threads): %s\n", V,
+            grid, threads, smem, fa.numRegs, fa.maxThreadsPerBlock, cudaGetErrorString(e));
+  }
+  return e;
 }
 
 cudaError_t launch_attention(const CUtensorMap& tq, const AttnParams& p, int max_qtiles, int nh, int T,
@@ -299,6 +317,14 @@ cudaError_t launch_attention(const CUtensorMap& tq, const AttnParams& p, int max
         case 6: e = launch_attn2_t<3, 6>(tq, p, items_ub, nh, T, s); break;
         case 8: e = launch_attn2_t<3, 8>(tq, p, items_ub, nh, T, s); break;
         default: e = launch_attn2_t<3, 4>(tq, p, items_ub, nh, T, s); break;
+      }
+    } else if (g_attn_variant == 5) {
+      switch (g_attn_npp) {
+        case 0: e = launch_attn2_t<5, 0>(tq, p, items_ub, nh, T, s); break;
+        case 2: e = launch_attn2_t<5, 2>(tq, p, items_ub, nh, T, s); break;
+        case 6: e = launch_attn2_t<5, 6>(tq, p, items_ub, nh, T, s); break;
+        case 8: e = launch_attn2_t<5, 8>(tq, p, items_ub, nh, T, s); break;
+        default: e = launch_attn2_t<5, 4>(tq, p, items_ub, nh, T, s); break;
       }
     } else {
       switch (g_attn_npp) {
@@ -456,6 +482,7 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   AttnParams ap{};
   ap.cu_seqlens = cu; ap.d_model = d; ap.out = w.obuf; ap.lse = want_lse ? w.lse : nullptr; ap.lse_ld = w.lse_ld;
   ap.scale_log2 = 1.4426950408889634f / std::sqrt((float)c->dh);
+  ap.stagger = g_attn_stagger;
   CFD_CUDA(launch_attention(tq, ap, max_qtiles, g.n_heads, T, s));
   if (want_lse && scores) {
     ScoreParams sp{};
@@ -548,6 +575,18 @@ const char* cfd_status_str(cfd_status s) {
 
 int64_t cfdx_launch_count(void) { return g_launches.load(); }
 
+cfd_status cfdx_attn_trace(uint64_t* dst, int32_t n_words) {
+#ifdef CFD_TRACE
+  if (!dst || n_words < ATTN_TRACE_WORDS) return CFD_E_ARG;
+  CFD_CUDA(cudaMemcpyFromSymbol(dst, g_attn_trace, sizeof(unsigned long long) * ATTN_TRACE_WORDS));
+  return CFD_OK;
+#else
+  (void)dst;
+  (void)n_words;
+  return CFD_E_ARG;
+#endif
+}
+
 cfd_status cfdx_mlp_trace(uint64_t* dst, int32_t n_words) {
 #ifdef CFD_TRACE
   if (!dst || n_words < MLP_TRACE_WORDS) return CFD_E_ARG;
@@ -576,7 +615,7 @@ cfd_status cfdx_probe_install(int32_t kind, void* const* h_start, void* const* h
 cfd_status cfdx_set_option(int32_t key, int32_t value) {
   switch (key) {
     case 0:
-      if (value < 1 || value > 4) return CFD_E_ARG;
+      if (value < 1 || value > 5) return CFD_E_ARG;
       g_attn_variant = value;
       return CFD_OK;
     case 1:
@@ -591,6 +630,10 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
       return CFD_OK;
     case 3:
       g_staged_epi = value ? 1 : 0;
+      return CFD_OK;
+    case 5:
+      if (value < 0 || value > 100000) return CFD_E_ARG;
+      g_attn_stagger = value;
       return CFD_OK;
   }
   return CFD_E_ARG;
@@ -943,6 +986,7 @@ cfd_status cfdx_attention(int32_t T, const int32_t* cu, int32_t max_seqlen, int3
   AttnParams ap{};
   ap.cu_seqlens = cu; ap.d_model = d; ap.out = (__nv_bfloat16*)out; ap.lse = lse; ap.lse_ld = lse_ld;
   ap.scale_log2 = 1.4426950408889634f / std::sqrt(32.0f);
+  ap.stagger = g_attn_stagger;
   CFD_CUDA(launch_attention(tq, ap, (max_seqlen + ATTN_BQ - 1) / ATTN_BQ, nh, T, static_cast<cudaStream_t>(stream)));
   return CFD_OK;
 }

@@ -304,7 +304,7 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(uint32_t M, uint32_t N, u
 // ------------------------------------------------------------------ misc math
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
-  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));  // pure: the scheduler may interleave it
   return y;
 }
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {

@@ -14,9 +14,11 @@ ap.add_argument("--variant", type=int, default=2)
 ap.add_argument("--npp", type=int, default=0)
 ap.add_argument("--lens", default="700x32")
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--stagger", type=int, default=0)
 a = ap.parse_args()
 lib = L.load()
 assert lib.cfdx_set_option(0, a.variant) == 0 and lib.cfdx_set_option(1, a.npp) == 0
+assert lib.cfdx_set_option(5, a.stagger) == 0
 lens = []
 for part in a.lens.split(","):
     n, c = part.split("x")
