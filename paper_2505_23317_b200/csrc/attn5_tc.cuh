@@ -69,18 +69,6 @@ struct Attn5Prod {
   int item, it, j, kvc, qdone, seq0, nkv, h, qp, nq;
 };
 
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, P1;\n\t}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-
 template <int DH, int STAGES, int NPP>
 __global__ void __launch_bounds__(ATTN5_THREADS, 1)
     attn5_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const AttnParams p, const int T, const int nh) {

@@ -218,6 +218,7 @@ bool make_qkvmap(CUtensorMap* m, const void* qkv, int rows, int d) {
 int g_attn_variant = 4;
 int g_attn_npp = 4;
 int g_attn_stagger = 0;
+int g_attn_stages = 4;  // v4 K/V ring depth (128-key stages): 4, 6 or 8
 int g_fused_mlp = 1;  // fused MLP kernel (d == 256) instead of two GEMM launches
 int g_staged_epi = 1; // TMA-staged residual + LayerNorm epilogue for the O-projection
 int g_mlp_cluster = 0; // fused MLP as CTA pairs (cta_group::2)
@@ -266,15 +267,15 @@ cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUte
   return cudaGetLastError();
 }
 
-template <int V, int NPP>
+template <int V, int NPP, int ST = 4>
 cudaError_t launch_attn2_t(const CUtensorMap& tq, const AttnParams& p, int items_ub, int nh, int T, cudaStream_t s) {
   auto kern = (V == 2)   ? attn2_tc_kernel<32, 4, NPP>
               : (V == 3) ? attn3_tc_kernel<32, 4, NPP>
-              : (V == 4) ? attn4_tc_kernel<32, 4, NPP>
+              : (V == 4) ? attn4_tc_kernel<32, ST, NPP>
                          : attn5_tc_kernel<32, 4, NPP>;
   constexpr int smem = (V == 2)   ? Attn2Smem<32, 4>::TOTAL
                        : (V == 3) ? Attn3Smem<32, 4>::TOTAL
-                       : (V == 4) ? Attn4Smem<32, 4>::TOTAL
+                       : (V == 4) ? Attn4Smem<32, ST>::TOTAL
                                   : Attn5Smem<32, 4>::TOTAL;
   constexpr int threads = V == 2 ? ATTN2_THREADS : V == 3 ? ATTN3_THREADS : V == 4 ? ATTN4_THREADS : ATTN5_THREADS;
   static bool attr = false;
@@ -334,7 +335,11 @@ cudaError_t launch_attention(const CUtensorMap& tq, const AttnParams& p, int max
         case 8: e = launch_attn2_t<4, 8>(tq, p, items_ub, nh, T, s); break;
         case 10: e = launch_attn2_t<4, 10>(tq, p, items_ub, nh, T, s); break;
         case 12: e = launch_attn2_t<4, 12>(tq, p, items_ub, nh, T, s); break;
-        default: e = launch_attn2_t<4, 4>(tq, p, items_ub, nh, T, s); break;
+        default:
+          e = g_attn_stages == 8   ? launch_attn2_t<4, 4, 8>(tq, p, items_ub, nh, T, s)
+              : g_attn_stages == 6 ? launch_attn2_t<4, 4, 6>(tq, p, items_ub, nh, T, s)
+                                   : launch_attn2_t<4, 4>(tq, p, items_ub, nh, T, s);
+          break;
       }
     }
   } else {
@@ -630,6 +635,10 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
       return CFD_OK;
     case 3:
       g_staged_epi = value ? 1 : 0;
+      return CFD_OK;
+    case 6:
+      if (value != 4 && value != 6 && value != 8) return CFD_E_ARG;
+      g_attn_stages = value;
       return CFD_OK;
     case 5:
       if (value < 0 || value > 100000) return CFD_E_ARG;

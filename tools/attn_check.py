@@ -13,6 +13,7 @@ d = int(sys.argv[4]) if len(sys.argv) > 4 else 256
 nh = d // 32
 lib = L.load()
 assert lib.cfdx_set_option(0, var) == 0 and lib.cfdx_set_option(1, npp) == 0
+assert lib.cfdx_set_option(6, int(os.environ.get("CFD_STAGES", "4"))) == 0
 cu_l = [0]
 for n in lens:
     cu_l.append(cu_l[-1] + n)
