@@ -114,7 +114,16 @@ int num_sms() {
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// ------------------------------------------------------------------ launches
+template <typename... KArgs, typename... Args>
+cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+  return cudaGetLastError();
+}
+
+
 // ------------------------------------------------------------------ GEMM dispatch
+int g_gemm_bres = 1;  // weight-stationary QKV GEMM (option 7)
 template <int BN>
 constexpr int gemm_stages() { return BN == 256 ? 4 : BN == 128 ? 6 : 8; }
 template <int BN>  // with the 32 KB bf16 output staging area
@@ -123,17 +132,21 @@ constexpr int gemm_stages_stg() { return BN == 256 ? 3 : BN == 128 ? 5 : 7; }
 // mode 0: 1 CTA/SM, 8 epilogue warps, double-buffered accumulator (many tiles);
 //         for EPI_F32_RESID_LN a 2-stage ring and the TMA-staged residual epilogue
 // mode 1: 2 CTAs/SM, 4 epilogue warps, single accumulator, 2-stage ring (N = d GEMMs)
+// mode 2 (BRES): mode 0 with the CTA's [BN, 256] weight slice resident in shared memory
+//         (bf16 outputs, K = 256): each CTA keeps one column block and walks row blocks, so
+//         the per-SM operand stream is A only (64 KB per 128x256 tile instead of 192 KB)
 template <int BN, int EPI, int MODE>
 cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows_for_grid,
                           cudaStream_t s, const CUtensorMap* tx, const CUtensorMap* tln) {
-  constexpr bool kTmaEpi = (EPI == EPI_F32_RESID_LN && MODE == 0);
-  constexpr bool kStgOut = (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_GELU) && MODE == 0;
-  constexpr int EW = MODE ? 4 : 8;
-  constexpr int NACC = MODE ? 1 : 2;
-  constexpr int ST = (MODE || kTmaEpi) ? 2 : kStgOut ? gemm_stages_stg<BN>() : gemm_stages<BN>();
-  auto kern = gemm_tc_kernel<BN, ST, EPI, EW, NACC>;
-  constexpr int smem = kTmaEpi ? GemmSmem<BN, ST, NACC>::TOTAL_TMA_EPI
-                       : kStgOut ? GemmSmem<BN, ST, NACC>::TOTAL_STG_OUT : GemmSmem<BN, ST, NACC>::TOTAL;
+  constexpr bool kBres = MODE == 2;
+  constexpr bool kTmaEpi = (EPI == EPI_F32_RESID_LN && MODE != 1);
+  constexpr bool kStgOut = (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_GELU) && MODE != 1;
+  constexpr int EW = MODE == 1 ? 4 : 8;
+  constexpr int NACC = MODE == 1 ? 1 : 2;
+  constexpr int ST = kBres ? 3 : (MODE == 1 || kTmaEpi) ? 2 : kStgOut ? gemm_stages_stg<BN>() : gemm_stages<BN>();
+  auto kern = gemm_tc_kernel<BN, ST, EPI, EW, NACC, kBres>;
+  using SM = GemmSmem<BN, ST, NACC, kBres>;
+  constexpr int smem = kTmaEpi ? SM::TOTAL_TMA_EPI : kStgOut ? SM::TOTAL_STG_OUT : SM::TOTAL;
   static_assert(smem <= 232448, "shared memory budget");
   CUtensorMap tout;
   if constexpr (kStgOut) {  // bf16 output [m_cap, N], 32 x 32 boxes
@@ -148,11 +161,12 @@ cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
     attr = true;
   }
   const int tiles = ((rows_for_grid + GEMM_BM - 1) / GEMM_BM) * (p.N / BN);
-  const int slots = num_sms() * (MODE ? 2 : 1);
-  const int grid = tiles < slots ? (tiles > 0 ? tiles : 1) : slots;
-  kern<<<grid, 64 + 32 * EW, smem, s>>>(ta, tb, p, tx ? *tx : ta, tln ? *tln : ta);
+  const int slots = num_sms() * (MODE == 1 ? 2 : 1);
+  int grid = tiles < slots ? (tiles > 0 ? tiles : 1) : slots;
+  if constexpr (kBres) grid = std::max(1, grid / (p.N / BN)) * (p.N / BN);  // whole column-block groups
+  cudaError_t le = launch_ex(kern, dim3(grid), dim3(64 + 32 * EW), smem, s, ta, tb, p, tx ? *tx : ta, tln ? *tln : ta);
   ++g_launches;
-  return cudaGetLastError();
+  return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 template <int EPI>
@@ -166,6 +180,10 @@ cudaError_t launch_gemm_bn(int BN, const CUtensorMap& ta, const CUtensorMap& tb,
       case 128: return launch_gemm_t<128, EPI, 1>(ta, tb, p, rows, s, tx, tln);
       default: return launch_gemm_t<64, EPI, 1>(ta, tb, p, rows, s, tx, tln);
     }
+  }
+  if constexpr (EPI == EPI_BF16_BIAS) {
+    if (g_gemm_bres && BN == 256 && p.K == GEMM_BRES_KB * GEMM_BK)
+      return launch_gemm_t<256, EPI, 2>(ta, tb, p, rows, s, tx, tln);
   }
   switch (BN) {
     case 256: return launch_gemm_t<256, EPI, 0>(ta, tb, p, rows, s, tx, tln);
@@ -262,7 +280,8 @@ cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUte
     return e != cudaSuccess ? e : cudaGetLastError();
   }
   const int grid = std::max(1, std::min(tiles, num_sms()));
-  mlp_tc_kernel<256, 1><<<grid, MLP_THREADS, smem, s>>>(th, tw1, tw2, q, mx, ml);
+  const cudaError_t le = launch_ex(mlp_tc_kernel<256, 1>, dim3(grid), dim3(MLP_THREADS), smem, s, th, tw1, tw2, q, mx, ml);
+  if (le != cudaSuccess) return le;
   ++g_launches;
   return cudaGetLastError();
 }
@@ -286,8 +305,8 @@ cudaError_t launch_attn2_t(const CUtensorMap& tq, const AttnParams& p, int items
   }
   // v5: two items (pairs) in flight per CTA
   const int grid = std::max(1, std::min(V == 5 ? (items_ub + 1) / 2 : items_ub, num_sms()));
-  kern<<<grid, threads, smem, s>>>(tq, p, T, nh);
-  const cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_ex(kern, dim3(grid), dim3(threads), smem, s, tq, p, T, nh);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess && getenv("CFD_VERBOSE")) {
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, kern);
@@ -369,7 +388,7 @@ cudaError_t launch_score(const CUtensorMap& tq, const ScoreParams& p, int B, cud
     attr = true;
   }
   probe_begin(PK_SCORE, s);
-  kern<<<dim3((p.n_coarse + 127) / 128, B), SCORE_THREADS, smem, s>>>(tq, p);
+  launch_ex(kern, dim3((p.n_coarse + 127) / 128, B), dim3(SCORE_THREADS), smem, s, tq, p);
   probe_end(PK_SCORE, s);
   ++g_launches;
   return cudaGetLastError();
@@ -382,10 +401,10 @@ cudaError_t launch_layernorm(int d, const float* x, const float* g, const float*
   blocks = std::max(1, std::min(blocks, num_sms() * 16));
   probe_begin(PK_LN, s);
   switch (d) {
-    case 64: layernorm_kernel<2><<<blocks, 256, 0, s>>>(x, g, b, y, M, m_dev, m_cap, eps); break;
-    case 128: layernorm_kernel<4><<<blocks, 256, 0, s>>>(x, g, b, y, M, m_dev, m_cap, eps); break;
-    case 256: layernorm_kernel<8><<<blocks, 256, 0, s>>>(x, g, b, y, M, m_dev, m_cap, eps); break;
-    case 512: layernorm_kernel<16><<<blocks, 256, 0, s>>>(x, g, b, y, M, m_dev, m_cap, eps); break;
+    case 64: launch_ex(layernorm_kernel<2>, dim3(blocks), dim3(256), 0, s, x, g, b, y, M, m_dev, m_cap, eps); break;
+    case 128: launch_ex(layernorm_kernel<4>, dim3(blocks), dim3(256), 0, s, x, g, b, y, M, m_dev, m_cap, eps); break;
+    case 256: launch_ex(layernorm_kernel<8>, dim3(blocks), dim3(256), 0, s, x, g, b, y, M, m_dev, m_cap, eps); break;
+    case 512: launch_ex(layernorm_kernel<16>, dim3(blocks), dim3(256), 0, s, x, g, b, y, M, m_dev, m_cap, eps); break;
     default: return cudaErrorInvalidValue;
   }
   probe_end(PK_LN, s);
@@ -636,6 +655,9 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
     case 3:
       g_staged_epi = value ? 1 : 0;
       return CFD_OK;
+    case 7:
+      g_gemm_bres = value ? 1 : 0;
+      return CFD_OK;
     case 6:
       if (value != 4 && value != 6 && value != 8) return CFD_E_ARG;
       g_attn_stages = value;
@@ -779,7 +801,7 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
   const cfd_config& g = c->cfg;
   const int d = g.d_model, M = B * c->Nc;
   probe_begin(PK_META, s);
-  coarse_meta_kernel<<<1, 256, 0, s>>>(w.ccu, w.meta, B, c->Nc);
+  launch_ex(coarse_meta_kernel, dim3(1), dim3(256), 0, s, w.ccu, w.meta, B, c->Nc);
   probe_end(PK_META, s);
   ++g_launches;
   CFD_CUDA(cudaGetLastError());
@@ -787,7 +809,7 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
     const long long vec = (long long)B * g.img_h * (g.img_w / g.patch_coarse) * ((g.patch_coarse * 6) / 16);
     const int blocks = (int)std::min<long long>((vec + 255) / 256, (long long)num_sms() * 8);
     probe_begin(PK_IM2COL, s);
-    im2col_kernel<<<blocks, 256, 0, s>>>(images, w.patches, B, g.img_h, g.img_w, g.patch_coarse);
+    launch_ex(im2col_kernel, dim3(blocks), dim3(256), 0, s, images, w.patches, B, g.img_h, g.img_w, g.patch_coarse);
     probe_end(PK_IM2COL, s);
     ++g_launches;
     CFD_CUDA(cudaGetLastError());
@@ -831,10 +853,10 @@ cfd_status cfd_select_regions(cfd_ctx* c, int32_t T, const float* scores, cfd_se
     int32_t* si = sel_idx + (size_t)t0 * Nc;
     int32_t* cnt = sel_count + t0;
     probe_begin(PK_SELECT, s);
-    if (Nc <= 512) select_kernel<512><<<nt, 512, 0, s>>>(sc, Nc, (int)mode, ks, threshold, si, cnt);
-    else if (Nc <= 1024) select_kernel<1024><<<nt, 512, 0, s>>>(sc, Nc, (int)mode, ks, threshold, si, cnt);
-    else if (Nc <= 2048) select_kernel<2048><<<nt, 512, 0, s>>>(sc, Nc, (int)mode, ks, threshold, si, cnt);
-    else select_kernel<4096><<<nt, 512, 0, s>>>(sc, Nc, (int)mode, ks, threshold, si, cnt);
+    if (Nc <= 512) launch_ex(select_kernel<512>, dim3(nt), dim3(512), 0, s, sc, Nc, (int)mode, ks, threshold, si, cnt);
+    else if (Nc <= 1024) launch_ex(select_kernel<1024>, dim3(nt), dim3(512), 0, s, sc, Nc, (int)mode, ks, threshold, si, cnt);
+    else if (Nc <= 2048) launch_ex(select_kernel<2048>, dim3(nt), dim3(512), 0, s, sc, Nc, (int)mode, ks, threshold, si, cnt);
+    else launch_ex(select_kernel<4096>, dim3(nt), dim3(512), 0, s, sc, Nc, (int)mode, ks, threshold, si, cnt);
     probe_end(PK_SELECT, s);
     ++g_launches;
     CFD_CUDA(cudaGetLastError());
@@ -854,7 +876,7 @@ static cfd_status launch_gather(cfd_ctx* c, int T, const uint16_t* images, const
   const int G = std::max(1, std::min(16, (c->Nc + 63) / 64));
   const size_t smem = (size_t)2 * c->Nc * sizeof(int32_t);
   probe_begin(PK_GATHER, s);
-  gather_kernel<<<dim3(T, G), 256, smem, s>>>(gp);
+  launch_ex(gather_kernel, dim3(T, G), dim3(256), smem, s, gp);
   probe_end(PK_GATHER, s);
   ++g_launches;
   CFD_CUDA(cudaGetLastError());
@@ -919,7 +941,7 @@ cfd_status cfd_hardness(cfd_ctx* c, int32_t B, int32_t Q, const float* conf, flo
   if (B == 0) return CFD_OK;
   if (B < 0 || Q < 0 || !conf || !hard) return CFD_E_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  hardness_kernel<<<(B + 127) / 128, 128, 0, s>>>(conf, B, Q, c_hi, tau, hard);
+  launch_ex(hardness_kernel, dim3((B + 127) / 128), dim3(128), 0, s, conf, B, Q, c_hi, tau, hard);
   ++g_launches;
   CFD_CUDA(cudaGetLastError());
   return CFD_OK;
@@ -932,8 +954,8 @@ cfd_status cfd_box_scores(cfd_ctx* c, int32_t B, int32_t Q, const float* boxes, 
   if (B < 0 || Q < 0 || Q > 4096 || !boxes || !conf || !scores) return CFD_E_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const cfd_config& g = c->cfg;
-  box_scores_kernel<<<B, 256, (size_t)std::max(Q, 1) * sizeof(int4), s>>>(
-      boxes, conf, Q, g.img_h, g.img_w, g.patch_coarse, c->gc_w, c->Nc, c_lo, c_hi, scores);
+  launch_ex(box_scores_kernel, dim3(B), dim3(256), (size_t)std::max(Q, 1) * sizeof(int4), s,
+           boxes, conf, Q, g.img_h, g.img_w, g.patch_coarse, c->gc_w, c->Nc, c_lo, c_hi, scores);
   ++g_launches;
   CFD_CUDA(cudaGetLastError());
   return CFD_OK;

@@ -77,17 +77,23 @@ constexpr int GEMM_THREADS = 64 + 32 * GEMM_EPI_WARPS;  // + TMA warp + MMA warp
 constexpr int GEMM_MAX_N = 2048;   // bias columns staged in shared memory
 constexpr int GEMM_MAX_LN = 512;   // LayerNorm width for EPI_F32_RESID_LN
 
-template <int BN, int STAGES, int NACC = 2>
+// BRES (weight-stationary, "B resident"): the CTA's whole [BN, K] weight slice (K = 256:
+// four 64-wide k-blocks) is loaded into shared memory once and stays there while the CTA
+// streams its row tiles through an A-only ring.  The default streams A and B per k-block.
+constexpr int GEMM_BRES_KB = 4;
+template <int BN, int STAGES, int NACC = 2, bool BRES = false>
 struct GemmSmem {
   static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr int B_BYTES = BN * GEMM_BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGE_BYTES = A_BYTES + (BRES ? 0 : B_BYTES);  // TMA bytes per ring stage
+  static constexpr int NB = BRES ? GEMM_BRES_KB : STAGES;            // B buffers
+  static constexpr int BAR_OFF = STAGES * A_BYTES + NB * B_BYTES;
   static constexpr int BAR_BYTES = 256 + 2 * 128 * 8;  // barriers + RESID_LN row statistics
   static constexpr int PAR_FLOATS = GEMM_MAX_N + 2 * GEMM_MAX_LN;  // bias | ln gamma | ln beta
   static constexpr int PAR_BYTES = ((PAR_FLOATS * 4 + 1023) / 1024) * 1024;
   static constexpr int STG_BYTES = 12288;  // per epilogue warp: x chunks [2] 4 KB + LN chunks [2] 2 KB
-  static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES + PAR_BYTES;
-  static constexpr int STG_OFF = STAGES * STAGE_BYTES + ((BAR_BYTES + PAR_BYTES + 1023) / 1024) * 1024;
+  static constexpr int TOTAL = 1024 /*align slack*/ + BAR_OFF + BAR_BYTES + PAR_BYTES;
+  static constexpr int STG_OFF = BAR_OFF + ((BAR_BYTES + PAR_BYTES + 1023) / 1024) * 1024;
   static constexpr int TOTAL_TMA_EPI = 1024 + STG_OFF + GEMM_EPI_WARPS * STG_BYTES;
   static constexpr int TOTAL_STG_OUT = 1024 + STG_OFF + GEMM_EPI_WARPS * 4096;  // bf16 out: 2 x 2 KB per warp
   static constexpr uint32_t TMEM_COLS = (NACC * BN <= 32) ? 32 : (NACC * BN <= 64) ? 64 : (NACC * BN <= 128) ? 128
@@ -431,42 +437,39 @@ __device__ __forceinline__ void store_bf16_tma(const CUtensorMap& tmO, uint8_t* 
   }
 }
 
-template <int BN, int STAGES, int EPI, int EW, int NACC>
+template <int BN, int STAGES, int EPI, int EW, int NACC, bool BRES = false>
 __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmParams p, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ CUtensorMap tmLN) {
   static_assert((EW == 8 && NACC == 2) || (EW == 4 && NACC == 1), "supported epilogue configurations");
-  using S = GemmSmem<BN, STAGES, NACC>;
+  using S = GemmSmem<BN, STAGES, NACC, BRES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * S::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2 + 16);
-  float2* ln_stats = reinterpret_cast<float2*>(smem + STAGES * S::STAGE_BYTES + 256);  // [2][128]
+  uint64_t* bres_full = tempty + 2 + 16;  // BRES: resident weight slice landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2 + 17);
+  float2* ln_stats = reinterpret_cast<float2*>(smem + S::BAR_OFF + 256);  // [2][128]
   uint64_t* xbar = tempty + 2;  // [8 warps][2] TMA-load barriers of the staged residual epilogue
-  float* par = reinterpret_cast<float*>(smem + STAGES * S::STAGE_BYTES + S::BAR_BYTES);
+  float* par = reinterpret_cast<float*>(smem + S::BAR_OFF + S::BAR_BYTES);
   float* bias_s = par;                       // [N]
   float* lng_s = par + GEMM_MAX_N;           // [N] (RESID_LN)
   float* lnb_s = lng_s + GEMM_MAX_LN;        // [N] (RESID_LN)
 
   const int warp = warp_id(), lane = lane_id();
-  const int M = p.m_dev ? __ldg(p.m_dev) : p.M;
   // bf16 outputs (QKV, MLP1) also cover the pad rows [M, pad_rows(M)) so attention's
   // tail tiles (which may start at any row of the last task) read finite values
   constexpr bool kPad = (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_GELU);
   // bf16 outputs of the one-CTA/SM configuration leave through smem + TMA store (tmX = out map)
   constexpr bool kStgOut = kPad && EW == 8;
-  const int m_store = kPad ? pad_rows(M, p.m_cap) : M;
-  // RESID_LN also visits the tiles of the pad rows (zeroed in ln_out, x untouched)
-  const int m_tiles = ((EPI == EPI_F32_RESID_LN ? pad_rows(M, p.ln_cap) : m_store) + GEMM_BM - 1) / GEMM_BM;
   const int n_tiles = p.N / BN;
   const int num_k = p.K / GEMM_BK;
-  const int total = m_tiles * n_tiles;
+  const int n_fix = BRES ? (int)blockIdx.x % n_tiles : 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -474,6 +477,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < NACC; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], EW); }
     for (int i = 0; i < 16; ++i) mbar_init(&xbar[i], 1);
+    mbar_init(bres_full, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<S::TMEM_COLS>(tmem_slot);
@@ -481,18 +485,35 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if constexpr (BRES) {  // the CTA's weight slice, once
+    if (warp == 0 && lane == 0) {
+      mbar_expect_tx(bres_full, GEMM_BRES_KB * S::B_BYTES);
+      for (int kb = 0; kb < GEMM_BRES_KB; ++kb)
+        tma_load_2d(sB + kb * S::B_BYTES, &tmB, bres_full, kb * GEMM_BK, n_fix * BN);
+    }
+  }
+  const int M = p.m_dev ? __ldg(p.m_dev) : p.M;
+  const int m_store = kPad ? pad_rows(M, p.m_cap) : M;
+  // RESID_LN also visits the tiles of the pad rows (zeroed in ln_out, x untouched)
+  const int m_tiles = ((EPI == EPI_F32_RESID_LN ? pad_rows(M, p.ln_cap) : m_store) + GEMM_BM - 1) / GEMM_BM;
+  const int total = m_tiles * n_tiles;
+  // tile walk: default tile = m_blk * n_tiles + n_blk over all tiles; BRES: the CTA keeps
+  // column block blockIdx % n_tiles and walks row blocks (gridDim is a multiple of n_tiles)
+  const int t_first = BRES ? (int)blockIdx.x / n_tiles : (int)blockIdx.x;
+  const int t_step = BRES ? (int)gridDim.x / n_tiles : (int)gridDim.x;
+  const int t_end = BRES ? ((int)blockIdx.x < t_step * n_tiles ? m_tiles : 0) : total;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        const int m_blk = tile / n_tiles, n_blk = tile % n_tiles;
+      for (int tile = t_first; tile < t_end; tile += t_step) {
+        const int m_blk = BRES ? tile : tile / n_tiles, n_blk = BRES ? n_fix : tile % n_tiles;
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], S::STAGE_BYTES);
           tma_load_2d(sA + stage * S::A_BYTES, &tmA, &full[stage], kb * GEMM_BK, m_blk * GEMM_BM);
-          tma_load_2d(sB + stage * S::B_BYTES, &tmB, &full[stage], kb * GEMM_BK, n_blk * BN);
+          if constexpr (!BRES) tma_load_2d(sB + stage * S::B_BYTES, &tmB, &full[stage], kb * GEMM_BK, n_blk * BN);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -504,7 +525,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      if constexpr (BRES) mbar_wait(bres_full, 0);  // also when this CTA has no tile: the load must land
+      for (int tile = t_first; tile < t_end; tile += t_step) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -512,7 +534,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * S::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * S::B_BYTES);
+          const uint32_t b0 = smem_u32(sB + (BRES ? kb : stage) * S::B_BYTES);
 #pragma unroll
           for (int k = 0; k < GEMM_BK / 16; ++k) {
             const uint64_t ad = make_smem_desc(a0 + k * 32, 16, 1024, kLayoutSW128);
@@ -539,8 +561,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t xph = 0;  // bit b: phase of this warp's staging barrier b
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const int m_blk = tile / n_tiles, n_blk = tile % n_tiles;
+    for (int tile = t_first; tile < t_end; tile += t_step) {
+      const int m_blk = BRES ? tile : tile / n_tiles, n_blk = BRES ? n_fix : tile % n_tiles;
       const int row0 = m_blk * GEMM_BM + quarter * 32;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + half * WCOLS;
       const int col_base = n_blk * BN + half * WCOLS;

@@ -26,7 +26,8 @@ def _s():
 # ------------------------------------------------------------------ GEMM
 @pytest.mark.parametrize("M,N,K,epi", [
     (1, 64, 64, 2), (128, 64, 64, 2), (129, 256, 256, 2), (300, 768, 256, 0), (1000, 1024, 256, 1),
-    (777, 256, 1024, 2), (400, 256, 3072, 2), (33, 128, 768, 0), (4800, 256, 768, 2), (12800, 768, 256, 0)])
+    (777, 256, 1024, 2), (400, 256, 3072, 2), (33, 128, 768, 0), (4800, 256, 768, 2), (12800, 768, 256, 0),
+    (1, 768, 256, 0), (22400, 768, 256, 0)])
 def test_gemm_matches_torch_fp32(M, N, K, epi):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
     A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
