@@ -69,11 +69,13 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 
 // 2^x for a pair, x <= 0, on the FMA pipe: x = j + f, j = round(x), f in [-1/2, 1/2];
 // 2^f by a degree-3 minimax polynomial (max rel. error 7.6e-5 < bf16 ulp/2), 2^j
-// inserted into the exponent field.  x is clamped at -127 (result ~ 6e-39 ~ 0).
+// inserted into the exponent field.  x is clamped at -126: with j = -126 the biased
+// exponent of 2^f (126 or 127) stays >= 0 (result ~1e-38 ~ 0); at -127 it wrapped into the
+// sign bit for f <= 0 and produced NaN for logits more than 2^127 below the row max.
 __device__ __forceinline__ void exp2_poly2(float& y0, float& y1, float x0, float x1) {
   constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: t = x + M rounds x to an integer in t's low bits
-  x0 = fmaxf(x0, -127.f);
-  x1 = fmaxf(x1, -127.f);
+  x0 = fmaxf(x0, -126.f);
+  x1 = fmaxf(x1, -126.f);
   float t0, t1, r0, r1, f0, f1, p0, p1;
   add2(t0, t1, x0, x1, kMagic, kMagic);
   add2(r0, r1, t0, t1, -kMagic, -kMagic);

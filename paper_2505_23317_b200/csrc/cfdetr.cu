@@ -28,6 +28,7 @@
 #include "attn3_tc.cuh"
 #include "attn4_tc.cuh"
 #include "attn5_tc.cuh"
+#include "attn6_tc.cuh"
 #include "gemm_tc.cuh"
 #include "misc_kernels.cuh"
 #include "mlp_tc.cuh"
@@ -291,12 +292,13 @@ cudaError_t launch_attn2_t(const CUtensorMap& tq, const AttnParams& p, int items
   auto kern = (V == 2)   ? attn2_tc_kernel<32, 4, NPP>
               : (V == 3) ? attn3_tc_kernel<32, 4, NPP>
               : (V == 4) ? attn4_tc_kernel<32, ST, NPP>
+              : (V == 6) ? attn6_tc_kernel<32, ST, NPP>
                          : attn5_tc_kernel<32, 4, NPP>;
   constexpr int smem = (V == 2)   ? Attn2Smem<32, 4>::TOTAL
                        : (V == 3) ? Attn3Smem<32, 4>::TOTAL
-                       : (V == 4) ? Attn4Smem<32, ST>::TOTAL
+                       : (V == 4 || V == 6) ? Attn4Smem<32, ST>::TOTAL
                                   : Attn5Smem<32, 4>::TOTAL;
-  constexpr int threads = V == 2 ? ATTN2_THREADS : V == 3 ? ATTN3_THREADS : V == 4 ? ATTN4_THREADS : ATTN5_THREADS;
+  constexpr int threads = V == 2 ? ATTN2_THREADS : V == 3 ? ATTN3_THREADS : (V == 4 || V == 6) ? ATTN4_THREADS : ATTN5_THREADS;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -337,6 +339,14 @@ cudaError_t launch_attention(const CUtensorMap& tq, const AttnParams& p, int max
         case 6: e = launch_attn2_t<3, 6>(tq, p, items_ub, nh, T, s); break;
         case 8: e = launch_attn2_t<3, 8>(tq, p, items_ub, nh, T, s); break;
         default: e = launch_attn2_t<3, 4>(tq, p, items_ub, nh, T, s); break;
+      }
+    } else if (g_attn_variant == 6) {
+      switch (g_attn_npp) {
+        case 0: e = launch_attn2_t<6, 0>(tq, p, items_ub, nh, T, s); break;
+        case 2: e = launch_attn2_t<6, 2>(tq, p, items_ub, nh, T, s); break;
+        case 6: e = launch_attn2_t<6, 6>(tq, p, items_ub, nh, T, s); break;
+        case 8: e = launch_attn2_t<6, 8>(tq, p, items_ub, nh, T, s); break;
+        default: e = launch_attn2_t<6, 4>(tq, p, items_ub, nh, T, s); break;
       }
     } else if (g_attn_variant == 5) {
       switch (g_attn_npp) {
@@ -639,7 +649,7 @@ cfd_status cfdx_probe_install(int32_t kind, void* const* h_start, void* const* h
 cfd_status cfdx_set_option(int32_t key, int32_t value) {
   switch (key) {
     case 0:
-      if (value < 1 || value > 5) return CFD_E_ARG;
+      if (value < 1 || value > 6) return CFD_E_ARG;
       g_attn_variant = value;
       return CFD_OK;
     case 1:

@@ -120,6 +120,28 @@ def test_attention_varlen_matches_torch_fp32(lens, d):
     torch.testing.assert_close(lse[:, :rows], rlse[:, :rows], rtol=1e-4, atol=1e-4)
 
 
+def test_attention_wide_logit_range_stays_finite():
+    """Keys whose logits sit > 2^127 (log2 units) below or far above the running row max
+    (a 30x-scaled block of keys): every output finite and within tolerance.  Pins the
+    polynomial exp2's clamp (at -127 the exponent insertion wrapped to NaN)."""
+    d, lens = 256, [700, 1600, 400]
+    cu_l = np.concatenate([[0], np.cumsum(lens)]).astype(int).tolist()
+    g = torch.Generator(device="cuda").manual_seed(11)
+    qkv = torch.randn(cu_l[-1] + 256, 3 * d, device="cuda", generator=g) * 1.5
+    for t in range(len(lens)):
+        qkv[cu_l[t] + 150:cu_l[t] + 160, d:2 * d] *= 30.0
+        qkv[cu_l[t] + 190:cu_l[t] + 195, d:2 * d] *= 6.0
+    qkv = qkv.to(torch.bfloat16)
+    _, _, out, lse = _run_attn(lens, d, qkv=qkv)
+    ref, rlse = _attn_ref(qkv, cu_l, d, d // 32)
+    rows = cu_l[-1]
+    got = out.float()[:rows]
+    assert torch.isfinite(got).all() and torch.isfinite(lse[:, :rows]).all()
+    rel = ((got - ref[:rows]).norm() / ref[:rows].norm()).item()
+    assert rel < 1e-2, rel
+    torch.testing.assert_close(lse[:, :rows], rlse[:, :rows], rtol=1e-4, atol=2e-3)
+
+
 def test_attention_rows_sum_to_one_v_ones_probe():
     """V == 1 -> every output is sum_j P_ij = 1 (within bf16 rounding of P and O)."""
     d, lens = 256, [400, 1600, 37]

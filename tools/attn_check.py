@@ -20,7 +20,16 @@ for n in lens:
 rows = cu_l[-1]
 cap = rows + 256
 g = torch.Generator(device="cuda").manual_seed(rows)
-qkv = (torch.randn(cap, 3 * d, device="cuda", generator=g) * 1.5).to(torch.bfloat16)
+qkv = (torch.randn(cap, 3 * d, device="cuda", generator=g) * 1.5)
+if os.environ.get("CFD_SPIKE"):
+    # keys far into each sequence with logits ~30x larger: exercises the rescale paths
+    # (lazy reference moves > 2^8, and > 2^64 recomputes in v6)
+    for t0 in range(len(lens)):
+        a_, b_ = cu_l[t0], cu_l[t0 + 1]
+        if b_ - a_ > 200:
+            qkv[a_ + 150:a_ + 160, d:2 * d] *= 30.0
+            qkv[a_ + 190:a_ + 195, d:2 * d] *= 6.0
+qkv = qkv.to(torch.bfloat16)
 cu = torch.tensor(cu_l, dtype=torch.int32, device="cuda")
 out = torch.zeros(cap, d, device="cuda", dtype=torch.bfloat16)
 lse = torch.zeros(nh, cap, device="cuda")
