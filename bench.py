@@ -392,6 +392,19 @@ def gpu_arm(args):
         except Exception:
             pass
     attn_roof = roofline_for("attention")
+    # At dh = 32 a score element carries 4*dh = 128 tensor FLOPs but one exp2 (SURVEY.md §8(d)
+    # "per-element ceilings"): the kernel is bounded by the exp / FMA issue, not the tensor
+    # pipe.  Exp-unit roofline beside the tensor one: exps per step / attention time against
+    # MUFU ex2 at 16 per clock per SM (profiles/r1_mufu_micro.txt) x SMs x max SM clock.
+    # (A quarter of the exps run as an FMA-pipe polynomial, so > 100 % is possible.)
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    sm_mhz = (clk or {}).get("sm_max_mhz") or 1965.0
+    exps = cfg.n_layers * B * cfg.n_heads * (cfg.n_coarse ** 2 + (cfg.n_coarse + (cfg.m ** 2 - 1) * k) ** 2)
+    exp_peak = 16 * n_sm * sm_mhz * 1e6 / 1e9  # Gexp/s
+    exp_ach = exps / (kern_ms["attention"] / 1e3) / 1e9 if kern_ms.get("attention") else 0.0
+    attn_exp_roof = {"kernel": "attention", "bound": "alu", "unit": "Gexp/s", "achieved": round(exp_ach, 1),
+                     "peak": round(exp_peak, 1), "frac": round(exp_ach / exp_peak, 4),
+                     "peak_src": f"MUFU ex2 16/clk/SM x {n_sm} SMs x {sm_mhz:.0f} MHz"}
 
     # ---------------------------------------------------------------- e2e through the public API, host buffers
     # Serving-style loop: frames arrive in pinned host memory, results return to pinned host
@@ -479,7 +492,8 @@ def gpu_arm(args):
                "warmup": args.warmup, "ms_per_step": round(total_ms_max / args.steps, 4), "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                "config": workload_config(args, world, "flushed between timed steps (256 MiB memset outside events)"),
-               "roofline": roofline, "attention_roofline": attn_roof, "cpu_baseline": cpu, "e2e": e2e,
+               "roofline": roofline, "attention_roofline": attn_roof, "attention_exp_roofline": attn_exp_roof,
+               "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": launches_per_step * args.steps, "clocks": clk, "kernels": kernels,
                "step_ms_min": round(min(step_ms), 4), "check": check,
                "impl": "ours", "library": lib.cfd_version().decode()}
