@@ -883,7 +883,7 @@ static cfd_status launch_gather(cfd_ctx* c, int T, const uint16_t* images, const
   gp.H = g.img_h; gp.W = g.img_w; gp.Pf = g.patch_fine;
   gp.images = images; gp.x0 = x0; gp.sel_idx = sel_idx; gp.sel_count = sel_count; gp.X = X; gp.cu_seqlens = cu;
   gp.mixed_src = msrc; gp.A_f = A_f; gp.frow = frow; gp.fidx = fidx; gp.meta = meta; gp.err = c->err;
-  const int G = std::max(1, std::min(16, (c->Nc + 63) / 64));
+  const int G = std::max(1, std::min(32, (c->Nc + 31) / 32));
   const size_t smem = (size_t)2 * c->Nc * sizeof(int32_t);
   probe_begin(PK_GATHER, s);
   launch_ex(gather_kernel, dim3(T, G), dim3(256), smem, s, gp);

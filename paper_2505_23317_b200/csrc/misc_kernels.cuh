@@ -95,19 +95,32 @@ __global__ void im2col_kernel(const uint16_t* __restrict__ img, uint16_t* __rest
   const int seg_vec = (P * 3 * 2) / 16;  // 16B vectors per segment
   const int gw = W / P;
   const long long total = (long long)B * H * gw * seg_vec;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int v = (int)(i % seg_vec);
-    long long rest = i / seg_vec;
-    const int cx = (int)(rest % gw);
-    rest /= gw;
-    const int y = (int)(rest % H);
-    const int b = (int)(rest / H);
-    const int cy = y / P, py = y % P;
-    const uint4* src = reinterpret_cast<const uint4*>(img + (((size_t)b * H + y) * W + (size_t)cx * P) * 3) + v;
-    const size_t c = (size_t)b * (H / P) * gw + (size_t)cy * gw + cx;
-    uint4* dst = reinterpret_cast<uint4*>(A + c * (size_t)(3 * P * P) + (size_t)py * P * 3) + v;
-    *dst = __ldg(src);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // the source is read in order (vector i = i-th 16 B of the image); IU vectors per thread
+  // are loaded before any is stored so each thread keeps several requests in flight
+  constexpr int IU = 4;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total; i0 += IU * stride) {
+    uint4 buf[IU];
+#pragma unroll
+    for (int u = 0; u < IU; ++u) {
+      const long long i = i0 + u * stride;
+      if (i < total) buf[u] = __ldg(reinterpret_cast<const uint4*>(img) + i);
+    }
+#pragma unroll
+    for (int u = 0; u < IU; ++u) {
+      const long long i = i0 + u * stride;
+      if (i >= total) break;
+      const int v = (int)(i % seg_vec);
+      long long rest = i / seg_vec;
+      const int cx = (int)(rest % gw);
+      rest /= gw;
+      const int y = (int)(rest % H);
+      const int b = (int)(rest / H);
+      const int cy = y / P, py = y % P;
+      const size_t c = (size_t)b * (H / P) * gw + (size_t)cy * gw + cx;
+      uint4* dst = reinterpret_cast<uint4*>(A + c * (size_t)(3 * P * P) + (size_t)py * P * 3) + v;
+      *dst = buf[u];
+    }
   }
 }
 
@@ -268,32 +281,61 @@ __global__ void gather_kernel(const GatherParams p) {
   const int dvec = p.d / 4;  // float4 per row
   const int seg_vec = (p.Pf * 3 * 2) / 16;  // 16B vectors per fine pixel-row segment
   const int fvec = p.Pf * seg_vec;           // 16B vectors per fine patch
+  // Copies are batched GU 16-byte vectors per lane: all loads of a batch are in flight
+  // before its stores (the copy is latency-bound: one load-store pair at a time per lane
+  // left most of the HBM bandwidth idle).
+  constexpr int GU = 8;
   for (int c = g * nw + wid; c < Nc; c += G * nw) {
     const int off = c + (m2 - 1) * pre[c];
     const int pc = pre[c];  // rank among selected cells when pos[c] != 0
     if (pos[c] == 0) {
       const float4* src = reinterpret_cast<const float4*>(p.x0 + ((size_t)t * Nc + c) * p.d);
       float4* dst = reinterpret_cast<float4*>(p.X + (size_t)(tok_base + off) * p.d);
-      for (int v = lane; v < dvec; v += 32) dst[v] = __ldg(src + v);
+      for (int v0 = 0; v0 < dvec; v0 += 32 * GU) {
+        float4 buf[GU];
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+          const int v = v0 + u * 32 + lane;
+          if (v < dvec) buf[u] = __ldg(src + v);
+        }
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+          const int v = v0 + u * 32 + lane;
+          if (v < dvec) dst[v] = buf[u];
+        }
+      }
       if (lane == 0) p.mixed_src[tok_base + off] = c;
     } else {
       const int cy = c / p.gc_w, cx = c % p.gc_w;
-      for (int q = 0; q < m2; ++q) {
+      for (int q = lane; q < m2; q += 32) {
         const int dy = q / p.m, dx = q % p.m;
-        const int fy = p.m * cy + dy, fx = p.m * cx + dx;
-        const int f = fy * p.gf_w + fx;
+        const int f = (p.m * cy + dy) * p.gf_w + (p.m * cx + dx);
         const int arow = fine_base + m2 * pc + q;
-        if (lane == 0) {
-          p.mixed_src[tok_base + off + q] = -1 - f;
-          p.frow[arow] = tok_base + off + q;
-          p.fidx[arow] = f;
+        p.mixed_src[tok_base + off + q] = -1 - f;
+        p.frow[arow] = tok_base + off + q;
+        p.fidx[arow] = f;
+      }
+      // the cell's m^2 fine patches: m^2 * fvec vectors, v -> (patch q, pixel row py, vector sv)
+      const int nv = m2 * fvec;
+      uint4* dst0 = reinterpret_cast<uint4*>(p.A_f + (size_t)(fine_base + m2 * pc) * (3 * p.Pf * p.Pf));
+      for (int v0 = 0; v0 < nv; v0 += 32 * GU) {
+        uint4 buf[GU];
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+          const int v = v0 + u * 32 + lane;
+          if (v < nv) {
+            const int q = v / fvec, r = v - q * fvec;
+            const int py = r / seg_vec, sv = r - py * seg_vec;
+            const int fy = p.m * cy + q / p.m, fx = p.m * cx + q % p.m;
+            const uint4* src = reinterpret_cast<const uint4*>(
+                                   p.images + (((size_t)t * p.H + (size_t)fy * p.Pf + py) * p.W + (size_t)fx * p.Pf) * 3) + sv;
+            buf[u] = __ldg(src);
+          }
         }
-        uint4* dst = reinterpret_cast<uint4*>(p.A_f + (size_t)arow * (3 * p.Pf * p.Pf));
-        for (int v = lane; v < fvec; v += 32) {
-          const int py = v / seg_vec, sv = v % seg_vec;
-          const uint4* src = reinterpret_cast<const uint4*>(
-                                 p.images + (((size_t)t * p.H + (size_t)fy * p.Pf + py) * p.W + (size_t)fx * p.Pf) * 3) + sv;
-          dst[v] = __ldg(src);
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+          const int v = v0 + u * 32 + lane;
+          if (v < nv) dst0[v] = buf[u];  // A_f rows of the cell are consecutive (q-major)
         }
       }
     }

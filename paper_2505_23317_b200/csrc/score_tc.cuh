@@ -9,7 +9,10 @@
 // owns one key column and sums its column in a fixed (head, q-tile, row) order:
 // deterministic, no atomics.
 //
-// One CTA = (key tile of 128, frame).  Warp 0 TMA, warp 1 MMA, warps 2..5 reduce.
+// One CTA = (key tile of 128, frame).  Warp 0 TMA, warp 1 MMA, warps 2..9 reduce: two
+// warps per TMEM lane quarter, each over half of the 128 query columns with four partial
+// sums (the exp pass is latency-bound with one warp per SMSP and a single add chain); the
+// two halves are combined in a fixed order at the end.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -27,12 +30,12 @@ struct ScoreParams {
   float* scores;      // [B, Nc]
 };
 
-constexpr int SCORE_THREADS = 192;
+constexpr int SCORE_THREADS = 320;
 
 template <int DH>
 struct ScoreSmem {
   static constexpr int T_BYTES = 128 * DH * 2;
-  static constexpr int TOTAL = 1024 + 3 * T_BYTES + 2 * 128 * 4 + 256;
+  static constexpr int TOTAL = 1024 + 3 * T_BYTES + 2 * 128 * 4 + 256 + 128 * 4;
 };
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(SCORE_THREADS, 1)
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 128);
+      mbar_init(&s_empty[i], 256);
     }
     fence_barrier_init();
   }
@@ -118,38 +121,49 @@ __global__ void __launch_bounds__(SCORE_THREADS, 1)
     }
   } else {
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;  // query columns [64 half, 64 half + 64)
     const int r = quarter * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const float c = p.scale_log2;
+    float* xch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [128] half-1 partial sums
     float acc = 0.f;
     for (int it = 0; it < total; ++it) {
       const int h = it / nq, qt = it % nq;
-      const int q = qt * 128 + r;
-      lse_s[(it & 1) * 128 + r] = (q < Nc) ? __ldg(p.lse + (size_t)h * p.lse_ld + row0 + q) * 1.4426950408889634f : 0.f;
-      named_bar_sync(1, 128);
+      if (half == 0) {
+        const int q = qt * 128 + r;
+        lse_s[(it & 1) * 128 + r] = (q < Nc) ? __ldg(p.lse + (size_t)h * p.lse_ld + row0 + q) * 1.4426950408889634f : 0.f;
+      }
+      named_bar_sync(1, 256);
       mbar_wait(&s_full[it & 1], (it >> 1) & 1);
       tc_fence_after();
-      uint32_t sr[128];
-      const uint32_t a = tmem + lane_off + (it & 1) * 128;
+      uint32_t sr[64];
+      const uint32_t a = tmem + lane_off + (it & 1) * 128 + half * 64;
       tmem_ld32(a + 0, *reinterpret_cast<uint32_t(*)[32]>(sr + 0));
       tmem_ld32(a + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
-      tmem_ld32(a + 64, *reinterpret_cast<uint32_t(*)[32]>(sr + 64));
-      tmem_ld32(a + 96, *reinterpret_cast<uint32_t(*)[32]>(sr + 96));
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&s_empty[it & 1]);
-      const int nvq = min(128, Nc - qt * 128);
-      const float* ls = lse_s + (it & 1) * 128;
-      float part = 0.f;
+      const int nvq = min(128, Nc - qt * 128) - half * 64;  // valid query columns of this half
+      const float* ls = lse_s + (it & 1) * 128 + half * 64;
+      float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
 #pragma unroll
-      for (int i = 0; i < 128; ++i) {
-        const float e = ex2_approx(fmaf(__uint_as_float(sr[i]), c, -ls[i]));
-        part += (i < nvq) ? e : 0.f;
+      for (int i = 0; i < 64; i += 4) {
+        const float e0 = ex2_approx(fmaf(__uint_as_float(sr[i]), c, -ls[i]));
+        const float e1 = ex2_approx(fmaf(__uint_as_float(sr[i + 1]), c, -ls[i + 1]));
+        const float e2 = ex2_approx(fmaf(__uint_as_float(sr[i + 2]), c, -ls[i + 2]));
+        const float e3 = ex2_approx(fmaf(__uint_as_float(sr[i + 3]), c, -ls[i + 3]));
+        p0 += (i < nvq) ? e0 : 0.f;
+        p1 += (i + 1 < nvq) ? e1 : 0.f;
+        p2 += (i + 2 < nvq) ? e2 : 0.f;
+        p3 += (i + 3 < nvq) ? e3 : 0.f;
       }
-      acc += part;
+      acc += (p0 + p1) + (p2 + p3);
     }
+    // fixed-order combination of the two column halves (deterministic)
+    if (half == 1) xch[r] = acc;
+    named_bar_sync(1, 256);
     const int key = kt * 128 + r;
-    if (key < Nc) p.scores[(size_t)b * Nc + key] = acc / (float)(p.n_heads * Nc);
+    if (half == 0 && key < Nc) p.scores[(size_t)b * Nc + key] = (acc + xch[r]) / (float)(p.n_heads * Nc);
   }
   tc_fence_before();
   __syncthreads();
