@@ -58,7 +58,11 @@ __device__ unsigned long long g_attn_trace[ATTN_TRACE_WORDS];
 constexpr int ATTN4_THREADS = 512;    // TMA warp, 3 MMA warps, 12 softmax warps
 constexpr int ATTN4_NWG = 3;
 
-template <int DH, int STAGES, int NPP>
+// TOKEN: the three warpgroups take turns on the exp (MUFU) phase — warpgroup w starts the
+// exponentials of a sub-tile only after warpgroup w-1 finished its own (a token ring of
+// mbarriers, one phase per sub-tile), so their exp phases are serialised and each one's
+// latency-bound phases (TMEM load, max, P store, hand-offs) overlap the others' exps.
+template <int DH, int STAGES, int NPP, bool TOKEN = false>
 __global__ void __launch_bounds__(ATTN4_THREADS, 1)
     attn4_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const AttnParams p, const int T, const int nh) {
   static_assert(DH == 32, "specialised for dh = 32 (64-byte rows, SW64)");
@@ -74,7 +78,8 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
   uint64_t* s_free = s_full + 3;            // [3 w]
   uint64_t* p_full = s_free + 3;            // [3 w]
   uint64_t* o_full = p_full + 3;            // [3 w]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 3);
+  uint64_t* exp_tok = o_full + 3;           // [3 w] TOKEN: warpgroup w finished its exps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(exp_tok + 3);
   int* prefix = reinterpret_cast<int*>(smem + S::PRE_OFF);
 
   const int warp = warp_id(), lane = lane_id();
@@ -96,6 +101,7 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
       mbar_init(&s_free[w], 128);
       mbar_init(&p_full[w], 128);
       mbar_init(&o_full[w], 1);
+      mbar_init(&exp_tok[w], 4);  // one arrival per warp of the warpgroup
     }
     fence_barrier_init();
   }
@@ -188,6 +194,7 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
           if ((u & 1) == 0) mbar_wait(&kv_full[st], ((kvc + j) / STAGES) & 1);
           const uint32_t ka = smem_u32(smem + S::K_OFF + st * S::TILE_BYTES) + (u & 1) * 64 * DH * 2;
           if (s_use > 0) mbar_wait(&s_free[w], (s_use - 1) & 1);
+          if (p.stagger == -2 && u > 0) ATTN_TR(w, it, u - 1, 5);  // (in sub-tile u-1's row) s_free passed
           ++s_use;
           tc_fence_after();
 #pragma unroll
@@ -197,21 +204,28 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
           mma_commit(&s_full[w]);
           ATTN_TR(w, it, u, 6);
         };
+        // trace mode "mma" (p.stagger == -2): events 0..5 of the MMA warp's sub-tile u
+        const bool tm = p.stagger == -2;
         issue_qk(0);
         for (int u = 0; u < nsub; ++u) {
+          if (tm) ATTN_TR(w, it, u, 0);
           if (u + 1 < nsub) issue_qk(u + 1);  // S_{u+1} overlaps the softmax of S_u
+          if (tm) ATTN_TR(w, it, u, 1);
           const int j = u >> 1;
           const int st = (kvc + j) % STAGES;
           const int valid = min(64, N - u * 64);
           const int ksteps = (valid + 15) / 16;
           const uint32_t va = smem_u32(smem + S::V_OFF + st * S::TILE_BYTES) + (u & 1) * 64 * DH * 2;
           mbar_wait(&p_full[w], p_cnt & 1);
+          if (tm) ATTN_TR(w, it, u, 2);
           ++p_cnt;
           tc_fence_after();
           for (int k = 0; k < ksteps; ++k)
             mma_ts(tmem + w * 128 + S::O_COL, tmem + w * 128 + S::P_COL + k * 8,
                    make_smem_desc(va + k * 16 * DH * 2, 4096, 512, kLayoutSW64), idesc_o, (u | k) != 0);
+          if (tm) ATTN_TR(w, it, u, 3);
           mma_commit(&o_full[w]);
+          if (tm) ATTN_TR(w, it, u, 4);
           ATTN_TR(w, it, u, 7);
           if ((u & 1) || u + 1 == nsub) mma_commit(&kv_empty[st]);
         }
@@ -230,8 +244,32 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
     const uint32_t o_addr = tmem + lane_off + wg * 128 + S::O_COL;
     const float c = p.scale_log2;
     uint32_t s_cnt = 0, o_cnt = 0;
-    const bool tr = (warp & 3) == 0 && lane == 0;
+    uint32_t g_tok = 0;  // TOKEN: sub-tiles (exp turns) of this warpgroup so far
+    const int prev_wg = (wg + ATTN4_NWG - 1) % ATTN4_NWG;
+    // wait for the previous warpgroup's turn g (warpgroup 0: the last warpgroup's turn g-1)
+    auto tok_wait = [&]() {
+      if constexpr (TOKEN) {
+        if (wg == 0) {
+          if (g_tok > 0) mbar_wait(&exp_tok[prev_wg], (g_tok - 1) & 1);
+        } else {
+          mbar_wait(&exp_tok[prev_wg], g_tok & 1);
+        }
+      }
+    };
+    auto tok_pass = [&]() {
+      if constexpr (TOKEN) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&exp_tok[wg]);
+        ++g_tok;
+      }
+    };
+    // trace: lane 0 of the quarter-0 warp; with p.stagger == -1 (trace mode "quarters") events
+    // 0..2 instead record the p_full arrival of the quarter 1..3 warps
+    const bool qmode = p.stagger == -1;
+    const bool tr = (warp & 3) == 0 && lane == 0 && !qmode && p.stagger != -2;
+    const bool trq = lane == 0 && qmode;
     (void)tr;
+    (void)trq;
     if (p.stagger > 0 && wg > 0) {  // de-phase the warpgroups so their exp phases interleave
       const long long t_end = clock64() + (long long)wg * p.stagger;
       while (clock64() < t_end) __nanosleep(64);
@@ -244,8 +282,16 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
       const int seq0 = __ldg(p.cu_seqlens + t);
       const int N = __ldg(p.cu_seqlens + t + 1) - seq0;
       const int qt = 3 * qp + wg;
-      if (qt * 128 >= N) continue;
       const int nsub = (N + 63) / 64;
+      if (qt * 128 >= N) {
+        if constexpr (TOKEN) {  // no query tile here: still take (and pass) every turn
+          for (int u = 0; u < nsub; ++u) {
+            tok_wait();
+            tok_pass();
+          }
+        }
+        continue;
+      }
       const int q_valid = N - qt * 128;
       const bool active = quarter * 32 < q_valid;
       float m_run = -INFINITY, l_run = 0.f;
@@ -283,6 +329,7 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
           if (upd) m_run = m_cand;
           const float neg = -m_run;
           float sum0 = 0.f, sum1 = 0.f, sum2 = 0.f, sum3 = 0.f;
+          tok_wait();
           if (valid == 64) {
             exp_chunk<NPP>(sr, c, neg, sum0, sum1);
             exp_chunk<NPP>(sr + 32, c, neg, sum2, sum3);
@@ -290,6 +337,7 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
             exp_chunk<0>(sr, c, neg, sum0, sum1);
             if (valid > 32) exp_chunk<0>(sr + 32, c, neg, sum2, sum3);
           }
+          tok_pass();
           l_run = l_run * alpha + ((sum0 + sum1) + (sum2 + sum3));
           if (tr) ATTN_TR(wg, it, u, 3);
           if (u > 0) {
@@ -320,6 +368,8 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
           // padding-only warp: still waits for PV_{u-1} so it cannot arrive on p_full for
           // sub-tile u before that barrier's previous phase (sub-tile u-1) has completed
           mbar_arrive(&s_free[wg]);
+          tok_wait();
+          tok_pass();
           if (u > 0) {
             mbar_wait(&o_full[wg], o_cnt & 1);
             ++o_cnt;
@@ -328,6 +378,7 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
         tc_fence_before();
         mbar_arrive(&p_full[wg]);
         if (tr) ATTN_TR(wg, it, u, 5);
+        if (trq) ATTN_TR(wg, it, u, (warp & 3) == 0 ? 5 : (warp & 3) - 1);
       }
       if (active) {
         mbar_wait(&o_full[wg], o_cnt & 1);
