@@ -62,7 +62,12 @@ constexpr int ATTN4_NWG = 3;
 // exponentials of a sub-tile only after warpgroup w-1 finished its own (a token ring of
 // mbarriers, one phase per sub-tile), so their exp phases are serialised and each one's
 // latency-bound phases (TMEM load, max, P store, hand-offs) overlap the others' exps.
-template <int DH, int STAGES, int NPP, bool TOKEN = false>
+// SPLIT: break the MMAs' accumulator dependency chains (a dependent tcgen05.mma at these
+// shapes costs ~150 cycles of latency, tools/tc_micro.cu): QK as two independent N = 32
+// halves (keys 0-31 / 32-63 of the sub-tile, each a K-chain of 2) and PV into two O
+// accumulators (keys 0-31 -> O_a, 32-63 -> O_b, each a chain of 2), O = O_a + O_b at the end.
+// TMEM per warpgroup: S 64 | P 32 | O_a 32 | O_b 32 at w*160.
+template <int DH, int STAGES, int NPP, bool TOKEN = false, bool SPLIT = false>
 __global__ void __launch_bounds__(ATTN4_THREADS, 1)
     attn4_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const AttnParams p, const int T, const int nh) {
   static_assert(DH == 32, "specialised for dh = 32 (64-byte rows, SW64)");
@@ -91,6 +96,7 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
     prefix[t + 1] = ((n + 383) / 384) * nh;
   }
   constexpr int kMmaWarp0 = 12, kTmaWarp = 15;
+  constexpr uint32_t WST = SPLIT ? 160 : 128;  // TMEM columns per warpgroup
   if (warp == kTmaWarp && lane == 0) {
     tma_prefetch(&tmQKV);
     // Q slots and K/V stages are released by all three MMA threads (one per warpgroup)
@@ -197,10 +203,20 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
           if (p.stagger == -2 && u > 0) ATTN_TR(w, it, u - 1, 5);  // (in sub-tile u-1's row) s_free passed
           ++s_use;
           tc_fence_after();
+          if constexpr (SPLIT) {
+            constexpr uint32_t idesc_h = make_idesc_bf16(128, 32, 0);
 #pragma unroll
-          for (int k = 0; k < DH / 16; ++k)
-            mma_ss(tmem + w * 128 + S::S_COL, make_smem_desc(qa + k * 32, 16, 512, kLayoutSW64),
-                   make_smem_desc(ka + k * 32, 16, 512, kLayoutSW64), idesc_s, k);
+            for (int k = 0; k < DH / 16; ++k)
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh)  // keys [32 hh, 32 hh + 32): rows 32 hh of the K tile
+                mma_ss(tmem + w * WST + S::S_COL + hh * 32, make_smem_desc(qa + k * 32, 16, 512, kLayoutSW64),
+                       make_smem_desc(ka + hh * 32 * DH * 2 + k * 32, 16, 512, kLayoutSW64), idesc_h, k);
+          } else {
+#pragma unroll
+            for (int k = 0; k < DH / 16; ++k)
+              mma_ss(tmem + w * WST + S::S_COL, make_smem_desc(qa + k * 32, 16, 512, kLayoutSW64),
+                     make_smem_desc(ka + k * 32, 16, 512, kLayoutSW64), idesc_s, k);
+          }
           mma_commit(&s_full[w]);
           ATTN_TR(w, it, u, 6);
         };
@@ -220,9 +236,22 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
           if (tm) ATTN_TR(w, it, u, 2);
           ++p_cnt;
           tc_fence_after();
-          for (int k = 0; k < ksteps; ++k)
-            mma_ts(tmem + w * 128 + S::O_COL, tmem + w * 128 + S::P_COL + k * 8,
-                   make_smem_desc(va + k * 16 * DH * 2, 4096, 512, kLayoutSW64), idesc_o, (u | k) != 0);
+          if constexpr (SPLIT) {
+            // O_a <- keys 0-31 (k-steps 0, 1), O_b <- keys 32-63 (k-steps 2, 3), interleaved
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const int k = hh * 2 + kk;
+                if (k < ksteps)
+                  mma_ts(tmem + w * WST + S::O_COL + hh * 32, tmem + w * WST + S::P_COL + k * 8,
+                         make_smem_desc(va + k * 16 * DH * 2, 4096, 512, kLayoutSW64), idesc_o, (u | kk) != 0);
+              }
+          } else {
+            for (int k = 0; k < ksteps; ++k)
+              mma_ts(tmem + w * WST + S::O_COL, tmem + w * WST + S::P_COL + k * 8,
+                     make_smem_desc(va + k * 16 * DH * 2, 4096, 512, kLayoutSW64), idesc_o, (u | k) != 0);
+          }
           if (tm) ATTN_TR(w, it, u, 3);
           mma_commit(&o_full[w]);
           if (tm) ATTN_TR(w, it, u, 4);
@@ -239,9 +268,9 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t s_base = tmem + lane_off + wg * 128 + S::S_COL;
-    const uint32_t p_addr = tmem + lane_off + wg * 128 + S::P_COL;
-    const uint32_t o_addr = tmem + lane_off + wg * 128 + S::O_COL;
+    const uint32_t s_base = tmem + lane_off + wg * WST + S::S_COL;
+    const uint32_t p_addr = tmem + lane_off + wg * WST + S::P_COL;
+    const uint32_t o_addr = tmem + lane_off + wg * WST + S::O_COL;  // SPLIT: O_a, O_b at +32
     const float c = p.scale_log2;
     uint32_t s_cnt = 0, o_cnt = 0;
     uint32_t g_tok = 0;  // TOKEN: sub-tiles (exp turns) of this warpgroup so far
@@ -346,18 +375,21 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
             ++o_cnt;
             tc_fence_after();
             if (__any_sync(0xffffffffu, upd)) {
-              uint32_t o[32];
-              tmem_ld32(o_addr, o);
-              tmem_wait_ld();
+#pragma unroll 1
+              for (int hh = 0; hh < (SPLIT && N > 32 ? 2 : 1); ++hh) {  // O_b exists once N > 32
+                uint32_t o[32];
+                tmem_ld32(o_addr + hh * 32, o);
+                tmem_wait_ld();
 #pragma unroll
-              for (int i = 0; i < DH; i += 2) {
-                float a0, a1;
-                fma2(a0, a1, __uint_as_float(o[i]), __uint_as_float(o[i + 1]), alpha, alpha, 0.f, 0.f);
-                o[i] = __float_as_uint(a0);
-                o[i + 1] = __float_as_uint(a1);
+                for (int i = 0; i < DH; i += 2) {
+                  float a0, a1;
+                  fma2(a0, a1, __uint_as_float(o[i]), __uint_as_float(o[i + 1]), alpha, alpha, 0.f, 0.f);
+                  o[i] = __float_as_uint(a0);
+                  o[i + 1] = __float_as_uint(a1);
+                }
+                tmem_st16(o_addr + hh * 32, *reinterpret_cast<const uint32_t(*)[16]>(o));
+                tmem_st16(o_addr + hh * 32 + 16, *reinterpret_cast<const uint32_t(*)[16]>(o + 16));
               }
-              tmem_st16(o_addr, *reinterpret_cast<const uint32_t(*)[16]>(o));
-              tmem_st16(o_addr + 16, *reinterpret_cast<const uint32_t(*)[16]>(o + 16));
             }
           }
           if (tr) ATTN_TR(wg, it, u, 4);
@@ -387,6 +419,21 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
         uint32_t o[32];
         tmem_ld32(o_addr, o);
         tmem_wait_ld();
+        if constexpr (SPLIT) {
+          if (N > 32) {  // O = O_a + O_b
+            uint32_t o2[32];
+            tmem_ld32(o_addr + 32, o2);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < DH; i += 2) {
+              float a0, a1;
+              add2(a0, a1, __uint_as_float(o[i]), __uint_as_float(o[i + 1]), __uint_as_float(o2[i]),
+                   __uint_as_float(o2[i + 1]));
+              o[i] = __float_as_uint(a0);
+              o[i + 1] = __float_as_uint(a1);
+            }
+          }
+        }
         if (r < q_valid) {
           const float inv = 1.f / l_run;
           uint32_t ob[DH / 2];

@@ -239,6 +239,7 @@ int g_attn_npp = 4;
 int g_attn_stagger = 0;
 int g_attn_stages = 4;  // v4 K/V ring depth (128-key stages): 4, 6 or 8
 int g_attn_token = 0;   // v4 exp-phase token ring (option 9)
+int g_attn_split = 0;   // v4 split MMA accumulator chains (option 10)
 int g_fused_mlp = 1;  // fused MLP kernel (d == 256) instead of two GEMM launches
 int g_staged_epi = 1; // TMA-staged residual + LayerNorm epilogue for the O-projection
 int g_mlp_cluster = 0; // fused MLP as CTA pairs (cta_group::2)
@@ -288,11 +289,11 @@ cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUte
   return cudaGetLastError();
 }
 
-template <int V, int NPP, int ST = 4, bool TOK = false>
+template <int V, int NPP, int ST = 4, bool TOK = false, bool SPL = false>
 cudaError_t launch_attn2_t(const CUtensorMap& tq, const AttnParams& p, int items_ub, int nh, int T, cudaStream_t s) {
   auto kern = (V == 2)   ? attn2_tc_kernel<32, 4, NPP>
               : (V == 3) ? attn3_tc_kernel<32, 4, NPP>
-              : (V == 4) ? attn4_tc_kernel<32, ST, NPP, TOK>
+              : (V == 4) ? attn4_tc_kernel<32, ST, NPP, TOK, SPL>
               : (V == 6) ? attn6_tc_kernel<32, ST, NPP>
                          : attn5_tc_kernel<32, 4, NPP>;
   constexpr int smem = (V == 2)   ? Attn2Smem<32, 4>::TOTAL
@@ -366,7 +367,8 @@ cudaError_t launch_attention(const CUtensorMap& tq, const AttnParams& p, int max
         case 10: e = launch_attn2_t<4, 10>(tq, p, items_ub, nh, T, s); break;
         case 12: e = launch_attn2_t<4, 12>(tq, p, items_ub, nh, T, s); break;
         default:
-          e = g_attn_token         ? launch_attn2_t<4, 4, 4, true>(tq, p, items_ub, nh, T, s)
+          e = g_attn_split         ? launch_attn2_t<4, 4, 4, false, true>(tq, p, items_ub, nh, T, s)
+              : g_attn_token       ? launch_attn2_t<4, 4, 4, true>(tq, p, items_ub, nh, T, s)
               : g_attn_stages == 8 ? launch_attn2_t<4, 4, 8>(tq, p, items_ub, nh, T, s)
               : g_attn_stages == 6 ? launch_attn2_t<4, 4, 6>(tq, p, items_ub, nh, T, s)
                                    : launch_attn2_t<4, 4>(tq, p, items_ub, nh, T, s);
@@ -672,6 +674,9 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
       return CFD_OK;
     case 9:
       g_attn_token = value ? 1 : 0;
+      return CFD_OK;
+    case 10:
+      g_attn_split = value ? 1 : 0;
       return CFD_OK;
     case 6:
       if (value != 4 && value != 6 && value != 8) return CFD_E_ARG;

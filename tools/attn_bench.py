@@ -17,12 +17,14 @@ ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--stagger", type=int, default=0)
 ap.add_argument("--stages", type=int, default=4)
 ap.add_argument("--token", type=int, default=0)
+ap.add_argument("--split", type=int, default=0)
 a = ap.parse_args()
 lib = L.load()
 assert lib.cfdx_set_option(0, a.variant) == 0 and lib.cfdx_set_option(1, a.npp) == 0
 assert lib.cfdx_set_option(5, a.stagger) == 0
 assert lib.cfdx_set_option(6, a.stages) == 0
 assert lib.cfdx_set_option(9, a.token) == 0
+assert lib.cfdx_set_option(10, a.split) == 0
 lens = []
 for part in a.lens.split(","):
     n, c = part.split("x")
@@ -48,4 +50,4 @@ e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) / a.reps * 1e3
 fl = sum(4 * n * n * d for n in lens)
-print(f"variant {a.variant} npp {a.npp} stages {a.stages} token {a.token} lens {a.lens}: {us:.1f} us  {fl / us / 1e6:.1f} TFLOP/s")
+print(f"variant {a.variant} npp {a.npp} stages {a.stages} token {a.token} split {a.split} lens {a.lens}: {us:.1f} us  {fl / us / 1e6:.1f} TFLOP/s")

@@ -15,6 +15,7 @@ lib = L.load()
 assert lib.cfdx_set_option(0, var) == 0 and lib.cfdx_set_option(1, npp) == 0
 assert lib.cfdx_set_option(6, int(os.environ.get("CFD_STAGES", "4"))) == 0
 assert lib.cfdx_set_option(9, int(os.environ.get("CFD_TOKEN", "0"))) == 0
+assert lib.cfdx_set_option(10, int(os.environ.get("CFD_SPLIT", "0"))) == 0
 cu_l = [0]
 for n in lens:
     cu_l.append(cu_l[-1] + n)
