@@ -243,17 +243,21 @@ int g_attn_split = 0;   // v4 split MMA accumulator chains (option 10)
 int g_fused_mlp = 1;  // fused MLP kernel (d == 256) instead of two GEMM launches
 int g_staged_epi = 1; // TMA-staged residual + LayerNorm epilogue for the O-projection
 int g_mlp_cluster = 0; // fused MLP as CTA pairs (cta_group::2)
+int g_fuse_oproj = 1;  // O-projection + residual + LN2 inside the fused MLP kernel (option 11)
 
 // tw1: W1 with 128-row boxes (single-CTA kernel); tw1h: 64-row boxes (CTA-pair kernel)
+// two (opj): th is the attention output o (the fused O-projection's A operand), two = W_o map
 cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUtensorMap& tw1h, const CUtensorMap& tw2,
                        const MlpParams& p, int rows_for_grid, cudaStream_t s, const CUtensorMap* tx = nullptr,
-                       const CUtensorMap* tln = nullptr) {
+                       const CUtensorMap* tln = nullptr, const CUtensorMap* two = nullptr) {
   constexpr int smem = MlpSmem<256>::TOTAL;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(mlp_tc_kernel<256, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(mlp_tc_kernel<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mlp_tc_kernel<256, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -278,12 +282,14 @@ cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUte
     la[0].val.clusterDim.z = 1;
     lc.attrs = la;
     lc.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&lc, mlp_tc_kernel<256, 2>, th, tw1h, tw2, q, mx, ml);
+    cudaError_t e = cudaLaunchKernelEx(&lc, mlp_tc_kernel<256, 2>, th, tw1h, tw2, q, mx, ml, th);
     ++g_launches;
     return e != cudaSuccess ? e : cudaGetLastError();
   }
   const int grid = std::max(1, std::min(tiles, num_sms()));
-  const cudaError_t le = launch_ex(mlp_tc_kernel<256, 1>, dim3(grid), dim3(MLP_THREADS), smem, s, th, tw1, tw2, q, mx, ml);
+  const cudaError_t le =
+      two ? launch_ex(mlp_tc_kernel<256, 1, true>, dim3(grid), dim3(MLP_THREADS), smem, s, th, tw1, tw2, q, mx, ml, *two)
+          : launch_ex(mlp_tc_kernel<256, 1>, dim3(grid), dim3(MLP_THREADS), smem, s, th, tw1, tw2, q, mx, ml, th);
   if (le != cudaSuccess) return le;
   ++g_launches;
   return cudaGetLastError();
@@ -434,6 +440,7 @@ struct LayerDev {
   float *b_qkv, *b_o, *b_1, *b_2, *ln1_g, *ln1_b, *ln2_g, *ln2_b;
   CUtensorMap tm_qkv, tm_o, tm_1, tm_2;
   CUtensorMap tm_1c, tm_2c;  // W1 / W2 with 128-row x 64-k boxes (fused MLP ring slots)
+  CUtensorMap tm_oc;         // W_o with 128-row x 64-k boxes (fused O-projection + MLP)
   CUtensorMap tm_1h;         // W1 with 64-row x 64-k boxes (CTA-pair fused MLP)
 };
 
@@ -527,6 +534,26 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
     sp.n_coarse = c->Nc; sp.n_heads = g.n_heads; sp.d_model = d; sp.lse = w.lse; sp.lse_ld = w.lse_ld;
     sp.scale_log2 = ap.scale_log2; sp.scores = scores;
     CFD_CUDA(launch_score(tq, sp, score_B, s));
+  }
+  const bool staged_ok = fuse_ln && g_staged_epi && (d % 64 == 0);
+  if (g_fuse_oproj && g_fused_mlp && !g_mlp_cluster && staged_ok && d == 256 && F % 128 == 0) {
+    // O projection + residual + LN2 fused into the MLP kernel (LN2 never leaves the SM)
+    CUtensorMap tx, tln;
+    if (!make_tmap(&tx, x, d, x_cap, d, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, true) ||
+        !make_tmap(&tln, w.hbuf, d, w.rows_cap, d, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+      return CFD_E_CUDA;
+    MlpParams mp{};
+    mp.M = M_static; mp.m_dev = m_dev; mp.F = F; mp.b1 = L.b_1; mp.b2 = L.b_2; mp.x = x; mp.ln_eps = g.ln_eps;
+    mp.bo = L.b_o; mp.ln2_g = L.ln2_g; mp.ln2_b = L.ln2_b;
+    mp.ln_cap = w.rows_cap;
+    if (l + 1 < g.n_layers) {
+      const LayerDev& Ln = c->layers[l + 1];
+      mp.ln_g = Ln.ln1_g; mp.ln_b = Ln.ln1_b; mp.ln_out = w.hbuf;
+    }
+    probe_begin(PK_MLP1, s);
+    CFD_CUDA(launch_mlp(ta_o, L.tm_1c, L.tm_1h, L.tm_2c, mp, rows_grid, s, &tx, &tln, &L.tm_oc));
+    probe_end(PK_MLP1, s);
+    return CFD_OK;
   }
   // O projection + residual (+ LN2 -> hbuf)
   p = GemmParams{};
@@ -678,6 +705,9 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
     case 10:
       g_attn_split = value ? 1 : 0;
       return CFD_OK;
+    case 11:
+      g_fuse_oproj = value ? 1 : 0;
+      return CFD_OK;
     case 6:
       if (value != 4 && value != 6 && value != 8) return CFD_E_ARG;
       g_attn_stages = value;
@@ -780,7 +810,8 @@ cfd_status cfd_create(const cfd_config* cfg, const cfd_weights* wts, void* strea
         !make_wmap(&ld.tm_1, ld.w1, F, d) || !make_wmap(&ld.tm_2, ld.w2, d, F) ||
         !make_tmap(&ld.tm_1c, ld.w1, d, F, d, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !make_tmap(&ld.tm_2c, ld.w2, F, d, F, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_tmap(&ld.tm_1h, ld.w1, d, F, d, GEMM_BK, 64, CU_TENSOR_MAP_SWIZZLE_128B))
+        !make_tmap(&ld.tm_1h, ld.w1, d, F, d, GEMM_BK, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap(&ld.tm_oc, ld.wo, d, d, d, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B))
       return fail(CFD_E_CUDA);
   }
   *out = c;

@@ -219,12 +219,16 @@ struct ResidLnArgs {
   float ln_eps;
 };
 
-template <int CH, bool LN>
+// LNT: the LayerNorm output goes to TMEM instead of memory — bf16 pairs of the row's columns
+// (col_base + 2i, +1) at column ln_tmem + i of this warp's lanes (the A-operand layout of a
+// TS-form MMA over the normalised row), used by the fused O-projection + MLP kernel.
+template <int CH, bool LN, bool LNT = false>
 __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtensorMap& tmX, const CUtensorMap& tmLN,
                                              const ResidStage& st, uint32_t tbase, int row0, int col_base, int M,
                                              const float* bias_s, const float* lng_s, const float* lnb_s,
                                              float2* stats, int quarter, int half, int lane, uint64_t* tfull_bar,
-                                             uint32_t tfull_parity, uint64_t* tempty_bar, int tempty_cta = -1) {
+                                             uint32_t tfull_parity, uint64_t* tempty_bar, int tempty_cta = -1,
+                                             uint32_t ln_tmem = 0) {
   // tempty_cta >= 0: the accumulator-empty barrier lives in that cluster CTA (CTA-pair MMA)
   auto release_acc = [&]() {
     if (tempty_cta >= 0) mbar_arrive_cluster(tempty_bar, static_cast<uint32_t>(tempty_cta));
@@ -327,6 +331,10 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
           pk[2 * q] = 0u;
           pk[2 * q + 1] = 0u;
         }
+      }
+      if constexpr (LNT) {
+        tmem_st16(ln_tmem + c * 16, pk);
+        continue;
       }
       const int b = c & 1;
       if (c >= (one_hb ? 1 : 2)) {  // the TMA store that last read this hb must be done reading

@@ -24,6 +24,15 @@
 // group is 4 slots and a W2 k-block always occupies two adjacent slots (one 256-row operand).
 // The 128 KB ring keeps ~2 operands of loads in flight ahead of the MMAs.  The epilogue warps
 // consume the h pieces (smem -> TMEM copy), the MMA warp everything else.
+//
+// OPJ (fused O-projection, single-CTA kernel): the tile starts from the attention output o
+// instead of h: MMA_o: acc2 = o . W_o^T (A and W_o through the ring), then the epilogue
+// warps form x1 = x + acc2 + b_o (x staged by TMA, x1 stored by TMA) and write
+// h = LN2(x1) straight into the TMEM h tile (bf16 pairs), so the O-projection launch, the
+// LN2 round trip through memory and the h load disappear.  Ring per tile:
+//   o0 o1 | Wo0 (2 slots: rows 0-127, 128-255) | Wo1 | o2 o3 | Wo2 | Wo3 | W1(0) | ...
+// (12 slots; every W_o pair starts on an even slot so it is one contiguous 256-row operand).
+// acc2 is used twice per tile (acc_o, then the MLP2 accumulation): a2_empty completes twice.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -46,6 +55,10 @@ struct MlpParams {
   int ln_cap;
   float ln_eps;
   int staged;            // 1: residual (+LN) epilogue staged through smem with TMA (tmX / tmLN valid)
+  // OPJ only: O-projection bias and this layer's LN2
+  const float* bo;
+  const float* ln2_g;
+  const float* ln2_b;
 };
 
 constexpr int MLP_THREADS = 320;  // TMA warp, MMA warp, 8 epilogue warps
@@ -83,7 +96,8 @@ struct MlpSmem {
   // staged final epilogue: each epilogue warp's x staging buffers are its own 4 KB slices of
   // H[0] / H[1] (the slices it writes during GELU, free once the last MMA2 has committed);
   // one 2 KB LN output buffer per warp lives here
-  static constexpr int LNSTG_OFF = ((PAR_OFF + (GEMM_MAX_N + 3 * D) * 4 + 1023) / 1024) * 1024;
+  // ... | b_o [D] | ln2 g [D] | ln2 b [D] (OPJ)
+  static constexpr int LNSTG_OFF = ((PAR_OFF + (GEMM_MAX_N + 6 * D) * 4 + 1023) / 1024) * 1024;
   static constexpr int TOTAL = 1024 + LNSTG_OFF + 8 * 2048;
 };
 
@@ -99,11 +113,13 @@ struct MlpSmem {
 // commits are multicast to both CTAs (w_empty, a1_full, h_empty, a2_full); the epilogues of
 // both CTAs arrive on the leader's ht_full / a1_empty / h_full / a2_empty.  The pair walks
 // tile pairs in lockstep; an odd last tile leaves CTA 1 a masked "ghost" tile.
-template <int D, int CL>
+template <int D, int CL, bool OPJ = false>
 __global__ void __launch_bounds__(MLP_THREADS, 1)
     mlp_tc_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW1,
                   const __grid_constant__ CUtensorMap tmW2, const MlpParams p,
-                  const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmLN) {
+                  const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmLN,
+                  const __grid_constant__ CUtensorMap tmWo) {
+  static_assert(!OPJ || CL == 1, "the fused O-projection is built for the single-CTA kernel");
   using S = MlpSmem<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
@@ -118,12 +134,16 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   uint64_t* a2_full = h_empty + 2;
   uint64_t* a2_empty = a2_full + 1;
   uint64_t* xbar = a2_empty + 1;             // [8 warps][2] staged-epilogue TMA loads
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + 16);
+  uint64_t* ao_full = xbar + 16;             // OPJ: acc_o = o . W_o^T complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ao_full + 1);
   float2* ln_stats = reinterpret_cast<float2*>(smem + S::STATS_OFF);
   float* b1_s = reinterpret_cast<float*>(smem + S::PAR_OFF);
   float* b2_s = b1_s + GEMM_MAX_N;
   float* lng_s = b2_s + D;
   float* lnb_s = lng_s + D;
+  float* bo_s = lnb_s + D;     // OPJ
+  float* g2_s = bo_s + D;
+  float* b2ln_s = g2_s + D;
 
   const int warp = warp_id(), lane = lane_id();
   const int M = p.m_dev ? __ldg(p.m_dev) : p.M;
@@ -132,7 +152,10 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   const int n_chunks = p.F / 128;
   constexpr int KB = D / 64;                 // k-blocks of the h tile (= its ring pieces)
   constexpr bool PAIR = (CL == 2);
-  const int slots_per_tile = KB + (PAIR ? 4 : 8) * n_chunks;
+  const int slots_per_tile = (OPJ ? 3 * KB : KB) + (PAIR ? 4 : 8) * n_chunks;
+  // OPJ ring offsets of k-block kb within a tile: o piece / first slot of the W_o pair
+  auto opj_o = [](int kb) { return (kb < 2) ? kb : 4 + kb; };          // 0 1 6 7
+  auto opj_w = [](int kb) { return (kb < 2) ? 2 + 2 * kb : 4 + 2 * kb; };  // 2 4 8 10
   const int rank = (CL == 2) ? static_cast<int>(cluster_ctarank()) : 0;
   const int t_first = (CL == 2) ? 2 * static_cast<int>(cluster_id_x()) + rank : static_cast<int>(blockIdx.x);
   const int t_step = (CL == 2) ? 2 * static_cast<int>(nclusters_x()) : static_cast<int>(gridDim.x);
@@ -143,6 +166,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     tma_prefetch(&tmH);
     tma_prefetch(&tmW1);
     tma_prefetch(&tmW2);
+    if constexpr (OPJ) tma_prefetch(&tmWo);
     for (int i = 0; i < MLP_SLOTS; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 1); }
     mbar_init(ht_full, CL);
     mbar_init(a1_full, 1);
@@ -151,6 +175,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     mbar_init(a2_full, 1);
     mbar_init(a2_empty, 8 * CL);
     for (int i = 0; i < 16; ++i) mbar_init(&xbar[i], 1);
+    mbar_init(ao_full, 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -216,7 +241,15 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
       MLP_TILES(tile) {
         MLP_TR(pit, 0);
         ++pit;
-        for (int kb = 0; kb < KB; ++kb) load(&tmH, kb * 64, tile * 128);
+        if constexpr (OPJ) {  // o0 o1 Wo0 Wo1 o2 o3 Wo2 Wo3 (W_o k-block = 2 slots of 128 rows)
+          for (int g2 = 0; g2 < 2; ++g2) {
+            for (int kb = 2 * g2; kb < 2 * g2 + 2; ++kb) load(&tmH, kb * 64, tile * 128);
+            for (int kb = 2 * g2; kb < 2 * g2 + 2; ++kb)
+              for (int nh = 0; nh < D / 128; ++nh) load(&tmWo, kb * 64, 128 * nh);
+          }
+        } else {
+          for (int kb = 0; kb < KB; ++kb) load(&tmH, kb * 64, tile * 128);
+        }
         load_w1(0);
         for (int j = 1; j < n_chunks; ++j) {
           load_w1(j);
@@ -308,7 +341,34 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
       };
       MLP_TILES(tile) {
         (void)tile;
-        pos = static_cast<uint32_t>(it) * slots_per_tile + KB;  // the h pieces belong to the epilogue
+        if constexpr (OPJ) {
+          // MMA_o: acc2 = o . W_o^T over the tile's first 12 ring positions
+          const uint32_t p0 = static_cast<uint32_t>(it) * slots_per_tile;
+          mbar_wait(a2_empty, (a2_cnt & 1) ^ 1);  // previous tile's final epilogue drained acc2
+          ++a2_cnt;
+          auto wait_pos = [&](uint32_t q) {
+            mbar_wait(&w_full[q % MLP_SLOTS], (q / MLP_SLOTS) & 1);
+            return smem_u32(smem + S::W_OFF + (q % MLP_SLOTS) * S::SLOT_BYTES);
+          };
+          for (int kb = 0; kb < KB; ++kb) {
+            const uint32_t qo = p0 + opj_o(kb), qw = p0 + opj_w(kb);
+            const uint32_t a = wait_pos(qo);
+            const uint32_t w = wait_pos(qw);
+            wait_pos(qw + 1);
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_ss(tmem + ACC2, make_smem_desc(a + k * 32, 16, 1024, kLayoutSW128),
+                     make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128), idesc2, (kb | k) != 0);
+            commit(&w_empty[qo % MLP_SLOTS]);
+            commit(&w_empty[qw % MLP_SLOTS]);
+            commit(&w_empty[(qw + 1) % MLP_SLOTS]);
+          }
+          commit(ao_full);
+          pos = p0 + 3 * KB;
+        } else {
+          pos = static_cast<uint32_t>(it) * slots_per_tile + KB;  // the h pieces belong to the epilogue
+        }
         mbar_wait(ht_full, it & 1);
         MLP_TR(it, 3);
         tc_fence_after();
@@ -331,6 +391,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     for (int i = et; i < D; i += 256) {
       b2_s[i] = __ldg(p.b2 + i);
       if (do_ln) { lng_s[i] = __ldg(p.ln_g + i); lnb_s[i] = __ldg(p.ln_b + i); }
+      if constexpr (OPJ) { bo_s[i] = __ldg(p.bo + i); g2_s[i] = __ldg(p.ln2_g + i); b2ln_s[i] = __ldg(p.ln2_b + i); }
     }
     asm volatile("bar.sync 5, 256;" ::: "memory");
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
@@ -340,6 +401,25 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     MLP_TILES(tile) {
       const int it = (tile - t_first) / t_step;
       const int row = tile * 128 + r_in_tile;
+      if constexpr (OPJ) {
+        // ---- x1 = x + acc_o + b_o -> x (TMA), h = LN2(x1) -> TMEM h tile (A operand of MMA1).
+        //      Staging: this warp's 4 KB slices of H[0] / H[1] (free until GELU(0)).
+        const int e = warp - 2;
+        uint8_t* hslice = smem + S::H_OFF + half * 16384 + quarter * 4096;
+        const ResidStage st{hslice, S::H_BYTES, nullptr, 0, xbar + 2 * e, &xph};
+        const ResidLnArgs la{D, p.ln_cap, p.ln_eps};
+        const uint32_t tb = tmem + lane_off + ACC2 + half * 128;
+        resid_ln_tma<4, true, true>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M, bo_s, g2_s,
+                                    b2ln_s, ln_stats, quarter, half, lane, ao_full, it & 1, a2_empty, -1,
+                                    tmem + lane_off + HT + half * 64);
+        tmem_wait_st();
+        tc_fence_before();
+        asm volatile("bar.sync 5, 256;" ::: "memory");
+        if (et == 0) {
+          MLP_TR(it, 2);
+          mbar_arrive(ht_full);
+        }
+      } else {
       // ---- h tile -> TMEM (A operand of MMA1): piece kb = k-block kb -> columns [32 kb, 32 kb + 32);
       //      this warp moves its 32 rows x 32 k (16 columns) of each piece.  The previous
       //      tile's MMA1s are complete (its acc2 epilogue below waited for them).
@@ -370,6 +450,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
           MLP_TR(it, 2);
           arrive_leader(ht_full);
         }
+      }
       }
       // ---- hidden chunks: GELU(acc1 + b1) -> bf16 -> H[j&1] (SW128 K-major, k-block = half)
       for (int j = 0; j < n_chunks; ++j) {
@@ -424,6 +505,10 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
       }
       // ---- x += acc2 + b2  (+ next LayerNorm)
       if (et == 0) MLP_TR(it, 36);
+      if constexpr (OPJ) {  // this warp's x1 TMA stores (same rows / columns) complete before reloading x
+        if (lane == 0) bulk_wait0();
+        __syncwarp();
+      }
       if (p.staged) {
         const int e = warp - 2;
         uint8_t* hslice = smem + S::H_OFF + half * 16384 + quarter * 4096;
