@@ -64,15 +64,24 @@ cfd_status cfdx_gather(cfd_ctx *ctx, int32_t n_tasks, const uint16_t *images, co
 cfd_status cfdx_probe_install(int32_t kind, void *const *h_start, void *const *h_end, int32_t capacity);
 int32_t cfdx_probe_count(int32_t kind);
 
-/* Tuning switches (process-wide): key 0 = attention kernel variant (1: one query tile
- * per CTA, 2: persistent two-tile ping-pong with 128-key steps, 3: same with 64-key
- * steps and double-buffered S, 4: three query tiles / warpgroups per CTA); key 1 = how many of every 16
- * column pairs variants 2-4 exponentiate with the FMA-pipe polynomial instead of MUFU
- * (0, 2, 4, 6, 8; 10 and 12 for variant 4 only; default 4); key 2 = fused MLP kernel on
- * (1, default) / off (0); key 3 = TMA-staged residual(+LayerNorm) epilogues of the
- * O-projection and the fused MLP on (1, default) / off (0); key 4 = fused MLP as 2-CTA
- * clusters sharing the weight stream by TMA multicast on (1) / off (0, default).  Other
- * keys / values: CFD_E_ARG. */
+/* Tuning switches (process-wide, for A/B measurement; every combination is parity-checked):
+ *   key 0  attention kernel variant: 1 one query tile per CTA, 2 persistent two-tile
+ *          ping-pong with 128-key steps, 3 same with 64-key steps, 4 three query tiles /
+ *          warpgroups per CTA (default), 5 two independent warpgroup pairs with self-issued
+ *          MMAs, 6 double-buffered S with the row max in the exp pass
+ *   key 1  how many of every 16 column pairs variants 2-6 exponentiate with the FMA-pipe
+ *          polynomial instead of MUFU (0, 2, 4, 6, 8; 10 and 12 for variant 4; default 4)
+ *   key 2  fused MLP kernel on (1, default) / off (0)
+ *   key 3  TMA-staged residual(+LayerNorm) epilogues on (1, default) / off (0)
+ *   key 4  fused MLP as CTA pairs (cta_group::2) on (1) / off (0, default)
+ *   key 5  attention v4/v5 warpgroup start stagger in cycles (0 default); -1 / -2 select the
+ *          debug library's "quarters" / "MMA warp" attention trace modes
+ *   key 6  attention v4 K/V ring depth in 128-key stages: 4 (default), 6, 8
+ *   key 7  weight-stationary QKV GEMM on (1, default) / off (0)
+ *   key 9  attention v4 exp-phase token ring on (1) / off (0, default)
+ *   key 10 attention v4 split MMA accumulator chains on (1) / off (0, default)
+ *   key 11 O-projection + residual + LN2 fused into the MLP kernel on (1, default) / off (0)
+ * Other keys / values: CFD_E_ARG. */
 cfd_status cfdx_set_option(int32_t key, int32_t value);
 
 /* Number of kernels the library launched since load (host counter; for bench's

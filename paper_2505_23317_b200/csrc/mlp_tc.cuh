@@ -350,7 +350,9 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
             mbar_wait(&w_full[q % MLP_SLOTS], (q / MLP_SLOTS) & 1);
             return smem_u32(smem + S::W_OFF + (q % MLP_SLOTS) * S::SLOT_BYTES);
           };
+          MLP_TR(it, 40);
           for (int kb = 0; kb < KB; ++kb) {
+            if (kb == 1) MLP_TR(it, 42);
             const uint32_t qo = p0 + opj_o(kb), qw = p0 + opj_w(kb);
             const uint32_t a = wait_pos(qo);
             const uint32_t w = wait_pos(qw);
@@ -365,6 +367,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
             commit(&w_empty[(qw + 1) % MLP_SLOTS]);
           }
           commit(ao_full);
+          MLP_TR(it, 41);
           pos = p0 + 3 * KB;
         } else {
           pos = static_cast<uint32_t>(it) * slots_per_tile + KB;  // the h pieces belong to the epilogue
@@ -409,9 +412,11 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         const ResidStage st{hslice, S::H_BYTES, nullptr, 0, xbar + 2 * e, &xph};
         const ResidLnArgs la{D, p.ln_cap, p.ln_eps};
         const uint32_t tb = tmem + lane_off + ACC2 + half * 128;
+        if (et == 0) MLP_TR(it, 38);
         resid_ln_tma<4, true, true>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M, bo_s, g2_s,
                                     b2ln_s, ln_stats, quarter, half, lane, ao_full, it & 1, a2_empty, -1,
                                     tmem + lane_off + HT + half * 64);
+        if (et == 0) MLP_TR(it, 39);
         tmem_wait_st();
         tc_fence_before();
         asm volatile("bar.sync 5, 256;" ::: "memory");

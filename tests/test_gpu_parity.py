@@ -271,3 +271,32 @@ def test_mlp_cta_pair_variant_matches_single_cta_bitwise():
         lib.cfdx_set_option(4, 0)
     for a, b in zip(outs[0], outs[1]):
         assert torch.equal(a, b)
+
+
+def test_fused_oproj_matches_separate_oproj_bitwise():
+    """O-projection + residual + LN2 inside the fused MLP kernel (cfdx_set_option(11, 1),
+    default) against the separate O-projection GEMM launch: the same products in the same
+    order (acc2 = o W_o^T, the same staged residual / LayerNorm pass, LN2 to TMEM instead of
+    memory), so every output agrees bit for bit on a ragged batch."""
+    from paper_2505_23317_b200 import _lib as L
+    lib = L.load()
+    cfg = ci.CONFIGS["c640"]
+    enc = enc_for("c640")
+    imgs = bf16_tensor(ci.make_frames(cfg, 4, task0=9), "cuda")
+    ks = [0, 100, 37, 400]
+    co = enc.coarse_encode(imgs)
+    sel = enc.select_regions(co["scores"], k=ks)
+    x0 = co["x0"].clone()
+    outs = []
+    try:
+        for opj in (1, 0):
+            assert lib.cfdx_set_option(11, opj) == 0
+            c2 = enc.coarse_encode(imgs, want_layers=True)
+            ro = enc.batch_refine(imgs, x0, sel["sel_idx"], sel["sel_count"], want_layers=True)
+            torch.cuda.synchronize()
+            n = int(ro["cu_seqlens"][-1])
+            outs.append((c2["layer_out"].clone(), c2["scores"].clone(), ro["layer_out"][:, :n].clone()))
+    finally:
+        lib.cfdx_set_option(11, 1)
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)

@@ -40,6 +40,11 @@ for j in range(8):
     names[28 + j] = f"epi: GELU({j}) done"
 names[36] = "epi: final epi start"
 names[37] = "epi: tile done"
+names[38] = "epi: OPJ resid start"
+names[39] = "epi: OPJ resid done"
+names[40] = "mma: MMA_o start"
+names[41] = "mma: MMA_o committed"
+names[42] = "mma: MMA_o kb1 start"
 for it in range(2):
     valid = t[:, it, 37] > 0 if it else np.ones(148, bool)
     if it and not valid.any():
