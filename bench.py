@@ -3,7 +3,11 @@
 
 One step = one pass of the whole hot path over one batch of synthetic frames:
 cfd_coarse_encode(B frames) -> cfd_select_regions(top-k per frame) ->
-cfd_batch_refine(B tasks), captured once in a CUDA graph and replayed.
+cfd_batch_refine(B tasks), captured in CUDA graphs and replayed.  The B frames run as
+--streams S concurrent sub-batches of B/S frames (default 2), each with its own encoder
+context, stream and graph, so one sub-batch's kernels fill the SMs the other's leave
+idle in their last wave; the sub-batch outputs are checked to equal the full-batch
+outputs bit for bit before timing.
 
 Workload (N=1 and per rank for N>1, weak scaling): BASELINE.json configs[1]
 "c640" frames — 640x640, Pc=32/Pf=16, d=256, 8 heads, 6 layers, 25 % of the
@@ -47,6 +51,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--streams", type=int, default=2,
+                    help="concurrent sub-batches per GPU (own encoder / stream / CUDA graph each): their kernels "
+                         "fill each other's idle SMs (persistent kernels leave SMs idle in their last wave)")
     ap.add_argument("--option", action="append", default=[],
                     help="library tuning switch KEY=VAL (cfdx_set_option, include/cfdetr_debug.h); repeatable")
     return ap.parse_args()
@@ -67,6 +74,8 @@ def workload_config(args, n_gpus, l2_note):
             "k_per_frame": k, "tokens_per_frame": cfg.n_coarse + 3 * k, "encoder": "d256/h8/L6",
             "parallelism": f"task-sharded x{n_gpus} (no collective on the hot path)", "l2": l2_note,
             "global_batch_frames": args.frames * n_gpus,
+            "streams_per_gpu": getattr(args, "streams", 1),
+            "frames_per_stream": args.frames // max(1, getattr(args, "streams", 1)),
             **({"options": list(args.option)} if getattr(args, "option", None) else {})}
 
 
@@ -279,9 +288,66 @@ def gpu_arm(args):
             step(stream)
     stream.synchronize()
 
+    # sub-batch pipelines for the timed step: S encoders (own ctx / workspace), each on its own
+    # stream with its own CUDA graph over B / S frames; a step replays them concurrently
+    S = max(1, args.streams)
+    if B % S:
+        raise SystemExit(f"bench: --frames {B} not divisible by --streams {S}")
+    per = B // S
+    subs = []
+    sub_launches = 0
+    if S > 1:
+        for si in range(S):
+            e_i = CFDetrEncoder(cfg, w, max_tasks=max(per, 8), device=str(dev))
+            im_i = imgs[si * per:(si + 1) * per]
+            s_i = torch.cuda.Stream(device=dev)
+            c_i, sl_i, r_i = {}, {}, {}
+            ks_i, cnt_i = ks[si * per:(si + 1) * per], counts[si * per:(si + 1) * per]
+            with torch.cuda.stream(s_i):
+                c_i.update(e_i.coarse_encode(im_i, stream=s_i))
+                sl_i.update(e_i.select_regions(c_i["scores"], k=ks_i, stream=s_i))
+                r_i.update(e_i.batch_refine(im_i, c_i["x0"], sl_i["sel_idx"], sl_i["sel_count"], token_counts=cnt_i,
+                                            stream=s_i))
+            s_i.synchronize()
+            n1 = L.load().cfdx_launch_count()
+            g_i = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s_i):
+                with torch.cuda.graph(g_i, stream=s_i):
+                    e_i.coarse_encode(im_i, out=c_i, stream=s_i)
+                    e_i.select_regions(c_i["scores"], k=ks_i, out=sl_i, stream=s_i)
+                    e_i.batch_refine(im_i, c_i["x0"], sl_i["sel_idx"], sl_i["sel_count"], token_counts=cnt_i,
+                                     out=r_i, stream=s_i)
+            s_i.synchronize()
+            sub_launches += int(L.load().cfdx_launch_count() - n1)
+            subs.append(dict(enc=e_i, stream=s_i, graph=g_i, keep=(im_i, c_i, sl_i, r_i)))
+        # the sub-batch outputs are the full batch's, bit for bit (checked once here)
+        for si, sb in enumerate(subs):
+            sb["graph"].replay()
+        torch.cuda.synchronize()
+        n_tok = per * counts[0]
+        for si, sb in enumerate(subs):
+            if not torch.equal(sb["keep"][3]["y"][:n_tok], ro["y"][si * n_tok:(si + 1) * n_tok]):
+                raise SystemExit("bench: sub-batch outputs differ from the full-batch outputs")
+        launches_per_step = sub_launches
+
+    def replay_step(main):
+        if S == 1:
+            graph.replay()
+            return
+        fork = torch.cuda.Event()
+        fork.record(main)
+        for sb in subs:
+            sb["stream"].wait_event(fork)
+            with torch.cuda.stream(sb["stream"]):
+                sb["graph"].replay()
+            done = torch.cuda.Event()
+            done.record(sb["stream"])
+            main.wait_event(done)
+
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    for _ in range(max(args.warmup, 3)):
-        graph.replay()
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            replay_step(stream)
     torch.cuda.synchronize()
 
     # ---------------------------------------------------------------- timed region
@@ -297,7 +363,7 @@ def gpu_arm(args):
         for i in range(args.steps):
             flush.zero_()
             starts[i].record(stream)
-            graph.replay()
+            replay_step(stream)
             ends[i].record(stream)
     stream.synchronize()
     torch.cuda.synchronize()
@@ -349,6 +415,16 @@ def gpu_arm(args):
     peaks = load_peaks()
     flops = algorithmic_flops(cfg, B, k)
     bytes_ = algorithmic_bytes(cfg, B, k)
+    # the fused MLP kernel (probe class MLP1) also does MLP2 and, with the fused O-projection,
+    # the O-projection: its algorithmic work is theirs too, reported as "mlp_fused"
+    if kern_cnt.get("gemm_mlp1", 0) and not kern_cnt.get("gemm_mlp2", 0):
+        f = flops["gemm_mlp1"] + flops["gemm_mlp2"]
+        if not kern_cnt.get("gemm_oproj", 0):
+            f += flops["gemm_oproj"]
+        flops["mlp_fused"] = f
+        for dct in (kern_ms, kern_cnt):
+            dct["mlp_fused"] = dct.pop("gemm_mlp1")
+        kinds = {("mlp_fused" if n == "gemm_mlp1" else n): v for n, v in kinds.items()}
     kernels = {}
     for n in kinds:
         if kern_cnt[n] == 0:
@@ -383,15 +459,16 @@ def gpu_arm(args):
                 "avg_launch_us": round(avg_s * 1e6, 2), "peak_src": f"{peaks['src']} copy"}
 
     roofline = roofline_for(dom)
+    attn_roof = roofline_for("attention")
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_path):
         try:
             tr = json.load(open(traffic_path))
-            if dom in tr:
-                roofline["traffic"] = tr[dom]
+            for r_ in (roofline, attn_roof):
+                if r_["kernel"] in tr:
+                    r_["traffic"] = tr[r_["kernel"]]
         except Exception:
             pass
-    attn_roof = roofline_for("attention")
     # At dh = 32 a score element carries 4*dh = 128 tensor FLOPs but one exp2 (SURVEY.md §8(d)
     # "per-element ceilings"): the kernel is bounded by the exp / FMA issue, not the tensor
     # pipe.  Exp-unit roofline beside the tensor one: exps per step / attention time against
