@@ -75,7 +75,7 @@ def workload_config(args, n_gpus, l2_note):
             "parallelism": f"task-sharded x{n_gpus} (no collective on the hot path)", "l2": l2_note,
             "global_batch_frames": args.frames * n_gpus,
             "streams_per_gpu": getattr(args, "streams", 1),
-            "frames_per_stream": args.frames // max(1, getattr(args, "streams", 1)),
+            "frames_per_stream": round(args.frames / max(1, getattr(args, "streams", 1)), 2),
             **({"options": list(args.option)} if getattr(args, "option", None) else {})}
 
 
@@ -290,19 +290,18 @@ def gpu_arm(args):
 
     # sub-batch pipelines for the timed step: S encoders (own ctx / workspace), each on its own
     # stream with its own CUDA graph over B / S frames; a step replays them concurrently
-    S = max(1, args.streams)
-    if B % S:
-        raise SystemExit(f"bench: --frames {B} not divisible by --streams {S}")
-    per = B // S
+    S = max(1, min(args.streams, B))
+    bounds = [round(B * si / S) for si in range(S + 1)]  # sub-batch si = frames [bounds[si], bounds[si+1])
     subs = []
     sub_launches = 0
     if S > 1:
         for si in range(S):
-            e_i = CFDetrEncoder(cfg, w, max_tasks=max(per, 8), device=str(dev))
-            im_i = imgs[si * per:(si + 1) * per]
+            f0, f1 = bounds[si], bounds[si + 1]
+            e_i = CFDetrEncoder(cfg, w, max_tasks=max(f1 - f0, 8), device=str(dev))
+            im_i = imgs[f0:f1]
             s_i = torch.cuda.Stream(device=dev)
             c_i, sl_i, r_i = {}, {}, {}
-            ks_i, cnt_i = ks[si * per:(si + 1) * per], counts[si * per:(si + 1) * per]
+            ks_i, cnt_i = ks[f0:f1], counts[f0:f1]
             with torch.cuda.stream(s_i):
                 c_i.update(e_i.coarse_encode(im_i, stream=s_i))
                 sl_i.update(e_i.select_regions(c_i["scores"], k=ks_i, stream=s_i))
@@ -324,9 +323,9 @@ def gpu_arm(args):
         for si, sb in enumerate(subs):
             sb["graph"].replay()
         torch.cuda.synchronize()
-        n_tok = per * counts[0]
         for si, sb in enumerate(subs):
-            if not torch.equal(sb["keep"][3]["y"][:n_tok], ro["y"][si * n_tok:(si + 1) * n_tok]):
+            t0, t1 = sum(counts[:bounds[si]]), sum(counts[:bounds[si + 1]])
+            if not torch.equal(sb["keep"][3]["y"][:t1 - t0], ro["y"][t0:t1]):
                 raise SystemExit("bench: sub-batch outputs differ from the full-batch outputs")
         launches_per_step = sub_launches
 
