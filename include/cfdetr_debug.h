@@ -81,6 +81,8 @@ int32_t cfdx_probe_count(int32_t kind);
  *   key 9  attention v4 exp-phase token ring on (1) / off (0, default)
  *   key 10 attention v4 split MMA accumulator chains on (1) / off (0, default)
  *   key 11 O-projection + residual + LN2 fused into the MLP kernel on (1, default) / off (0)
+ *   key 12 attention v4 q-triple-major item order for equal-length (coarse) batches on (1,
+ *          default) / off (0)
  * Other keys / values: CFD_E_ARG. */
 cfd_status cfdx_set_option(int32_t key, int32_t value);
 

@@ -23,6 +23,23 @@
 
 namespace cfd {
 
+// item -> (task, query triple, head).  Ragged batches: task-major (decode_item).  Equal
+// lengths (the coarse pass): q-triple-major, so that with the static round-robin item
+// assignment the costly full triples (384 rows) and the short tail triples (N = 400: 16
+// rows) spread over the CTAs instead of pairing up (max per-CTA load 2 full + 2 tail -> 1 + 1).
+__device__ __forceinline__ void decode_item4(const AttnParams& p, const int* prefix, int T, int nh, int item, int& t,
+                                             int& qp, int& h) {
+  if (p.uniform_n > 0) {
+    const int per = T * nh;
+    qp = item / per;
+    const int r = item - qp * per;
+    t = r / nh;
+    h = r - t * nh;
+  } else {
+    decode_item(prefix, T, nh, item, t, qp, h);
+  }
+}
+
 template <int DH, int STAGES>
 struct Attn4Smem {
   static constexpr int TILE_BYTES = 128 * DH * 2;
@@ -141,7 +158,7 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
       int it = 0, kvc = 0;
       for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
         int t, qp, h;
-        decode_item(prefix, T, nh, item, t, qp, h);
+        decode_item4(p, prefix, T, nh, item, t, qp, h);
         const int seq0 = __ldg(p.cu_seqlens + t);
         const int N = __ldg(p.cu_seqlens + t + 1) - seq0;
         const int nq = min(ATTN4_NWG, (N - 3 * qp * 128 + 127) / 128);
@@ -175,7 +192,7 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
       uint32_t s_use = 0;   // QKs issued into S_w
       for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
         int t, qp, h;
-        decode_item(prefix, T, nh, item, t, qp, h);
+        decode_item4(p, prefix, T, nh, item, t, qp, h);
         const int seq0 = __ldg(p.cu_seqlens + t);
         const int N = __ldg(p.cu_seqlens + t + 1) - seq0;
         const int nkv = (N + 127) / 128;
@@ -307,7 +324,7 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
     for (int item = blockIdx.x; item < total; item += gridDim.x) {
       ++it;
       int t, qp, h;
-      decode_item(prefix, T, nh, item, t, qp, h);
+      decode_item4(p, prefix, T, nh, item, t, qp, h);
       const int seq0 = __ldg(p.cu_seqlens + t);
       const int N = __ldg(p.cu_seqlens + t + 1) - seq0;
       const int qt = 3 * qp + wg;

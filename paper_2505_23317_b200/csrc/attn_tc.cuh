@@ -33,6 +33,8 @@ struct AttnParams {
   int lse_ld;
   float scale_log2;        // log2(e) / sqrt(dh)
   int stagger = 0;         // v4: softmax warpgroup w starts w * stagger cycles late (0 = off)
+  int uniform_n = 0;       // > 0: every task has this many tokens (coarse pass) -> v4 walks its
+                           // items q-triple-major (all first triples, then all second ones, ...)
 };
 
 constexpr int ATTN_THREADS = 192;

@@ -240,6 +240,7 @@ int g_attn_stagger = 0;
 int g_attn_stages = 4;  // v4 K/V ring depth (128-key stages): 4, 6 or 8
 int g_attn_token = 0;   // v4 exp-phase token ring (option 9)
 int g_attn_split = 0;   // v4 split MMA accumulator chains (option 10)
+int g_attn_qmajor = 1;  // v4 q-triple-major item order for equal-length batches (option 12)
 int g_fused_mlp = 1;  // fused MLP kernel (d == 256) instead of two GEMM launches
 int g_staged_epi = 1; // TMA-staged residual + LayerNorm epilogue for the O-projection
 int g_mlp_cluster = 0; // fused MLP as CTA pairs (cta_group::2)
@@ -507,7 +508,7 @@ Workspace carve(const cfd_ctx* c, int n, void* base) {
 // O-projection epilogue the same way.
 cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const int* m_dev, int rows_grid,
                      const int32_t* cu, int T, int max_qtiles, Workspace& w, bool want_lse, float* scores,
-                     int score_B, cudaStream_t s) {
+                     int score_B, cudaStream_t s, int uniform_n = 0) {
   const cfd_config& g = c->cfg;
   const int d = g.d_model, F = g.d_ff;
   const bool fuse_ln = pick_bn(d) == d;  // one GEMM tile spans a whole row
@@ -528,6 +529,7 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   ap.cu_seqlens = cu; ap.d_model = d; ap.out = w.obuf; ap.lse = want_lse ? w.lse : nullptr; ap.lse_ld = w.lse_ld;
   ap.scale_log2 = 1.4426950408889634f / std::sqrt((float)c->dh);
   ap.stagger = g_attn_stagger;
+  ap.uniform_n = g_attn_qmajor ? uniform_n : 0;
   CFD_CUDA(launch_attention(tq, ap, max_qtiles, g.n_heads, T, s));
   if (want_lse && scores) {
     ScoreParams sp{};
@@ -708,6 +710,9 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
     case 11:
       g_fuse_oproj = value ? 1 : 0;
       return CFD_OK;
+    case 12:
+      g_attn_qmajor = value ? 1 : 0;
+      return CFD_OK;
     case 6:
       if (value != 4 && value != 6 && value != 8) return CFD_E_ARG;
       g_attn_stages = value;
@@ -874,7 +879,7 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
   const int max_qtiles = (c->Nc + ATTN_BQ - 1) / ATTN_BQ;
   for (int l = 0; l < g.n_layers; ++l) {
     const bool sl = (l == g.score_layer);
-    cfd_status st = run_layer(c, l, y, M, M, nullptr, M, w.ccu, B, max_qtiles, w, sl && scores, scores, B, s);
+    cfd_status st = run_layer(c, l, y, M, M, nullptr, M, w.ccu, B, max_qtiles, w, sl && scores, scores, B, s, c->Nc);
     if (st != CFD_OK) return st;
     if (layer_out)
       CFD_CUDA(cudaMemcpyAsync(layer_out + (size_t)l * M * d, y, (size_t)M * d * 4, cudaMemcpyDeviceToDevice, s));
