@@ -83,6 +83,8 @@ int32_t cfdx_probe_count(int32_t kind);
  *   key 11 O-projection + residual + LN2 fused into the MLP kernel on (1, default) / off (0)
  *   key 12 attention v4 q-triple-major item order for equal-length (coarse) batches on (1,
  *          default) / off (0)
+ *   key 13 patch-embed GEMMs with one CTA per SM and a 4-stage ring (1, default) instead of
+ *          two CTAs per SM with 2 stages (0)
  * Other keys / values: CFD_E_ARG. */
 cfd_status cfdx_set_option(int32_t key, int32_t value);
 

@@ -125,6 +125,7 @@ cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
 
 // ------------------------------------------------------------------ GEMM dispatch
 int g_gemm_bres = 1;  // weight-stationary QKV GEMM (option 7)
+int g_embed_mode0 = 1;  // patch-embed GEMMs: 1 CTA/SM, 4-stage ring (option 13)
 template <int BN>
 constexpr int gemm_stages() { return BN == 256 ? 4 : BN == 128 ? 6 : 8; }
 template <int BN>  // with the 32 KB bf16 output staging area
@@ -175,7 +176,10 @@ cudaError_t launch_gemm_bn(int BN, const CUtensorMap& ta, const CUtensorMap& tb,
                            cudaStream_t s, const CUtensorMap* tx, const CUtensorMap* tln) {
   // N = BN: a single column tile per row block -> the 2-CTA/SM configuration, except the
   // residual+LN epilogue with staging maps, which runs 1 CTA/SM with TMA-staged I/O
-  if (p.N == BN && !(EPI == EPI_F32_RESID_LN && tx && tln)) {
+  // the patch embeds (K = 3Pc^2 / 3Pf^2, long k loops over ~100 tiles) keep one CTA per SM with a
+  // 4-stage ring when g_embed_mode0 (option 13): the k loop is latency-bound with 2 stages
+  const bool embed = (EPI == EPI_EMBED_COARSE || EPI == EPI_EMBED_FINE) && g_embed_mode0;
+  if (p.N == BN && !(EPI == EPI_F32_RESID_LN && tx && tln) && !embed) {
     switch (BN) {
       case 256: return launch_gemm_t<256, EPI, 1>(ta, tb, p, rows, s, tx, tln);
       case 128: return launch_gemm_t<128, EPI, 1>(ta, tb, p, rows, s, tx, tln);
@@ -712,6 +716,9 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
       return CFD_OK;
     case 12:
       g_attn_qmajor = value ? 1 : 0;
+      return CFD_OK;
+    case 13:
+      g_embed_mode0 = value ? 1 : 0;
       return CFD_OK;
     case 6:
       if (value != 4 && value != 6 && value != 8) return CFD_E_ARG;
