@@ -126,6 +126,7 @@ cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
 // ------------------------------------------------------------------ GEMM dispatch
 int g_gemm_bres = 1;  // weight-stationary QKV GEMM (option 7)
 int g_embed_mode0 = 1;  // patch-embed GEMMs: 1 CTA/SM, 4-stage ring (option 13)
+int g_embed_img = 1;    // coarse patch embed gathers A from the image by TMA, no im2col (option 14)
 template <int BN>
 constexpr int gemm_stages() { return BN == 256 ? 4 : BN == 128 ? 6 : 8; }
 template <int BN>  // with the 32 KB bf16 output staging area
@@ -137,17 +138,20 @@ constexpr int gemm_stages_stg() { return BN == 256 ? 3 : BN == 128 ? 5 : 7; }
 // mode 2 (BRES): mode 0 with the CTA's [BN, 256] weight slice resident in shared memory
 //         (bf16 outputs, K = 256): each CTA keeps one column block and walks row blocks, so
 //         the per-SM operand stream is A only (64 KB per 128x256 tile instead of 192 KB)
+// mode 3 (IMG): mode 0 for the coarse patch embed with A gathered from the image by a 5-D
+//         tensor map (no im2col), 32-wide k-blocks, 8-stage ring of 8 + 16 KB
 template <int BN, int EPI, int MODE>
 cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows_for_grid,
                           cudaStream_t s, const CUtensorMap* tx, const CUtensorMap* tln) {
+  constexpr bool kImg = MODE == 3;
   constexpr bool kBres = MODE == 2;
   constexpr bool kTmaEpi = (EPI == EPI_F32_RESID_LN && MODE != 1);
   constexpr bool kStgOut = (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_GELU) && MODE != 1;
   constexpr int EW = MODE == 1 ? 4 : 8;
   constexpr int NACC = MODE == 1 ? 1 : 2;
-  constexpr int ST = kBres ? 3 : (MODE == 1 || kTmaEpi) ? 2 : kStgOut ? gemm_stages_stg<BN>() : gemm_stages<BN>();
-  auto kern = gemm_tc_kernel<BN, ST, EPI, EW, NACC, kBres>;
-  using SM = GemmSmem<BN, ST, NACC, kBres>;
+  constexpr int ST = kImg ? 8 : kBres ? 3 : (MODE == 1 || kTmaEpi) ? 2 : kStgOut ? gemm_stages_stg<BN>() : gemm_stages<BN>();
+  auto kern = gemm_tc_kernel<BN, ST, EPI, EW, NACC, kBres, kImg>;
+  using SM = GemmSmem<BN, ST, NACC, kBres, kImg ? 32 : GEMM_BK>;
   constexpr int smem = kTmaEpi ? SM::TOTAL_TMA_EPI : kStgOut ? SM::TOTAL_STG_OUT : SM::TOTAL;
   static_assert(smem <= 232448, "shared memory budget");
   CUtensorMap tout;
@@ -162,7 +166,8 @@ cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int tiles = ((rows_for_grid + GEMM_BM - 1) / GEMM_BM) * (p.N / BN);
+  const int rpt = kImg ? p.img_rb * p.img_gw : GEMM_BM;
+  const int tiles = ((rows_for_grid + rpt - 1) / rpt) * (p.N / BN);
   const int slots = num_sms() * (MODE == 1 ? 2 : 1);
   int grid = tiles < slots ? (tiles > 0 ? tiles : 1) : slots;
   if constexpr (kBres) grid = std::max(1, grid / (p.N / BN)) * (p.N / BN);  // whole column-block groups
@@ -226,6 +231,24 @@ cudaError_t launch_gemm(int epi, const CUtensorMap& ta, const CUtensorMap& tb, c
 }
 
 // B tensor map for a K-major weight [N, K]
+// 5-D map over HWC bf16 frames [B][H][W][3] for the image-sourced coarse embed:
+//   d0 = 32 elements of a pixel segment, d1 = segment third j (3Pc/32), d2 = patch column cx,
+//   d3 = pixel row in the patch py, d4 = coarse row R = b * gh + cy;  box {32, 1, gw, 1, rb}
+//   -> rb * gw rows of 64 B, row (R, cx) = A[patch][(py*Pc + px)*3 + ch] for the 32 k of (py, j)
+bool make_img_map(CUtensorMap* m, const void* img, int B, int H, int W, int Pc, int rb) {
+  PFN_encodeTiled enc = get_encode_fn();
+  if (!enc) return false;
+  const int gw = W / Pc, gh = H / Pc, thirds = 3 * Pc / 32;
+  cuuint64_t dims[5] = {32, (cuuint64_t)thirds, (cuuint64_t)gw, (cuuint64_t)Pc, (cuuint64_t)B * gh};
+  cuuint64_t strides[4] = {64, (cuuint64_t)3 * Pc * 2, (cuuint64_t)W * 3 * 2, (cuuint64_t)Pc * W * 3 * 2};
+  cuuint32_t box[5] = {32, 1, (cuuint32_t)gw, 1, (cuuint32_t)rb};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(img), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool make_wmap(CUtensorMap* m, const void* w, int N, int K) {
   return make_tmap(m, w, K, N, K, GEMM_BK, pick_bn(N), CU_TENSOR_MAP_SWIZZLE_128B);
 }
@@ -458,6 +481,8 @@ struct cfd_ctx {
   int* err = nullptr;
   std::vector<LayerDev> layers;
   CUtensorMap tm_wc, tm_wf;
+  CUtensorMap tm_wc32;  // W_c with 32-k x 256-row SW64 boxes (image-sourced coarse embed)
+  bool has_wc32 = false;
 };
 
 namespace {
@@ -720,6 +745,9 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
     case 13:
       g_embed_mode0 = value ? 1 : 0;
       return CFD_OK;
+    case 14:
+      g_embed_img = value ? 1 : 0;
+      return CFD_OK;
     case 6:
       if (value != 4 && value != 6 && value != 8) return CFD_E_ARG;
       g_attn_stages = value;
@@ -791,6 +819,7 @@ cfd_status cfd_create(const cfd_config* cfg, const cfd_weights* wts, void* strea
       cudaMemsetAsync(c->err, 0, 16, s) != cudaSuccess)
     return fail(CFD_E_CUDA);
   if (!make_wmap(&c->tm_wc, c->wc, d, c->Kc) || !make_wmap(&c->tm_wf, c->wf, d, c->Kf)) return fail(CFD_E_CUDA);
+  c->has_wc32 = d == 256 && make_tmap(&c->tm_wc32, c->wc, c->Kc, d, c->Kc, 32, 256, CU_TENSOR_MAP_SWIZZLE_64B);
   c->layers.resize(L);
   for (int l = 0; l < L; ++l) {
     const cfd_layer_weights& hw = wts->h_layers[l];
@@ -868,21 +897,38 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
   probe_end(PK_META, s);
   ++g_launches;
   CFD_CUDA(cudaGetLastError());
-  {
-    const long long vec = (long long)B * g.img_h * (g.img_w / g.patch_coarse) * ((g.patch_coarse * 6) / 16);
-    const int blocks = (int)std::min<long long>((vec + 255) / 256, (long long)num_sms() * 8);
-    probe_begin(PK_IM2COL, s);
-    launch_ex(im2col_kernel, dim3(blocks), dim3(256), 0, s, images, w.patches, B, g.img_h, g.img_w, g.patch_coarse);
-    probe_end(PK_IM2COL, s);
-    ++g_launches;
-    CFD_CUDA(cudaGetLastError());
-  }
-  CUtensorMap ta;
-  if (!make_amap(&ta, w.patches, M, c->Kc)) return CFD_E_CUDA;
   GemmParams p{};
   p.M = M; p.m_cap = M; p.N = d; p.K = c->Kc; p.bias = c->bc; p.out_f32 = y; p.out2_f32 = x0; p.ld_out = d;
   p.pe = c->pec; p.pe_rows = c->Nc;
-  CFD_CUDA(launch_gemm(EPI_EMBED_COARSE, ta, c->tm_wc, p, M, s, PK_EMBED_C));
+  const int Pc = g.patch_coarse, gw = g.img_w / Pc, gh = g.img_h / Pc;
+  // image-sourced embed: 3Pc-element segments split into 32-element k-blocks, whole coarse
+  // rows per 128-row tile, box dims <= 256
+  const bool img_ok = g_embed_img && d == 256 && (3 * Pc) % 32 == 0 && gw <= 128 && (128 / gw) <= 256 && c->has_wc32;
+  if (img_ok) {
+    CUtensorMap ti;
+    p.img_gw = gw;
+    p.img_rb = 128 / gw;
+    p.img_thirds = 3 * Pc / 32;
+    if (!make_img_map(&ti, images, B, g.img_h, g.img_w, Pc, p.img_rb)) return CFD_E_CUDA;
+    probe_begin(PK_EMBED_C, s);
+    cudaError_t e = launch_gemm_t<256, EPI_EMBED_COARSE, 3>(ti, c->tm_wc32, p, M, s, nullptr, nullptr);
+    probe_end(PK_EMBED_C, s);
+    CFD_CUDA(e);
+  } else {
+    {
+      const long long vec = (long long)B * g.img_h * (g.img_w / g.patch_coarse) * ((g.patch_coarse * 6) / 16);
+      const int blocks = (int)std::min<long long>((vec + 255) / 256, (long long)num_sms() * 8);
+      probe_begin(PK_IM2COL, s);
+      launch_ex(im2col_kernel, dim3(blocks), dim3(256), 0, s, images, w.patches, B, g.img_h, g.img_w, g.patch_coarse);
+      probe_end(PK_IM2COL, s);
+      ++g_launches;
+      CFD_CUDA(cudaGetLastError());
+    }
+    CUtensorMap ta;
+    if (!make_amap(&ta, w.patches, M, c->Kc)) return CFD_E_CUDA;
+    CFD_CUDA(launch_gemm(EPI_EMBED_COARSE, ta, c->tm_wc, p, M, s, PK_EMBED_C));
+  }
+  (void)gh;
   const int max_qtiles = (c->Nc + ATTN_BQ - 1) / ATTN_BQ;
   for (int l = 0; l < g.n_layers; ++l) {
     const bool sl = (l == g.score_layer);

@@ -62,6 +62,10 @@ struct GemmParams {
   __nv_bfloat16* ln_out;     // [ln_cap, N]
   int ln_cap;                // rows of ln_out (pad rows [M, pad_rows) are zeroed)
   float ln_eps;
+  // IMG (coarse patch embed straight from the image): a tile = img_rb coarse rows x img_gw
+  // patches (rows_per_tile = img_rb * img_gw <= 128), k-block kb = (patch row py = kb / img_thirds,
+  // third j = kb % img_thirds of its 3*Pc-element pixel segment), 32 k per block
+  int img_rb, img_gw, img_thirds;
 };
 
 constexpr int GEMM_BM = 128;
@@ -81,10 +85,10 @@ constexpr int GEMM_MAX_LN = 512;   // LayerNorm width for EPI_F32_RESID_LN
 // four 64-wide k-blocks) is loaded into shared memory once and stays there while the CTA
 // streams its row tiles through an A-only ring.  The default streams A and B per k-block.
 constexpr int GEMM_BRES_KB = 4;
-template <int BN, int STAGES, int NACC = 2, bool BRES = false>
+template <int BN, int STAGES, int NACC = 2, bool BRES = false, int BKX = GEMM_BK>
 struct GemmSmem {
-  static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
-  static constexpr int B_BYTES = BN * GEMM_BK * 2;
+  static constexpr int A_BYTES = GEMM_BM * BKX * 2;
+  static constexpr int B_BYTES = BN * BKX * 2;
   static constexpr int STAGE_BYTES = A_BYTES + (BRES ? 0 : B_BYTES);  // TMA bytes per ring stage
   static constexpr int NB = BRES ? GEMM_BRES_KB : STAGES;            // B buffers
   static constexpr int BAR_OFF = STAGES * A_BYTES + NB * B_BYTES;
@@ -445,13 +449,18 @@ __device__ __forceinline__ void store_bf16_tma(const CUtensorMap& tmO, uint8_t* 
   }
 }
 
-template <int BN, int STAGES, int EPI, int EW, int NACC, bool BRES = false>
+// IMG: A tiles are TMA-gathered from the HWC image through a 5-D tensor map (reading R2:
+// patch vector (py, px, ch) = one Pc*3-element pixel segment per patch row), so no im2col
+// buffer is written or read; 32-wide k-blocks in 64-byte (SW64) rows.
+template <int BN, int STAGES, int EPI, int EW, int NACC, bool BRES = false, bool IMG = false>
 __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmParams p, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ CUtensorMap tmLN) {
   static_assert((EW == 8 && NACC == 2) || (EW == 4 && NACC == 1), "supported epilogue configurations");
-  using S = GemmSmem<BN, STAGES, NACC, BRES>;
+  static_assert(!IMG || (EPI == EPI_EMBED_COARSE && !BRES), "IMG is the coarse patch embed");
+  constexpr int BKX = IMG ? 32 : GEMM_BK;
+  using S = GemmSmem<BN, STAGES, NACC, BRES, BKX>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
   uint8_t* sA = smem;
@@ -476,7 +485,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
   // bf16 outputs of the one-CTA/SM configuration leave through smem + TMA store (tmX = out map)
   constexpr bool kStgOut = kPad && EW == 8;
   const int n_tiles = p.N / BN;
-  const int num_k = p.K / GEMM_BK;
+  const int num_k = p.K / BKX;
+  const int rpt = IMG ? p.img_rb * p.img_gw : GEMM_BM;  // rows per tile
   const int n_fix = BRES ? (int)blockIdx.x % n_tiles : 0;
 
   if (warp == 0 && lane == 0) {
@@ -503,7 +513,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
   const int M = p.m_dev ? __ldg(p.m_dev) : p.M;
   const int m_store = kPad ? pad_rows(M, p.m_cap) : M;
   // RESID_LN also visits the tiles of the pad rows (zeroed in ln_out, x untouched)
-  const int m_tiles = ((EPI == EPI_F32_RESID_LN ? pad_rows(M, p.ln_cap) : m_store) + GEMM_BM - 1) / GEMM_BM;
+  const int m_tiles = ((EPI == EPI_F32_RESID_LN ? pad_rows(M, p.ln_cap) : m_store) + rpt - 1) / rpt;
   const int total = m_tiles * n_tiles;
   // tile walk: default tile = m_blk * n_tiles + n_blk over all tiles; BRES: the CTA keeps
   // column block blockIdx % n_tiles and walks row blocks (gridDim is a multiple of n_tiles)
@@ -519,9 +529,15 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
         const int m_blk = BRES ? tile : tile / n_tiles, n_blk = BRES ? n_fix : tile % n_tiles;
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], S::STAGE_BYTES);
-          tma_load_2d(sA + stage * S::A_BYTES, &tmA, &full[stage], kb * GEMM_BK, m_blk * GEMM_BM);
-          if constexpr (!BRES) tma_load_2d(sB + stage * S::B_BYTES, &tmB, &full[stage], kb * GEMM_BK, n_blk * BN);
+          if constexpr (IMG) {  // rpt rows of 64 B (OOB rows of the last tile are zero-filled)
+            mbar_expect_tx(&full[stage], rpt * 64 + S::B_BYTES);
+            tma_load_5d(sA + stage * S::A_BYTES, &tmA, &full[stage], 0, kb % p.img_thirds, 0, kb / p.img_thirds,
+                        m_blk * p.img_rb);
+          } else {
+            mbar_expect_tx(&full[stage], S::STAGE_BYTES);
+            tma_load_2d(sA + stage * S::A_BYTES, &tmA, &full[stage], kb * BKX, m_blk * GEMM_BM);
+          }
+          if constexpr (!BRES) tma_load_2d(sB + stage * S::B_BYTES, &tmB, &full[stage], kb * BKX, n_blk * BN);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -544,9 +560,11 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
           const uint32_t a0 = smem_u32(sA + stage * S::A_BYTES);
           const uint32_t b0 = smem_u32(sB + (BRES ? kb : stage) * S::B_BYTES);
 #pragma unroll
-          for (int k = 0; k < GEMM_BK / 16; ++k) {
-            const uint64_t ad = make_smem_desc(a0 + k * 32, 16, 1024, kLayoutSW128);
-            const uint64_t bd = make_smem_desc(b0 + k * 32, 16, 1024, kLayoutSW128);
+          for (int k = 0; k < BKX / 16; ++k) {
+            const uint64_t ad = IMG ? make_smem_desc(a0 + k * 32, 16, 512, kLayoutSW64)
+                                    : make_smem_desc(a0 + k * 32, 16, 1024, kLayoutSW128);
+            const uint64_t bd = IMG ? make_smem_desc(b0 + k * 32, 16, 512, kLayoutSW64)
+                                    : make_smem_desc(b0 + k * 32, 16, 1024, kLayoutSW128);
             mma_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
           mma_commit(&empty[stage]);
@@ -571,7 +589,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
     uint32_t xph = 0;  // bit b: phase of this warp's staging barrier b
     for (int tile = t_first; tile < t_end; tile += t_step) {
       const int m_blk = BRES ? tile : tile / n_tiles, n_blk = BRES ? n_fix : tile % n_tiles;
-      const int row0 = m_blk * GEMM_BM + quarter * 32;
+      // IMG: tile-local rows >= rpt are the MMA's padding rows (never stored): pushed past m_store
+      const int row0 = (IMG && quarter * 32 + lane >= rpt) ? (1 << 30) - lane : m_blk * rpt + quarter * 32;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + half * WCOLS;
       const int col_base = n_blk * BN + half * WCOLS;
       float s1 = 0.f, s2 = 0.f;  // RESID_LN row statistics (lane = row)
