@@ -87,6 +87,8 @@ int32_t cfdx_probe_count(int32_t kind);
  *          two CTAs per SM with 2 stages (0)
  *   key 14 coarse patch embed gathering its A tiles straight from the image with a 5-D TMA
  *          tensor map (1, default; d = 256, 3Pc % 32 == 0) instead of im2col + GEMM (0)
+ *   key 15 layer-0 LN1 of the coarse pass fused into the coarse embed epilogue (1, default)
+ *          instead of a standalone LayerNorm launch (0)
  * Other keys / values: CFD_E_ARG. */
 cfd_status cfdx_set_option(int32_t key, int32_t value);
 

@@ -127,6 +127,7 @@ cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
 int g_gemm_bres = 1;  // weight-stationary QKV GEMM (option 7)
 int g_embed_mode0 = 1;  // patch-embed GEMMs: 1 CTA/SM, 4-stage ring (option 13)
 int g_embed_img = 1;    // coarse patch embed gathers A from the image by TMA, no im2col (option 14)
+int g_embed_ln = 1;     // layer-0 LN1 fused into the coarse embed epilogue (option 15)
 template <int BN>
 constexpr int gemm_stages() { return BN == 256 ? 4 : BN == 128 ? 6 : 8; }
 template <int BN>  // with the 32 KB bf16 output staging area
@@ -537,7 +538,7 @@ Workspace carve(const cfd_ctx* c, int n, void* base) {
 // O-projection epilogue the same way.
 cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const int* m_dev, int rows_grid,
                      const int32_t* cu, int T, int max_qtiles, Workspace& w, bool want_lse, float* scores,
-                     int score_B, cudaStream_t s, int uniform_n = 0) {
+                     int score_B, cudaStream_t s, int uniform_n = 0, bool ln1_ready = false) {
   const cfd_config& g = c->cfg;
   const int d = g.d_model, F = g.d_ff;
   const bool fuse_ln = pick_bn(d) == d;  // one GEMM tile spans a whole row
@@ -546,7 +547,7 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   if (!make_amap(&ta_h, w.hbuf, w.rows_cap, d) || !make_amap(&ta_o, w.obuf, w.rows_cap, d) ||
       !make_amap(&ta_f, w.ff, w.rows_cap, F) || !make_qkvmap(&tq, w.qkv, w.rows_cap, d))
     return CFD_E_CUDA;
-  if (l == 0 || !fuse_ln)  // LN1
+  if ((l == 0 && !ln1_ready) || !fuse_ln)  // LN1
     CFD_CUDA(launch_layernorm(d, x, L.ln1_g, L.ln1_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
   // QKV
   GemmParams p{};
@@ -748,6 +749,9 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
     case 14:
       g_embed_img = value ? 1 : 0;
       return CFD_OK;
+    case 15:
+      g_embed_ln = value ? 1 : 0;
+      return CFD_OK;
     case 6:
       if (value != 4 && value != 6 && value != 8) return CFD_E_ARG;
       g_attn_stages = value;
@@ -900,6 +904,15 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
   GemmParams p{};
   p.M = M; p.m_cap = M; p.N = d; p.K = c->Kc; p.bias = c->bc; p.out_f32 = y; p.out2_f32 = x0; p.ld_out = d;
   p.pe = c->pec; p.pe_rows = c->Nc;
+  // layer-0 LN1 fused into the embed epilogue (option 15): hbuf rows [0, M) here, the pad
+  // rows [M, pad_rows) that attention tail tiles may read zeroed by a memset
+  const bool ln0 = g_embed_ln && d == pick_bn(d);
+  if (ln0) {
+    const LayerDev& L0 = c->layers[0];
+    p.ln_g = L0.ln1_g; p.ln_b = L0.ln1_b; p.ln_out = w.hbuf; p.ln_cap = w.rows_cap; p.ln_eps = g.ln_eps;
+    const int pr = pad_rows(M, w.rows_cap);
+    if (pr > M) CFD_CUDA(cudaMemsetAsync(w.hbuf + (size_t)M * d, 0, (size_t)(pr - M) * d * 2, s));
+  }
   const int Pc = g.patch_coarse, gw = g.img_w / Pc, gh = g.img_h / Pc;
   // image-sourced embed: 3Pc-element segments split into 32-element k-blocks, whole coarse
   // rows per 128-row tile, box dims <= 256
@@ -932,7 +945,8 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
   const int max_qtiles = (c->Nc + ATTN_BQ - 1) / ATTN_BQ;
   for (int l = 0; l < g.n_layers; ++l) {
     const bool sl = (l == g.score_layer);
-    cfd_status st = run_layer(c, l, y, M, M, nullptr, M, w.ccu, B, max_qtiles, w, sl && scores, scores, B, s, c->Nc);
+    cfd_status st =
+        run_layer(c, l, y, M, M, nullptr, M, w.ccu, B, max_qtiles, w, sl && scores, scores, B, s, c->Nc, ln0 && l == 0);
     if (st != CFD_OK) return st;
     if (layer_out)
       CFD_CUDA(cudaMemcpyAsync(layer_out + (size_t)l * M * d, y, (size_t)M * d * 4, cudaMemcpyDeviceToDevice, s));

@@ -180,6 +180,8 @@ __device__ __forceinline__ void direct_chunk(const GemmParams& p, float (&v)[32]
       const float4 o = make_float4(v[4 * i] + e.x, v[4 * i + 1] + e.y, v[4 * i + 2] + e.z, v[4 * i + 3] + e.w);
       d1[i] = o;
       d2[i] = o;
+      s1 += (o.x + o.y) + (o.z + o.w);  // row statistics for the optional fused LN1 (p.ln_g)
+      s2 += (o.x * o.x + o.y * o.y) + (o.z * o.z + o.w * o.w);
     }
   } else if constexpr (EPI == EPI_EMBED_FINE) {
     if (row >= m_store) return;
@@ -581,7 +583,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
     constexpr int WCOLS = BN / (EW / 4);                // columns per epilogue warp
     const int et = threadIdx.x - 64;                    // index among the epilogue threads
     for (int i = et; i < p.N; i += 32 * EW) bias_s[i] = __ldg(p.bias + i);
-    if constexpr (EPI == EPI_F32_RESID_LN)
+    if (EPI == EPI_F32_RESID_LN || (EPI == EPI_EMBED_COARSE && p.ln_g))
       for (int i = et; i < p.N; i += 32 * EW) { lng_s[i] = __ldg(p.ln_g + i); lnb_s[i] = __ldg(p.ln_b + i); }
     asm volatile("bar.sync 5, %0;" ::"n"(32 * EW) : "memory");  // epilogue warps only
     int acc = 0;
@@ -684,7 +686,10 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
         }
       }
       }
-      if constexpr (EPI == EPI_F32_RESID_LN && EW != 8) {
+      // LayerNorm of the rows just written (RESID_LN direct path; coarse embed + layer-0 LN1
+      // when p.ln_g: the embedding rows are read back from L2 and normalised)
+      if (((EPI == EPI_F32_RESID_LN && EW != 8) || EPI == EPI_EMBED_COARSE) &&
+          (EPI != EPI_EMBED_COARSE || p.ln_g != nullptr)) {
         // row statistics; with EW=8 the two warps sharing these rows exchange halves
         float2 o = make_float2(0.f, 0.f);
         if constexpr (EW == 8) {
