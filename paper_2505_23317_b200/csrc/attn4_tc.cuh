@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
   uint64_t* o_full = p_full + 3;            // [3 w]
   uint64_t* exp_tok = o_full + 3;           // [3 w] TOKEN: warpgroup w finished its exps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(exp_tok + 3);
+  volatile int* item_slot = reinterpret_cast<volatile int*>(smem + S::BAR_OFF + 448);  // [2] item of a Q slot
   int* prefix = reinterpret_cast<int*>(smem + S::PRE_OFF);
 
   const int warp = warp_id(), lane = lane_id();
@@ -155,16 +156,27 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
   if (warp == kTmaWarp) {
     // ================================================================ TMA producer
     if (lane == 0) {
-      int it = 0, kvc = 0;
-      for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
+      // Items: the first is blockIdx.x; later ones are claimed from p.work_counter (dynamic:
+      // the longest-running CTAs take fewer items) or round-robin.  The item index travels
+      // to the MMA and softmax warps in item_slot[Q slot], published by the q_full arrive; an
+      // index >= total (arrive without TMA bytes) tells them to stop.
+      int kvc = 0;
+      for (int it = 0;; ++it) {
+        const int item = (it == 0 || !p.work_counter) ? (int)blockIdx.x + it * (int)gridDim.x
+                                                      : (int)gridDim.x + atomicAdd(p.work_counter, 1);
+        const int slot = it & 1;
+        mbar_wait(&q_empty[slot], ((it >> 1) & 1) ^ 1);
+        item_slot[slot] = item;
+        if (item >= total) {
+          mbar_arrive(&q_full[slot]);
+          break;
+        }
         int t, qp, h;
         decode_item4(p, prefix, T, nh, item, t, qp, h);
         const int seq0 = __ldg(p.cu_seqlens + t);
         const int N = __ldg(p.cu_seqlens + t + 1) - seq0;
         const int nq = min(ATTN4_NWG, (N - 3 * qp * 128 + 127) / 128);
         const int nkv = (N + 127) / 128;
-        const int slot = it & 1;
-        mbar_wait(&q_empty[slot], ((it >> 1) & 1) ^ 1);
         mbar_expect_tx(&q_full[slot], nq * S::TILE_BYTES);
         for (int w = 0; w < nq; ++w)
           tma_load_2d(smem + S::Q_OFF + (slot * 3 + w) * S::TILE_BYTES, &tmQKV, &q_full[slot], h * DH,
@@ -187,17 +199,19 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
       const int w = warp - kMmaWarp0;
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, 0);  // S_u = Q K_u^T (64 keys)
       constexpr uint32_t idesc_o = make_idesc_bf16(128, DH, 1);  // O += P_u V_u (V MN-major)
-      int it = 0, kvc = 0;
+      int kvc = 0;
       uint32_t p_cnt = 0;
       uint32_t s_use = 0;   // QKs issued into S_w
-      for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
+      for (int it = 0;; ++it) {
+        const int slot = it & 1;
+        mbar_wait(&q_full[slot], (it >> 1) & 1);
+        const int item = item_slot[slot];
+        if (item >= total) break;
         int t, qp, h;
         decode_item4(p, prefix, T, nh, item, t, qp, h);
         const int seq0 = __ldg(p.cu_seqlens + t);
         const int N = __ldg(p.cu_seqlens + t + 1) - seq0;
         const int nkv = (N + 127) / 128;
-        const int slot = it & 1;
-        mbar_wait(&q_full[slot], (it >> 1) & 1);
         if ((3 * qp + w) * 128 >= N) {
           // no query tile for this warpgroup: release the item's stages in step
           for (int j = 0; j < nkv; ++j) {
@@ -321,8 +335,13 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
       while (clock64() < t_end) __nanosleep(64);
     }
     int it = -1;
-    for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    for (;;) {
       ++it;
+      // the item of this Q slot (q_full publishes it; the Q tiles themselves are read by the
+      // MMA warps only)
+      mbar_wait(&q_full[it & 1], (it >> 1) & 1);
+      const int item = item_slot[it & 1];
+      if (item >= total) break;
       int t, qp, h;
       decode_item4(p, prefix, T, nh, item, t, qp, h);
       const int seq0 = __ldg(p.cu_seqlens + t);

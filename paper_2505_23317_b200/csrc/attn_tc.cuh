@@ -35,6 +35,8 @@ struct AttnParams {
   int stagger = 0;         // v4: softmax warpgroup w starts w * stagger cycles late (0 = off)
   int uniform_n = 0;       // > 0: every task has this many tokens (coarse pass) -> v4 walks its
                            // items q-triple-major (all first triples, then all second ones, ...)
+  int* work_counter = nullptr;  // v4: zeroed int; non-null -> items after the first are claimed
+                                // dynamically (atomicAdd) instead of the static round-robin
 };
 
 constexpr int ATTN_THREADS = 192;

@@ -269,6 +269,7 @@ int g_attn_stages = 4;  // v4 K/V ring depth (128-key stages): 4, 6 or 8
 int g_attn_token = 0;   // v4 exp-phase token ring (option 9)
 int g_attn_split = 0;   // v4 split MMA accumulator chains (option 10)
 int g_attn_qmajor = 1;  // v4 q-triple-major item order for equal-length batches (option 12)
+int g_attn_dyn = 0;     // v4 dynamic item claiming through a work counter (option 16; measured slower in graphs)
 int g_fused_mlp = 1;  // fused MLP kernel (d == 256) instead of two GEMM launches
 int g_staged_epi = 1; // TMA-staged residual + LayerNorm epilogue for the O-projection
 int g_mlp_cluster = 0; // fused MLP as CTA pairs (cta_group::2)
@@ -560,6 +561,10 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   ap.scale_log2 = 1.4426950408889634f / std::sqrt((float)c->dh);
   ap.stagger = g_attn_stagger;
   ap.uniform_n = g_attn_qmajor ? uniform_n : 0;
+  if (g_attn_dyn) {  // dynamic item claiming: the ctx's counter word (err[2]), zeroed per launch
+    ap.work_counter = c->err + 2;
+    CFD_CUDA(cudaMemsetAsync(ap.work_counter, 0, sizeof(int), s));
+  }
   CFD_CUDA(launch_attention(tq, ap, max_qtiles, g.n_heads, T, s));
   if (want_lse && scores) {
     ScoreParams sp{};
@@ -751,6 +756,9 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
       return CFD_OK;
     case 15:
       g_embed_ln = value ? 1 : 0;
+      return CFD_OK;
+    case 16:
+      g_attn_dyn = value ? 1 : 0;
       return CFD_OK;
     case 6:
       if (value != 4 && value != 6 && value != 8) return CFD_E_ARG;
@@ -1141,6 +1149,12 @@ cfd_status cfdx_attention(int32_t T, const int32_t* cu, int32_t max_seqlen, int3
   ap.cu_seqlens = cu; ap.d_model = d; ap.out = (__nv_bfloat16*)out; ap.lse = lse; ap.lse_ld = lse_ld;
   ap.scale_log2 = 1.4426950408889634f / std::sqrt(32.0f);
   ap.stagger = g_attn_stagger;
+  if (g_attn_dyn) {
+    static int* counter = nullptr;  // debug entry point: one process-wide counter word
+    if (!counter && cudaMalloc(&counter, sizeof(int)) != cudaSuccess) return CFD_E_CUDA;
+    ap.work_counter = counter;
+    CFD_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), static_cast<cudaStream_t>(stream)));
+  }
   CFD_CUDA(launch_attention(tq, ap, (max_seqlen + ATTN_BQ - 1) / ATTN_BQ, nh, T, static_cast<cudaStream_t>(stream)));
   return CFD_OK;
 }

@@ -142,6 +142,25 @@ def test_attention_wide_logit_range_stays_finite():
     torch.testing.assert_close(lse[:, :rows], rlse[:, :rows], rtol=1e-4, atol=2e-3)
 
 
+@pytest.mark.parametrize("opt", [(16, 1), (10, 1), (9, 1), (0, 5), (0, 6)])
+def test_attention_alternative_schedules_match_torch(opt):
+    """The non-default attention schedules kept for A/B measurement (dynamic item claiming,
+    split MMA chains, exp token ring, v5, v6) against torch on a ragged batch."""
+    key, val = opt
+    default = {16: 0, 10: 0, 9: 0, 0: 4}[key]
+    assert LIB.cfdx_set_option(key, val) == 0
+    try:
+        lens = [400, 700, 3, 1600, 129]
+        qkv, cu_l, out, lse = _run_attn(lens, 256, seed=21)
+    finally:
+        LIB.cfdx_set_option(key, default)
+    ref, rlse = _attn_ref(qkv, cu_l, 256, 8)
+    rows = cu_l[-1]
+    rel = ((out.float()[:rows] - ref[:rows]).norm() / ref[:rows].norm()).item()
+    assert rel < 1e-2, rel
+    torch.testing.assert_close(lse[:, :rows], rlse[:, :rows], rtol=1e-4, atol=1e-4)
+
+
 def test_attention_rows_sum_to_one_v_ones_probe():
     """V == 1 -> every output is sum_j P_ij = 1 (within bf16 rounding of P and O)."""
     d, lens = 256, [400, 1600, 37]
