@@ -91,6 +91,8 @@ int32_t cfdx_probe_count(int32_t kind);
  *          instead of a standalone LayerNorm launch (0)
  *   key 16 attention v4 dynamic item claiming through a work counter (1) instead of the static
  *          round-robin (0, default: the graph-replayed step measured 1.504 vs 1.471 ms)
+ *   key 17 cap on the persistent kernels' grid size (0 = every SM, default; caps measured
+ *          slower with two concurrent pipelines: 74 SMs 1.514, 100 1.399, 148 1.393 ms)
  * Other keys / values: CFD_E_ARG. */
 cfd_status cfdx_set_option(int32_t key, int32_t value);
 

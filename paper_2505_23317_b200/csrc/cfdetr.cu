@@ -103,6 +103,7 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
 }
 
 int g_num_sms = 0;
+int g_sm_cap = 0;  // option 17: cap on the persistent grids (0 = all SMs), for concurrent pipelines
 int num_sms() {
   if (!g_num_sms) {
     int dev = 0;
@@ -110,7 +111,7 @@ int num_sms() {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
   }
-  return g_num_sms;
+  return g_sm_cap > 0 ? std::min(g_sm_cap, g_num_sms) : g_num_sms;
 }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -759,6 +760,10 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
       return CFD_OK;
     case 16:
       g_attn_dyn = value ? 1 : 0;
+      return CFD_OK;
+    case 17:
+      if (value < 0 || value > 4096) return CFD_E_ARG;
+      g_sm_cap = value;
       return CFD_OK;
     case 6:
       if (value != 4 && value != 6 && value != 8) return CFD_E_ARG;
