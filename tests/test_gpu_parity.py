@@ -300,3 +300,30 @@ def test_fused_oproj_matches_separate_oproj_bitwise():
         lib.cfdx_set_option(11, 1)
     for a, b in zip(outs[0], outs[1]):
         assert torch.equal(a, b)
+
+
+def test_split_factor_m3_the_papers_3x3_to_9x9_example():
+    """Split factor m = 3 (a 3x3 coarse grid refined into 9x9 fine patches): 144x144
+    frames, Pc = 48, Pf = 16, Nc = 9, Nf = 81; ragged k = (3, 0, 9) against the oracle."""
+    cfg = ci.ModelConfig(144, 144, 48, 16, 64, 2, 1, 256, 0)
+    w = ci.make_weights(cfg, seed=3)
+    enc = CFDetrEncoder(cfg, w, max_tasks=8)
+    ks = [3, 0, 9]
+    imgs = ci.make_frames(cfg, len(ks), task0=2)
+    dimg = bf16_tensor(imgs, "cuda")
+    co = enc.coarse_encode(dimg, want_layers=True)
+    sel = enc.select_regions(co["scores"], k=ks)
+    ro = enc.batch_refine(dimg, co["x0"], sel["sel_idx"], sel["sel_count"], want_layers=True)
+    torch.cuda.synchronize()
+    enc.check()
+    cu = ro["cu_seqlens"].cpu().numpy()
+    assert np.diff(cu).tolist() == [cfg.n_coarse + 8 * k for k in ks]
+    for t in range(len(ks)):
+        oc = O.coarse_encode(cfg, w, [imgs[t]])[0]
+        _tol(co["layer_out"][0, t].cpu().numpy(), oc["layers"][0], f"m3 task {t} coarse")
+        sel_o = O.select_topk(co["scores"][t].cpu().numpy(), ks[t])
+        assert np.array_equal(sel["sel_idx"][t, :ks[t]].cpu().numpy(), sel_o)
+        rr = O.refine_encode(cfg, w, imgs[t], oc["x0"], sel_o)
+        assert np.array_equal(ro["mixed_src"][cu[t]:cu[t + 1]].cpu().numpy(), rr["mixed_src"])
+        _tol(ro["layer_out"][0, cu[t]:cu[t + 1]].cpu().numpy(), rr["layers"][0], f"m3 task {t} refine")
+    enc.close()
