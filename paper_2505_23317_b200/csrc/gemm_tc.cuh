@@ -215,8 +215,9 @@ struct ResidStage {
   int xb_stride;
   uint8_t* hb;
   int hb_stride;
-  uint64_t* bar;   // [2] this warp's TMA-load barriers
+  uint64_t* bar;   // [2] ([3] with xb3) this warp's TMA-load barriers
   uint32_t* xph;   // bit b: phase of bar[b]
+  uint8_t* xb3 = nullptr;  // optional third 4 KB x buffer: three residual chunks in flight
 };
 
 struct ResidLnArgs {
@@ -243,20 +244,23 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
   const int r = lane;
   const bool live = row0 + r < M;
   const bool one_hb = st.hb_stride == 0;
+  const int NB = st.xb3 ? 3 : 2;  // x staging buffers
+  auto buf = [&](int b) { return b == 2 ? st.xb3 : st.xb + b * st.xb_stride; };
   auto load = [&](int c, int b) {
     if (lane == 0) {
       mbar_expect_tx(&st.bar[b], 4096);
-      tma_load_2d(st.xb + b * st.xb_stride, &tmX, &st.bar[b], col_base + c * 32, row0);
+      tma_load_2d(buf(b), &tmX, &st.bar[b], col_base + c * 32, row0);
     }
   };
   auto wait = [&](int b) {
     mbar_wait(&st.bar[b], (*st.xph >> b) & 1);
     *st.xph ^= 1u << b;
   };
-  auto row_ptr = [&](int b, int q) { return reinterpret_cast<float4*>(st.xb + b * st.xb_stride + r * 128 + ((q ^ (r & 7)) << 4)); };
+  auto row_ptr = [&](int b, int q) { return reinterpret_cast<float4*>(buf(b) + r * 128 + ((q ^ (r & 7)) << 4)); };
   float mean = 0.f, rstd = 0.f;
   load(0, 0);
   if (CH > 1) load(1, 1);
+  if (NB == 3 && CH > 2) load(2, 2);
   mbar_wait(tfull_bar, tfull_parity);
   tc_fence_after();
   if constexpr (LN) {
@@ -266,7 +270,7 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll 1
     for (int c = 0; c < CH; ++c) {
-      const int b = c & 1;
+      const int b = c % NB;
       uint32_t a[32];
       tmem_ld32(tbase + c * 32, a);
       wait(b);
@@ -292,13 +296,13 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(&tmX, st.xb + b * st.xb_stride, col0, row0);
+        tma_store_2d(&tmX, buf(b), col0, row0);
         bulk_commit();
       }
-      if (c + 2 < CH) {
-        if (lane == 0) bulk_wait_read0();  // xb[b] is reloaded next
+      if (c + NB < CH) {
+        if (lane == 0) bulk_wait_read0();  // buffer b is reloaded next
         __syncwarp();
-        load(c + 2, b);
+        load(c + NB, b);
       }
     }
     tmem_wait_st();
@@ -364,7 +368,7 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
     // ---- single pass: x_new = x_old + acc + bias -> x (TMA store)
 #pragma unroll 1
     for (int c = 0; c < CH; ++c) {
-      const int b = c & 1;
+      const int b = c % NB;
       uint32_t a[32];
       tmem_ld32(tbase + c * 32, a);
       wait(b);
@@ -391,13 +395,13 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(&tmX, st.xb + b * st.xb_stride, col0, row0);
+        tma_store_2d(&tmX, buf(b), col0, row0);
         bulk_commit();
       }
-      if (c + 2 < CH) {
-        if (lane == 0) bulk_wait_read0();  // xb[b] is reloaded next
+      if (c + NB < CH) {
+        if (lane == 0) bulk_wait_read0();  // buffer b is reloaded next
         __syncwarp();
-        load(c + 2, b);
+        load(c + NB, b);
       }
     }
   }

@@ -81,7 +81,7 @@ __device__ unsigned long long g_mlp_trace[MLP_TRACE_WORDS];
 #else
 #define MLP_TR(it_, ev_) do { } while (0)
 #endif
-constexpr int MLP_SLOTS = 8;
+constexpr int MLP_SLOTS = 6;  // 8 measured no faster; the 32 KB go to a third x staging buffer per warp
 
 template <int D>
 struct MlpSmem {
@@ -98,7 +98,8 @@ struct MlpSmem {
   // one 2 KB LN output buffer per warp lives here
   // ... | b_o [D] | ln2 g [D] | ln2 b [D] (OPJ)
   static constexpr int LNSTG_OFF = ((PAR_OFF + (GEMM_MAX_N + 6 * D) * 4 + 1023) / 1024) * 1024;
-  static constexpr int TOTAL = 1024 + LNSTG_OFF + 8 * 2048;
+  static constexpr int XSTG_OFF = LNSTG_OFF + 8 * 2048;    // [8 warps] third 4 KB x staging buffer
+  static constexpr int TOTAL = 1024 + XSTG_OFF + 8 * 4096;
 };
 
 // CL = 2: CTA-pair kernel (2-CTA clusters, tcgen05 cta_group::2).  The single-CTA kernel is
@@ -133,8 +134,8 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   uint64_t* h_empty = h_full + 2;            // [2]
   uint64_t* a2_full = h_empty + 2;
   uint64_t* a2_empty = a2_full + 1;
-  uint64_t* xbar = a2_empty + 1;             // [8 warps][2] staged-epilogue TMA loads
-  uint64_t* ao_full = xbar + 16;             // OPJ: acc_o = o . W_o^T complete
+  uint64_t* xbar = a2_empty + 1;             // [8 warps][3] staged-epilogue TMA loads
+  uint64_t* ao_full = xbar + 24;             // OPJ: acc_o = o . W_o^T complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ao_full + 1);
   float2* ln_stats = reinterpret_cast<float2*>(smem + S::STATS_OFF);
   float* b1_s = reinterpret_cast<float*>(smem + S::PAR_OFF);
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     for (int i = 0; i < 2; ++i) { mbar_init(&h_full[i], 8 * CL); mbar_init(&h_empty[i], 1); }
     mbar_init(a2_full, 1);
     mbar_init(a2_empty, 8 * CL);
-    for (int i = 0; i < 16; ++i) mbar_init(&xbar[i], 1);
+    for (int i = 0; i < 24; ++i) mbar_init(&xbar[i], 1);
     mbar_init(ao_full, 1);
     fence_barrier_init();
   }
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         //      Staging: this warp's 4 KB slices of H[0] / H[1] (free until GELU(0)).
         const int e = warp - 2;
         uint8_t* hslice = smem + S::H_OFF + half * 16384 + quarter * 4096;
-        const ResidStage st{hslice, S::H_BYTES, nullptr, 0, xbar + 2 * e, &xph};
+        const ResidStage st{hslice, S::H_BYTES, nullptr, 0, xbar + 3 * e, &xph, smem + S::XSTG_OFF + e * 4096};
         const ResidLnArgs la{D, p.ln_cap, p.ln_eps};
         const uint32_t tb = tmem + lane_off + ACC2 + half * 128;
         if (et == 0) MLP_TR(it, 38);
@@ -518,7 +519,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         const int e = warp - 2;
         uint8_t* hslice = smem + S::H_OFF + half * 16384 + quarter * 4096;
         uint8_t* lnb = smem + S::LNSTG_OFF + e * 2048;
-        const ResidStage st{hslice, S::H_BYTES, lnb, 0, xbar + 2 * e, &xph};
+        const ResidStage st{hslice, S::H_BYTES, lnb, 0, xbar + 3 * e, &xph, smem + S::XSTG_OFF + e * 4096};
         const ResidLnArgs la{D, p.ln_cap, p.ln_eps};
         const uint32_t tb = tmem + lane_off + ACC2 + half * 128;
         if (do_ln)
