@@ -24,7 +24,7 @@ from typing import Dict, List, Sequence
 import numpy as np
 
 __all__ = [
-    "ModelConfig", "Workload", "CONFIGS", "WORKLOADS", "bf16_round", "bf16_bits",
+    "ModelConfig", "Workload", "CONFIGS", "WORKLOADS", "bf16_round", "bf16_bits", "make_decoder_weights",
     "bf16_from_bits", "make_frame", "make_frames", "make_weights", "frame_seed",
     "pe_table", "ks_for_ratios", "multi48_group_ks", "make_queries",
 ]
@@ -225,6 +225,25 @@ def _xavier(rng, fan_in: int, fan_out: int, scale: float = 1.0) -> np.ndarray:
     bound = math.sqrt(6.0 / (fan_in + fan_out))
     w = rng.uniform(-bound, bound, size=(fan_in, fan_out)) * scale
     return bf16_round(w.astype(np.float32))
+
+
+def make_decoder_weights(cfg: ModelConfig, n_queries: int = 128, seed: int = 1) -> dict:
+    """Random-init NEXT-f3 decoder block (reading R24), layout (in, out): learned queries
+    U(-1, 1) fp32 [Q, d]; LN gammas 1 + U(+-0.1), betas U(+-0.1); W_q [d, d], W_kv [d, 2d],
+    W_o [d, d] (x0.5) xavier-uniform bf16-rounded; W_head [d, 5] xavier bf16-rounded (stored
+    fp32); biases U(+-0.02)."""
+    rng = np.random.default_rng(seed)
+    d = cfg.d_model
+    g = lambda: (1.0 + rng.uniform(-0.1, 0.1, size=d)).astype(np.float32)
+    b = lambda n: rng.uniform(-0.02, 0.02, size=n).astype(np.float32)
+    return {
+        "queries": rng.uniform(-1.0, 1.0, size=(n_queries, d)).astype(np.float32),
+        "ln_q_g": g(), "ln_q_b": rng.uniform(-0.1, 0.1, size=d).astype(np.float32),
+        "ln_m_g": g(), "ln_m_b": rng.uniform(-0.1, 0.1, size=d).astype(np.float32),
+        "w_q": _xavier(rng, d, d), "w_kv": _xavier(rng, d, 2 * d), "w_o": _xavier(rng, d, d, 0.5),
+        "b_q": b(d), "b_kv": b(2 * d), "b_o": b(d),
+        "w_head": _xavier(rng, d, 5), "b_head": b(5),
+    }
 
 
 def make_weights(cfg: ModelConfig, seed: int = 0, tied: bool = False, pe: bool = True) -> dict:

@@ -161,6 +161,37 @@ cfd_status cfd_hardness(cfd_ctx *ctx, int32_t n_frames, int32_t n_queries, const
 cfd_status cfd_box_scores(cfd_ctx *ctx, int32_t n_frames, int32_t n_queries, const float *boxes, const float *conf,
                           float c_lo, float c_hi, float *scores, void *stream);
 
+/* NEXT row f3 — DETR decoder cross-attention + detection heads ("each
+ * query attends to the encoded patch features (through encoder-decoder cross-attention) ...
+ * and each query outputs a bounding box with a class label ... and a confidence score";
+ * 128 object queries).  One block, reading R24:
+ *   h_q = LN_q(Q0);  q = h_q W_q + b_q                       (Q0: n_queries learned queries)
+ *   per task t:  h_m = LN_m(y_t);  [k | v] = h_m W_kv + b_kv  (y_t: task t's encoder output)
+ *   o = concat_h softmax(q_h k_h^T / sqrt(dh)) v_h;  z = Q0 + o W_o + b_o
+ *   [box | c] = sigmoid(z W_head + b_head)                   (box = (cx, cy, w, h), c = confidence)
+ * Weights (device pointers, copied into the ctx by cfd_set_decoder, caller may free them
+ * after the stream syncs): queries fp32 [Q, d]; ln_q / ln_m gamma, beta fp32 [d]; w_q bf16
+ * [d, d], w_kv bf16 [d, 2d], w_o bf16 [d, d], w_head fp32 [d, 5], all (in, out); biases fp32.
+ * Q <= 128.  Errors: CFD_E_ARG (null / Q out of range), CFD_E_UNSUPPORTED (dh != 32). */
+typedef struct {
+  int32_t n_queries;
+  const float *queries;
+  const float *ln_q_g, *ln_q_b, *ln_m_g, *ln_m_b;
+  const uint16_t *w_q, *w_kv, *w_o;
+  const float *b_q, *b_kv, *b_o;
+  const float *w_head, *b_head;
+} cfd_decoder_weights;
+cfd_status cfd_set_decoder(cfd_ctx *ctx, const cfd_decoder_weights *w, void *stream);
+
+/* Decode n_tasks packed encoder outputs (the y / cu_seqlens of cfd_coarse_encode (cu =
+ * [0, Nc, 2Nc, ...]) or cfd_batch_refine).  y fp32 [rows, d] device; cu_seqlens int32
+ * [T+1] device; h_max_tokens: host upper bound of cu_seqlens[T] (sizes the launches).
+ * Out (device): z fp32 [T, Q, d] (decoded query embeddings, may be NULL), boxes fp32
+ * [T, Q, 4], conf fp32 [T, Q].  ws / ws_bytes: a workspace from cfd_query for >= n_tasks
+ * tasks.  CFD_E_ARG without cfd_set_decoder. */
+cfd_status cfd_decode(cfd_ctx *ctx, int32_t n_tasks, const float *y, const int32_t *cu_seqlens, int32_t h_max_tokens,
+                      float *z, float *boxes, float *conf, void *ws, size_t ws_bytes, void *stream);
+
 /* Synchronise `stream`; return CFD_E_DEVICE (and clear the word) if a kernel flagged
  * invalid device-side input since the last check, CFD_E_CUDA on a sticky CUDA error. */
 cfd_status cfd_check(cfd_ctx *ctx, void *stream);

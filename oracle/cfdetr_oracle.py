@@ -24,6 +24,8 @@ Parity status (see tests/test_oracle_pins.py):
   batch_refine ........ pinned (== per-task refine; cu_seqlens closed form)
   hardness_gate ....... pinned (vectorised fp64 mean; all-critical / single-query cases)
   box_cell_scores ..... pinned (brute-force pixel-mask rasterisation; full-image box)
+  decode .............. pinned (torch nn.MultiheadAttention cross-attention fp64; one-token
+                        memory -> output = v; equal keys -> mean of v; sigmoid heads)
 """
 from __future__ import annotations
 
@@ -38,7 +40,7 @@ __all__ = [
     "encoder_layer", "encoder", "criticality_score", "select_topk",
     "select_threshold", "merge_tokens", "gather_layout", "coarse_encode",
     "refine_encode", "batch_refine", "fine_pass", "as_f64_image", "hardness_gate", "box_pixel_rect",
-    "box_cell_scores",
+    "box_cell_scores", "decode",
 ]
 
 
@@ -359,3 +361,34 @@ def box_cell_scores(cfg, boxes: np.ndarray, conf: np.ndarray, c_lo: float = 0.05
             oy = max(0, min(y1, (gy + 1) * P) - max(y0, gy * P))
             s[cell] += ox * oy
     return s.astype(np.float64)
+
+
+# ----------------------------------------------------------------------------
+# NEXT f3: DETR decoder cross-attention + detection heads (reading R24)
+# ----------------------------------------------------------------------------
+def decode(wd: dict, y: np.ndarray, n_heads: int, eps: float):
+    """One decoder block over a task's encoder output y [N, d] ("each
+    query attends to the encoded patch features (through encoder-decoder cross-attention)
+    ... each query outputs a bounding box with a class label ... and a confidence score";
+    128 queries).  fp64:
+
+        h_q = LN_q(Q0);  q = h_q W_q + b_q
+        h_m = LN_m(y);   [k | v] = h_m W_kv + b_kv
+        o = concat_h softmax(q_h k_h^T / sqrt(dh)) v_h
+        z = Q0 + o W_o + b_o
+        [box | c] = sigmoid(z W_head + b_head)
+    Returns (z [Q, d], boxes [Q, 4], conf [Q])."""
+    f = lambda a: np.asarray(a, dtype=np.float64)
+    Q0 = f(wd["queries"])
+    d = Q0.shape[1]
+    dh = d // n_heads
+    q = layer_norm(Q0, wd["ln_q_g"], wd["ln_q_b"], eps) @ f(wd["w_q"]) + f(wd["b_q"])
+    kv = layer_norm(f(y), wd["ln_m_g"], wd["ln_m_b"], eps) @ f(wd["w_kv"]) + f(wd["b_kv"])
+    k, v = kv[:, :d], kv[:, d:]
+    o = np.empty((Q0.shape[0], d))
+    for hh in range(n_heads):
+        cols = slice(hh * dh, (hh + 1) * dh)
+        o[:, cols] = attention_probs(q[:, cols], k[:, cols]) @ v[:, cols]
+    z = Q0 + o @ f(wd["w_o"]) + f(wd["b_o"])
+    out = 1.0 / (1.0 + np.exp(-(z @ f(wd["w_head"]) + f(wd["b_head"]))))
+    return z, out[:, :4], out[:, 4]

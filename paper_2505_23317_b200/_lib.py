@@ -23,7 +23,7 @@ STATUS = {0: "CFD_OK", -1: "CFD_E_ARG", -2: "CFD_E_SHAPE", -3: "CFD_E_UNSUPPORTE
 # public symbols of include/cfdetr.h and include/cfdetr_debug.h
 PUBLIC_SYMBOLS = ["cfd_create", "cfd_destroy", "cfd_query", "cfd_coarse_encode", "cfd_select_regions",
                   "cfd_refine_encode", "cfd_batch_refine", "cfd_check", "cfd_status_str", "cfd_version",
-                  "cfd_hardness", "cfd_box_scores"]
+                  "cfd_hardness", "cfd_box_scores", "cfd_set_decoder", "cfd_decode"]
 DEBUG_SYMBOLS = ["cfdx_gemm", "cfdx_gemm_resid_ln", "cfdx_attention", "cfdx_layernorm", "cfdx_score", "cfdx_gather",
                  "cfdx_launch_count", "cfdx_mlp_trace", "cfdx_attn_trace", "cfdx_probe_install", "cfdx_probe_count", "cfdx_set_option"]
 PROBE_KINDS = {"attention": 0, "score": 1, "gemm_qkv": 2, "gemm_oproj": 3, "gemm_mlp1": 4, "gemm_mlp2": 5,
@@ -45,6 +45,12 @@ class cfd_layer_weights(C.Structure):
 class cfd_weights(C.Structure):
     _fields_ = [("w_embed_c", P), ("w_embed_f", P), ("b_embed_c", P), ("b_embed_f", P), ("pe_c", P),
                 ("pe_f", P), ("h_layers", C.POINTER(cfd_layer_weights))]
+
+
+class cfd_decoder_weights(C.Structure):
+    _fields_ = [("n_queries", I32), ("queries", P), ("ln_q_g", P), ("ln_q_b", P), ("ln_m_g", P), ("ln_m_b", P),
+                ("w_q", P), ("w_kv", P), ("w_o", P), ("b_q", P), ("b_kv", P), ("b_o", P), ("w_head", P),
+                ("b_head", P)]
 
 
 class CfdError(RuntimeError):
@@ -76,6 +82,8 @@ def load() -> C.CDLL:
         "cfd_check": [P, P],
         "cfd_hardness": [P, I32, I32, P, F32, F32, P, P],
         "cfd_box_scores": [P, I32, I32, P, P, F32, F32, P, P],
+        "cfd_set_decoder": [P, C.POINTER(cfd_decoder_weights), P],
+        "cfd_decode": [P, I32, P, P, I32, P, P, P, P, SZ, P],
         "cfd_status_str": [I32],
         "cfd_version": [],
         "cfdx_gemm": [I32, I32, I32, P, P, P, I32, P, P, P],

@@ -199,6 +199,34 @@ def _box_scores(self, boxes: torch.Tensor, conf: torch.Tensor, c_lo: float = 0.0
     return scores
 
 
+def _set_decoder(self, wdec: dict, stream=None) -> None:
+    """Load the NEXT-f3 decoder block (cfd_set_decoder): dict from cfd_inputs.make_decoder_weights."""
+    dev = self.device
+    t = {k: (bf16_tensor(v, dev) if k in ("w_q", "w_kv", "w_o") else f32_tensor(v, dev)) for k, v in wdec.items()}
+    dw = L.cfd_decoder_weights(int(wdec["queries"].shape[0]), *[t[k].data_ptr() for k in (
+        "queries", "ln_q_g", "ln_q_b", "ln_m_g", "ln_m_b", "w_q", "w_kv", "w_o", "b_q", "b_kv", "b_o", "w_head",
+        "b_head")])
+    L.check("cfd_set_decoder", self.lib.cfd_set_decoder(self.ctx, C.byref(dw), _stream(stream)))
+    (stream or torch.cuda.current_stream()).synchronize()
+    self.n_queries = int(wdec["queries"].shape[0])
+
+
+def _decode(self, y: torch.Tensor, cu_seqlens: torch.Tensor, n_tasks: int, max_tokens: int, stream=None) -> dict:
+    """Decoder cross-attention + heads (NEXT f3) over packed encoder outputs:
+    -> z [T, Q, d] fp32, boxes [T, Q, 4] (cx, cy, w, h), conf [T, Q]."""
+    T, Q, d = int(n_tasks), self.n_queries, self.cfg.d_model
+    z = torch.empty(T, Q, d, dtype=torch.float32, device=self.device)
+    boxes = torch.empty(T, Q, 4, dtype=torch.float32, device=self.device)
+    conf = torch.empty(T, Q, dtype=torch.float32, device=self.device)
+    ws = self.workspace(T)
+    L.check("cfd_decode", self.lib.cfd_decode(self.ctx, T, y.data_ptr(), cu_seqlens.data_ptr(), int(max_tokens),
+                                              z.data_ptr(), boxes.data_ptr(), conf.data_ptr(), ws.data_ptr(),
+                                              ws.numel(), _stream(stream)))
+    return {"z": z, "boxes": boxes, "conf": conf}
+
+
+CFDetrEncoder.set_decoder = _set_decoder
+CFDetrEncoder.decode = _decode
 CFDetrEncoder.hardness = _hardness
 CFDetrEncoder.box_scores = _box_scores
 

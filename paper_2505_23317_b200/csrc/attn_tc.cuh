@@ -37,6 +37,7 @@ struct AttnParams {
                            // items q-triple-major (all first triples, then all second ones, ...)
   int* work_counter = nullptr;  // v4: zeroed int; non-null -> items after the first are claimed
                                 // dynamically (atomicAdd) instead of the static round-robin
+  int n_q = 0;             // v1 CROSS: queries per task (one 128-row tile shared by every task)
 };
 
 constexpr int ATTN_THREADS = 192;
@@ -56,17 +57,25 @@ struct AttnSmem {
   static constexpr uint32_t TMEM_COLS = 512;
 };
 
-template <int DH, int STAGES>
+// CROSS (NEXT f3, decoder cross-attention, reading R24): the query tile is the n_q <= 128
+// learned object queries' projection (rows 0..n_q-1 of the q map, shared by every task),
+// keys / values are task t's packed encoder tokens [cu[t], cu[t+1]) of the kv map ([k | v]
+// columns), and the output goes to rows t * n_q + r.  Otherwise the self-attention path:
+// q, k, v from one [q | k | v] map (tmKV == tmQ).
+template <int DH, int STAGES, bool CROSS = false>
 __global__ void __launch_bounds__(ATTN_THREADS, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const AttnParams p) {
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const AttnParams p,
+                   const __grid_constant__ CUtensorMap tmKV) {
   static_assert(DH == 32, "this kernel is specialised for dh = 32 (64-byte rows, SW64)");
   using S = AttnSmem<DH, STAGES>;
   const int t = blockIdx.z, h = blockIdx.y, qt = blockIdx.x;
   const int seq0 = __ldg(p.cu_seqlens + t);
   const int N = __ldg(p.cu_seqlens + t + 1) - seq0;
-  if (qt * ATTN_BQ >= N) return;  // CTA-uniform, before any barrier / TMEM use
+  const int NQ = CROSS ? p.n_q : N;  // query rows of this task
+  if (qt * ATTN_BQ >= NQ || N <= 0) return;  // CTA-uniform, before any barrier / TMEM use
   const int nkv = (N + ATTN_BKV - 1) / ATTN_BKV;
-  const int q_row0 = seq0 + qt * ATTN_BQ;
+  const int q_row0 = CROSS ? 0 : seq0 + qt * ATTN_BQ;           // rows of the q map
+  const int out_row0 = CROSS ? t * p.n_q : q_row0;              // rows of the output
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
@@ -103,10 +112,12 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int col_q = h * DH, col_k = p.d_model + h * DH, col_v = 2 * p.d_model + h * DH;
+  const int col_q = h * DH, col_k = (CROSS ? 0 : p.d_model) + h * DH, col_v = (CROSS ? 1 : 2) * p.d_model + h * DH;
+  const CUtensorMap* tkv = CROSS ? &tmKV : &tmQKV;
 
   if (warp == 0) {
     if (lane == 0) {
+      tma_prefetch(tkv);
       mbar_expect_tx(q_full, S::Q_BYTES);
       tma_load_2d(sQ, &tmQKV, q_full, col_q, q_row0);
       int stage = 0;
@@ -114,8 +125,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
       for (int j = 0; j < nkv; ++j) {
         mbar_wait(&kv_empty[stage], phase ^ 1);
         mbar_expect_tx(&kv_full[stage], S::K_BYTES + S::V_BYTES);
-        tma_load_2d(sK + stage * S::K_BYTES, &tmQKV, &kv_full[stage], col_k, seq0 + j * ATTN_BKV);
-        tma_load_2d(sV + stage * S::V_BYTES, &tmQKV, &kv_full[stage], col_v, seq0 + j * ATTN_BKV);
+        tma_load_2d(sK + stage * S::K_BYTES, tkv, &kv_full[stage], col_k, seq0 + j * ATTN_BKV);
+        tma_load_2d(sV + stage * S::V_BYTES, tkv, &kv_full[stage], col_v, seq0 + j * ATTN_BKV);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
@@ -226,16 +237,16 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
     }
     absorb(nkv - 1, alpha_prev);
 
-    const int q_valid = N - qt * ATTN_BQ;
+    const int q_valid = NQ - qt * ATTN_BQ;
     if (r < q_valid) {
       const float inv = 1.f / l_run;
       uint32_t ob[DH / 2];
 #pragma unroll
       for (int i = 0; i < DH / 2; ++i) ob[i] = pack_bf16x2(o_acc[2 * i] * inv, o_acc[2 * i + 1] * inv);
-      uint4* dst = reinterpret_cast<uint4*>(p.out + (size_t)(q_row0 + r) * p.d_model + h * DH);
+      uint4* dst = reinterpret_cast<uint4*>(p.out + (size_t)(out_row0 + r) * p.d_model + h * DH);
 #pragma unroll
       for (int i = 0; i < DH / 8; ++i) dst[i] = make_uint4(ob[4 * i], ob[4 * i + 1], ob[4 * i + 2], ob[4 * i + 3]);
-      if (p.lse) p.lse[(size_t)h * p.lse_ld + q_row0 + r] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+      if (p.lse) p.lse[(size_t)h * p.lse_ld + out_row0 + r] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
     }
   }
   tc_fence_before();

@@ -421,7 +421,7 @@ cudaError_t launch_attention(const CUtensorMap& tq, const AttnParams& p, int max
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    kern<<<dim3(max_qtiles, nh, T), ATTN_THREADS, smem, s>>>(tq, p);
+    kern<<<dim3(max_qtiles, nh, T), ATTN_THREADS, smem, s>>>(tq, p, tq);
     e = cudaGetLastError();
   }
   probe_end(PK_ATTN, s);
@@ -486,6 +486,13 @@ struct cfd_ctx {
   CUtensorMap tm_wc, tm_wf;
   CUtensorMap tm_wc32;  // W_c with 32-k x 256-row SW64 boxes (image-sourced coarse embed)
   bool has_wc32 = false;
+  // NEXT f3 decoder (cfd_set_decoder): its own device block
+  void* dec_block = nullptr;
+  int dec_q = 0;
+  float *dq0 = nullptr, *dlnq_g = nullptr, *dlnq_b = nullptr, *dlnm_g = nullptr, *dlnm_b = nullptr;
+  uint16_t *dwq = nullptr, *dwkv = nullptr, *dwo = nullptr;  // K-major [N, K]
+  float *dbq = nullptr, *dbkv = nullptr, *dbo = nullptr, *dwh = nullptr, *dbh = nullptr;
+  CUtensorMap tm_dq, tm_dkv, tm_do;
 };
 
 namespace {
@@ -880,6 +887,7 @@ cfd_status cfd_destroy(cfd_ctx* c) {
   if (!c) return CFD_OK;
   cudaDeviceSynchronize();
   cudaFree(c->block);
+  if (c->dec_block) cudaFree(c->dec_block);
   delete c;
   return CFD_OK;
 }
@@ -1069,6 +1077,122 @@ cfd_status cfd_refine_encode(cfd_ctx* c, const uint16_t* image, const float* x0,
                              void* ws, size_t ws_bytes, void* stream) {
   return cfd_batch_refine(c, 1, image, x0, sel_idx, sel_count, nullptr, y, cu, msrc, layer_out, ws, ws_bytes,
                           stream);
+}
+
+// ------------------------------------------------------------------ NEXT f3: decoder
+cfd_status cfd_set_decoder(cfd_ctx* c, const cfd_decoder_weights* dw, void* stream) {
+  if (!c || !dw || !dw->queries || !dw->ln_q_g || !dw->ln_q_b || !dw->ln_m_g || !dw->ln_m_b || !dw->w_q ||
+      !dw->w_kv || !dw->w_o || !dw->b_q || !dw->b_kv || !dw->b_o || !dw->w_head || !dw->b_head)
+    return CFD_E_ARG;
+  if (dw->n_queries <= 0 || dw->n_queries > 128) return CFD_E_ARG;
+  if (c->dh != 32 || pick_bn(c->cfg.d_model) != c->cfg.d_model) return CFD_E_UNSUPPORTED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int d = c->cfg.d_model, Q = dw->n_queries;
+  if (c->dec_block) {
+    cudaStreamSynchronize(s);
+    cudaFree(c->dec_block);
+    c->dec_block = nullptr;
+  }
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+  const size_t o_q0 = take((size_t)Q * d * 4), o_ln = take((size_t)4 * d * 4), o_wq = take((size_t)d * d * 2),
+               o_wkv = take((size_t)2 * d * d * 2), o_wo = take((size_t)d * d * 2), o_b = take((size_t)4 * d * 4),
+               o_wh = take((size_t)d * 5 * 4 + 5 * 4);
+  if (cudaMalloc(&c->dec_block, off) != cudaSuccess) return CFD_E_CUDA;
+  char* B = static_cast<char*>(c->dec_block);
+  c->dec_q = Q;
+  c->dq0 = (float*)(B + o_q0);
+  c->dlnq_g = (float*)(B + o_ln); c->dlnq_b = c->dlnq_g + d; c->dlnm_g = c->dlnq_b + d; c->dlnm_b = c->dlnm_g + d;
+  c->dwq = (uint16_t*)(B + o_wq); c->dwkv = (uint16_t*)(B + o_wkv); c->dwo = (uint16_t*)(B + o_wo);
+  c->dbq = (float*)(B + o_b); c->dbkv = c->dbq + d; c->dbo = c->dbkv + 2 * d;
+  c->dwh = (float*)(B + o_wh); c->dbh = c->dwh + (size_t)d * 5;
+  auto cp = [&](void* dst, const void* src, size_t bytes) {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
+  };
+  auto transpose = [&](const uint16_t* in, uint16_t* outp, int K, int N) {
+    dim3 grid((N + 31) / 32, (K + 31) / 32);
+    transpose_bf16_kernel<<<grid, dim3(32, 8), 0, s>>>(in, outp, K, N);
+    ++g_launches;
+    return cudaGetLastError() == cudaSuccess;
+  };
+  if (!cp(c->dq0, dw->queries, (size_t)Q * d * 4) || !cp(c->dlnq_g, dw->ln_q_g, d * 4) ||
+      !cp(c->dlnq_b, dw->ln_q_b, d * 4) || !cp(c->dlnm_g, dw->ln_m_g, d * 4) || !cp(c->dlnm_b, dw->ln_m_b, d * 4) ||
+      !cp(c->dbq, dw->b_q, d * 4) || !cp(c->dbkv, dw->b_kv, 2 * d * 4) || !cp(c->dbo, dw->b_o, d * 4) ||
+      !cp(c->dwh, dw->w_head, (size_t)d * 5 * 4) || !cp(c->dbh, dw->b_head, 5 * 4) ||
+      !transpose(dw->w_q, c->dwq, d, d) || !transpose(dw->w_kv, c->dwkv, d, 2 * d) || !transpose(dw->w_o, c->dwo, d, d))
+    return CFD_E_CUDA;
+  if (!make_wmap(&c->tm_dq, c->dwq, d, d) || !make_wmap(&c->tm_dkv, c->dwkv, 2 * d, d) ||
+      !make_wmap(&c->tm_do, c->dwo, d, d))
+    return CFD_E_CUDA;
+  return CFD_OK;
+}
+
+cfd_status cfd_decode(cfd_ctx* c, int32_t T, const float* y, const int32_t* cu, int32_t max_tokens, float* z,
+                      float* boxes, float* conf, void* ws, size_t ws_bytes, void* stream) {
+  if (!c) return CFD_E_ARG;
+  if (T == 0) return CFD_OK;
+  if (T < 0 || !y || !cu || !boxes || !conf || !ws || max_tokens <= 0 || !c->dec_block) return CFD_E_ARG;
+  if (T > c->cfg.max_tasks) return CFD_E_CAPACITY;
+  Workspace w = carve(c, T, align_ws(ws));
+  if (w.bytes + 1024 > ws_bytes || max_tokens > T * c->Nf) return CFD_E_CAPACITY;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const cfd_config& g = c->cfg;
+  const int d = g.d_model, Q = c->dec_q, QR = T * Q;
+  // workspace reuse: LN_m(y) -> hbuf, [k | v] -> qkv (2d columns), o -> obuf (T*Q rows),
+  // LN_q(Q0) and q -> the ff region (256 rows each), z (if not requested) -> the patches region
+  __nv_bfloat16* hq = w.ff;
+  __nv_bfloat16* qb = w.ff + (size_t)256 * d;
+  __nv_bfloat16* kvb = w.qkv;
+  float* zz = z ? z : reinterpret_cast<float*>(w.patches);
+  CUtensorMap tmhq, tmhm, tmq, tmkv, tmo;
+  if (!make_amap(&tmhq, hq, 256, d) || !make_amap(&tmhm, w.hbuf, w.rows_cap, d) ||
+      !make_tmap(&tmq, qb, d, 256, d, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !make_tmap(&tmkv, kvb, 2 * d, w.rows_cap, 2 * d, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !make_amap(&tmo, w.obuf, w.rows_cap, d))
+    return CFD_E_CUDA;
+  // queries: q = LN_q(Q0) W_q + b_q (rows >= Q zero / padding)
+  CFD_CUDA(launch_layernorm(d, c->dq0, c->dlnq_g, c->dlnq_b, hq, Q, nullptr, 256, g.ln_eps, Q, s));
+  GemmParams p{};
+  p.M = Q; p.m_cap = 256; p.N = d; p.K = d; p.bias = c->dbq; p.out_bf16 = qb;
+  CFD_CUDA(launch_gemm(EPI_BF16_BIAS, tmhq, c->tm_dq, p, Q, s));
+  // memory: [k | v] = LN_m(y) W_kv + b_kv over the packed tokens (count cu[T] on the device)
+  const int* m_dev = cu + T;
+  CFD_CUDA(launch_layernorm(d, y, c->dlnm_g, c->dlnm_b, w.hbuf, max_tokens, m_dev, w.rows_cap, g.ln_eps, max_tokens, s));
+  p = GemmParams{};
+  p.M = max_tokens; p.m_dev = m_dev; p.m_cap = w.rows_cap; p.N = 2 * d; p.K = d; p.bias = c->dbkv; p.out_bf16 = kvb;
+  CFD_CUDA(launch_gemm(EPI_BF16_BIAS, tmhm, c->tm_dkv, p, max_tokens, s));
+  // cross-attention: one CTA per (head, task), the Q query rows against task t's tokens
+  {
+    auto kern = attn_tc_kernel<32, 3, true>;
+    constexpr int smem = AttnSmem<32, 3>::TOTAL;
+    static bool attr = false;
+    if (!attr) {
+      CFD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    AttnParams ap{};
+    ap.cu_seqlens = cu; ap.d_model = d; ap.out = w.obuf; ap.n_q = Q;
+    ap.scale_log2 = 1.4426950408889634f / std::sqrt((float)c->dh);
+    kern<<<dim3(1, g.n_heads, T), ATTN_THREADS, smem, s>>>(tmq, ap, tmkv);
+    ++g_launches;
+    CFD_CUDA(cudaGetLastError());
+  }
+  // z = Q0 + o W_o + b_o
+  {
+    const long long vec = (long long)QR * d / 4;
+    const int blocks = (int)std::min<long long>((vec + 255) / 256, (long long)num_sms() * 4);
+    launch_ex(broadcast_rows_kernel, dim3(blocks), dim3(256), 0, s, c->dq0, zz, T, Q, d);
+    ++g_launches;
+    CFD_CUDA(cudaGetLastError());
+  }
+  p = GemmParams{};
+  p.M = QR; p.m_cap = w.rows_cap; p.N = d; p.K = d; p.bias = c->dbo; p.out_f32 = zz; p.ld_out = d;
+  CFD_CUDA(launch_gemm(EPI_F32_RESID, tmo, c->tm_do, p, QR, s));
+  // heads: [box | c] = sigmoid(z W_head + b_head)
+  launch_ex(detect_heads_kernel, dim3((QR + 7) / 8), dim3(256), 0, s, zz, c->dwh, c->dbh, boxes, conf, QR, d);
+  ++g_launches;
+  CFD_CUDA(cudaGetLastError());
+  return CFD_OK;
 }
 
 cfd_status cfd_hardness(cfd_ctx* c, int32_t B, int32_t Q, const float* conf, float c_hi, float tau,

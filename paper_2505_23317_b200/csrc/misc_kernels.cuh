@@ -429,4 +429,43 @@ __global__ void box_scores_kernel(const float* __restrict__ boxes, const float* 
   }
 }
 
+// ------------------------------------------------------------------ decoder helpers (NEXT f3)
+// z[t * Q + r, :] = Q0[r, :]  (the residual stream of the decoder block starts at the queries)
+__global__ void broadcast_rows_kernel(const float* __restrict__ q0, float* __restrict__ z, int T, int Q, int d) {
+  const int vec = d / 4;
+  const long long total = (long long)T * Q * vec;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int v = (int)(i % vec);
+    const int r = (int)((i / vec) % Q);
+    reinterpret_cast<float4*>(z)[i] = __ldg(reinterpret_cast<const float4*>(q0) + (size_t)r * vec + v);
+  }
+}
+
+// [box | c] = sigmoid(z W_head + b_head) per decoded query: one warp per row, lane-strided dot
+// products over d (fp32), a fixed shuffle-tree reduction (deterministic)
+__global__ void detect_heads_kernel(const float* __restrict__ z, const float* __restrict__ w_head,
+                                    const float* __restrict__ b_head, float* __restrict__ boxes,
+                                    float* __restrict__ conf, int rows, int d) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const float* zr = z + (size_t)row * d;
+  float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int i = lane; i < d; i += 32) {
+    const float zi = zr[i];
+#pragma unroll
+    for (int o = 0; o < 5; ++o) acc[o] = fmaf(zi, __ldg(w_head + (size_t)i * 5 + o), acc[o]);
+  }
+#pragma unroll
+  for (int o = 0; o < 5; ++o)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], off);
+  if (lane < 5) {
+    const float a = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : lane == 3 ? acc[3] : acc[4];
+    const float sgm = 1.f / (1.f + __expf(-(a + __ldg(b_head + lane))));
+    if (lane < 4) boxes[(size_t)row * 4 + lane] = sgm;
+    else conf[row] = sgm;
+  }
+}
+
 }  // namespace cfd

@@ -361,3 +361,54 @@ def test_box_cell_scores_closed_forms():
     inner = np.array([[40 / 128, 40 / 128, 8 / 128, 8 / 128]], np.float32)           # pixels [36,44)^2 in cell (1,1)
     s = O.box_cell_scores(cfg, inner, np.array([0.3], np.float32))
     assert s[1 * 4 + 1] == 64 and s.sum() == 64
+
+
+# ------------------------------------------------------------------ NEXT f3 decoder
+def _torch_decode(wd, y, n_heads, eps):
+    """Reference from library routines: torch nn.MultiheadAttention (cross-attention, fp64,
+    in_proj = [W_q | W_k | W_v]^T) on F.layer_norm'd queries / memory, + residual, + heads."""
+    F = torch.nn.functional
+    t = lambda a: torch.as_tensor(np.asarray(a, np.float64))
+    Q0, Y = t(wd["queries"]), t(y)
+    d = Q0.shape[1]
+    mha = torch.nn.MultiheadAttention(d, n_heads, batch_first=True, dtype=torch.float64)
+    with torch.no_grad():
+        wkv = t(wd["w_kv"])
+        mha.in_proj_weight.copy_(torch.cat([t(wd["w_q"]), wkv[:, :d], wkv[:, d:]], dim=1).T)
+        mha.in_proj_bias.copy_(torch.cat([t(wd["b_q"]), t(wd["b_kv"])]))
+        mha.out_proj.weight.copy_(t(wd["w_o"]).T)
+        mha.out_proj.bias.copy_(t(wd["b_o"]))
+        hq = F.layer_norm(Q0, (d,), t(wd["ln_q_g"]), t(wd["ln_q_b"]), eps)
+        hm = F.layer_norm(Y, (d,), t(wd["ln_m_g"]), t(wd["ln_m_b"]), eps)
+        o, _ = mha(hq[None], hm[None], hm[None], need_weights=False)
+        z = Q0 + o[0]
+        out = torch.sigmoid(z @ t(wd["w_head"]) + t(wd["b_head"]))
+    return z.numpy(), out[:, :4].numpy(), out[:, 4].numpy()
+
+
+@pytest.mark.parametrize("N,Q,d,nh", [(28, 16, 64, 2), (400, 128, 256, 8), (1, 8, 64, 2)])
+def test_decode_matches_torch_multihead_cross_attention(N, Q, d, nh):
+    cfg = ci.ModelConfig(128, 128, 32, 16, d, nh, 1, 4 * d, 0)
+    wd = ci.make_decoder_weights(cfg, Q, seed=N)
+    y = np.random.default_rng(N).normal(size=(N, d))
+    z, box, conf = O.decode(wd, y, nh, 1e-6)
+    zr, br, cr = _torch_decode(wd, y, nh, 1e-6)
+    np.testing.assert_allclose(z, zr, rtol=0, atol=1e-10)
+    np.testing.assert_allclose(box, br, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(conf, cr, rtol=0, atol=1e-12)
+    assert ((box > 0) & (box < 1)).all() and ((conf > 0) & (conf < 1)).all()
+
+
+def test_decode_closed_forms():
+    """One memory token: every query's attention output is that token's v, so
+    z - Q0 is the same row for all queries.  Identical memory tokens: the same (uniform
+    attention over equal values)."""
+    cfg = ci.ModelConfig(128, 128, 32, 16, 64, 2, 1, 256, 0)
+    wd = ci.make_decoder_weights(cfg, 12, seed=5)
+    Q0 = wd["queries"].astype(np.float64)
+    row = np.random.default_rng(1).normal(size=(1, 64))
+    z1, _, _ = O.decode(wd, row, 2, 1e-6)
+    zk, _, _ = O.decode(wd, np.repeat(row, 7, axis=0), 2, 1e-6)
+    delta = z1 - Q0
+    assert np.allclose(delta, delta[0], atol=1e-12, rtol=0)
+    np.testing.assert_allclose(zk, z1, atol=1e-12, rtol=0)
