@@ -93,6 +93,8 @@ int32_t cfdx_probe_count(int32_t kind);
  *          round-robin (0, default: the graph-replayed step measured 1.504 vs 1.471 ms)
  *   key 17 cap on the persistent kernels' grid size (0 = every SM, default; caps measured
  *          slower with two concurrent pipelines: 74 SMs 1.514, 100 1.399, 148 1.393 ms)
+ *   key 18 balanced persistent grids: the fewest CTAs with the same number of rounds (1) /
+ *          min(units, SMs) (0, default; measured neutral with two pipelines, 1 % slower alone)
  * Other keys / values: CFD_E_ARG. */
 cfd_status cfdx_set_option(int32_t key, int32_t value);
 

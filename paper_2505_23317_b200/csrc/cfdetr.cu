@@ -116,6 +116,19 @@ int num_sms() {
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Persistent grid for `units` equal work units on at most `slots` CTAs: the fewest CTAs that
+// keep the same number of rounds (ceil(units / slots)), so a launch whose last round would
+// be partial leaves whole SMs to a concurrent stream instead of idling them in its tail
+// (option 18; e.g. 256 attention items: 128 CTAs x 2 rounds instead of 148 CTAs with 40 idle
+// in round 2).
+int g_balanced_grid = 0;  // off: 2-stream step 1.385 vs 1.389 ms (noise), 1-stream 1.479 vs 1.462 ms
+inline int balanced_grid(int units, int slots) {
+  if (units <= 0) return 1;
+  if (!g_balanced_grid || units <= slots) return std::min(units, slots);
+  const int rounds = (units + slots - 1) / slots;
+  return (units + rounds - 1) / rounds;
+}
+
 // ------------------------------------------------------------------ launches
 template <typename... KArgs, typename... Args>
 cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
@@ -171,8 +184,11 @@ cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
   const int rpt = kImg ? p.img_rb * p.img_gw : GEMM_BM;
   const int tiles = ((rows_for_grid + rpt - 1) / rpt) * (p.N / BN);
   const int slots = num_sms() * (MODE == 1 ? 2 : 1);
-  int grid = tiles < slots ? (tiles > 0 ? tiles : 1) : slots;
-  if constexpr (kBres) grid = std::max(1, grid / (p.N / BN)) * (p.N / BN);  // whole column-block groups
+  int grid = balanced_grid(tiles, slots);
+  if constexpr (kBres) {  // whole column-block groups, each balanced over its row blocks
+    const int nt = p.N / BN, mt = (rows_for_grid + rpt - 1) / rpt;
+    grid = balanced_grid(mt, std::max(1, slots / nt)) * nt;
+  }
   cudaError_t le = launch_ex(kern, dim3(grid), dim3(64 + 32 * EW), smem, s, ta, tb, p, tx ? *tx : ta, tln ? *tln : ta);
   ++g_launches;
   return le != cudaSuccess ? le : cudaGetLastError();
@@ -317,7 +333,7 @@ cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUte
     ++g_launches;
     return e != cudaSuccess ? e : cudaGetLastError();
   }
-  const int grid = std::max(1, std::min(tiles, num_sms()));
+  const int grid = std::max(1, balanced_grid(tiles, num_sms()));
   const cudaError_t le =
       two ? launch_ex(mlp_tc_kernel<256, 1, true>, dim3(grid), dim3(MLP_THREADS), smem, s, th, tw1, tw2, q, mx, ml, *two)
           : launch_ex(mlp_tc_kernel<256, 1>, dim3(grid), dim3(MLP_THREADS), smem, s, th, tw1, tw2, q, mx, ml, th);
@@ -345,7 +361,7 @@ cudaError_t launch_attn2_t(const CUtensorMap& tq, const AttnParams& p, int items
     attr = true;
   }
   // v5: two items (pairs) in flight per CTA
-  const int grid = std::max(1, std::min(V == 5 ? (items_ub + 1) / 2 : items_ub, num_sms()));
+  const int grid = std::max(1, balanced_grid(V == 5 ? (items_ub + 1) / 2 : items_ub, num_sms()));
   cudaError_t e = launch_ex(kern, dim3(grid), dim3(threads), smem, s, tq, p, T, nh);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess && getenv("CFD_VERBOSE")) {
@@ -771,6 +787,9 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
     case 17:
       if (value < 0 || value > 4096) return CFD_E_ARG;
       g_sm_cap = value;
+      return CFD_OK;
+    case 18:
+      g_balanced_grid = value ? 1 : 0;
       return CFD_OK;
     case 6:
       if (value != 4 && value != 6 && value != 8) return CFD_E_ARG;
