@@ -45,6 +45,8 @@ def test_host_side_argument_errors_without_gpu(lib):
     assert lib.cfd_coarse_encode(None, 1, None, None, None, None, None, None, 0, None) == -1
     assert lib.cfd_batch_refine(None, 1, None, None, None, None, None, None, None, None, None, None, 0, None) == -1
     assert lib.cfd_destroy(None) == 0
+    assert lib.cfd_set_decoder(None, None, None) == -1
+    assert lib.cfd_decode(None, 1, None, None, 1, None, None, None, None, 0, None) == -1
     # debug entry points validate shapes before touching the device
     assert lib.cfdx_gemm(0, 64, 64, None, None, None, 0, None, None, None) == -1
     assert lib.cfdx_gemm(10, 60, 64, 1, 1, 1, 0, 1, None, None) == -1
