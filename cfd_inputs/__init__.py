@@ -160,17 +160,8 @@ def frame_seed(task: int, frame: int) -> int:
     return 2505233 + 1000 * task + frame
 
 
-def make_frame(h: int, w: int, seed: int, constant: bool = False) -> np.ndarray:
-    """One synthetic camera frame, returned as bf16 bits [H, W, 3] (HWC, uint16).
-
-    Sky-to-road vertical gradient + Poisson(8) axis-aligned rectangles of random
-    colour with log-uniform side in [8, 192] px (some above the 16384 px^2
-    critical size, PAPER.md:168; many small, O2 PAPER.md:156), Gaussian noise
-    sigma=0.05, per-channel normalisation to mean 0 / std 1, then bf16.
-    `constant=True` returns an all-0.5 frame (used by the equal-score pin).
-    """
-    if constant:
-        return bf16_bits(np.full((h, w, 3), 0.5, dtype=np.float32))
+def _scene(h: int, w: int, seed: int) -> np.ndarray:
+    """fp64 [H, W, 3] scene in ~[0, 1] before normalisation (see make_frame)."""
     rng = np.random.default_rng(seed)
     t = np.linspace(0.0, 1.0, h, dtype=np.float64)[:, None]
     sky = np.array([0.55, 0.70, 0.95])
@@ -189,10 +180,50 @@ def make_frame(h: int, w: int, seed: int, constant: bool = False) -> np.ndarray:
         y0 = int(rng.integers(0, max(1, h - sh + 1)))
         img[y0:y0 + sh, x0:x0 + sw, :] = rng.random(3)
     img += rng.normal(0.0, 0.05, size=img.shape)
+    return img
+
+
+def make_frame(h: int, w: int, seed: int, constant: bool = False) -> np.ndarray:
+    """One synthetic camera frame, returned as bf16 bits [H, W, 3] (HWC, uint16).
+
+    Sky-to-road vertical gradient + Poisson(8) axis-aligned rectangles of random
+    colour with log-uniform side in [8, 192] px (some above the 16384 px^2
+    critical size, PAPER.md:168; many small, O2 PAPER.md:156), Gaussian noise
+    sigma=0.05, per-channel normalisation to mean 0 / std 1, then bf16.
+    `constant=True` returns an all-0.5 frame (used by the equal-score pin).
+    """
+    if constant:
+        return bf16_bits(np.full((h, w, 3), 0.5, dtype=np.float32))
+    img = _scene(h, w, seed)
     mu = img.mean(axis=(0, 1), keepdims=True)
     sd = img.std(axis=(0, 1), keepdims=True)
     img = (img - mu) / np.maximum(sd, 1e-6)
     return bf16_bits(img.astype(np.float32))
+
+
+def make_frame_u8(h: int, w: int, seed: int) -> np.ndarray:
+    """The same scene as make_frame(seed) as an 8-bit camera frame [H, W, 3] uint8
+    (clip to [0, 1], x 255, round) -- the serving-path input of cfd_frames_from_u8."""
+    return np.clip(np.rint(_scene(h, w, seed) * 255.0), 0, 255).astype(np.uint8)
+
+
+def make_frames_u8(cfg: "ModelConfig", n: int, task0: int = 0, frame: int = 0) -> np.ndarray:
+    """[n, H, W, 3] uint8; frame i uses seed(task0 + i, frame)."""
+    return np.stack([make_frame_u8(cfg.img_h, cfg.img_w, frame_seed(task0 + i, frame)) for i in range(n)])
+
+
+# per-channel ingest constants for 8-bit frames: (p/255 - mean_c) / std_c as one fp32 FMA,
+# scale_c = 1 / (255 std_c), shift_c = -mean_c / std_c (ImageNet statistics, the usual DETR
+# input normalisation), rounded once to fp32
+U8_MEAN = (0.485, 0.456, 0.406)
+U8_STD = (0.229, 0.224, 0.225)
+
+
+def u8_affine(mean=U8_MEAN, std=U8_STD):
+    """-> (scale[3], shift[3]) as float32 arrays."""
+    m = np.asarray(mean, dtype=np.float64)
+    s = np.asarray(std, dtype=np.float64)
+    return (1.0 / (255.0 * s)).astype(np.float32), (-m / s).astype(np.float32)
 
 
 def make_frames(cfg: ModelConfig, n: int, task0: int = 0, frame: int = 0) -> np.ndarray:

@@ -192,6 +192,20 @@ cfd_status cfd_set_decoder(cfd_ctx *ctx, const cfd_decoder_weights *w, void *str
 cfd_status cfd_decode(cfd_ctx *ctx, int32_t n_tasks, const float *y, const int32_t *cu_seqlens, int32_t h_max_tokens,
                       float *z, float *boxes, float *conf, void *ws, size_t ws_bytes, void *stream);
 
+/* Frame ingest (serving path; not a step of the paper's method, which starts from camera
+ * images, "images ... from the cameras"): 8-bit HWC frames -> the bf16 HWC
+ * frames cfd_coarse_encode / cfd_batch_refine read, so a host uploads 1 byte per channel
+ * value instead of 2.  Element i (channel c = i mod 3) of each frame:
+ *   images[i] = bf16_rn( fp32_fma(src[i], scale[c], shift[c]) )
+ * i.e. one fp32 fused multiply-add (single rounding) then round-to-nearest-even to bf16; with
+ * scale = 1 / (255 std_c) and shift = -mean_c / std_c this is the usual (p/255 - mean)/std.
+ * src uint8 [n_frames, H, W, 3] device; images uint16 (bf16 bits) [n_frames, H, W, 3]
+ * device (may be the buffer later passed to the encode calls); scale, shift: HOST arrays of
+ * 3 floats, read during the call (capture-safe: the values are baked into the launch).
+ * n_frames = 0 is a no-op.  Errors: CFD_E_ARG (null pointer, n_frames < 0). */
+cfd_status cfd_frames_from_u8(cfd_ctx *ctx, int32_t n_frames, const uint8_t *src, const float *scale,
+                              const float *shift, uint16_t *images, void *stream);
+
 /* Synchronise `stream`; return CFD_E_DEVICE (and clear the word) if a kernel flagged
  * invalid device-side input since the last check, CFD_E_CUDA on a sticky CUDA error. */
 cfd_status cfd_check(cfd_ctx *ctx, void *stream);

@@ -107,6 +107,11 @@ int64_t cfdx_launch_count(void);
  * first two tiles of every CTA, 148 x 96 uint64 (layout in csrc/mlp_tc.cuh), into the host
  * buffer dst (n_words >= 148 * 96).  CFD_E_ARG when the library was built without tracing. */
 cfd_status cfdx_mlp_trace(uint64_t* dst, int32_t n_words);
+/* cfd_frames_from_u8 on a flat array of n elements (any n >= 0, including n % 16 != 0:
+ * the ragged tail path); element i uses channel i mod 3. */
+cfd_status cfdx_frames_u8(long long n, const uint8_t* src, const float* scale, const float* shift, uint16_t* dst,
+                          void* stream);
+
 /* Debug library only: copies the attention (v4/v5) pipeline trace of the last launch
  * (ATTN_TRACE_WORDS = 148*4*2*12*8 + 148 uint64 clock64 values, layout in attn4_tc.cuh) to
  * host `dst`.  CFD_E_ARG in the release library or if n_words is too small. */

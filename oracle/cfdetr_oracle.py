@@ -26,10 +26,13 @@ Parity status (see tests/test_oracle_pins.py):
   box_cell_scores ..... pinned (brute-force pixel-mask rasterisation; full-image box)
   decode .............. pinned (torch nn.MultiheadAttention cross-attention fp64; one-token
                         memory -> output = v; equal keys -> mean of v; sigmoid heads)
+  frames_from_u8 ...... pinned (torch fp64 -> fp32 -> bf16 conversions where fp64 is exact;
+                        integer identity; bf16 ties to even; the fp32-first double rounding)
 """
 from __future__ import annotations
 
 import math
+from fractions import Fraction
 from typing import List, Sequence, Tuple
 
 import numpy as np
@@ -40,7 +43,7 @@ __all__ = [
     "encoder_layer", "encoder", "criticality_score", "select_topk",
     "select_threshold", "merge_tokens", "gather_layout", "coarse_encode",
     "refine_encode", "batch_refine", "fine_pass", "as_f64_image", "hardness_gate", "box_pixel_rect",
-    "box_cell_scores", "decode",
+    "box_cell_scores", "decode", "round_to_float", "frames_from_u8",
 ]
 
 
@@ -392,3 +395,52 @@ def decode(wd: dict, y: np.ndarray, n_heads: int, eps: float):
     z = Q0 + o @ f(wd["w_o"]) + f(wd["b_o"])
     out = 1.0 / (1.0 + np.exp(-(z @ f(wd["w_head"]) + f(wd["b_head"]))))
     return z, out[:, :4], out[:, 4]
+
+
+# ----------------------------------------------------------------------------
+# Serving-path ingest: 8-bit camera frames -> bf16 frames (not a step of the method;
+# its definition is the one include/cfdetr.h states for cfd_frames_from_u8)
+# ----------------------------------------------------------------------------
+def round_to_float(v: Fraction, sig_bits: int, emin: int = -126) -> Fraction:
+    """Round the exact rational v to the nearest binary floating-point number with
+    `sig_bits` significand bits (implicit bit included) and minimum exponent emin
+    (subnormals: exponent held at emin), ties to even (IEEE 754 roundTiesToEven).
+    fp32: sig_bits = 24; bf16: sig_bits = 8.  No overflow handling (|v| < 2^127)."""
+    if v == 0:
+        return Fraction(0)
+    a = abs(v)
+    e = a.numerator.bit_length() - a.denominator.bit_length()  # floor(log2 a) or one above
+    if Fraction(2) ** e > a:
+        e -= 1
+    e = max(e, emin)
+    ulp = Fraction(2) ** (e - (sig_bits - 1))
+    q = a / ulp
+    n = q.numerator // q.denominator
+    r = q - n
+    if r > Fraction(1, 2) or (r == Fraction(1, 2) and n % 2 == 1):
+        n += 1
+    return (n * ulp) if v > 0 else -(n * ulp)
+
+
+def frames_from_u8(src: np.ndarray, scale, shift) -> np.ndarray:
+    """8-bit HWC frames -> bf16 bits, element i of channel c = i mod 3:
+        out = bf16_rn( fp32_rn( p * scale[c] + shift[c] ) )
+    (one fp32 fused multiply-add -- the exact product-sum rounded once to fp32 -- then
+    round-to-nearest-even to bf16), computed exactly in rationals for each of the 256
+    byte values per channel.  scale / shift are taken as fp32 values.  uint16 out."""
+    src = np.asarray(src, dtype=np.uint8)
+    lead = src.shape
+    flat = src.reshape(-1)
+    out = np.empty(flat.shape, dtype=np.uint16)
+    ch = np.arange(flat.size) % 3
+    for c in range(3):
+        sc = Fraction(float(np.float32(scale[c])))
+        sh = Fraction(float(np.float32(shift[c])))
+        lut = np.empty(256, dtype=np.uint16)
+        for p_ in range(256):
+            v = round_to_float(round_to_float(p_ * sc + sh, 24), 8)
+            f32 = np.float32(float(v))  # exact: v has 8 significant bits
+            lut[p_] = np.uint16(f32.view(np.uint32) >> 16)
+        m = ch == c
+        out[m] = lut[flat[m]]
+    return out.reshape(lead)

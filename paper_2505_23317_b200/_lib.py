@@ -23,9 +23,10 @@ STATUS = {0: "CFD_OK", -1: "CFD_E_ARG", -2: "CFD_E_SHAPE", -3: "CFD_E_UNSUPPORTE
 # public symbols of include/cfdetr.h and include/cfdetr_debug.h
 PUBLIC_SYMBOLS = ["cfd_create", "cfd_destroy", "cfd_query", "cfd_coarse_encode", "cfd_select_regions",
                   "cfd_refine_encode", "cfd_batch_refine", "cfd_check", "cfd_status_str", "cfd_version",
-                  "cfd_hardness", "cfd_box_scores", "cfd_set_decoder", "cfd_decode"]
+                  "cfd_hardness", "cfd_box_scores", "cfd_set_decoder", "cfd_decode", "cfd_frames_from_u8"]
 DEBUG_SYMBOLS = ["cfdx_gemm", "cfdx_gemm_resid_ln", "cfdx_attention", "cfdx_layernorm", "cfdx_score", "cfdx_gather",
-                 "cfdx_launch_count", "cfdx_mlp_trace", "cfdx_attn_trace", "cfdx_probe_install", "cfdx_probe_count", "cfdx_set_option"]
+                 "cfdx_launch_count", "cfdx_mlp_trace", "cfdx_attn_trace", "cfdx_probe_install", "cfdx_probe_count", "cfdx_set_option",
+                 "cfdx_frames_u8"]
 PROBE_KINDS = {"attention": 0, "score": 1, "gemm_qkv": 2, "gemm_oproj": 3, "gemm_mlp1": 4, "gemm_mlp2": 5,
                "gemm_embed_c": 6, "gemm_embed_f": 7, "layernorm": 8, "select": 9, "gather": 10, "im2col": 11,
                "meta": 12}
@@ -84,6 +85,8 @@ def load() -> C.CDLL:
         "cfd_box_scores": [P, I32, I32, P, P, F32, F32, P, P],
         "cfd_set_decoder": [P, C.POINTER(cfd_decoder_weights), P],
         "cfd_decode": [P, I32, P, P, I32, P, P, P, P, SZ, P],
+        "cfd_frames_from_u8": [P, I32, P, C.POINTER(F32), C.POINTER(F32), P, P],
+        "cfdx_frames_u8": [I64, P, C.POINTER(F32), C.POINTER(F32), P, P],
         "cfd_status_str": [I32],
         "cfd_version": [],
         "cfdx_gemm": [I32, I32, I32, P, P, P, I32, P, P, P],

@@ -225,10 +225,42 @@ def _decode(self, y: torch.Tensor, cu_seqlens: torch.Tensor, n_tasks: int, max_t
     return {"z": z, "boxes": boxes, "conf": conf}
 
 
+
+def _f3(v) -> "C.Array":
+    a = [float(x) for x in v]
+    if len(a) != 3:
+        raise ValueError("expected 3 per-channel values")
+    return (L.F32 * 3)(*a)
+
+
+def frames_from_u8_flat(src: torch.Tensor, scale, shift, out: Optional[torch.Tensor] = None,
+                        stream=None) -> torch.Tensor:
+    """cfdx_frames_u8 on a flat uint8 device tensor (any length; element i is channel i mod 3)."""
+    n = src.numel()
+    o = out if out is not None else torch.empty(n, dtype=_BF16, device=src.device)
+    L.check("cfdx_frames_u8", L.load().cfdx_frames_u8(n, src.data_ptr(), _f3(scale), _f3(shift), o.data_ptr(),
+                                                      _stream(stream)))
+    return o
+
+
+def _frames_from_u8(self, src: torch.Tensor, scale, shift, out: Optional[torch.Tensor] = None,
+                    stream=None) -> torch.Tensor:
+    """8-bit HWC frames [B, H, W, 3] uint8 (device) -> bf16 frames for the encode calls
+    (cfd_frames_from_u8: bf16_rn(fma_f32(p, scale[c], shift[c])))."""
+    if src.dtype != torch.uint8 or not src.is_contiguous():
+        raise ValueError("frames_from_u8: src must be a contiguous uint8 tensor")
+    B = src.shape[0]
+    o = out if out is not None else torch.empty(B, self.cfg.img_h, self.cfg.img_w, 3, dtype=_BF16,
+                                                device=self.device)
+    L.check("cfd_frames_from_u8", self.lib.cfd_frames_from_u8(self.ctx, B, src.data_ptr(), _f3(scale), _f3(shift),
+                                                              o.data_ptr(), _stream(stream)))
+    return o
+
 CFDetrEncoder.set_decoder = _set_decoder
 CFDetrEncoder.decode = _decode
 CFDetrEncoder.hardness = _hardness
 CFDetrEncoder.box_scores = _box_scores
+CFDetrEncoder.frames_from_u8 = _frames_from_u8
 
 
 def launch_count() -> int:

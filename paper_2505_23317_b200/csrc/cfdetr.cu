@@ -1240,6 +1240,34 @@ cfd_status cfd_box_scores(cfd_ctx* c, int32_t B, int32_t Q, const float* boxes, 
   return CFD_OK;
 }
 
+static cfd_status launch_frames_u8(long long n, const uint8_t* src, const float* scale, const float* shift,
+                                   uint16_t* dst, cudaStream_t s) {
+  if (n == 0) return CFD_OK;
+  if (n < 0 || !src || !dst || !scale || !shift) return CFD_E_ARG;
+  FrameAffine a;
+  for (int i = 0; i < 3; ++i) { a.scale[i] = scale[i]; a.shift[i] = shift[i]; }
+  const long long units = std::max(n >> 4, 1LL);
+  const int blocks = (int)std::min<long long>((units + 255) / 256, (long long)num_sms() * 8);
+  launch_ex(frames_u8_kernel, dim3(blocks), dim3(256), 0, s, src, dst, n, a);
+  ++g_launches;
+  CFD_CUDA(cudaGetLastError());
+  return CFD_OK;
+}
+
+cfd_status cfd_frames_from_u8(cfd_ctx* c, int32_t n_frames, const uint8_t* src, const float* scale,
+                              const float* shift, uint16_t* images, void* stream) {
+  if (!c) return CFD_E_ARG;
+  if (n_frames == 0) return CFD_OK;
+  if (n_frames < 0) return CFD_E_ARG;
+  const long long n = (long long)n_frames * c->cfg.img_h * c->cfg.img_w * 3;
+  return launch_frames_u8(n, src, scale, shift, images, static_cast<cudaStream_t>(stream));
+}
+
+cfd_status cfdx_frames_u8(long long n, const uint8_t* src, const float* scale, const float* shift, uint16_t* dst,
+                          void* stream) {
+  return launch_frames_u8(n, src, scale, shift, dst, static_cast<cudaStream_t>(stream));
+}
+
 cfd_status cfd_check(cfd_ctx* c, void* stream) {
   if (!c) return CFD_E_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -468,4 +468,49 @@ __global__ void detect_heads_kernel(const float* __restrict__ z, const float* __
   }
 }
 
+// ---------------------------------------------------------------------------- frame ingest
+// 8-bit HWC camera frames -> the bf16 HWC frames the embeds read (cfd_frames_from_u8):
+// out = bf16_rn(fmaf(p, scale[c], shift[c])), c = channel = element index mod 3.  HBM-bound
+// (1 B in, 2 B out per element): each thread converts 16 consecutive bytes (one coalesced
+// 16-B load, two 16-B stores); 16 = 1 (mod 3), so unit u's first element has channel u mod 3.
+struct FrameAffine {
+  float scale[3], shift[3];
+};
+
+__global__ void frames_u8_kernel(const uint8_t* __restrict__ src, uint16_t* __restrict__ dst, long long n,
+                                 const FrameAffine a) {
+  const long long units = n >> 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < units; u += stride) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(src) + u);
+    const int rot = static_cast<int>(u % 3);
+    const float s0 = rot == 0 ? a.scale[0] : (rot == 1 ? a.scale[1] : a.scale[2]);
+    const float s1 = rot == 0 ? a.scale[1] : (rot == 1 ? a.scale[2] : a.scale[0]);
+    const float s2 = rot == 0 ? a.scale[2] : (rot == 1 ? a.scale[0] : a.scale[1]);
+    const float t0 = rot == 0 ? a.shift[0] : (rot == 1 ? a.shift[1] : a.shift[2]);
+    const float t1 = rot == 0 ? a.shift[1] : (rot == 1 ? a.shift[2] : a.shift[0]);
+    const float t2 = rot == 0 ? a.shift[2] : (rot == 1 ? a.shift[0] : a.shift[1]);
+    const float sc[3] = {s0, s1, s2}, sh[3] = {t0, t1, t2};
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[8];
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+      const float x0 = fmaf(static_cast<float>((w[j >> 2] >> (8 * (j & 3))) & 0xFF), sc[j % 3], sh[j % 3]);
+      const float x1 =
+          fmaf(static_cast<float>((w[(j + 1) >> 2] >> (8 * ((j + 1) & 3))) & 0xFF), sc[(j + 1) % 3], sh[(j + 1) % 3]);
+      const __nv_bfloat162 b = __floats2bfloat162_rn(x0, x1);
+      o[j >> 1] = *reinterpret_cast<const uint32_t*>(&b);
+    }
+    uint4* d = reinterpret_cast<uint4*>(dst) + 2 * u;
+    __stcs(d, make_uint4(o[0], o[1], o[2], o[3]));
+    __stcs(d + 1, make_uint4(o[4], o[5], o[6], o[7]));
+  }
+  // ragged tail (n % 16 elements), one element per thread of block 0
+  if (blockIdx.x == 0 && threadIdx.x < (n & 15)) {
+    const long long i = (units << 4) + threadIdx.x;
+    const int c = static_cast<int>(i % 3);
+    dst[i] = __bfloat16_as_ushort(__float2bfloat16_rn(fmaf(static_cast<float>(src[i]), a.scale[c], a.shift[c])));
+  }
+}
+
 }  // namespace cfd

@@ -412,3 +412,54 @@ def test_decode_closed_forms():
     delta = z1 - Q0
     assert np.allclose(delta, delta[0], atol=1e-12, rtol=0)
     np.testing.assert_allclose(zk, z1, atol=1e-12, rtol=0)
+
+
+# ---------------------------------------------------------------------------- frame ingest
+def test_round_to_float_matches_numpy_fp32_and_torch_bf16():
+    """The oracle's exact rounding helper against library conversions (RNE, subnormals)."""
+    from fractions import Fraction
+    import torch
+    rng = np.random.default_rng(5)
+    xs = np.concatenate([rng.normal(0, 1, 2000), rng.normal(0, 1, 200) * 1e-39, rng.normal(0, 1, 200) * 1e30,
+                         [0.0, 1.0, -1.0, 2.0 ** -149, 3 * 2.0 ** -150]])
+    for x in xs:
+        assert float(O.round_to_float(Fraction(float(x)), 24)) == float(np.float32(x)), x
+    f32 = rng.normal(0, 10, 3000).astype(np.float32)
+    bf = torch.from_numpy(f32).bfloat16().float().numpy()
+    for x, y in zip(f32, bf):
+        assert float(O.round_to_float(Fraction(float(x)), 8)) == float(y), x
+
+
+def test_frames_from_u8_against_library_conversions():
+    """Where p*scale+shift is exact in fp64, fp64 -> fp32 -> bf16 by torch must agree."""
+    from fractions import Fraction
+    import torch
+    sc, sh = ci.u8_affine()
+    src = np.repeat(np.arange(256, dtype=np.uint8), 3).reshape(256, 3)
+    v64 = src.astype(np.float64) * sc.astype(np.float64) + sh.astype(np.float64)
+    for p in range(256):
+        for c in range(3):
+            assert Fraction(p) * Fraction(float(sc[c])) + Fraction(float(sh[c])) == Fraction(v64[p, c])
+    ref = torch.from_numpy(v64).float().bfloat16().view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(O.frames_from_u8(src, sc, sh), ref)
+
+
+def test_frames_from_u8_closed_forms():
+    one, zero = np.ones(3, np.float32), np.zeros(3, np.float32)
+    src = np.repeat(np.arange(256, dtype=np.uint8), 3).reshape(256, 3)
+    # identity: integers <= 256 are exact in bf16
+    ident = O.frames_from_u8(src, one, zero)
+    assert np.array_equal(ident, (np.arange(256, dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)[:, None]
+                          .repeat(3, 1))
+    bits = lambda v: np.uint16(np.float32(v).view(np.uint32) >> 16)  # noqa: E731
+    # ties to even in [256, 512) (bf16 spacing 2): 257 -> 256, 259 -> 260; channel = index mod 3
+    out = O.frames_from_u8(np.array([[255, 255, 253]], np.uint8), one, np.array([2.0, 4.0, 2.0], np.float32))
+    assert list(out[0]) == [bits(256.0), bits(260.0), bits(255.0)]
+    # fp32 first: 257 + 2^-20 rounds to 257 in fp32 (ulp 2^-15), then ties to 256 -- a direct
+    # bf16 rounding of the exact value would give 258
+    out = O.frames_from_u8(np.array([[255, 0, 0]], np.uint8), one, np.array([2.0 + 2.0 ** -20, 0.0, 0.0], np.float32))
+    assert out[0, 0] == bits(256.0)
+    # p = 0 gives bf16(shift); a negative scale flips the sign
+    out = O.frames_from_u8(np.array([[0, 10, 0]], np.uint8), np.array([1, -1, 1], np.float32),
+                           np.array([-0.5, 0.0, 3.0], np.float32))
+    assert list(out[0]) == [bits(-0.5), bits(-10.0), bits(3.0)]
