@@ -554,7 +554,7 @@ def gpu_arm(args):
                                  up=torch.cuda.Event(), done=torch.cuda.Event(), down=torch.cuda.Event()))
             lanes.append(dict(h_in=h_in, sets=sets, s=s_l, n_out=n_out_l, copy_s=torch.cuda.Stream(device=dev),
                               down_s=torch.cuda.Stream(device=dev)))
-        n_steps_t = max(4, min(args.steps, 16))
+        n_steps_t = max(8, args.steps)
 
         def e2e_run(n_steps, main):
             fork = torch.cuda.Event()
