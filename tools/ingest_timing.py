@@ -1,3 +1,7 @@
+"""The encoder step (coarse -> select -> refine, one 32-frame CUDA graph) on bf16 frames vs
+on 8-bit frames converted on the device by cfd_frames_from_u8: selection counts, finite
+outputs and step time (the work is fixed by k, so the times must match).
+python tools/ingest_timing.py"""
 import sys, torch, numpy as np
 sys.path.insert(0, '/root/repo')
 import cfd_inputs as ci
