@@ -2,8 +2,12 @@
 on 8-bit frames converted on the device by cfd_frames_from_u8: selection counts, finite
 outputs and step time (the work is fixed by k, so the times must match).
 python tools/ingest_timing.py"""
-import sys, torch, numpy as np
-sys.path.insert(0, '/root/repo')
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
 import cfd_inputs as ci
 from paper_2505_23317_b200.api import CFDetrEncoder, bf16_tensor
 cfg = ci.CONFIGS["c640"]; B = 32; k = 100
