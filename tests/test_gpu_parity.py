@@ -327,3 +327,57 @@ def test_split_factor_m3_the_papers_3x3_to_9x9_example():
         assert np.array_equal(ro["mixed_src"][cu[t]:cu[t + 1]].cpu().numpy(), rr["mixed_src"])
         _tol(ro["layer_out"][0, cu[t]:cu[t + 1]].cpu().numpy(), rr["layers"][0], f"m3 task {t} refine")
     enc.close()
+
+
+def test_bench_lanes_concurrent_equal_full_batch_and_oracle():
+    """bench.py's timed configuration: the 32-frame batch as two 16-frame lanes (own
+    encoder context / workspace / stream / CUDA graph) replayed concurrently.  The lanes'
+    packed outputs equal the single 32-frame launch bit for bit, and a frame of each lane
+    matches the oracle (shared-score protocol)."""
+    cfg = ci.CONFIGS["c640"]
+    w = ci.make_weights(cfg, seed=0)
+    B, k = 32, 100
+    imgs_np = ci.make_frames(cfg, B)
+    imgs = bf16_tensor(imgs_np, "cuda")
+    counts = [cfg.n_coarse + 3 * k] * B
+    full = enc_for("c640")
+    co = full.coarse_encode(imgs)
+    sel = full.select_regions(co["scores"], k=[k] * B)
+    ro = full.batch_refine(imgs, co["x0"], sel["sel_idx"], sel["sel_count"], token_counts=counts)
+    torch.cuda.synchronize()
+    lanes = []
+    for f0, f1 in ((0, 16), (16, 32)):
+        e = CFDetrEncoder(cfg, w, max_tasks=16)
+        s = torch.cuda.Stream()
+        im = imgs[f0:f1]
+        ks, cnt = [k] * (f1 - f0), counts[f0:f1]
+        with torch.cuda.stream(s):
+            c_ = e.coarse_encode(im, stream=s)
+            s_ = e.select_regions(c_["scores"], k=ks, stream=s)
+            r_ = e.batch_refine(im, c_["x0"], s_["sel_idx"], s_["sel_count"], token_counts=cnt, stream=s)
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                e.coarse_encode(im, out=c_, stream=s)
+                e.select_regions(c_["scores"], k=ks, out=s_, stream=s)
+                e.batch_refine(im, c_["x0"], s_["sel_idx"], s_["sel_count"], token_counts=cnt, out=r_, stream=s)
+        s.synchronize()
+        r_["y"].zero_()
+        lanes.append((e, s, g, c_, r_, f0, f1))
+    torch.cuda.synchronize()
+    for _, s, g, *_ in lanes:  # concurrent replays
+        with torch.cuda.stream(s):
+            g.replay()
+    torch.cuda.synchronize()
+    for e, s, g, c_, r_, f0, f1 in lanes:
+        t0, t1 = sum(counts[:f0]), sum(counts[:f1])
+        assert torch.equal(r_["y"][:t1 - t0], ro["y"][t0:t1])
+        assert torch.equal(c_["scores"], co["scores"][f0:f1])
+        t = f0 + 5
+        oc = O.coarse_encode(cfg, w, [imgs_np[t]])[0]
+        s_gpu = co["scores"][t].cpu().numpy()
+        rr = O.refine_encode(cfg, w, imgs_np[t], oc["x0"], O.select_topk(s_gpu, k))
+        cu = ro["cu_seqlens"].cpu().numpy()
+        _tol(ro["y"][cu[t]:cu[t + 1]].cpu().numpy(), rr["y"], f"lane frame {t} refine output")
+        e.close()
