@@ -95,6 +95,9 @@ int32_t cfdx_probe_count(int32_t kind);
  *          slower with two concurrent pipelines: 74 SMs 1.514, 100 1.399, 148 1.393 ms)
  *   key 18 balanced persistent grids: the fewest CTAs with the same number of rounds (1) /
  *          min(units, SMs) (0, default; measured neutral with two pipelines, 1 % slower alone)
+ *   key 19 fused O-projection keeps x1 = x + o W_o + b_o in TMEM and the MLP's MMA2s
+ *          accumulate onto it, so x1 is neither stored nor re-read (1, default) / x1 stored
+ *          and the final epilogue reads it back (0)
  * Other keys / values: CFD_E_ARG. */
 cfd_status cfdx_set_option(int32_t key, int32_t value);
 

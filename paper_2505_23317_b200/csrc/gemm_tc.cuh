@@ -229,7 +229,10 @@ struct ResidLnArgs {
 // LNT: the LayerNorm output goes to TMEM instead of memory — bf16 pairs of the row's columns
 // (col_base + 2i, +1) at column ln_tmem + i of this warp's lanes (the A-operand layout of a
 // TS-form MMA over the normalised row), used by the fused O-projection + MLP kernel.
-template <int CH, bool LN, bool LNT = false>
+// LOADX = false (LN only): the accumulator already holds x_old (an MMA accumulated onto it),
+//   so x_new = acc + bias and x is not read; dead rows (>= M) are stored as zeros.
+// STOREX = false (LN only): x_new is kept in the accumulator's TMEM columns only (not stored).
+template <int CH, bool LN, bool LNT = false, bool LOADX = true, bool STOREX = true>
 __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtensorMap& tmX, const CUtensorMap& tmLN,
                                              const ResidStage& st, uint32_t tbase, int row0, int col_base, int M,
                                              const float* bias_s, const float* lng_s, const float* lnb_s,
@@ -257,10 +260,13 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
     *st.xph ^= 1u << b;
   };
   auto row_ptr = [&](int b, int q) { return reinterpret_cast<float4*>(buf(b) + r * 128 + ((q ^ (r & 7)) << 4)); };
+  static_assert(LN || STOREX, "STOREX = false is a LayerNorm-path option");
   float mean = 0.f, rstd = 0.f;
-  load(0, 0);
-  if (CH > 1) load(1, 1);
-  if (NB == 3 && CH > 2) load(2, 2);
+  if (LOADX) {
+    load(0, 0);
+    if (CH > 1) load(1, 1);
+    if (NB == 3 && CH > 2) load(2, 2);
+  }
   mbar_wait(tfull_bar, tfull_parity);
   tc_fence_after();
   if constexpr (LN) {
@@ -273,17 +279,33 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
       const int b = c % NB;
       uint32_t a[32];
       tmem_ld32(tbase + c * 32, a);
-      wait(b);
+      if (LOADX) wait(b);
+      if (!LOADX && STOREX && c >= NB) {  // the TMA store that last read buffer b is done reading
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+      }
       tmem_wait_ld();
       const int col0 = col_base + c * 32;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         float4* px = row_ptr(b, q);
-        float4 x = *px;
         const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + 4 * q);
-        const float v0 = x.x + (__uint_as_float(a[4 * q]) + bb.x), v1 = x.y + (__uint_as_float(a[4 * q + 1]) + bb.y);
-        const float v2 = x.z + (__uint_as_float(a[4 * q + 2]) + bb.z), v3 = x.w + (__uint_as_float(a[4 * q + 3]) + bb.w);
-        if (live) *px = make_float4(v0, v1, v2, v3);
+        float v0, v1, v2, v3;
+        if constexpr (LOADX) {
+          const float4 x = *px;
+          v0 = x.x + (__uint_as_float(a[4 * q]) + bb.x);
+          v1 = x.y + (__uint_as_float(a[4 * q + 1]) + bb.y);
+          v2 = x.z + (__uint_as_float(a[4 * q + 2]) + bb.z);
+          v3 = x.w + (__uint_as_float(a[4 * q + 3]) + bb.w);
+          if (STOREX && live) *px = make_float4(v0, v1, v2, v3);
+        } else {
+          v0 = __uint_as_float(a[4 * q]) + bb.x;
+          v1 = __uint_as_float(a[4 * q + 1]) + bb.y;
+          v2 = __uint_as_float(a[4 * q + 2]) + bb.z;
+          v3 = __uint_as_float(a[4 * q + 3]) + bb.w;
+          if (!live) v0 = v1 = v2 = v3 = 0.f;
+          if (STOREX) *px = make_float4(v0, v1, v2, v3);
+        }
         s1 += (v0 + v1) + (v2 + v3);
         s2 += (v0 * v0 + v1 * v1) + (v2 * v2 + v3 * v3);
         a[4 * q] = __float_as_uint(v0);
@@ -293,14 +315,20 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
       }
       tmem_st16(tbase + c * 32, *reinterpret_cast<const uint32_t(*)[16]>(a));
       tmem_st16(tbase + c * 32 + 16, *reinterpret_cast<const uint32_t(*)[16]>(a + 16));
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) {
-        tma_store_2d(&tmX, buf(b), col0, row0);
-        bulk_commit();
+      if constexpr (STOREX) {
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmX, buf(b), col0, row0);
+          bulk_commit();
+        }
       }
-      if (c + NB < CH) {
-        if (lane == 0) bulk_wait_read0();  // buffer b is reloaded next
+      if (LOADX && c + NB < CH) {
+        if (STOREX) {
+          if (lane == 0) bulk_wait_read0();  // buffer b is reloaded next
+        } else {
+          fence_proxy_async();  // this warp's generic reads of buffer b before the TMA overwrite
+        }
         __syncwarp();
         load(c + NB, b);
       }
@@ -371,7 +399,11 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
       const int b = c % NB;
       uint32_t a[32];
       tmem_ld32(tbase + c * 32, a);
-      wait(b);
+      if (LOADX) wait(b);
+      if (!LOADX && c >= NB) {  // the TMA store that last read buffer b is done reading
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+      }
       tmem_wait_ld();
       if (c + 1 == CH) {
         tc_fence_before();
@@ -382,14 +414,20 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         float4* px = row_ptr(b, q);
-        float4 x = *px;
         const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + 4 * q);
-        if (live) {
-          x.x += __uint_as_float(a[4 * q]) + bb.x;
-          x.y += __uint_as_float(a[4 * q + 1]) + bb.y;
-          x.z += __uint_as_float(a[4 * q + 2]) + bb.z;
-          x.w += __uint_as_float(a[4 * q + 3]) + bb.w;
-          *px = x;
+        if constexpr (LOADX) {
+          float4 x = *px;
+          if (live) {
+            x.x += __uint_as_float(a[4 * q]) + bb.x;
+            x.y += __uint_as_float(a[4 * q + 1]) + bb.y;
+            x.z += __uint_as_float(a[4 * q + 2]) + bb.z;
+            x.w += __uint_as_float(a[4 * q + 3]) + bb.w;
+            *px = x;
+          }
+        } else {
+          *px = live ? make_float4(__uint_as_float(a[4 * q]) + bb.x, __uint_as_float(a[4 * q + 1]) + bb.y,
+                                   __uint_as_float(a[4 * q + 2]) + bb.z, __uint_as_float(a[4 * q + 3]) + bb.w)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
       fence_proxy_async();
@@ -398,7 +436,7 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
         tma_store_2d(&tmX, buf(b), col0, row0);
         bulk_commit();
       }
-      if (c + NB < CH) {
+      if (LOADX && c + NB < CH) {
         if (lane == 0) bulk_wait_read0();  // buffer b is reloaded next
         __syncwarp();
         load(c + NB, b);

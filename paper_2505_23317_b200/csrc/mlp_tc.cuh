@@ -59,6 +59,10 @@ struct MlpParams {
   const float* bo;
   const float* ln2_g;
   const float* ln2_b;
+  // OPJ only: keep x1 = x + o W_o + b_o in the acc2 TMEM columns instead of storing it; the
+  // MLP's MMA2s then accumulate onto it and the final epilogue computes x2 = acc2 + b2 without
+  // reading x (saves the x1 store + reload: 2 x 128 KB per tile)
+  int keep_x1;
 };
 
 constexpr int MLP_THREADS = 320;  // TMA warp, MMA warp, 8 epilogue warps
@@ -332,8 +336,9 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
           for (int k = 0; k < 4; ++k) {
             const uint64_t ad = make_smem_desc(h_base + kb * 16384 + k * 32, 16, 1024, kLayoutSW128);
             const uint64_t bd = make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128);
-            if constexpr (PAIR) mma_ss_2sm(tmem + ACC2, ad, bd, idesc2, (j | kb | k) != 0);
-            else mma_ss(tmem + ACC2, ad, bd, idesc2, (j | kb | k) != 0);
+            const bool acc = (OPJ && p.keep_x1) || (j | kb | k) != 0;  // keep_x1: onto x1
+            if constexpr (PAIR) mma_ss_2sm(tmem + ACC2, ad, bd, idesc2, acc);
+            else mma_ss(tmem + ACC2, ad, bd, idesc2, acc);
           }
           give();
           if constexpr (!PAIR) give();
@@ -414,9 +419,14 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         const ResidLnArgs la{D, p.ln_cap, p.ln_eps};
         const uint32_t tb = tmem + lane_off + ACC2 + half * 128;
         if (et == 0) MLP_TR(it, 38);
-        resid_ln_tma<4, true, true>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M, bo_s, g2_s,
-                                    b2ln_s, ln_stats, quarter, half, lane, ao_full, it & 1, a2_empty, -1,
-                                    tmem + lane_off + HT + half * 64);
+        if (p.keep_x1)
+          resid_ln_tma<4, true, true, true, false>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M,
+                                                   bo_s, g2_s, b2ln_s, ln_stats, quarter, half, lane, ao_full, it & 1,
+                                                   a2_empty, -1, tmem + lane_off + HT + half * 64);
+        else
+          resid_ln_tma<4, true, true>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M, bo_s, g2_s,
+                                      b2ln_s, ln_stats, quarter, half, lane, ao_full, it & 1, a2_empty, -1,
+                                      tmem + lane_off + HT + half * 64);
         if (et == 0) MLP_TR(it, 39);
         tmem_wait_st();
         tc_fence_before();
@@ -522,7 +532,15 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         const ResidStage st{hslice, S::H_BYTES, lnb, 0, xbar + 3 * e, &xph, smem + S::XSTG_OFF + e * 4096};
         const ResidLnArgs la{D, p.ln_cap, p.ln_eps};
         const uint32_t tb = tmem + lane_off + ACC2 + half * 128;
-        if (do_ln)
+        if (OPJ && p.keep_x1) {  // acc2 = x1 + MLP(x1): x2 = acc2 + b2, x not read
+          if (do_ln)
+            resid_ln_tma<4, true, false, false>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M, b2_s,
+                                                lng_s, lnb_s, ln_stats, quarter, half, lane, a2_full, it & 1, a2_empty);
+          else
+            resid_ln_tma<4, false, false, false>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M,
+                                                 b2_s, lng_s, lnb_s, ln_stats, quarter, half, lane, a2_full, it & 1,
+                                                 a2_empty);
+        } else if (do_ln)
           resid_ln_tma<4, true>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M, b2_s, lng_s, lnb_s,
                                 ln_stats, quarter, half, lane, a2_full, it & 1, a2_empty, PAIR && rank ? 0 : -1);
         else
