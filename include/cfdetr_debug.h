@@ -98,6 +98,9 @@ int32_t cfdx_probe_count(int32_t kind);
  *   key 19 fused O-projection keeps x1 = x + o W_o + b_o in TMEM and the MLP's MMA2s
  *          accumulate onto it, so x1 is neither stored nor re-read (1, default) / x1 stored
  *          and the final epilogue reads it back (0)
+ *   key 20 with key 19 = 1: the epilogue warps load x into acc2 while o / W_o stream in and
+ *          MMA_o accumulates onto it, so the residual pass does not wait for x (1) / 0 (default:
+ *          the x load competes with o / W_o for the SM's ingress, MLP launch 52.7 -> 54.1 us)
  * Other keys / values: CFD_E_ARG. */
 cfd_status cfdx_set_option(int32_t key, int32_t value);
 

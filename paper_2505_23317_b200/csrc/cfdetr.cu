@@ -290,6 +290,7 @@ int g_attn_dyn = 0;     // v4 dynamic item claiming through a work counter (opti
 int g_fused_mlp = 1;  // fused MLP kernel (d == 256) instead of two GEMM launches
 int g_staged_epi = 1; // TMA-staged residual + LayerNorm epilogue for the O-projection
 int g_mlp_cluster = 0; // fused MLP as CTA pairs (cta_group::2)
+int g_preload_x = 0;   // with option 19: x loaded into acc2 before MMA_o (option 20; measured slower)
 int g_keep_x1 = 1;     // fused O-projection: x1 stays in TMEM, MMA2 accumulates onto it (option 19)
 int g_fuse_oproj = 1;  // O-projection + residual + LN2 inside the fused MLP kernel (option 11)
 
@@ -607,6 +608,7 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
     MlpParams mp{};
     mp.M = M_static; mp.m_dev = m_dev; mp.F = F; mp.b1 = L.b_1; mp.b2 = L.b_2; mp.x = x; mp.ln_eps = g.ln_eps;
     mp.bo = L.b_o; mp.ln2_g = L.ln2_g; mp.ln2_b = L.ln2_b; mp.keep_x1 = g_keep_x1;
+    mp.preload_x = g_keep_x1 && g_preload_x;
     mp.ln_cap = w.rows_cap;
     if (l + 1 < g.n_layers) {
       const LayerDev& Ln = c->layers[l + 1];
@@ -794,6 +796,9 @@ cfd_status cfdx_set_option(int32_t key, int32_t value) {
       return CFD_OK;
     case 19:
       g_keep_x1 = value ? 1 : 0;
+      return CFD_OK;
+    case 20:
+      g_preload_x = value ? 1 : 0;
       return CFD_OK;
     case 6:
       if (value != 4 && value != 6 && value != 8) return CFD_E_ARG;

@@ -57,9 +57,9 @@ def test_tuning_option_validation_without_gpu(lib):
     assert lib.cfdx_set_option(0, 7) == -1 and lib.cfdx_set_option(0, 0) == -1
     assert lib.cfdx_set_option(1, 3) == -1 and lib.cfdx_set_option(1, 14) == -1 and lib.cfdx_set_option(1, -2) == -1
     assert lib.cfdx_set_option(5, -3) == -1 and lib.cfdx_set_option(6, 5) == -1
-    assert lib.cfdx_set_option(8, 0) == -1 and lib.cfdx_set_option(20, 0) == -1
+    assert lib.cfdx_set_option(8, 0) == -1 and lib.cfdx_set_option(21, 0) == -1
     for key, val in ((0, 3), (0, 6), (1, 12), (2, 0), (3, 0), (4, 1), (5, 300), (6, 8), (7, 0), (9, 1), (10, 1),
-                     (11, 0), (19, 0)):
+                     (11, 0), (19, 0), (20, 0)):
         assert lib.cfdx_set_option(key, val) == 0
     for key, val in ((0, 4), (1, 4), (2, 1), (3, 1), (4, 0), (5, 0), (6, 4), (7, 1), (9, 0), (10, 0),
                      (11, 1)):  # restore the defaults
