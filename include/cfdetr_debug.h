@@ -89,8 +89,11 @@ int32_t cfdx_probe_count(int32_t kind);
  *          tensor map (1, default; d = 256, 3Pc % 32 == 0) instead of im2col + GEMM (0)
  *   key 15 layer-0 LN1 of the coarse pass fused into the coarse embed epilogue (1, default)
  *          instead of a standalone LayerNorm launch (0)
- *   key 16 attention v4 dynamic item claiming through a work counter (1) instead of the static
- *          round-robin (0, default: the graph-replayed step measured 1.504 vs 1.471 ms)
+ *   key 16 attention v4 dynamic item claiming through a work counter (1, default) instead of
+ *          the static round-robin (0).  The counter pair [claims, finished CTAs] is reset by the
+ *          launch's last CTA (no memset launch): one pipeline 1.433 -> 1.415 ms per step, two
+ *          lanes neutral (1.362 / 1.365 ms; the other lane already fills the tails).  (With a
+ *          memset per launch it measured slower: 1.504 vs 1.471 ms.)
  *   key 17 cap on the persistent kernels' grid size (0 = every SM, default; caps measured
  *          slower with two concurrent pipelines: 74 SMs 1.514, 100 1.399, 148 1.393 ms)
  *   key 18 balanced persistent grids: the fewest CTAs with the same number of rounds (1) /

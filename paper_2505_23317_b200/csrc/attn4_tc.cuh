@@ -169,6 +169,16 @@ __global__ void __launch_bounds__(ATTN4_THREADS, 1)
         item_slot[slot] = item;
         if (item >= total) {
           mbar_arrive(&q_full[slot]);
+          if (p.work_counter) {
+            // self-resetting claim counter: the last CTA to make its final claim zeroes
+            // [claims, finished] for the next launch on this stream (no memset launch)
+            __threadfence();
+            if (atomicAdd(p.work_counter + 1, 1) == (int)gridDim.x - 1) {
+              p.work_counter[0] = 0;
+              p.work_counter[1] = 0;
+              __threadfence();
+            }
+          }
           break;
         }
         int t, qp, h;

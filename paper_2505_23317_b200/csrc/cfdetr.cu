@@ -286,7 +286,7 @@ int g_attn_stages = 4;  // v4 K/V ring depth (128-key stages): 4, 6 or 8
 int g_attn_token = 0;   // v4 exp-phase token ring (option 9)
 int g_attn_split = 0;   // v4 split MMA accumulator chains (option 10)
 int g_attn_qmajor = 1;  // v4 q-triple-major item order for equal-length batches (option 12)
-int g_attn_dyn = 0;     // v4 dynamic item claiming through a work counter (option 16; measured slower in graphs)
+int g_attn_dyn = 1;     // v4 dynamic item claiming through a self-resetting work counter (option 16)
 int g_fused_mlp = 1;  // fused MLP kernel (d == 256) instead of two GEMM launches
 int g_staged_epi = 1; // TMA-staged residual + LayerNorm epilogue for the O-projection
 int g_mlp_cluster = 0; // fused MLP as CTA pairs (cta_group::2)
@@ -587,9 +587,8 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   ap.scale_log2 = 1.4426950408889634f / std::sqrt((float)c->dh);
   ap.stagger = g_attn_stagger;
   ap.uniform_n = g_attn_qmajor ? uniform_n : 0;
-  if (g_attn_dyn) {  // dynamic item claiming: the ctx's counter word (err[2]), zeroed per launch
-    ap.work_counter = c->err + 2;
-    CFD_CUDA(cudaMemsetAsync(ap.work_counter, 0, sizeof(int), s));
+  if (g_attn_dyn) {  // dynamic item claiming: the ctx's words err[2] (claims), err[3] (finished CTAs),
+    ap.work_counter = c->err + 2;  // zeroed at create and reset by the kernel's last CTA
   }
   CFD_CUDA(launch_attention(tq, ap, max_qtiles, g.n_heads, T, s));
   if (want_lse && scores) {
@@ -1335,10 +1334,12 @@ cfd_status cfdx_attention(int32_t T, const int32_t* cu, int32_t max_seqlen, int3
   ap.scale_log2 = 1.4426950408889634f / std::sqrt(32.0f);
   ap.stagger = g_attn_stagger;
   if (g_attn_dyn) {
-    static int* counter = nullptr;  // debug entry point: one process-wide counter word
-    if (!counter && cudaMalloc(&counter, sizeof(int)) != cudaSuccess) return CFD_E_CUDA;
+    static int* counter = nullptr;  // debug entry point: one process-wide [claims, finished] pair
+    if (!counter) {
+      if (cudaMalloc(&counter, 2 * sizeof(int)) != cudaSuccess) return CFD_E_CUDA;
+      CFD_CUDA(cudaMemsetAsync(counter, 0, 2 * sizeof(int), static_cast<cudaStream_t>(stream)));
+    }
     ap.work_counter = counter;
-    CFD_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), static_cast<cudaStream_t>(stream)));
   }
   CFD_CUDA(launch_attention(tq, ap, (max_seqlen + ATTN_BQ - 1) / ATTN_BQ, nh, T, static_cast<cudaStream_t>(stream)));
   return CFD_OK;
