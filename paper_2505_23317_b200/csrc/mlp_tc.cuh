@@ -88,7 +88,8 @@ __device__ unsigned long long g_mlp_trace[MLP_TRACE_WORDS];
 #else
 #define MLP_TR(it_, ev_) do { } while (0)
 #endif
-constexpr int MLP_SLOTS = 6;  // 8 measured no faster; the 32 KB go to a third x staging buffer per warp
+constexpr int MLP_SLOTS = 8;  // with x1 kept in TMEM (option 19) the third x staging buffer is worth less
+                              // than two more ring slots (MLP launch 52.7 -> 52.2 us; before: 6 slots)
 
 template <int D>
 struct MlpSmem {
@@ -105,8 +106,8 @@ struct MlpSmem {
   // one 2 KB LN output buffer per warp lives here
   // ... | b_o [D] | ln2 g [D] | ln2 b [D] (OPJ)
   static constexpr int LNSTG_OFF = ((PAR_OFF + (GEMM_MAX_N + 6 * D) * 4 + 1023) / 1024) * 1024;
-  static constexpr int XSTG_OFF = LNSTG_OFF + 8 * 2048;    // [8 warps] third 4 KB x staging buffer
-  static constexpr int TOTAL = 1024 + XSTG_OFF + 8 * 4096;
+  static constexpr int XSTG_OFF = LNSTG_OFF + 8 * 2048;    // end of the LN staging (no third x buffer)
+  static constexpr int TOTAL = 1024 + XSTG_OFF;
 };
 
 // CL = 2: CTA-pair kernel (2-CTA clusters, tcgen05 cta_group::2).  The single-CTA kernel is
@@ -421,7 +422,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         //      Staging: this warp's 4 KB slices of H[0] / H[1] (free until GELU(0)).
         const int e = warp - 2;
         uint8_t* hslice = smem + S::H_OFF + half * 16384 + quarter * 4096;
-        const ResidStage st{hslice, S::H_BYTES, nullptr, 0, xbar + 3 * e, &xph, smem + S::XSTG_OFF + e * 4096};
+        const ResidStage st{hslice, S::H_BYTES, nullptr, 0, xbar + 3 * e, &xph, nullptr};
         const ResidLnArgs la{D, p.ln_cap, p.ln_eps};
         const uint32_t tb = tmem + lane_off + ACC2 + half * 128;
         if (p.preload_x) {
@@ -580,7 +581,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         const int e = warp - 2;
         uint8_t* hslice = smem + S::H_OFF + half * 16384 + quarter * 4096;
         uint8_t* lnb = smem + S::LNSTG_OFF + e * 2048;
-        const ResidStage st{hslice, S::H_BYTES, lnb, 0, xbar + 3 * e, &xph, smem + S::XSTG_OFF + e * 4096};
+        const ResidStage st{hslice, S::H_BYTES, lnb, 0, xbar + 3 * e, &xph, nullptr};
         const ResidLnArgs la{D, p.ln_cap, p.ln_eps};
         const uint32_t tb = tmem + lane_off + ACC2 + half * 128;
         if (OPJ && p.keep_x1) {  // acc2 = x1 + MLP(x1): x2 = acc2 + b2, x not read
