@@ -280,8 +280,8 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
       uint32_t a[32];
       tmem_ld32(tbase + c * 32, a);
       if (LOADX) wait(b);
-      if (!LOADX && STOREX && c >= NB) {  // the TMA store that last read buffer b is done reading
-        if (lane == 0) bulk_wait_read0();
+      if (!LOADX && STOREX && c >= NB) {  // the TMA store of chunk c - NB (buffer b) is done reading
+        if (lane == 0) { if (NB == 3) bulk_wait_read2(); else bulk_wait_read1(); }
         __syncwarp();
       }
       tmem_wait_ld();
@@ -400,8 +400,8 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
       uint32_t a[32];
       tmem_ld32(tbase + c * 32, a);
       if (LOADX) wait(b);
-      if (!LOADX && c >= NB) {  // the TMA store that last read buffer b is done reading
-        if (lane == 0) bulk_wait_read0();
+      if (!LOADX && c >= NB) {  // the TMA store of chunk c - NB (buffer b) is done reading
+        if (lane == 0) { if (NB == 3) bulk_wait_read2(); else bulk_wait_read1(); }
         __syncwarp();
       }
       tmem_wait_ld();
