@@ -523,7 +523,7 @@ def gpu_arm(args):
             ks_l, cnt_l = ks[f0:f1], counts[f0:f1]
             n_out_l = sum(cnt_l)
             sets = []
-            for bset in range(2):
+            for _bset in range(2):
                 d_in = torch.empty(h_in.shape, dtype=h_in.dtype, device=dev)
                 d_im = torch.empty((f1 - f0, *imgs.shape[1:]), dtype=imgs.dtype, device=dev)
                 o_co, o_sel, o_ro = {}, {}, {}
