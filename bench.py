@@ -172,7 +172,8 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", os.environ.get("CFD_BENCH_CLOCK_MS", "100")], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except Exception:
@@ -375,6 +376,10 @@ def gpu_arm(args):
         dist.barrier()
     torch.cuda.synchronize()
     with torch.cuda.stream(stream):
+        # hold the GPU (outside the timed steps) while the host enqueues all K steps, so a
+        # host-side hiccup (GC, the clock-sampler thread) can never open an idle gap inside
+        # a step's events: the device time measured is the device's alone
+        torch.cuda._sleep(int(1e6) * max(20, min(args.steps, 500)))
         for i in range(args.steps):
             flush.zero_()
             starts[i].record(stream)
@@ -641,7 +646,7 @@ def gpu_arm(args):
                "roofline": roofline, "attention_roofline": attn_roof, "attention_exp_roofline": attn_exp_roof,
                "cpu_baseline": cpu, "e2e": e2e, "e2e_bf16_input": e2e_bf16,
                "gpu_launches": launches_per_step * args.steps, "clocks": clk, "kernels": kernels,
-               "step_ms_min": round(min(step_ms), 4), "check": check,
+               "step_ms_min": round(min(step_ms), 4), "step_ms_max": round(max(step_ms), 4), "check": check,
                "impl": "ours", "library": lib.cfd_version().decode()}
         print(json.dumps(out), flush=True)
     if world > 1:
