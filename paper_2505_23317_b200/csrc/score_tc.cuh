@@ -127,13 +127,17 @@ __global__ void __launch_bounds__(SCORE_THREADS, 1)
     const float c = p.scale_log2;
     float* xch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [128] half-1 partial sums
     float acc = 0.f;
+    // row LSEs of iteration it (head h, query tile qt), staged one iteration ahead so the
+    // global load latency is hidden behind the previous iteration's exp pass
+    auto lse_of = [&](int it) {
+      const int h = it / nq, q = (it % nq) * 128 + r;
+      return (q < Nc) ? __ldg(p.lse + (size_t)h * p.lse_ld + row0 + q) * 1.4426950408889634f : 0.f;
+    };
+    if (half == 0) lse_s[r] = lse_of(0);
     for (int it = 0; it < total; ++it) {
-      const int h = it / nq, qt = it % nq;
-      if (half == 0) {
-        const int q = qt * 128 + r;
-        lse_s[(it & 1) * 128 + r] = (q < Nc) ? __ldg(p.lse + (size_t)h * p.lse_ld + row0 + q) * 1.4426950408889634f : 0.f;
-      }
-      named_bar_sync(1, 256);
+      const int qt = it % nq;
+      named_bar_sync(1, 256);  // lse_s[it & 1] complete; everyone is done with lse_s[(it + 1) & 1]
+      const float lse_next = (half == 0 && it + 1 < total) ? lse_of(it + 1) : 0.f;
       mbar_wait(&s_full[it & 1], (it >> 1) & 1);
       tc_fence_after();
       uint32_t sr[64];
@@ -158,6 +162,7 @@ __global__ void __launch_bounds__(SCORE_THREADS, 1)
         p3 += (i + 3 < nvq) ? e3 : 0.f;
       }
       acc += (p0 + p1) + (p2 + p3);
+      if (half == 0 && it + 1 < total) lse_s[((it + 1) & 1) * 128 + r] = lse_next;
     }
     // fixed-order combination of the two column halves (deterministic)
     if (half == 1) xch[r] = acc;
