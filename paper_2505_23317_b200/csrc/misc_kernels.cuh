@@ -68,12 +68,24 @@ __global__ void layernorm_kernel(const float* __restrict__ x, const float* __res
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     const float rstd = rsqrtf(ss * (1.0f / D) + eps);
+    float gv[VPT], bv[VPT];
+    if constexpr (VPT % 4 == 0) {  // vector loads of this lane's gamma / beta
+#pragma unroll
+      for (int i = 0; i < VPT; i += 4) {
+        const float4 gq = __ldg(reinterpret_cast<const float4*>(g + lane * VPT + i));
+        const float4 bq = __ldg(reinterpret_cast<const float4*>(b + lane * VPT + i));
+        gv[i] = gq.x; gv[i + 1] = gq.y; gv[i + 2] = gq.z; gv[i + 3] = gq.w;
+        bv[i] = bq.x; bv[i + 1] = bq.y; bv[i + 2] = bq.z; bv[i + 3] = bq.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) { gv[i] = __ldg(g + lane * VPT + i); bv[i] = __ldg(b + lane * VPT + i); }
+    }
     uint32_t pk[VPT / 2];
 #pragma unroll
     for (int i = 0; i < VPT; i += 2) {
-      const int col = lane * VPT + i;
-      const float a = (v[i] - mean) * rstd * __ldg(g + col) + __ldg(b + col);
-      const float c = (v[i + 1] - mean) * rstd * __ldg(g + col + 1) + __ldg(b + col + 1);
+      const float a = (v[i] - mean) * rstd * gv[i] + bv[i];
+      const float c = (v[i + 1] - mean) * rstd * gv[i + 1] + bv[i + 1];
       __nv_bfloat162 t2 = __floats2bfloat162_rn(a, c);
       pk[i / 2] = *reinterpret_cast<uint32_t*>(&t2);
     }
