@@ -17,10 +17,15 @@ Parity status (see tests/test_oracle_pins.py):
   embed ............... pinned (tied-mode pooling closed form, torch linear)
   layer_norm / gelu ... pinned (torch F.layer_norm, torch F.gelu, closed forms)
   encoder_layer ....... pinned (torch.nn.TransformerEncoderLayer, norm_first, fp64)
+  encoder (L layers) .. pinned (torch.nn.TransformerEncoder, L = 6, six distinct weight sets:
+                        every per-layer output, so the layer order is fixed)
   attention_probs ..... pinned (torch MHA weights, row sums, 1-token/equal-key forms)
-  criticality_score ... pinned (torch MHA head-averaged weights; sum=1; constant image)
-  select_topk/thresh .. pinned (brute force over all C(16,4) subsets; NaN/+-0 cases)
-  merge / gather ...... pinned (offset closed form; k=0 == coarse; k=Nc == fine pass)
+  criticality_score ... pinned (torch MHA head-averaged weights, also through a hook on layer
+                        score_layer of the L = 6 torch stack; sum=1; constant image)
+  select_topk/thresh .. pinned (brute force over all C(16,4) subsets; NaN/+-0 cases;
+                        hand-written index sets at s == tau ties for the strict threshold)
+  merge / gather ...... pinned (offset closed form; k=0 == coarse; k=Nc == fine pass; A_f rows
+                        == an independent reshape tiling of the task's frame)
   batch_refine ........ pinned (== per-task refine; cu_seqlens closed form)
   hardness_gate ....... pinned (vectorised fp64 mean; all-critical / single-query cases)
   box_cell_scores ..... pinned (brute-force pixel-mask rasterisation; full-image box)

@@ -186,6 +186,73 @@ def test_single_token_attention_output_is_v():
     np.testing.assert_allclose(y, ref, rtol=0, atol=1e-12)
 
 
+def _torch_stack_with_hooks(layers, d, nh, score_layer):
+    """torch.nn.TransformerEncoder(num_layers=L, norm_first, gelu) in fp64 with the given
+    per-layer weights; returns a closure x -> (y, [per-layer outputs], score column means at
+    `score_layer`) where the per-layer outputs come from forward hooks on encoder.layers[l]
+    and the score from the head-averaged attention weights of encoder.layers[score_layer]
+    (torch MHA need_weights on the LN1 output that layer's self-attention receives)."""
+    L = len(layers)
+    proto = torch.nn.TransformerEncoderLayer(d, nh, 4 * d, dropout=0.0, activation="gelu", layer_norm_eps=1e-6,
+                                             batch_first=True, norm_first=True, dtype=torch.float64)
+    stack = torch.nn.TransformerEncoder(proto, num_layers=L, enable_nested_tensor=False)
+    for l, lw in enumerate(layers):
+        src = _torch_layer(lw, d, nh, 4 * d)
+        stack.layers[l].load_state_dict(src.state_dict())
+    stack.eval()
+    outs, attn_in = [], []
+    for l in range(L):
+        stack.layers[l].register_forward_hook(lambda m, a, o: outs.append(o.detach()[0].numpy().copy()))
+    stack.layers[score_layer].self_attn.register_forward_pre_hook(lambda m, a: attn_in.append(a[0].detach()))
+
+    def run(x):
+        outs.clear()
+        attn_in.clear()
+        # grad enabled (no torch.no_grad) keeps torch off its fused inference fast path, so
+        # the module hooks fire on the plain layer code
+        y = stack(torch.tensor(x)[None]).detach()[0].numpy()
+        h = attn_in[0]
+        _, avg = stack.layers[score_layer].self_attn(h, h, h, need_weights=True, average_attn_weights=True)
+        return y, list(outs), avg.detach()[0].numpy().mean(axis=0)
+    return run
+
+
+@pytest.mark.parametrize("d,nh,N,score_layer", [(64, 2, 21, 5), (64, 2, 21, 2), (256, 8, 40, 5)])
+def test_encoder_L6_matches_torch_transformer_encoder(d, nh, N, score_layer):
+    """O.encoder at L = 6 (§V-A "six encoder/decoder layers"; the stack of global
+    self-attention blocks of PAPER.md:120-122 §II-A) against torch.nn.TransformerEncoder with
+    the same six distinct weight sets: every per-layer output (so the layer ORDER is pinned:
+    the blocks do not commute) and the criticality score taken from the attention map of layer
+    `score_layer` (so probs_at is pinned: a different layer's map gives a different score)."""
+    cfg = ci.ModelConfig(64, 64, 32, 16, d, nh, 6, 4 * d, score_layer)
+    w = ci.make_weights(cfg, seed=17)
+    x = _rng(18).normal(size=(N, d))
+    y, outs, probs = O.encoder(x, w["layers"], nh, 1e-6, probs_at=score_layer)
+    yr, outs_r, s_r = _torch_stack_with_hooks(w["layers"], d, nh, score_layer)(x)
+    assert len(outs) == len(outs_r) == 6
+    for l in range(6):
+        np.testing.assert_allclose(outs[l], outs_r[l], rtol=0, atol=1e-10, err_msg=f"layer {l}")
+    np.testing.assert_allclose(y, yr, rtol=0, atol=1e-10)
+    assert len(probs) == nh
+    np.testing.assert_allclose(O.criticality_score(probs), s_r, rtol=0, atol=1e-13)
+
+
+def test_coarse_encode_L6_scores_come_from_the_configured_score_layer():
+    """O.coarse_encode end to end at L = 6: its per-layer outputs and scores against the torch
+    stack fed the (separately pinned) patch embedding, for score_layer = L-1 (reading R15) and
+    for another layer, so a coarse_encode that ignored cfg.score_layer fails one of them."""
+    for sl in (5, 1):
+        cfg = ci.ModelConfig(128, 128, 32, 16, 64, 2, 6, 256, sl)
+        w = ci.make_weights(cfg, seed=19)
+        img = ci.make_frame(128, 128, 23)
+        out = O.coarse_encode(cfg, w, [img])[0]
+        x0 = O.patch_embed(O.patchify(O.as_f64_image(img), 32), w["w_embed_c"], w["b_embed_c"], w["pe_c"])
+        yr, outs_r, s_r = _torch_stack_with_hooks(w["layers"], 64, 2, sl)(x0)
+        for l in range(6):
+            np.testing.assert_allclose(out["layers"][l], outs_r[l], rtol=0, atol=1e-10)
+        np.testing.assert_allclose(out["scores"], s_r, rtol=0, atol=1e-13)
+
+
 def test_encoder_permutation_equivariance():
     d, nh = 64, 2
     cfg = ci.ModelConfig(64, 64, 32, 16, d, nh, 2, 4 * d, 1)
@@ -259,6 +326,23 @@ def test_threshold_count():
         assert (np.diff(sel) > 0).all()
 
 
+def test_threshold_is_strict_at_ties():
+    """Reading R7 ("exceeds", PAPER.md:454 [draft]): s == tau is NOT selected.  Hand-written
+    expected index sets (not recomputed from a formula) on vectors that hit tau exactly,
+    including -0 == +0, NaN (never selected) and +-inf."""
+    f = np.float32
+    s = np.array([0.1, 0.5, 0.5, 0.7, np.nan, -0.0, 0.0, np.inf, -np.inf, 0.5000001], f)
+    assert O.select_threshold(s, f(0.5)).tolist() == [3, 7, 9]
+    assert O.select_threshold(s, f(0.0)).tolist() == [0, 1, 2, 3, 7, 9]
+    assert O.select_threshold(s, f(-0.0)).tolist() == [0, 1, 2, 3, 7, 9]
+    assert O.select_threshold(s, np.nextafter(f(0.5), f(0))).tolist() == [1, 2, 3, 7, 9]
+    assert O.select_threshold(s, f(np.inf)).tolist() == []
+    assert O.select_threshold(s, f(-np.inf)).tolist() == [0, 1, 2, 3, 5, 6, 7, 9]
+    eq = np.full(16, f(1 / 16))
+    assert O.select_threshold(eq, f(1 / 16)).tolist() == []                       # all tied at tau
+    assert O.select_threshold(eq, np.nextafter(f(1 / 16), f(0))).tolist() == list(range(16))
+
+
 # --------------------------------------------------------------------------- merge / layout
 def test_gather_layout_closed_forms():
     cfg = TINY
@@ -280,6 +364,35 @@ def test_gather_layout_closed_forms():
                 assert seq[off] == c
     assert len(frow) == len(fidx) == af.shape[0] == m2 * sum(len(s) for s in sels)
     assert (msrc[frow] == -1 - fidx).all()
+
+
+def test_gather_layout_af_rows_are_the_fine_patch_pixels():
+    """A_f row r holds exactly the pixel bytes of fine patch fidx[r] of its own task's frame,
+    against an independent reshape/transpose tiling of the frame (not O.patchify); frow is
+    strictly increasing (fine tokens in packed order) and the m^2 rows of one selected region
+    reassemble that region's coarse patch byte for byte."""
+    cfg = TINY
+    rng = _rng(4)
+    sels = [np.sort(rng.choice(16, size=k, replace=False)) for k in (3, 0, 16, 5)]
+    imgs = [ci.make_frame(128, 128, 70 + t) for t in range(4)]
+    cu, msrc, frow, fidx, af = O.gather_layout(cfg, sels, imgs)
+    P, H, W, m = 16, 128, 128, cfg.m
+
+    def tiles(img, p):
+        return img.reshape(H // p, p, W // p, p, 3).transpose(0, 2, 1, 3, 4).reshape((H // p) * (W // p), -1)
+
+    assert (np.diff(frow) > 0).all()
+    task = np.searchsorted(cu, frow, side="right") - 1
+    for r in range(len(frow)):
+        assert np.array_equal(af[r], tiles(imgs[task[r]], P)[fidx[r]]), r
+    r = 0
+    for t, sel in enumerate(sels):
+        for c in sel:
+            rows = af[r:r + m * m].reshape(m, m, P, P, 3)           # (dy, dx, py, px, ch)
+            patch = rows.transpose(0, 2, 1, 3, 4).reshape(32 * 32 * 3)
+            assert np.array_equal(patch, tiles(imgs[t], 32)[c])
+            r += m * m
+    assert r == len(frow)
 
 
 def test_refine_k0_equals_coarse_pass():
