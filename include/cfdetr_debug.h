@@ -33,10 +33,13 @@ cfd_status cfdx_gemm_resid_ln(int32_t M, int32_t N, int32_t K, const uint16_t *A
 
 /* Varlen multi-head attention over packed qkv [rows, 3d] (q | k | v) with
  * cu_seqlens [T+1]; writes O [rows, d] bf16 and, if lse != NULL, the natural-log
- * row log-sum-exp [nh, lse_ld].  rows_cap = rows allocated in qkv. */
+ * row log-sum-exp [nh, lse_ld].  rows_cap = rows allocated in qkv.  work_counter: a
+ * caller-owned device int[2], zero before the first launch that uses it (each launch's last
+ * CTA resets it), for dynamic item claiming; NULL = static round-robin.  One counter must not
+ * be shared by launches that can run concurrently. */
 cfd_status cfdx_attention(int32_t n_tasks, const int32_t *cu_seqlens, int32_t max_seqlen, int32_t rows_cap,
                           int32_t d_model, int32_t n_heads, const uint16_t *qkv, uint16_t *out, float *lse,
-                          int32_t lse_ld, void *stream);
+                          int32_t lse_ld, int32_t *work_counter, void *stream);
 
 /* Row LayerNorm of fp32 x [M, d] -> bf16 y [M, d] (d in {64,128,256,512}). */
 cfd_status cfdx_layernorm(int32_t M, int32_t d, const float *x, const float *g, const float *b, float eps,
@@ -64,22 +67,19 @@ cfd_status cfdx_gather(cfd_ctx *ctx, int32_t n_tasks, const uint16_t *images, co
 cfd_status cfdx_probe_install(int32_t kind, void *const *h_start, void *const *h_end, int32_t capacity);
 int32_t cfdx_probe_count(int32_t kind);
 
-/* Tuning switches (process-wide, for A/B measurement; every combination is parity-checked):
- *   key 0  attention kernel variant: 1 one query tile per CTA, 2 persistent two-tile
- *          ping-pong with 128-key steps, 3 same with 64-key steps, 4 three query tiles /
- *          warpgroups per CTA (default), 5 two independent warpgroup pairs with self-issued
- *          MMAs, 6 double-buffered S with the row max in the exp pass
- *   key 1  how many of every 16 column pairs variants 2-6 exponentiate with the FMA-pipe
- *          polynomial instead of MUFU (0, 2, 4, 6, 8; 10 and 12 for variant 4; default 4)
+/* Tuning switches for A/B measurement (every combination is parity-checked).  ctx != NULL:
+ * the switch of that context only (each context starts at the defaults); ctx == NULL: the
+ * switches the ctx-less debug entry points above use.
+ *   key 0  attention kernel: 1 one query tile per CTA (v1), 4 three query tiles / warpgroups
+ *          per CTA (v4, default)
+ *   key 1  v4: how many of every 16 column pairs are exponentiated by the FMA-pipe polynomial
+ *          instead of MUFU (0, 2, 4 default, 6, 8)
  *   key 2  fused MLP kernel on (1, default) / off (0)
  *   key 3  TMA-staged residual(+LayerNorm) epilogues on (1, default) / off (0)
  *   key 4  fused MLP as CTA pairs (cta_group::2) on (1) / off (0, default)
- *   key 5  attention v4/v5 warpgroup start stagger in cycles (0 default); -1 / -2 select the
+ *   key 5  attention v4 warpgroup start stagger in cycles (0 default); -1 / -2 select the
  *          debug library's "quarters" / "MMA warp" attention trace modes
- *   key 6  attention v4 K/V ring depth in 128-key stages: 4 (default), 6, 8
  *   key 7  weight-stationary QKV GEMM on (1, default) / off (0)
- *   key 9  attention v4 exp-phase token ring on (1) / off (0, default)
- *   key 10 attention v4 split MMA accumulator chains on (1) / off (0, default)
  *   key 11 O-projection + residual + LN2 fused into the MLP kernel on (1, default) / off (0)
  *   key 12 attention v4 q-triple-major item order for equal-length (coarse) batches on (1,
  *          default) / off (0)
@@ -89,23 +89,16 @@ int32_t cfdx_probe_count(int32_t kind);
  *          tensor map (1, default; d = 256, 3Pc % 32 == 0) instead of im2col + GEMM (0)
  *   key 15 layer-0 LN1 of the coarse pass fused into the coarse embed epilogue (1, default)
  *          instead of a standalone LayerNorm launch (0)
- *   key 16 attention v4 dynamic item claiming through a work counter (1, default) instead of
- *          the static round-robin (0).  The counter pair [claims, finished CTAs] is reset by the
- *          launch's last CTA (no memset launch): one pipeline 1.433 -> 1.415 ms per step, two
- *          lanes neutral (1.362 / 1.365 ms; the other lane already fills the tails).  (With a
- *          memset per launch it measured slower: 1.504 vs 1.471 ms.)
- *   key 17 cap on the persistent kernels' grid size (0 = every SM, default; caps measured
- *          slower with two concurrent pipelines: 74 SMs 1.514, 100 1.399, 148 1.393 ms)
+ *   key 16 attention v4 dynamic item claiming through the call workspace's work counter (1,
+ *          default) instead of the static round-robin (0)
+ *   key 17 cap on the persistent kernels' grid size (0 = every SM, default)
  *   key 18 balanced persistent grids: the fewest CTAs with the same number of rounds (1) /
- *          min(units, SMs) (0, default; measured neutral with two pipelines, 1 % slower alone)
+ *          min(units, SMs) (0, default)
  *   key 19 fused O-projection keeps x1 = x + o W_o + b_o in TMEM and the MLP's MMA2s
- *          accumulate onto it, so x1 is neither stored nor re-read (1, default) / x1 stored
- *          and the final epilogue reads it back (0)
- *   key 20 with key 19 = 1: the epilogue warps load x into acc2 while o / W_o stream in and
- *          MMA_o accumulates onto it, so the residual pass does not wait for x (1) / 0 (default:
- *          the x load competes with o / W_o for the SM's ingress, MLP launch 52.7 -> 54.1 us)
+ *          accumulate onto it (1, default) / x1 stored and read back (0)
+ *   key 20 with key 19 = 1: x loaded into acc2 while o / W_o stream in (1) / 0 (default)
  * Other keys / values: CFD_E_ARG. */
-cfd_status cfdx_set_option(int32_t key, int32_t value);
+cfd_status cfdx_set_option(cfd_ctx *ctx, int32_t key, int32_t value);
 
 /* Number of kernels the library launched since load (host counter; for bench's
  * gpu_launches claim). */

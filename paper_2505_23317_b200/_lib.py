@@ -91,7 +91,7 @@ def load() -> C.CDLL:
         "cfd_version": [],
         "cfdx_gemm": [I32, I32, I32, P, P, P, I32, P, P, P],
         "cfdx_gemm_resid_ln": [I32, I32, I32, P, P, P, P, P, P, F32, P, I32, I32, P],
-        "cfdx_attention": [I32, P, I32, I32, I32, I32, P, P, P, I32, P],
+        "cfdx_attention": [I32, P, I32, I32, I32, I32, P, P, P, I32, P, P],
         "cfdx_layernorm": [I32, I32, P, P, P, F32, P, P],
         "cfdx_score": [I32, I32, I32, I32, P, I32, P, I32, P, P],
         "cfdx_gather": [P, I32, P, P, P, P, P, P, P, P, P, P, P, P],
@@ -100,7 +100,7 @@ def load() -> C.CDLL:
         "cfdx_attn_trace": [P, I32],
         "cfdx_probe_install": [I32, C.POINTER(P), C.POINTER(P), I32],
         "cfdx_probe_count": [I32],
-        "cfdx_set_option": [I32, I32],
+        "cfdx_set_option": [P, I32, I32],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)

@@ -98,6 +98,10 @@ class CFDetrEncoder:
         except Exception:
             pass
 
+    def set_option(self, key: int, value: int) -> None:
+        """Tuning switch of this context (cfdx_set_option, include/cfdetr_debug.h)."""
+        L.check("cfdx_set_option", self.lib.cfdx_set_option(self.ctx, int(key), int(value)))
+
     def check(self, stream=None):
         L.check("cfd_check", self.lib.cfd_check(self.ctx, _stream(stream)))
 
@@ -209,6 +213,7 @@ def _set_decoder(self, wdec: dict, stream=None) -> None:
     L.check("cfd_set_decoder", self.lib.cfd_set_decoder(self.ctx, C.byref(dw), _stream(stream)))
     (stream or torch.cuda.current_stream()).synchronize()
     self.n_queries = int(wdec["queries"].shape[0])
+    self._ws = {}  # the workspace size depends on the query count (cfd_query after cfd_set_decoder)
 
 
 def _decode(self, y: torch.Tensor, cu_seqlens: torch.Tensor, n_tasks: int, max_tokens: int, stream=None) -> dict:

@@ -1,7 +1,7 @@
-// attn4_tc.cuh — attention v4: like attn3 (persistent, 64-key softmax steps, per-warpgroup
-// MMA issuers, lazy rescale, MUFU/polynomial exp2) but with THREE softmax warpgroups per
-// CTA, so an item is (task, triple of 128-row query tiles, head) and every K/V tile the
-// TMA warp streams serves three query tiles.
+// attn4_tc.cuh — attention v4: persistent, 64-key softmax steps, per-warpgroup MMA issuers,
+// lazy rescale, MUFU/polynomial exp2, THREE softmax warpgroups per CTA, so an item is (task,
+// triple of 128-row query tiles, head) and every K/V tile the TMA warp streams serves three
+// query tiles.
 //
 //   TMEM per warpgroup w (128 columns, 3 x 128 = 384 of 512):
 //     S_w  64 fp32 cols  — single-buffered: the warpgroup moves S_u into registers at the
@@ -18,8 +18,7 @@
 #include <cuda_bf16.h>
 #include "ptx.cuh"
 #include "attn_tc.cuh"
-#include "attn2_tc.cuh"
-#include "attn3_tc.cuh"
+#include "attn_common.cuh"
 
 namespace cfd {
 
@@ -48,7 +47,7 @@ struct Attn4Smem {
   static constexpr int V_OFF = K_OFF + STAGES * TILE_BYTES;    // [STAGES]
   static constexpr int BAR_OFF = V_OFF + STAGES * TILE_BYTES;
   static constexpr int PRE_OFF = BAR_OFF + 512;
-  static constexpr int TOTAL = 1024 + PRE_OFF + (ATTN2_MAX_T + 1) * 4;
+  static constexpr int TOTAL = 1024 + PRE_OFF + (ATTN_MAX_T + 1) * 4;
   static constexpr uint32_t S_COL = 0;    // S_w at w*128
   static constexpr uint32_t P_COL = 64;   // P_w at w*128 + 64
   static constexpr uint32_t O_COL = 96;   // O_w at w*128 + 96

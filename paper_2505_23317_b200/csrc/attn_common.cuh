@@ -1,0 +1,89 @@
+// attn_common.cuh — softmax arithmetic shared by the attention kernels (dh = 32): packed
+// f32x2 FMA / ADD wrappers, the 3-input max, the FMA-pipe exp2 polynomial, the exp chunk of
+// one score row (MUFU / polynomial split) and the item decode of ragged batches.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include "ptx.cuh"
+#include "attn_tc.cuh"
+
+namespace cfd {
+
+constexpr int ATTN_MAX_T = 4096;  // tasks per persistent attention launch (prefix table in smem)
+
+// ---------------------------------------------------------------- packed fp32 helpers
+__device__ __forceinline__ void fma2(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0,
+                                     float c1) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+__device__ __forceinline__ void add2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// 2^x for a pair, x <= 0, on the FMA pipe: x = j + f, j = round(x), f in [-1/2, 1/2];
+// 2^f by a degree-3 minimax polynomial (max rel. error 7.6e-5 < bf16 ulp/2), 2^j
+// inserted into the exponent field.  x is clamped at -126: with j = -126 the biased
+// exponent of 2^f (126 or 127) stays >= 0 (result ~1e-38 ~ 0); at -127 it wrapped into the
+// sign bit for f <= 0 and produced NaN for logits more than 2^127 below the row max.
+__device__ __forceinline__ void exp2_poly2(float& y0, float& y1, float x0, float x1) {
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: t = x + M rounds x to an integer in t's low bits
+  x0 = fmaxf(x0, -126.f);
+  x1 = fmaxf(x1, -126.f);
+  float t0, t1, r0, r1, f0, f1, p0, p1;
+  add2(t0, t1, x0, x1, kMagic, kMagic);
+  add2(r0, r1, t0, t1, -kMagic, -kMagic);
+  add2(f0, f1, x0, x1, -r0, -r1);
+  fma2(p0, p1, f0, f1, 0.05517025f, 0.05517025f, 0.24260790f, 0.24260790f);
+  fma2(p0, p1, p0, p1, f0, f1, 0.69326093f, 0.69326093f);
+  fma2(p0, p1, p0, p1, f0, f1, 0.99992828f, 0.99992828f);
+  y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
+
+// One 32-column chunk of a score row: p = 2^(s*c - m) for 16 pairs, running pair sums,
+// bf16x2-packed results written to sr[0..15].  Pairs [16-NPP, 16) use the polynomial.
+template <int NPP>
+__device__ __forceinline__ void exp_chunk(uint32_t* sr, float c, float neg, float& sum0, float& sum1) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    float x0, x1, p0, p1;
+    fma2(x0, x1, __uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1]), c, c, neg, neg);
+    if (i >= 16 - NPP) {
+      exp2_poly2(p0, p1, x0, x1);
+    } else {
+      p0 = ex2_approx(x0);
+      p1 = ex2_approx(x1);
+    }
+    add2(sum0, sum1, sum0, sum1, p0, p1);
+    sr[i] = pack_bf16x2(p0, p1);
+  }
+}
+
+// item -> (task, query pair, head): prefix[t] = first item of task t
+__device__ __forceinline__ void decode_item(const int* prefix, int T, int nh, int item, int& t, int& qp, int& h) {
+  int lo = 0, hi = T - 1;
+  while (lo < hi) {  // last t with prefix[t] <= item
+    const int mid = (lo + hi + 1) >> 1;
+    if (prefix[mid] <= item) lo = mid; else hi = mid - 1;
+  }
+  t = lo;
+  const int r = item - prefix[lo];
+  qp = r / nh;
+  h = r % nh;
+}
+
+}  // namespace cfd

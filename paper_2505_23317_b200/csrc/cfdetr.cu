@@ -18,17 +18,17 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
+#include <set>
+#include <utility>
 #include <vector>
 
 #include "../../include/cfdetr.h"
 #include "../../include/cfdetr_debug.h"
 #include "attn_tc.cuh"
-#include "attn2_tc.cuh"
-#include "attn3_tc.cuh"
+#include "attn_common.cuh"
 #include "attn4_tc.cuh"
-#include "attn5_tc.cuh"
-#include "attn6_tc.cuh"
 #include "gemm_tc.cuh"
 #include "misc_kernels.cuh"
 #include "mlp_tc.cuh"
@@ -102,16 +102,66 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
   return r == CUDA_SUCCESS;
 }
 
-int g_num_sms = 0;
-int g_sm_cap = 0;  // option 17: cap on the persistent grids (0 = all SMs), for concurrent pipelines
-int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+// Tuning switches (cfdx_set_option, include/cfdetr_debug.h).  Every context carries its own
+// copy (set per ctx); the ctx-less debug entry points use g_dbg_opts.  Defaults = the measured
+// best configuration.
+struct Opts {
+  int attn_variant = 4;   // 1: one q-tile per CTA (v1), 4: three q-tiles per CTA (v4)
+  int attn_npp = 4;       // v4: polynomial-exp pairs of every 16
+  int attn_stagger = 0;   // v4: warpgroup start stagger; -1 / -2 trace modes (debug library)
+  int attn_qmajor = 1;    // v4: q-triple-major item order for equal-length batches (option 12)
+  int attn_dyn = 1;       // v4: dynamic item claiming through the workspace work counter (16)
+  int fused_mlp = 1;      // fused MLP kernel (d == 256) instead of two GEMM launches (2)
+  int staged_epi = 1;     // TMA-staged residual + LayerNorm epilogues (3)
+  int mlp_cluster = 0;    // fused MLP as CTA pairs (cta_group::2) (4)
+  int gemm_bres = 1;      // weight-stationary QKV GEMM (7)
+  int fuse_oproj = 1;     // O-projection + residual + LN2 inside the fused MLP kernel (11)
+  int embed_mode0 = 1;    // patch-embed GEMMs: 1 CTA/SM, 4-stage ring (13)
+  int embed_img = 1;      // coarse patch embed gathers A from the image by TMA, no im2col (14)
+  int embed_ln = 1;       // layer-0 LN1 fused into the coarse embed epilogue (15)
+  int sm_cap = 0;         // cap on the persistent grids (0 = all SMs) (17)
+  int balanced_grid = 0;  // fewest CTAs with the same number of rounds (18)
+  int keep_x1 = 1;        // fused O-projection: x1 stays in TMEM, MMA2 accumulates onto it (19)
+  int preload_x = 0;      // with 19: x loaded into acc2 before MMA_o (20; measured slower)
+};
+Opts g_dbg_opts;
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+// SM count of the current device (cached per device)
+int device_sms() {
+  static std::atomic<int> cache[64];
+  const int dev = current_device();
+  if (dev < 0 || dev >= 64) return 148;
+  int n = cache[dev].load();
+  if (!n) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    cache[dev].store(n);
   }
-  return g_sm_cap > 0 ? std::min(g_sm_cap, g_num_sms) : g_num_sms;
+  return n;
+}
+int num_sms(const Opts& o) {
+  const int n = device_sms();
+  return o.sm_cap > 0 ? std::min(o.sm_cap, n) : n;
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device property of a kernel: set it
+// once per (kernel, device).
+template <typename K>
+cudaError_t ensure_smem_attr(K* kern, int smem) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  const std::pair<const void*, int> key{reinterpret_cast<const void*>(kern), current_device()};
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(key)) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
 }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -121,10 +171,10 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // be partial leaves whole SMs to a concurrent stream instead of idling them in its tail
 // (option 18; e.g. 256 attention items: 128 CTAs x 2 rounds instead of 148 CTAs with 40 idle
 // in round 2).
-int g_balanced_grid = 0;  // off: 2-stream step 1.385 vs 1.389 ms (noise), 1-stream 1.479 vs 1.462 ms
-inline int balanced_grid(int units, int slots) {
+// off by default: 2-stream step 1.385 vs 1.389 ms (noise), 1-stream 1.479 vs 1.462 ms
+inline int balanced_grid(const Opts& o, int units, int slots) {
   if (units <= 0) return 1;
-  if (!g_balanced_grid || units <= slots) return std::min(units, slots);
+  if (!o.balanced_grid || units <= slots) return std::min(units, slots);
   const int rounds = (units + slots - 1) / slots;
   return (units + rounds - 1) / rounds;
 }
@@ -138,10 +188,6 @@ cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
 
 
 // ------------------------------------------------------------------ GEMM dispatch
-int g_gemm_bres = 1;  // weight-stationary QKV GEMM (option 7)
-int g_embed_mode0 = 1;  // patch-embed GEMMs: 1 CTA/SM, 4-stage ring (option 13)
-int g_embed_img = 1;    // coarse patch embed gathers A from the image by TMA, no im2col (option 14)
-int g_embed_ln = 1;     // layer-0 LN1 fused into the coarse embed epilogue (option 15)
 template <int BN>
 constexpr int gemm_stages() { return BN == 256 ? 4 : BN == 128 ? 6 : 8; }
 template <int BN>  // with the 32 KB bf16 output staging area
@@ -156,8 +202,8 @@ constexpr int gemm_stages_stg() { return BN == 256 ? 3 : BN == 128 ? 5 : 7; }
 // mode 3 (IMG): mode 0 for the coarse patch embed with A gathered from the image by a 5-D
 //         tensor map (no im2col), 32-wide k-blocks, 8-stage ring of 8 + 16 KB
 template <int BN, int EPI, int MODE>
-cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows_for_grid,
-                          cudaStream_t s, const CUtensorMap* tx, const CUtensorMap* tln) {
+cudaError_t launch_gemm_t(const Opts& o, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                          int rows_for_grid, cudaStream_t s, const CUtensorMap* tx, const CUtensorMap* tln) {
   constexpr bool kImg = MODE == 3;
   constexpr bool kBres = MODE == 2;
   constexpr bool kTmaEpi = (EPI == EPI_F32_RESID_LN && MODE != 1);
@@ -175,19 +221,14 @@ cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
       return cudaErrorInvalidValue;
     tx = &tout;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = ensure_smem_attr(kern, smem); e != cudaSuccess) return e;
   const int rpt = kImg ? p.img_rb * p.img_gw : GEMM_BM;
   const int tiles = ((rows_for_grid + rpt - 1) / rpt) * (p.N / BN);
-  const int slots = num_sms() * (MODE == 1 ? 2 : 1);
-  int grid = balanced_grid(tiles, slots);
+  const int slots = num_sms(o) * (MODE == 1 ? 2 : 1);
+  int grid = balanced_grid(o, tiles, slots);
   if constexpr (kBres) {  // whole column-block groups, each balanced over its row blocks
     const int nt = p.N / BN, mt = (rows_for_grid + rpt - 1) / rpt;
-    grid = balanced_grid(mt, std::max(1, slots / nt)) * nt;
+    grid = balanced_grid(o, mt, std::max(1, slots / nt)) * nt;
   }
   cudaError_t le = launch_ex(kern, dim3(grid), dim3(64 + 32 * EW), smem, s, ta, tb, p, tx ? *tx : ta, tln ? *tln : ta);
   ++g_launches;
@@ -195,43 +236,44 @@ cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
 }
 
 template <int EPI>
-cudaError_t launch_gemm_bn(int BN, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows,
-                           cudaStream_t s, const CUtensorMap* tx, const CUtensorMap* tln) {
+cudaError_t launch_gemm_bn(const Opts& o, int BN, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                           int rows, cudaStream_t s, const CUtensorMap* tx, const CUtensorMap* tln) {
   // N = BN: a single column tile per row block -> the 2-CTA/SM configuration, except the
   // residual+LN epilogue with staging maps, which runs 1 CTA/SM with TMA-staged I/O
   // the patch embeds (K = 3Pc^2 / 3Pf^2, long k loops over ~100 tiles) keep one CTA per SM with a
-  // 4-stage ring when g_embed_mode0 (option 13): the k loop is latency-bound with 2 stages
-  const bool embed = (EPI == EPI_EMBED_COARSE || EPI == EPI_EMBED_FINE) && g_embed_mode0;
+  // 4-stage ring when embed_mode0 (option 13): the k loop is latency-bound with 2 stages
+  const bool embed = (EPI == EPI_EMBED_COARSE || EPI == EPI_EMBED_FINE) && o.embed_mode0;
   if (p.N == BN && !(EPI == EPI_F32_RESID_LN && tx && tln) && !embed) {
     switch (BN) {
-      case 256: return launch_gemm_t<256, EPI, 1>(ta, tb, p, rows, s, tx, tln);
-      case 128: return launch_gemm_t<128, EPI, 1>(ta, tb, p, rows, s, tx, tln);
-      default: return launch_gemm_t<64, EPI, 1>(ta, tb, p, rows, s, tx, tln);
+      case 256: return launch_gemm_t<256, EPI, 1>(o, ta, tb, p, rows, s, tx, tln);
+      case 128: return launch_gemm_t<128, EPI, 1>(o, ta, tb, p, rows, s, tx, tln);
+      default: return launch_gemm_t<64, EPI, 1>(o, ta, tb, p, rows, s, tx, tln);
     }
   }
   if constexpr (EPI == EPI_BF16_BIAS) {
-    if (g_gemm_bres && BN == 256 && p.K == GEMM_BRES_KB * GEMM_BK)
-      return launch_gemm_t<256, EPI, 2>(ta, tb, p, rows, s, tx, tln);
+    if (o.gemm_bres && BN == 256 && p.K == GEMM_BRES_KB * GEMM_BK)
+      return launch_gemm_t<256, EPI, 2>(o, ta, tb, p, rows, s, tx, tln);
   }
   switch (BN) {
-    case 256: return launch_gemm_t<256, EPI, 0>(ta, tb, p, rows, s, tx, tln);
-    case 128: return launch_gemm_t<128, EPI, 0>(ta, tb, p, rows, s, tx, tln);
-    default: return launch_gemm_t<64, EPI, 0>(ta, tb, p, rows, s, tx, tln);
+    case 256: return launch_gemm_t<256, EPI, 0>(o, ta, tb, p, rows, s, tx, tln);
+    case 128: return launch_gemm_t<128, EPI, 0>(o, ta, tb, p, rows, s, tx, tln);
+    default: return launch_gemm_t<64, EPI, 0>(o, ta, tb, p, rows, s, tx, tln);
   }
 }
 
 int pick_bn(int N) { return (N % 256 == 0) ? 256 : (N % 128 == 0) ? 128 : 64; }
 
-cudaError_t launch_gemm_impl(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows,
-                             cudaStream_t s, const CUtensorMap* tx, const CUtensorMap* tln) {
+cudaError_t launch_gemm_impl(const Opts& o, int epi, const CUtensorMap& ta, const CUtensorMap& tb,
+                             const GemmParams& p, int rows, cudaStream_t s, const CUtensorMap* tx,
+                             const CUtensorMap* tln) {
   const int BN = pick_bn(p.N);
   switch (epi) {
-    case EPI_BF16_BIAS: return launch_gemm_bn<EPI_BF16_BIAS>(BN, ta, tb, p, rows, s, nullptr, nullptr);
-    case EPI_BF16_BIAS_GELU: return launch_gemm_bn<EPI_BF16_BIAS_GELU>(BN, ta, tb, p, rows, s, nullptr, nullptr);
-    case EPI_F32_RESID: return launch_gemm_bn<EPI_F32_RESID>(BN, ta, tb, p, rows, s, nullptr, nullptr);
-    case EPI_EMBED_COARSE: return launch_gemm_bn<EPI_EMBED_COARSE>(BN, ta, tb, p, rows, s, nullptr, nullptr);
-    case EPI_F32_RESID_LN: return launch_gemm_bn<EPI_F32_RESID_LN>(BN, ta, tb, p, rows, s, tx, tln);
-    default: return launch_gemm_bn<EPI_EMBED_FINE>(BN, ta, tb, p, rows, s, nullptr, nullptr);
+    case EPI_BF16_BIAS: return launch_gemm_bn<EPI_BF16_BIAS>(o, BN, ta, tb, p, rows, s, nullptr, nullptr);
+    case EPI_BF16_BIAS_GELU: return launch_gemm_bn<EPI_BF16_BIAS_GELU>(o, BN, ta, tb, p, rows, s, nullptr, nullptr);
+    case EPI_F32_RESID: return launch_gemm_bn<EPI_F32_RESID>(o, BN, ta, tb, p, rows, s, nullptr, nullptr);
+    case EPI_EMBED_COARSE: return launch_gemm_bn<EPI_EMBED_COARSE>(o, BN, ta, tb, p, rows, s, nullptr, nullptr);
+    case EPI_F32_RESID_LN: return launch_gemm_bn<EPI_F32_RESID_LN>(o, BN, ta, tb, p, rows, s, tx, tln);
+    default: return launch_gemm_bn<EPI_EMBED_FINE>(o, BN, ta, tb, p, rows, s, nullptr, nullptr);
   }
 }
 
@@ -239,11 +281,11 @@ cudaError_t launch_gemm_impl(int epi, const CUtensorMap& ta, const CUtensorMap& 
 enum : int { PK_ATTN = 0, PK_SCORE = 1, PK_QKV = 2, PK_OPROJ = 3, PK_MLP1 = 4, PK_MLP2 = 5, PK_EMBED_C = 6,
              PK_EMBED_F = 7, PK_LN = 8, PK_SELECT = 9, PK_GATHER = 10, PK_IM2COL = 11, PK_META = 12 };
 
-cudaError_t launch_gemm(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int rows,
-                        cudaStream_t s, int kind = -1, const CUtensorMap* tx = nullptr,
+cudaError_t launch_gemm(const Opts& o, int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                        int rows, cudaStream_t s, int kind = -1, const CUtensorMap* tx = nullptr,
                         const CUtensorMap* tln = nullptr) {
   probe_begin(kind, s);
-  cudaError_t e = launch_gemm_impl(epi, ta, tb, p, rows, s, tx, tln);
+  cudaError_t e = launch_gemm_impl(o, epi, ta, tb, p, rows, s, tx, tln);
   probe_end(kind, s);
   return e;
 }
@@ -277,48 +319,28 @@ bool make_qkvmap(CUtensorMap* m, const void* qkv, int rows, int d) {
   return make_tmap(m, qkv, 3 * d, rows, 3 * d, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
-// runtime options (cfdx_set_option): attention variant (1 = one q-tile per CTA,
-// 2 = persistent two-tile ping-pong) and the polynomial-exp2 share of variant 2.
-int g_attn_variant = 4;
-int g_attn_npp = 4;
-int g_attn_stagger = 0;
-int g_attn_stages = 4;  // v4 K/V ring depth (128-key stages): 4, 6 or 8
-int g_attn_token = 0;   // v4 exp-phase token ring (option 9)
-int g_attn_split = 0;   // v4 split MMA accumulator chains (option 10)
-int g_attn_qmajor = 1;  // v4 q-triple-major item order for equal-length batches (option 12)
-int g_attn_dyn = 1;     // v4 dynamic item claiming through a self-resetting work counter (option 16)
-int g_fused_mlp = 1;  // fused MLP kernel (d == 256) instead of two GEMM launches
-int g_staged_epi = 1; // TMA-staged residual + LayerNorm epilogue for the O-projection
-int g_mlp_cluster = 0; // fused MLP as CTA pairs (cta_group::2)
-int g_preload_x = 0;   // with option 19: x loaded into acc2 before MMA_o (option 20; measured slower)
-int g_keep_x1 = 1;     // fused O-projection: x1 stays in TMEM, MMA2 accumulates onto it (option 19)
-int g_fuse_oproj = 1;  // O-projection + residual + LN2 inside the fused MLP kernel (option 11)
-
 // tw1: W1 with 128-row boxes (single-CTA kernel); tw1h: 64-row boxes (CTA-pair kernel)
 // two (opj): th is the attention output o (the fused O-projection's A operand), two = W_o map
-cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUtensorMap& tw1h, const CUtensorMap& tw2,
-                       const MlpParams& p, int rows_for_grid, cudaStream_t s, const CUtensorMap* tx = nullptr,
-                       const CUtensorMap* tln = nullptr, const CUtensorMap* two = nullptr) {
+cudaError_t launch_mlp(const Opts& o, const CUtensorMap& th, const CUtensorMap& tw1, const CUtensorMap& tw1h,
+                       const CUtensorMap& tw2, const MlpParams& p, int rows_for_grid, cudaStream_t s,
+                       const CUtensorMap* tx = nullptr, const CUtensorMap* tln = nullptr,
+                       const CUtensorMap* two = nullptr) {
   constexpr int smem = MlpSmem<256>::TOTAL;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(mlp_tc_kernel<256, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(mlp_tc_kernel<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(mlp_tc_kernel<256, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    cudaError_t e = ensure_smem_attr(mlp_tc_kernel<256, 1>, smem);
+    if (e == cudaSuccess) e = ensure_smem_attr(mlp_tc_kernel<256, 2>, smem);
+    if (e == cudaSuccess) e = ensure_smem_attr(mlp_tc_kernel<256, 1, true>, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int tiles = (pad_rows(rows_for_grid, p.ln_cap > 0 ? p.ln_cap : rows_for_grid + 256) + 127) / 128;
   MlpParams q = p;
   q.staged = (tx != nullptr && (tln != nullptr || p.ln_g == nullptr)) ? 1 : 0;
   const CUtensorMap& mx = tx ? *tx : th;
   const CUtensorMap& ml = tln ? *tln : th;
-  if (g_mlp_cluster && num_sms() >= 2) {
+  if (o.mlp_cluster && num_sms(o) >= 2) {
     // CTA pairs (cta_group::2 MMAs, each SM holding half of every weight operand)
     const int pairs = (tiles + 1) / 2;
-    const int clusters = std::max(1, std::min(pairs, num_sms() / 2));
+    const int clusters = std::max(1, std::min(pairs, num_sms(o) / 2));
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(2 * clusters);
     lc.blockDim = dim3(MLP_THREADS);
@@ -335,7 +357,7 @@ cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUte
     ++g_launches;
     return e != cudaSuccess ? e : cudaGetLastError();
   }
-  const int grid = std::max(1, balanced_grid(tiles, num_sms()));
+  const int grid = std::max(1, balanced_grid(o, tiles, num_sms(o)));
   const cudaError_t le =
       two ? launch_ex(mlp_tc_kernel<256, 1, true>, dim3(grid), dim3(MLP_THREADS), smem, s, th, tw1, tw2, q, mx, ml, *two)
           : launch_ex(mlp_tc_kernel<256, 1>, dim3(grid), dim3(MLP_THREADS), smem, s, th, tw1, tw2, q, mx, ml, th);
@@ -344,101 +366,42 @@ cudaError_t launch_mlp(const CUtensorMap& th, const CUtensorMap& tw1, const CUte
   return cudaGetLastError();
 }
 
-template <int V, int NPP, int ST = 4, bool TOK = false, bool SPL = false>
-cudaError_t launch_attn2_t(const CUtensorMap& tq, const AttnParams& p, int items_ub, int nh, int T, cudaStream_t s) {
-  auto kern = (V == 2)   ? attn2_tc_kernel<32, 4, NPP>
-              : (V == 3) ? attn3_tc_kernel<32, 4, NPP>
-              : (V == 4) ? attn4_tc_kernel<32, ST, NPP, TOK, SPL>
-              : (V == 6) ? attn6_tc_kernel<32, ST, NPP>
-                         : attn5_tc_kernel<32, 4, NPP>;
-  constexpr int smem = (V == 2)   ? Attn2Smem<32, 4>::TOTAL
-                       : (V == 3) ? Attn3Smem<32, 4>::TOTAL
-                       : (V == 4 || V == 6) ? Attn4Smem<32, ST>::TOTAL
-                                  : Attn5Smem<32, 4>::TOTAL;
-  constexpr int threads = V == 2 ? ATTN2_THREADS : V == 3 ? ATTN3_THREADS : (V == 4 || V == 6) ? ATTN4_THREADS : ATTN5_THREADS;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  // v5: two items (pairs) in flight per CTA
-  const int grid = std::max(1, balanced_grid(V == 5 ? (items_ub + 1) / 2 : items_ub, num_sms()));
-  cudaError_t e = launch_ex(kern, dim3(grid), dim3(threads), smem, s, tq, p, T, nh);
+template <int NPP>
+cudaError_t launch_attn4_t(const Opts& o, const CUtensorMap& tq, const AttnParams& p, int items_ub, int nh, int T,
+                           cudaStream_t s) {
+  auto kern = attn4_tc_kernel<32, 4, NPP>;
+  constexpr int smem = Attn4Smem<32, 4>::TOTAL;
+  if (cudaError_t e = ensure_smem_attr(kern, smem); e != cudaSuccess) return e;
+  const int grid = std::max(1, balanced_grid(o, items_ub, num_sms(o)));
+  cudaError_t e = launch_ex(kern, dim3(grid), dim3(ATTN4_THREADS), smem, s, tq, p, T, nh);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess && getenv("CFD_VERBOSE")) {
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, kern);
-    fprintf(stderr, "attention v%d launch (grid %d, %d threads, %d B smem; kernel: %d regs, max %d threads): %s\n", V,
-            grid, threads, smem, fa.numRegs, fa.maxThreadsPerBlock, cudaGetErrorString(e));
+    fprintf(stderr, "attention v4 launch (grid %d, %d threads, %d B smem; kernel: %d regs): %s\n", grid,
+            ATTN4_THREADS, smem, fa.numRegs, cudaGetErrorString(e));
   }
   return e;
 }
 
-cudaError_t launch_attention(const CUtensorMap& tq, const AttnParams& p, int max_qtiles, int nh, int T,
+cudaError_t launch_attention(const Opts& o, const CUtensorMap& tq, const AttnParams& p, int max_qtiles, int nh, int T,
                              cudaStream_t s) {
   probe_begin(PK_ATTN, s);
   cudaError_t e;
-  if (g_attn_variant >= 2 && T <= ATTN2_MAX_T) {
-    const int items_ub = T * ((max_qtiles + 1) / 2) * nh;
-    if (g_attn_variant == 2) {
-      switch (g_attn_npp) {
-        case 0: e = launch_attn2_t<2, 0>(tq, p, items_ub, nh, T, s); break;
-        case 2: e = launch_attn2_t<2, 2>(tq, p, items_ub, nh, T, s); break;
-        case 6: e = launch_attn2_t<2, 6>(tq, p, items_ub, nh, T, s); break;
-        case 8: e = launch_attn2_t<2, 8>(tq, p, items_ub, nh, T, s); break;
-        default: e = launch_attn2_t<2, 4>(tq, p, items_ub, nh, T, s); break;
-      }
-    } else if (g_attn_variant == 3) {
-      switch (g_attn_npp) {
-        case 0: e = launch_attn2_t<3, 0>(tq, p, items_ub, nh, T, s); break;
-        case 2: e = launch_attn2_t<3, 2>(tq, p, items_ub, nh, T, s); break;
-        case 6: e = launch_attn2_t<3, 6>(tq, p, items_ub, nh, T, s); break;
-        case 8: e = launch_attn2_t<3, 8>(tq, p, items_ub, nh, T, s); break;
-        default: e = launch_attn2_t<3, 4>(tq, p, items_ub, nh, T, s); break;
-      }
-    } else if (g_attn_variant == 6) {
-      switch (g_attn_npp) {
-        case 0: e = launch_attn2_t<6, 0>(tq, p, items_ub, nh, T, s); break;
-        case 2: e = launch_attn2_t<6, 2>(tq, p, items_ub, nh, T, s); break;
-        case 6: e = launch_attn2_t<6, 6>(tq, p, items_ub, nh, T, s); break;
-        case 8: e = launch_attn2_t<6, 8>(tq, p, items_ub, nh, T, s); break;
-        default: e = launch_attn2_t<6, 4>(tq, p, items_ub, nh, T, s); break;
-      }
-    } else if (g_attn_variant == 5) {
-      switch (g_attn_npp) {
-        case 0: e = launch_attn2_t<5, 0>(tq, p, items_ub, nh, T, s); break;
-        case 2: e = launch_attn2_t<5, 2>(tq, p, items_ub, nh, T, s); break;
-        case 6: e = launch_attn2_t<5, 6>(tq, p, items_ub, nh, T, s); break;
-        case 8: e = launch_attn2_t<5, 8>(tq, p, items_ub, nh, T, s); break;
-        default: e = launch_attn2_t<5, 4>(tq, p, items_ub, nh, T, s); break;
-      }
-    } else {
-      switch (g_attn_npp) {
-        case 0: e = launch_attn2_t<4, 0>(tq, p, items_ub, nh, T, s); break;
-        case 2: e = launch_attn2_t<4, 2>(tq, p, items_ub, nh, T, s); break;
-        case 6: e = launch_attn2_t<4, 6>(tq, p, items_ub, nh, T, s); break;
-        case 8: e = launch_attn2_t<4, 8>(tq, p, items_ub, nh, T, s); break;
-        case 10: e = launch_attn2_t<4, 10>(tq, p, items_ub, nh, T, s); break;
-        case 12: e = launch_attn2_t<4, 12>(tq, p, items_ub, nh, T, s); break;
-        default:
-          e = g_attn_split         ? launch_attn2_t<4, 4, 4, false, true>(tq, p, items_ub, nh, T, s)
-              : g_attn_token       ? launch_attn2_t<4, 4, 4, true>(tq, p, items_ub, nh, T, s)
-              : g_attn_stages == 8 ? launch_attn2_t<4, 4, 8>(tq, p, items_ub, nh, T, s)
-              : g_attn_stages == 6 ? launch_attn2_t<4, 4, 6>(tq, p, items_ub, nh, T, s)
-                                   : launch_attn2_t<4, 4>(tq, p, items_ub, nh, T, s);
-          break;
-      }
+  if (o.attn_variant == 4 && T <= ATTN_MAX_T) {
+    const int items_ub = T * ((max_qtiles + ATTN4_NWG - 1) / ATTN4_NWG) * nh;
+    switch (o.attn_npp) {
+      case 0: e = launch_attn4_t<0>(o, tq, p, items_ub, nh, T, s); break;
+      case 2: e = launch_attn4_t<2>(o, tq, p, items_ub, nh, T, s); break;
+      case 6: e = launch_attn4_t<6>(o, tq, p, items_ub, nh, T, s); break;
+      case 8: e = launch_attn4_t<8>(o, tq, p, items_ub, nh, T, s); break;
+      default: e = launch_attn4_t<4>(o, tq, p, items_ub, nh, T, s); break;
     }
   } else {
     auto kern = attn_tc_kernel<32, 3>;
     constexpr int smem = AttnSmem<32, 3>::TOTAL;
-    static bool attr = false;
-    if (!attr) {
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
+    e = ensure_smem_attr(kern, smem);
+    if (e != cudaSuccess) return e;
     kern<<<dim3(max_qtiles, nh, T), ATTN_THREADS, smem, s>>>(tq, p, tq);
     e = cudaGetLastError();
   }
@@ -450,12 +413,7 @@ cudaError_t launch_attention(const CUtensorMap& tq, const AttnParams& p, int max
 cudaError_t launch_score(const CUtensorMap& tq, const ScoreParams& p, int B, cudaStream_t s) {
   auto kern = score_tc_kernel<32>;
   constexpr int smem = ScoreSmem<32>::TOTAL;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = ensure_smem_attr(kern, smem); e != cudaSuccess) return e;
   probe_begin(PK_SCORE, s);
   launch_ex(kern, dim3((p.n_coarse + 127) / 128, B), dim3(SCORE_THREADS), smem, s, tq, p);
   probe_end(PK_SCORE, s);
@@ -463,11 +421,11 @@ cudaError_t launch_score(const CUtensorMap& tq, const ScoreParams& p, int B, cud
   return cudaGetLastError();
 }
 
-cudaError_t launch_layernorm(int d, const float* x, const float* g, const float* b, __nv_bfloat16* y, int M,
+cudaError_t launch_layernorm(const Opts& o, int d, const float* x, const float* g, const float* b, __nv_bfloat16* y, int M,
                              const int* m_dev, int m_cap, float eps, int rows_for_grid, cudaStream_t s) {
   const int rows_pad = pad_rows(rows_for_grid, m_cap);
   int blocks = (rows_pad + 7) / 8;
-  blocks = std::max(1, std::min(blocks, num_sms() * 16));
+  blocks = std::max(1, std::min(blocks, num_sms(o) * 16));
   probe_begin(PK_LN, s);
   switch (d) {
     case 64: launch_ex(layernorm_kernel<2>, dim3(blocks), dim3(256), 0, s, x, g, b, y, M, m_dev, m_cap, eps); break;
@@ -495,6 +453,7 @@ struct LayerDev {
 
 struct cfd_ctx {
   cfd_config cfg;
+  Opts opt;  // tuning switches of this context (cfdx_set_option)
   int Nc, Nf, m, dh, Kc, Kf, gc_w, gf_w;
   void* block = nullptr;  // single device allocation for all ctx-owned data
   uint16_t *wc = nullptr, *wf = nullptr;
@@ -519,6 +478,9 @@ struct Workspace {
   __nv_bfloat16 *hbuf, *qkv, *obuf, *ff;
   uint16_t* patches;
   int32_t *frow, *fidx, *meta, *ccu;
+  int32_t* attn_work;  // [2] attention work counter {claims, finished CTAs} of this workspace:
+                       // zeroed by the first kernel of every call, reset by each attention
+                       // launch's last CTA (so calls on different workspaces never share it)
   float* lse;
   int rows_cap;   // token capacity of hbuf/qkv/obuf/ff
   int lse_ld;
@@ -529,7 +491,9 @@ struct Workspace {
 Workspace carve(const cfd_ctx* c, int n, void* base) {
   Workspace w{};
   const cfd_config& g = c->cfg;
-  const size_t rows = (size_t)n * c->Nf + 128;
+  // rows per task: Nf tokens, or the decoder's query count when larger (its cross-attention
+  // output o has T * Q rows in obuf)
+  const size_t rows = (size_t)n * std::max(c->Nf, c->dec_q) + 128;
   w.rows_cap = (int)rows;
   w.lse_ld = n * c->Nc;
   size_t off = 0;
@@ -547,6 +511,7 @@ Workspace carve(const cfd_ctx* c, int n, void* base) {
   w.fidx = (int32_t*)take((size_t)n * c->Nf * 4 + 16);
   w.meta = (int32_t*)take(64);
   w.ccu = (int32_t*)take((size_t)(n + 1) * 4);
+  w.attn_work = (int32_t*)take(16);
   w.lse = (float*)take((size_t)g.n_heads * n * c->Nc * 4 + 16);
   w.bytes = off;
   return w;
@@ -567,6 +532,7 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
                      const int32_t* cu, int T, int max_qtiles, Workspace& w, bool want_lse, float* scores,
                      int score_B, cudaStream_t s, int uniform_n = 0, bool ln1_ready = false) {
   const cfd_config& g = c->cfg;
+  const Opts& o = c->opt;
   const int d = g.d_model, F = g.d_ff;
   const bool fuse_ln = pick_bn(d) == d;  // one GEMM tile spans a whole row
   LayerDev& L = c->layers[l];
@@ -575,30 +541,28 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
       !make_amap(&ta_f, w.ff, w.rows_cap, F) || !make_qkvmap(&tq, w.qkv, w.rows_cap, d))
     return CFD_E_CUDA;
   if ((l == 0 && !ln1_ready) || !fuse_ln)  // LN1
-    CFD_CUDA(launch_layernorm(d, x, L.ln1_g, L.ln1_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
+    CFD_CUDA(launch_layernorm(o, d, x, L.ln1_g, L.ln1_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
   // QKV
   GemmParams p{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = w.rows_cap; p.N = 3 * d; p.K = d; p.bias = L.b_qkv;
   p.out_bf16 = w.qkv;
-  CFD_CUDA(launch_gemm(EPI_BF16_BIAS, ta_h, L.tm_qkv, p, rows_grid, s, PK_QKV));
+  CFD_CUDA(launch_gemm(o, EPI_BF16_BIAS, ta_h, L.tm_qkv, p, rows_grid, s, PK_QKV));
   // attention
   AttnParams ap{};
   ap.cu_seqlens = cu; ap.d_model = d; ap.out = w.obuf; ap.lse = want_lse ? w.lse : nullptr; ap.lse_ld = w.lse_ld;
   ap.scale_log2 = 1.4426950408889634f / std::sqrt((float)c->dh);
-  ap.stagger = g_attn_stagger;
-  ap.uniform_n = g_attn_qmajor ? uniform_n : 0;
-  if (g_attn_dyn) {  // dynamic item claiming: the ctx's words err[2] (claims), err[3] (finished CTAs),
-    ap.work_counter = c->err + 2;  // zeroed at create and reset by the kernel's last CTA
-  }
-  CFD_CUDA(launch_attention(tq, ap, max_qtiles, g.n_heads, T, s));
+  ap.stagger = o.attn_stagger;
+  ap.uniform_n = o.attn_qmajor ? uniform_n : 0;
+  if (o.attn_dyn) ap.work_counter = w.attn_work;  // dynamic item claiming (per-workspace counter)
+  CFD_CUDA(launch_attention(o, tq, ap, max_qtiles, g.n_heads, T, s));
   if (want_lse && scores) {
     ScoreParams sp{};
     sp.n_coarse = c->Nc; sp.n_heads = g.n_heads; sp.d_model = d; sp.lse = w.lse; sp.lse_ld = w.lse_ld;
     sp.scale_log2 = ap.scale_log2; sp.scores = scores;
     CFD_CUDA(launch_score(tq, sp, score_B, s));
   }
-  const bool staged_ok = fuse_ln && g_staged_epi && (d % 64 == 0);
-  if (g_fuse_oproj && g_fused_mlp && !g_mlp_cluster && staged_ok && d == 256 && F % 128 == 0) {
+  const bool staged_ok = fuse_ln && o.staged_epi && (d % 64 == 0);
+  if (o.fuse_oproj && o.fused_mlp && !o.mlp_cluster && staged_ok && d == 256 && F % 128 == 0) {
     // O projection + residual + LN2 fused into the MLP kernel (LN2 never leaves the SM)
     CUtensorMap tx, tln;
     if (!make_tmap(&tx, x, d, x_cap, d, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, true) ||
@@ -606,15 +570,15 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
       return CFD_E_CUDA;
     MlpParams mp{};
     mp.M = M_static; mp.m_dev = m_dev; mp.F = F; mp.b1 = L.b_1; mp.b2 = L.b_2; mp.x = x; mp.ln_eps = g.ln_eps;
-    mp.bo = L.b_o; mp.ln2_g = L.ln2_g; mp.ln2_b = L.ln2_b; mp.keep_x1 = g_keep_x1;
-    mp.preload_x = g_keep_x1 && g_preload_x;
+    mp.bo = L.b_o; mp.ln2_g = L.ln2_g; mp.ln2_b = L.ln2_b; mp.keep_x1 = o.keep_x1;
+    mp.preload_x = o.keep_x1 && o.preload_x;
     mp.ln_cap = w.rows_cap;
     if (l + 1 < g.n_layers) {
       const LayerDev& Ln = c->layers[l + 1];
       mp.ln_g = Ln.ln1_g; mp.ln_b = Ln.ln1_b; mp.ln_out = w.hbuf;
     }
     probe_begin(PK_MLP1, s);
-    CFD_CUDA(launch_mlp(ta_o, L.tm_1c, L.tm_1h, L.tm_2c, mp, rows_grid, s, &tx, &tln, &L.tm_oc));
+    CFD_CUDA(launch_mlp(o, ta_o, L.tm_1c, L.tm_1h, L.tm_2c, mp, rows_grid, s, &tx, &tln, &L.tm_oc));
     probe_end(PK_MLP1, s);
     return CFD_OK;
   }
@@ -622,18 +586,18 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   p = GemmParams{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = x_cap; p.N = d; p.K = d; p.bias = L.b_o; p.out_f32 = x; p.ld_out = d;
   CUtensorMap tx, tln;  // staging maps: fp32 x [x_cap, d] and bf16 LN out, 32 x 32 boxes
-  const bool staged = fuse_ln && g_staged_epi && (d % 64 == 0) &&
+  const bool staged = fuse_ln && o.staged_epi && (d % 64 == 0) &&
                       make_tmap(&tx, x, d, x_cap, d, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, true) &&
                       make_tmap(&tln, w.hbuf, d, w.rows_cap, d, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (fuse_ln) {
     p.ln_g = L.ln2_g; p.ln_b = L.ln2_b; p.ln_out = w.hbuf; p.ln_cap = w.rows_cap; p.ln_eps = g.ln_eps;
-    CFD_CUDA(launch_gemm(EPI_F32_RESID_LN, ta_o, L.tm_o, p, rows_grid, s, PK_OPROJ, staged ? &tx : nullptr,
+    CFD_CUDA(launch_gemm(o, EPI_F32_RESID_LN, ta_o, L.tm_o, p, rows_grid, s, PK_OPROJ, staged ? &tx : nullptr,
                          staged ? &tln : nullptr));
   } else {
-    CFD_CUDA(launch_gemm(EPI_F32_RESID, ta_o, L.tm_o, p, rows_grid, s, PK_OPROJ));
-    CFD_CUDA(launch_layernorm(d, x, L.ln2_g, L.ln2_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
+    CFD_CUDA(launch_gemm(o, EPI_F32_RESID, ta_o, L.tm_o, p, rows_grid, s, PK_OPROJ));
+    CFD_CUDA(launch_layernorm(o, d, x, L.ln2_g, L.ln2_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
   }
-  if (g_fused_mlp && fuse_ln && d == 256 && F % 128 == 0) {
+  if (o.fused_mlp && fuse_ln && d == 256 && F % 128 == 0) {
     // fused MLP1 + GELU + MLP2 + residual (+ next LN1): the hidden activations stay on chip
     MlpParams mp{};
     mp.M = M_static; mp.m_dev = m_dev; mp.F = F; mp.b1 = L.b_1; mp.b2 = L.b_2; mp.x = x; mp.ln_eps = g.ln_eps;
@@ -642,23 +606,23 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
       mp.ln_g = Ln.ln1_g; mp.ln_b = Ln.ln1_b; mp.ln_out = w.hbuf; mp.ln_cap = w.rows_cap;
     }
     probe_begin(PK_MLP1, s);
-    CFD_CUDA(launch_mlp(ta_h, L.tm_1c, L.tm_1h, L.tm_2c, mp, rows_grid, s, staged ? &tx : nullptr, staged ? &tln : nullptr));
+    CFD_CUDA(launch_mlp(o, ta_h, L.tm_1c, L.tm_1h, L.tm_2c, mp, rows_grid, s, staged ? &tx : nullptr, staged ? &tln : nullptr));
     probe_end(PK_MLP1, s);
     return CFD_OK;
   }
   // MLP1 + GELU
   p = GemmParams{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = w.rows_cap; p.N = F; p.K = d; p.bias = L.b_1; p.out_bf16 = w.ff;
-  CFD_CUDA(launch_gemm(EPI_BF16_BIAS_GELU, ta_h, L.tm_1, p, rows_grid, s, PK_MLP1));
+  CFD_CUDA(launch_gemm(o, EPI_BF16_BIAS_GELU, ta_h, L.tm_1, p, rows_grid, s, PK_MLP1));
   // MLP2 + residual (+ next layer's LN1 -> hbuf)
   p = GemmParams{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = x_cap; p.N = d; p.K = F; p.bias = L.b_2; p.out_f32 = x; p.ld_out = d;
   if (fuse_ln && l + 1 < g.n_layers) {
     const LayerDev& Ln = c->layers[l + 1];
     p.ln_g = Ln.ln1_g; p.ln_b = Ln.ln1_b; p.ln_out = w.hbuf; p.ln_cap = w.rows_cap; p.ln_eps = g.ln_eps;
-    CFD_CUDA(launch_gemm(EPI_F32_RESID_LN, ta_f, L.tm_2, p, rows_grid, s, PK_MLP2));
+    CFD_CUDA(launch_gemm(o, EPI_F32_RESID_LN, ta_f, L.tm_2, p, rows_grid, s, PK_MLP2));
   } else {
-    CFD_CUDA(launch_gemm(EPI_F32_RESID, ta_f, L.tm_2, p, rows_grid, s, PK_MLP2));
+    CFD_CUDA(launch_gemm(o, EPI_F32_RESID, ta_f, L.tm_2, p, rows_grid, s, PK_MLP2));
   }
   return CFD_OK;
 }
@@ -740,73 +704,39 @@ cfd_status cfdx_probe_install(int32_t kind, void* const* h_start, void* const* h
   return CFD_OK;
 }
 
-cfd_status cfdx_set_option(int32_t key, int32_t value) {
+cfd_status cfdx_set_option(cfd_ctx* ctx, int32_t key, int32_t value) {
+  Opts& o = ctx ? ctx->opt : g_dbg_opts;
+  const int b = value ? 1 : 0;
   switch (key) {
     case 0:
-      if (value < 1 || value > 6) return CFD_E_ARG;
-      g_attn_variant = value;
+      if (value != 1 && value != 4) return CFD_E_ARG;
+      o.attn_variant = value;
       return CFD_OK;
     case 1:
-      if (value < 0 || value > 12 || (value & 1)) return CFD_E_ARG;  // 10, 12: variant 4 only
-      g_attn_npp = value;
+      if (value < 0 || value > 8 || (value & 1)) return CFD_E_ARG;
+      o.attn_npp = value;
       return CFD_OK;
-    case 2:
-      g_fused_mlp = value ? 1 : 0;
-      return CFD_OK;
-    case 4:
-      g_mlp_cluster = value ? 1 : 0;
-      return CFD_OK;
-    case 3:
-      g_staged_epi = value ? 1 : 0;
-      return CFD_OK;
-    case 7:
-      g_gemm_bres = value ? 1 : 0;
-      return CFD_OK;
-    case 9:
-      g_attn_token = value ? 1 : 0;
-      return CFD_OK;
-    case 10:
-      g_attn_split = value ? 1 : 0;
-      return CFD_OK;
-    case 11:
-      g_fuse_oproj = value ? 1 : 0;
-      return CFD_OK;
-    case 12:
-      g_attn_qmajor = value ? 1 : 0;
-      return CFD_OK;
-    case 13:
-      g_embed_mode0 = value ? 1 : 0;
-      return CFD_OK;
-    case 14:
-      g_embed_img = value ? 1 : 0;
-      return CFD_OK;
-    case 15:
-      g_embed_ln = value ? 1 : 0;
-      return CFD_OK;
-    case 16:
-      g_attn_dyn = value ? 1 : 0;
-      return CFD_OK;
-    case 17:
-      if (value < 0 || value > 4096) return CFD_E_ARG;
-      g_sm_cap = value;
-      return CFD_OK;
-    case 18:
-      g_balanced_grid = value ? 1 : 0;
-      return CFD_OK;
-    case 19:
-      g_keep_x1 = value ? 1 : 0;
-      return CFD_OK;
-    case 20:
-      g_preload_x = value ? 1 : 0;
-      return CFD_OK;
-    case 6:
-      if (value != 4 && value != 6 && value != 8) return CFD_E_ARG;
-      g_attn_stages = value;
-      return CFD_OK;
+    case 2: o.fused_mlp = b; return CFD_OK;
+    case 3: o.staged_epi = b; return CFD_OK;
+    case 4: o.mlp_cluster = b; return CFD_OK;
     case 5:
       if (value < -2 || value > 100000) return CFD_E_ARG;  // -1 / -2: attention trace modes (debug library)
-      g_attn_stagger = value;
+      o.attn_stagger = value;
       return CFD_OK;
+    case 7: o.gemm_bres = b; return CFD_OK;
+    case 11: o.fuse_oproj = b; return CFD_OK;
+    case 12: o.attn_qmajor = b; return CFD_OK;
+    case 13: o.embed_mode0 = b; return CFD_OK;
+    case 14: o.embed_img = b; return CFD_OK;
+    case 15: o.embed_ln = b; return CFD_OK;
+    case 16: o.attn_dyn = b; return CFD_OK;
+    case 17:
+      if (value < 0 || value > 4096) return CFD_E_ARG;
+      o.sm_cap = value;
+      return CFD_OK;
+    case 18: o.balanced_grid = b; return CFD_OK;
+    case 19: o.keep_x1 = b; return CFD_OK;
+    case 20: o.preload_x = b; return CFD_OK;
   }
   return CFD_E_ARG;
 }
@@ -912,7 +842,8 @@ cfd_status cfd_create(const cfd_config* cfg, const cfd_weights* wts, void* strea
 
 cfd_status cfd_destroy(cfd_ctx* c) {
   if (!c) return CFD_OK;
-  cudaDeviceSynchronize();
+  // the caller guarantees no enqueued work still uses ctx (cfdetr.h); cudaFree itself waits
+  // for the device to be idle before releasing the block
   cudaFree(c->block);
   if (c->dec_block) cudaFree(c->dec_block);
   delete c;
@@ -943,9 +874,10 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
   if (w.bytes + 1024 > ws_bytes) return CFD_E_CAPACITY;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const cfd_config& g = c->cfg;
+  const Opts& o = c->opt;
   const int d = g.d_model, M = B * c->Nc;
   probe_begin(PK_META, s);
-  launch_ex(coarse_meta_kernel, dim3(1), dim3(256), 0, s, w.ccu, w.meta, B, c->Nc);
+  launch_ex(coarse_meta_kernel, dim3(1), dim3(256), 0, s, w.ccu, w.meta, B, c->Nc, w.attn_work);
   probe_end(PK_META, s);
   ++g_launches;
   CFD_CUDA(cudaGetLastError());
@@ -954,7 +886,7 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
   p.pe = c->pec; p.pe_rows = c->Nc;
   // layer-0 LN1 fused into the embed epilogue (option 15): hbuf rows [0, M) here, the pad
   // rows [M, pad_rows) that attention tail tiles may read zeroed by a memset
-  const bool ln0 = g_embed_ln && d == pick_bn(d);
+  const bool ln0 = o.embed_ln && d == pick_bn(d);
   if (ln0) {
     const LayerDev& L0 = c->layers[0];
     p.ln_g = L0.ln1_g; p.ln_b = L0.ln1_b; p.ln_out = w.hbuf; p.ln_cap = w.rows_cap; p.ln_eps = g.ln_eps;
@@ -964,7 +896,7 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
   const int Pc = g.patch_coarse, gw = g.img_w / Pc, gh = g.img_h / Pc;
   // image-sourced embed: 3Pc-element segments split into 32-element k-blocks, whole coarse
   // rows per 128-row tile, box dims <= 256
-  const bool img_ok = g_embed_img && d == 256 && (3 * Pc) % 32 == 0 && gw <= 128 && (128 / gw) <= 256 && c->has_wc32;
+  const bool img_ok = o.embed_img && d == 256 && (3 * Pc) % 32 == 0 && gw <= 128 && (128 / gw) <= 256 && c->has_wc32;
   if (img_ok) {
     CUtensorMap ti;
     p.img_gw = gw;
@@ -972,13 +904,13 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
     p.img_thirds = 3 * Pc / 32;
     if (!make_img_map(&ti, images, B, g.img_h, g.img_w, Pc, p.img_rb)) return CFD_E_CUDA;
     probe_begin(PK_EMBED_C, s);
-    cudaError_t e = launch_gemm_t<256, EPI_EMBED_COARSE, 3>(ti, c->tm_wc32, p, M, s, nullptr, nullptr);
+    cudaError_t e = launch_gemm_t<256, EPI_EMBED_COARSE, 3>(o, ti, c->tm_wc32, p, M, s, nullptr, nullptr);
     probe_end(PK_EMBED_C, s);
     CFD_CUDA(e);
   } else {
     {
       const long long vec = (long long)B * g.img_h * (g.img_w / g.patch_coarse) * ((g.patch_coarse * 6) / 16);
-      const int blocks = (int)std::min<long long>((vec + 255) / 256, (long long)num_sms() * 8);
+      const int blocks = (int)std::min<long long>((vec + 255) / 256, (long long)num_sms(o) * 8);
       probe_begin(PK_IM2COL, s);
       launch_ex(im2col_kernel, dim3(blocks), dim3(256), 0, s, images, w.patches, B, g.img_h, g.img_w, g.patch_coarse);
       probe_end(PK_IM2COL, s);
@@ -987,7 +919,7 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
     }
     CUtensorMap ta;
     if (!make_amap(&ta, w.patches, M, c->Kc)) return CFD_E_CUDA;
-    CFD_CUDA(launch_gemm(EPI_EMBED_COARSE, ta, c->tm_wc, p, M, s, PK_EMBED_C));
+    CFD_CUDA(launch_gemm(o, EPI_EMBED_COARSE, ta, c->tm_wc, p, M, s, PK_EMBED_C));
   }
   (void)gh;
   const int max_qtiles = (c->Nc + ATTN_BQ - 1) / ATTN_BQ;
@@ -1037,13 +969,14 @@ cfd_status cfd_select_regions(cfd_ctx* c, int32_t T, const float* scores, cfd_se
 
 static cfd_status launch_gather(cfd_ctx* c, int T, const uint16_t* images, const float* x0, const int32_t* sel_idx,
                                 const int32_t* sel_count, float* X, int32_t* cu, int32_t* msrc, uint16_t* A_f,
-                                int32_t* frow, int32_t* fidx, int32_t* meta, cudaStream_t s) {
+                                int32_t* frow, int32_t* fidx, int32_t* meta, int32_t* attn_work, cudaStream_t s) {
   GatherParams gp{};
   const cfd_config& g = c->cfg;
   gp.T = T; gp.Nc = c->Nc; gp.gc_w = c->gc_w; gp.m = c->m; gp.gf_w = c->gf_w; gp.d = g.d_model;
   gp.H = g.img_h; gp.W = g.img_w; gp.Pf = g.patch_fine;
   gp.images = images; gp.x0 = x0; gp.sel_idx = sel_idx; gp.sel_count = sel_count; gp.X = X; gp.cu_seqlens = cu;
   gp.mixed_src = msrc; gp.A_f = A_f; gp.frow = frow; gp.fidx = fidx; gp.meta = meta; gp.err = c->err;
+  gp.zero2 = attn_work;
   const int G = std::max(1, std::min(32, (c->Nc + 31) / 32));
   const size_t smem = (size_t)2 * c->Nc * sizeof(int32_t);
   probe_begin(PK_GATHER, s);
@@ -1081,14 +1014,14 @@ cfd_status cfd_batch_refine(cfd_ctx* c, int32_t T, const uint16_t* images, const
     fine_grid = (m2 > 1) ? (int)((tot - (long long)T * c->Nc) / (m2 - 1) * m2) : 0;
   }
   cfd_status st = launch_gather(c, T, images, x0, sel_idx, sel_count, y, cu, msrc, w.patches, w.frow, w.fidx,
-                                w.meta, s);
+                                w.meta, w.attn_work, s);
   if (st != CFD_OK) return st;
   CUtensorMap ta;
   if (!make_amap(&ta, w.patches, cap + 128, c->Kf)) return CFD_E_CUDA;
   GemmParams p{};
   p.M = 0; p.m_dev = w.meta + 1; p.m_cap = cap; p.N = d; p.K = c->Kf; p.bias = c->bf; p.out_f32 = y; p.ld_out = d;
   p.pe = c->pef; p.pe_rows = c->Nf; p.frow = w.frow; p.fidx = w.fidx;
-  CFD_CUDA(launch_gemm(EPI_EMBED_FINE, ta, c->tm_wf, p, std::max(fine_grid, 1), s, PK_EMBED_F));
+  CFD_CUDA(launch_gemm(c->opt, EPI_EMBED_FINE, ta, c->tm_wf, p, std::max(fine_grid, 1), s, PK_EMBED_F));
   const int max_qtiles = (c->Nf + ATTN_BQ - 1) / ATTN_BQ;
   for (int l = 0; l < g.n_layers; ++l) {
     st = run_layer(c, l, y, cap, 0, w.meta, std::max(rows_grid, 1), cu, T, max_qtiles, w, false, nullptr, 0, s);
@@ -1165,6 +1098,7 @@ cfd_status cfd_decode(cfd_ctx* c, int32_t T, const float* y, const int32_t* cu, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const cfd_config& g = c->cfg;
   const int d = g.d_model, Q = c->dec_q, QR = T * Q;
+  if ((size_t)QR + 128 > (size_t)w.rows_cap) return CFD_E_CAPACITY;  // obuf rows (carve sizes them)
   // workspace reuse: LN_m(y) -> hbuf, [k | v] -> qkv (2d columns), o -> obuf (T*Q rows),
   // LN_q(Q0) and q -> the ff region (256 rows each), z (if not requested) -> the patches region
   __nv_bfloat16* hq = w.ff;
@@ -1178,25 +1112,22 @@ cfd_status cfd_decode(cfd_ctx* c, int32_t T, const float* y, const int32_t* cu, 
       !make_amap(&tmo, w.obuf, w.rows_cap, d))
     return CFD_E_CUDA;
   // queries: q = LN_q(Q0) W_q + b_q (rows >= Q zero / padding)
-  CFD_CUDA(launch_layernorm(d, c->dq0, c->dlnq_g, c->dlnq_b, hq, Q, nullptr, 256, g.ln_eps, Q, s));
+  const Opts& o = c->opt;
+  CFD_CUDA(launch_layernorm(o, d, c->dq0, c->dlnq_g, c->dlnq_b, hq, Q, nullptr, 256, g.ln_eps, Q, s));
   GemmParams p{};
   p.M = Q; p.m_cap = 256; p.N = d; p.K = d; p.bias = c->dbq; p.out_bf16 = qb;
-  CFD_CUDA(launch_gemm(EPI_BF16_BIAS, tmhq, c->tm_dq, p, Q, s));
+  CFD_CUDA(launch_gemm(o, EPI_BF16_BIAS, tmhq, c->tm_dq, p, Q, s));
   // memory: [k | v] = LN_m(y) W_kv + b_kv over the packed tokens (count cu[T] on the device)
   const int* m_dev = cu + T;
-  CFD_CUDA(launch_layernorm(d, y, c->dlnm_g, c->dlnm_b, w.hbuf, max_tokens, m_dev, w.rows_cap, g.ln_eps, max_tokens, s));
+  CFD_CUDA(launch_layernorm(o, d, y, c->dlnm_g, c->dlnm_b, w.hbuf, max_tokens, m_dev, w.rows_cap, g.ln_eps, max_tokens, s));
   p = GemmParams{};
   p.M = max_tokens; p.m_dev = m_dev; p.m_cap = w.rows_cap; p.N = 2 * d; p.K = d; p.bias = c->dbkv; p.out_bf16 = kvb;
-  CFD_CUDA(launch_gemm(EPI_BF16_BIAS, tmhm, c->tm_dkv, p, max_tokens, s));
+  CFD_CUDA(launch_gemm(o, EPI_BF16_BIAS, tmhm, c->tm_dkv, p, max_tokens, s));
   // cross-attention: one CTA per (head, task), the Q query rows against task t's tokens
   {
     auto kern = attn_tc_kernel<32, 3, true>;
     constexpr int smem = AttnSmem<32, 3>::TOTAL;
-    static bool attr = false;
-    if (!attr) {
-      CFD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = true;
-    }
+    CFD_CUDA(ensure_smem_attr(kern, smem));
     AttnParams ap{};
     ap.cu_seqlens = cu; ap.d_model = d; ap.out = w.obuf; ap.n_q = Q;
     ap.scale_log2 = 1.4426950408889634f / std::sqrt((float)c->dh);
@@ -1207,14 +1138,14 @@ cfd_status cfd_decode(cfd_ctx* c, int32_t T, const float* y, const int32_t* cu, 
   // z = Q0 + o W_o + b_o
   {
     const long long vec = (long long)QR * d / 4;
-    const int blocks = (int)std::min<long long>((vec + 255) / 256, (long long)num_sms() * 4);
+    const int blocks = (int)std::min<long long>((vec + 255) / 256, (long long)num_sms(o) * 4);
     launch_ex(broadcast_rows_kernel, dim3(blocks), dim3(256), 0, s, c->dq0, zz, T, Q, d);
     ++g_launches;
     CFD_CUDA(cudaGetLastError());
   }
   p = GemmParams{};
   p.M = QR; p.m_cap = w.rows_cap; p.N = d; p.K = d; p.bias = c->dbo; p.out_f32 = zz; p.ld_out = d;
-  CFD_CUDA(launch_gemm(EPI_F32_RESID, tmo, c->tm_do, p, QR, s));
+  CFD_CUDA(launch_gemm(o, EPI_F32_RESID, tmo, c->tm_do, p, QR, s));
   // heads: [box | c] = sigmoid(z W_head + b_head)
   launch_ex(detect_heads_kernel, dim3((QR + 7) / 8), dim3(256), 0, s, zz, c->dwh, c->dbh, boxes, conf, QR, d);
   ++g_launches;
@@ -1255,7 +1186,7 @@ static cfd_status launch_frames_u8(long long n, const uint8_t* src, const float*
   FrameAffine a;
   for (int i = 0; i < 3; ++i) { a.scale[i] = scale[i]; a.shift[i] = shift[i]; }
   const long long units = std::max(n >> 4, 1LL);
-  const int blocks = (int)std::min<long long>((units + 255) / 256, (long long)num_sms() * 8);
+  const int blocks = (int)std::min<long long>((units + 255) / 256, (long long)num_sms(g_dbg_opts) * 8);
   launch_ex(frames_u8_kernel, dim3(blocks), dim3(256), 0, s, src, dst, n, a);
   ++g_launches;
   CFD_CUDA(cudaGetLastError());
@@ -1299,7 +1230,7 @@ cfd_status cfdx_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* A, const u
   GemmParams p{};
   p.M = M; p.m_cap = M; p.N = N; p.K = K; p.bias = bias; p.out_bf16 = (__nv_bfloat16*)out_bf16; p.out_f32 = out_f32;
   p.ld_out = N;
-  CFD_CUDA(launch_gemm(epi, ta, tb, p, M, static_cast<cudaStream_t>(stream)));
+  CFD_CUDA(launch_gemm(g_dbg_opts, epi, ta, tb, p, M, static_cast<cudaStream_t>(stream)));
   return CFD_OK;
 }
 
@@ -1317,14 +1248,15 @@ cfd_status cfdx_gemm_resid_ln(int32_t M, int32_t N, int32_t K, const uint16_t* A
   GemmParams p{};
   p.M = M; p.m_cap = M; p.N = N; p.K = K; p.bias = bias; p.out_f32 = x; p.ld_out = N;
   p.ln_g = ln_g; p.ln_b = ln_b; p.ln_out = (__nv_bfloat16*)ln_out; p.ln_cap = ln_cap; p.ln_eps = eps;
-  CFD_CUDA(launch_gemm(EPI_F32_RESID_LN, ta, tb, p, M, static_cast<cudaStream_t>(stream), -1, staged ? &tx : nullptr,
+  CFD_CUDA(launch_gemm(g_dbg_opts, EPI_F32_RESID_LN, ta, tb, p, M, static_cast<cudaStream_t>(stream), -1,
+                       staged ? &tx : nullptr,
                        staged ? &tln : nullptr));
   return CFD_OK;
 }
 
 cfd_status cfdx_attention(int32_t T, const int32_t* cu, int32_t max_seqlen, int32_t rows_cap, int32_t d,
                           int32_t nh, const uint16_t* qkv, uint16_t* out, float* lse, int32_t lse_ld,
-                          void* stream) {
+                          int32_t* work_counter, void* stream) {
   if (T <= 0 || !cu || !qkv || !out || max_seqlen <= 0 || rows_cap <= 0 || nh <= 0 || d % nh || d / nh != 32)
     return CFD_E_ARG;
   CUtensorMap tq;
@@ -1332,23 +1264,19 @@ cfd_status cfdx_attention(int32_t T, const int32_t* cu, int32_t max_seqlen, int3
   AttnParams ap{};
   ap.cu_seqlens = cu; ap.d_model = d; ap.out = (__nv_bfloat16*)out; ap.lse = lse; ap.lse_ld = lse_ld;
   ap.scale_log2 = 1.4426950408889634f / std::sqrt(32.0f);
-  ap.stagger = g_attn_stagger;
-  if (g_attn_dyn) {
-    static int* counter = nullptr;  // debug entry point: one process-wide [claims, finished] pair
-    if (!counter) {
-      if (cudaMalloc(&counter, 2 * sizeof(int)) != cudaSuccess) return CFD_E_CUDA;
-      CFD_CUDA(cudaMemsetAsync(counter, 0, 2 * sizeof(int), static_cast<cudaStream_t>(stream)));
-    }
-    ap.work_counter = counter;
-  }
-  CFD_CUDA(launch_attention(tq, ap, (max_seqlen + ATTN_BQ - 1) / ATTN_BQ, nh, T, static_cast<cudaStream_t>(stream)));
+  ap.stagger = g_dbg_opts.attn_stagger;
+  // work_counter: caller-owned zeroed int[2] (dynamic claims, reset by the launch's last CTA)
+  // or NULL (static round-robin); no state is shared between calls
+  if (g_dbg_opts.attn_dyn) ap.work_counter = work_counter;
+  CFD_CUDA(launch_attention(g_dbg_opts, tq, ap, (max_seqlen + ATTN_BQ - 1) / ATTN_BQ, nh, T, static_cast<cudaStream_t>(stream)));
   return CFD_OK;
 }
 
 cfd_status cfdx_layernorm(int32_t M, int32_t d, const float* x, const float* g, const float* b, float eps,
                           uint16_t* y, void* stream) {
   if (M <= 0 || !x || !g || !b || !y) return CFD_E_ARG;
-  CFD_CUDA(launch_layernorm(d, x, g, b, (__nv_bfloat16*)y, M, nullptr, M, eps, M, static_cast<cudaStream_t>(stream)));
+  CFD_CUDA(launch_layernorm(g_dbg_opts, d, x, g, b, (__nv_bfloat16*)y, M, nullptr, M, eps, M,
+                            static_cast<cudaStream_t>(stream)));
   return CFD_OK;
 }
 
@@ -1370,7 +1298,7 @@ cfd_status cfdx_gather(cfd_ctx* c, int32_t T, const uint16_t* images, const floa
   if (!c || T <= 0 || !images || !x0 || !sel_idx || !sel_count || !X || !cu || !msrc || !A_f || !frow || !fidx ||
       !meta)
     return CFD_E_ARG;
-  return launch_gather(c, T, images, x0, sel_idx, sel_count, X, cu, msrc, A_f, frow, fidx, meta,
+  return launch_gather(c, T, images, x0, sel_idx, sel_count, X, cu, msrc, A_f, frow, fidx, meta, nullptr,
                        static_cast<cudaStream_t>(stream));
 }
 

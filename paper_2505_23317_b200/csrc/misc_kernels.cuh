@@ -221,6 +221,8 @@ struct GatherParams {
   int32_t* fidx;                    // [Rcap]
   int32_t* meta;                    // [0] = total tokens, [1] = total fine rows
   int* err;
+  int32_t* zero2;                   // [2] or nullptr: zeroed by block (0, 0) (the call's attention
+                                    // work counter; every later kernel of the call runs after this one)
 };
 
 // grid = (T, G); block = 256 (8 warps).  Every block of task t rebuilds the task's
@@ -235,15 +237,24 @@ __global__ void gather_kernel(const GatherParams p) {
   int32_t* pre = gsm;               // [Nc] number of selected cells before c
   int32_t* pos = gsm + p.Nc;        // [Nc] position in sel list, -1 if unselected
   __shared__ int s_tok_base, s_fine_base, s_k;
+  __shared__ int s_part[32];
   const int t = blockIdx.x, G = gridDim.y, g = blockIdx.y;
   const int Nc = p.Nc, m2 = p.m * p.m;
+  if (p.zero2 && t == 0 && g == 0 && threadIdx.x == 0) { p.zero2[0] = 0; p.zero2[1] = 0; }
+  // K_t = sum of the (clamped) selection counts of tasks u < t: a block-wide strided sum
+  // (O(t / blockDim) loads per thread) instead of a serial walk by one thread
+  {
+    int part = 0;
+    for (int u = threadIdx.x; u < t; u += blockDim.x) part += min(max(p.sel_count[u], 0), Nc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = part;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    int tb = 0, fb = 0;
-    for (int u = 0; u < t; ++u) {
-      const int ku = min(max(p.sel_count[u], 0), Nc);
-      tb += Nc + (m2 - 1) * ku;
-      fb += m2 * ku;
-    }
+    int ksum = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) ksum += s_part[i];
+    const int tb = t * Nc + (m2 - 1) * ksum, fb = m2 * ksum;
     int k = p.sel_count[t];
     if (k < 0 || k > Nc) { atomicOr(p.err, ERR_SEL_COUNT); k = min(max(k, 0), Nc); }
     s_tok_base = tb; s_fine_base = fb; s_k = k;
@@ -371,9 +382,14 @@ __global__ void transpose_bf16_kernel(const uint16_t* __restrict__ in, uint16_t*
 }
 
 // coarse cu_seqlens = [0, Nc, 2Nc, ...] and meta[0] = B*Nc
-__global__ void coarse_meta_kernel(int32_t* cu, int32_t* meta, int B, int Nc) {
+// (+ zeroes the call's attention work counter zero2[2], if any)
+__global__ void coarse_meta_kernel(int32_t* cu, int32_t* meta, int B, int Nc, int32_t* zero2) {
   for (int i = threadIdx.x; i <= B; i += blockDim.x) cu[i] = i * Nc;
-  if (threadIdx.x == 0) { meta[0] = B * Nc; meta[1] = 0; }
+  if (threadIdx.x == 0) {
+    meta[0] = B * Nc;
+    meta[1] = 0;
+    if (zero2) { zero2[0] = 0; zero2[1] = 0; }
+  }
 }
 
 }  // namespace cfd

@@ -123,6 +123,12 @@ def test_decoder_cross_attention_tiny_ragged():
     _check_decode(ci.CONFIGS["tiny"], 3, 16, 0, [0, 4, 16, 1])
 
 
+def test_decoder_tiny_128_queries_more_queries_than_tokens():
+    """Q = 128 queries per task on the tiny geometry (Nf = 64 < Q, 8 tasks): the workspace
+    is sized for T * Q attention-output rows once the decoder is set (obuf overflow)."""
+    _check_decode(ci.CONFIGS["tiny"], 3, 128, 2, [0, 4, 16, 1, 7, 0, 16, 3])
+
+
 def test_decoder_cross_attention_c640_128_queries():
     _check_decode(ci.CONFIGS["c640"], 4, 128, 5, [0, 100, 400])
 

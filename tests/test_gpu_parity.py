@@ -6,6 +6,9 @@ Selection / layouts: bit-exact under the shared-score protocol (both sides selec
 from the GPU's fp32 score tensor).  At the bench's full size
 (c640, 32 frames in flight) the oracle checks a sample of frames.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -21,7 +24,11 @@ if not torch.cuda.is_available():
 from paper_2505_23317_b200.api import CFDetrEncoder, bf16_tensor  # noqa: E402
 
 REL, ABS = 2e-2, 5e-2
+# scores are ~1/Nc (2.5e-3 at c640), so north_star's 5e-2 max-abs bound says nothing about
+# them: they are held to rel-L2 <= REL and a per-element relative bound instead
+SCORE_REL_MAX = 5e-2
 _ENC = {}
+FLIPS = []   # oracle-own-score selection report (SURVEY.md §8(c) shared-score protocol)
 
 
 def enc_for(name):
@@ -38,6 +45,32 @@ def _tol(gpu, ref, what):
     mx = np.abs(gpu - ref).max() if ref.size else 0.0
     assert rel <= REL and mx <= ABS, f"{what}: rel-L2 {rel:.3e} max-abs {mx:.3e}"
     return rel, mx
+
+
+def _score_tol(gpu, ref, what):
+    """Scores: rel-L2 <= REL and max_j |s_gpu[j] - s_ref[j]| / s_ref[j] <= SCORE_REL_MAX
+    (s_ref > 0: softmax columns); still a distribution (sum 1 within fp32 summation)."""
+    gpu = np.asarray(gpu, np.float64)
+    rel = np.linalg.norm(gpu - ref) / np.linalg.norm(ref)
+    relmax = float(np.max(np.abs(gpu - ref) / ref))
+    assert rel <= REL and relmax <= SCORE_REL_MAX, f"{what}: rel-L2 {rel:.3e} max-rel {relmax:.3e}"
+    assert abs(gpu.sum() - 1.0) < 1e-4, f"{what}: sum {gpu.sum()}"
+    return rel, relmax
+
+
+def _own_score_flips(name, t, s_gpu, s_ref, k, sel_shared):
+    """Oracle-own-score run: the oracle selects from its own fp64 scores.
+    Its set may differ from the shared-score set only at the selection boundary: every region
+    swapped in must score (oracle) within twice the measured score error of a region swapped
+    out.  The flip count is recorded (FLIPS, printed by the last test of the module)."""
+    sel_own = O.select_topk(s_ref, k)
+    a, b = set(sel_shared.tolist()), set(sel_own.tolist())
+    only_gpu, only_own = sorted(a - b), sorted(b - a)
+    err = float(np.max(np.abs(np.asarray(s_gpu, np.float64) - s_ref)))
+    if only_own:
+        gap = max(s_ref[i] for i in only_own) - min(s_ref[j] for j in only_gpu)
+        assert gap <= 2 * err + 1e-12, f"{name} task {t}: flip not explained by score error ({gap} > 2*{err})"
+    FLIPS.append((name, t, k, len(only_own), err))
 
 
 def run_workload(name, ks, frames=None, sample=None, task0=0):
@@ -63,10 +96,11 @@ def run_workload(name, ks, frames=None, sample=None, task0=0):
         for l in range(cfg.n_layers):
             _tol(co["layer_out"][l, t].cpu().numpy(), oc["layers"][l], f"{name} task {t} coarse layer {l}")
         s_gpu = co["scores"][t].cpu().numpy()
-        _tol(s_gpu, oc["scores"], f"{name} task {t} scores")
+        _score_tol(s_gpu, oc["scores"], f"{name} task {t} scores")
         # shared-score protocol: the oracle selects from the GPU's scores, bit-exact
         sel_o = O.select_topk(s_gpu, ks[t])
         assert np.array_equal(sel["sel_idx"][t, :ks[t]].cpu().numpy(), sel_o)
+        _own_score_flips(name, t, s_gpu, oc["scores"], ks[t], sel_o)
         rr = O.refine_encode(cfg, w, imgs[t], oc["x0"], sel_o)
         assert np.array_equal(ro["mixed_src"][cu[t]:cu[t + 1]].cpu().numpy(), rr["mixed_src"])
         for l in range(cfg.n_layers):
@@ -189,10 +223,8 @@ def test_cuda_graph_capture_replays_identically():
 def test_fused_mlp_matches_two_gemm_path():
     """The fused MLP kernel (default) against the MLP1 + MLP2 GEMM launches it replaces
     (same selection for both runs: near-tie scores may otherwise pick different regions)."""
-    from paper_2505_23317_b200 import _lib as L
-    lib = L.load()
     cfg = ci.CONFIGS["c640"]
-    enc = enc_for("c640")
+    enc = CFDetrEncoder(cfg, ci.make_weights(cfg, seed=0), max_tasks=8)
     imgs = bf16_tensor(ci.make_frames(cfg, 3, task0=7), "cuda")
     ks = [0, 100, 400]
     co = enc.coarse_encode(imgs)
@@ -201,14 +233,14 @@ def test_fused_mlp_matches_two_gemm_path():
     outs = []
     try:
         for fused in (1, 0):
-            assert lib.cfdx_set_option(2, fused) == 0
+            enc.set_option(2, fused)
             c2 = enc.coarse_encode(imgs)
             ro = enc.batch_refine(imgs, x0, sel["sel_idx"], sel["sel_count"])
             torch.cuda.synchronize()
             n = int(ro["cu_seqlens"][-1])
             outs.append((c2["y"].clone(), ro["y"][:n].clone()))
     finally:
-        lib.cfdx_set_option(2, 1)
+        enc.set_option(2, 1)
     for a, b in zip(outs[0], outs[1]):
         rel = ((a - b).norm() / b.norm()).item()
         assert rel < 3e-3, rel
@@ -219,10 +251,8 @@ def test_staged_epilogues_match_direct_epilogues():
     the per-row direct-store epilogues on a ragged batch.  Not bitwise: with staging off the
     O-projection runs the two-CTA/SM configuration whose LayerNorm row sums are taken by one
     warp over all 256 columns instead of two 128-column halves (different rounding order)."""
-    from paper_2505_23317_b200 import _lib as L
-    lib = L.load()
     cfg = ci.CONFIGS["c640"]
-    enc = enc_for("c640")
+    enc = CFDetrEncoder(cfg, ci.make_weights(cfg, seed=0), max_tasks=8)
     imgs = bf16_tensor(ci.make_frames(cfg, 3, task0=11), "cuda")
     ks = [0, 37, 400]
     co = enc.coarse_encode(imgs)
@@ -231,14 +261,14 @@ def test_staged_epilogues_match_direct_epilogues():
     outs = []
     try:
         for staged in (1, 0):
-            assert lib.cfdx_set_option(3, staged) == 0
+            enc.set_option(3, staged)
             c2 = enc.coarse_encode(imgs)
             ro = enc.batch_refine(imgs, x0, sel["sel_idx"], sel["sel_count"])
             torch.cuda.synchronize()
             n = int(ro["cu_seqlens"][-1])
             outs.append((c2["y"].clone(), c2["scores"].clone(), ro["y"][:n].clone()))
     finally:
-        lib.cfdx_set_option(3, 1)
+        enc.set_option(3, 1)
     for a, b in zip(outs[0], outs[1]):
         rel = ((a - b).norm() / b.norm()).item()
         assert rel < 3e-3, rel
@@ -249,10 +279,8 @@ def test_mlp_cta_pair_variant_matches_single_cta_bitwise():
     operand; cfdx_set_option(4, 1)) accumulates the same products in the same k order as the
     single-CTA kernel: outputs agree bit for bit, including an odd tile count (ghost tile in
     the last pair)."""
-    from paper_2505_23317_b200 import _lib as L
-    lib = L.load()
     cfg = ci.CONFIGS["c640"]
-    enc = enc_for("c640")
+    enc = CFDetrEncoder(cfg, ci.make_weights(cfg, seed=0), max_tasks=8)
     imgs = bf16_tensor(ci.make_frames(cfg, 3, task0=5), "cuda")
     ks = [0, 100, 37]
     co = enc.coarse_encode(imgs)
@@ -262,17 +290,17 @@ def test_mlp_cta_pair_variant_matches_single_cta_bitwise():
     try:
         # the pair kernel has no fused O-projection; the single-CTA side runs with x1 stored
         # (option 19 = 0), which is bitwise the separate O-projection (test below)
-        assert lib.cfdx_set_option(19, 0) == 0
+        enc.set_option(19, 0)
         for cl in (0, 1):
-            assert lib.cfdx_set_option(4, cl) == 0
+            enc.set_option(4, cl)
             c2 = enc.coarse_encode(imgs)
             ro = enc.batch_refine(imgs, x0, sel["sel_idx"], sel["sel_count"])
             torch.cuda.synchronize()
             n = int(ro["cu_seqlens"][-1])
             outs.append((c2["y"].clone(), ro["y"][:n].clone()))
     finally:
-        lib.cfdx_set_option(4, 0)
-        lib.cfdx_set_option(19, 1)
+        enc.set_option(4, 0)
+        enc.set_option(19, 1)
     for a, b in zip(outs[0], outs[1]):
         assert torch.equal(a, b)
 
@@ -282,10 +310,8 @@ def test_fused_oproj_matches_separate_oproj_bitwise():
     default) against the separate O-projection GEMM launch: the same products in the same
     order (acc2 = o W_o^T, the same staged residual / LayerNorm pass, LN2 to TMEM instead of
     memory), so every output agrees bit for bit on a ragged batch."""
-    from paper_2505_23317_b200 import _lib as L
-    lib = L.load()
     cfg = ci.CONFIGS["c640"]
-    enc = enc_for("c640")
+    enc = CFDetrEncoder(cfg, ci.make_weights(cfg, seed=0), max_tasks=8)
     imgs = bf16_tensor(ci.make_frames(cfg, 4, task0=9), "cuda")
     ks = [0, 100, 37, 400]
     co = enc.coarse_encode(imgs)
@@ -294,15 +320,16 @@ def test_fused_oproj_matches_separate_oproj_bitwise():
     outs = []
     try:
         for opj, keep in ((1, 0), (0, 0), (1, 1)):
-            assert lib.cfdx_set_option(11, opj) == 0 and lib.cfdx_set_option(19, keep) == 0
+            enc.set_option(11, opj)
+            enc.set_option(19, keep)
             c2 = enc.coarse_encode(imgs, want_layers=True)
             ro = enc.batch_refine(imgs, x0, sel["sel_idx"], sel["sel_count"], want_layers=True)
             torch.cuda.synchronize()
             n = int(ro["cu_seqlens"][-1])
             outs.append((c2["layer_out"].clone(), c2["scores"].clone(), ro["layer_out"][:, :n].clone()))
     finally:
-        lib.cfdx_set_option(11, 1)
-        lib.cfdx_set_option(19, 1)
+        enc.set_option(11, 1)
+        enc.set_option(19, 1)
     for a, b in zip(outs[0], outs[1]):
         assert torch.equal(a, b)
     # option 19 (default): x1 kept in TMEM and the MLP accumulated onto it, x2 = (x1 + MLP) + b2
@@ -394,3 +421,17 @@ def test_bench_lanes_concurrent_equal_full_batch_and_oracle():
         cu = ro["cu_seqlens"].cpu().numpy()
         _tol(ro["y"][cu[t]:cu[t + 1]].cpu().numpy(), rr["y"], f"lane frame {t} refine output")
         e.close()
+
+
+def test_zz_own_score_flip_report():
+    """Prints the oracle-own-score boundary-flip counts gathered by the parity runs above."""
+    if not FLIPS:
+        pytest.skip("no parity run recorded flips in this session")
+    tot = sum(f[3] for f in FLIPS)
+    lines = [f"{n} task {t} k={k}: {fl} flip(s), max |ds| {e:.2e}" for n, t, k, fl, e in FLIPS]
+    print("\noracle-own-score selection flips: %d over %d tasks\n  " % (tot, len(FLIPS)) + "\n  ".join(lines))
+    out = os.environ.get("CFD_PARITY_REPORT")
+    if out:
+        with open(out, "w") as f:
+            json.dump([dict(config=n, task=t, k=k, flips=fl, max_abs_score_err=e) for n, t, k, fl, e in FLIPS], f,
+                      indent=1)

@@ -1,4 +1,4 @@
-"""One attention correctness case: python tools/attn_check.py VARIANT NPP 400,640,1 [d]"""
+"""One attention correctness case: python tools/attn_check.py VARIANT NPP 400,640,1 [d]  (cfdx_set_option keys 0 / 1)"""
 import os
 import sys
 
@@ -12,10 +12,7 @@ lens = [int(x) for x in sys.argv[3].split(",")]
 d = int(sys.argv[4]) if len(sys.argv) > 4 else 256
 nh = d // 32
 lib = L.load()
-assert lib.cfdx_set_option(0, var) == 0 and lib.cfdx_set_option(1, npp) == 0
-assert lib.cfdx_set_option(6, int(os.environ.get("CFD_STAGES", "4"))) == 0
-assert lib.cfdx_set_option(9, int(os.environ.get("CFD_TOKEN", "0"))) == 0
-assert lib.cfdx_set_option(10, int(os.environ.get("CFD_SPLIT", "0"))) == 0
+assert lib.cfdx_set_option(None, 0, var) == 0 and lib.cfdx_set_option(None, 1, npp) == 0
 cu_l = [0]
 for n in lens:
     cu_l.append(cu_l[-1] + n)
@@ -35,8 +32,9 @@ qkv = qkv.to(torch.bfloat16)
 cu = torch.tensor(cu_l, dtype=torch.int32, device="cuda")
 out = torch.zeros(cap, d, device="cuda", dtype=torch.bfloat16)
 lse = torch.zeros(nh, cap, device="cuda")
+work = torch.zeros(2, dtype=torch.int32, device="cuda")
 st = lib.cfdx_attention(len(lens), cu.data_ptr(), max(lens), cap, d, nh, qkv.data_ptr(), out.data_ptr(),
-                        lse.data_ptr(), cap, torch.cuda.current_stream().cuda_stream)
+                        lse.data_ptr(), cap, work.data_ptr(), torch.cuda.current_stream().cuda_stream)
 torch.cuda.synchronize()
 q, k, v = qkv[:, :d].float(), qkv[:, d:2 * d].float(), qkv[:, 2 * d:].float()
 ref = torch.zeros(cap, d, device="cuda")

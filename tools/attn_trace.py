@@ -17,12 +17,12 @@ import cfd_inputs as ci  # noqa: E402
 from paper_2505_23317_b200 import _lib as L  # noqa: E402
 from paper_2505_23317_b200.api import CFDetrEncoder, bf16_tensor  # noqa: E402
 
-for kv in os.environ.get("CFD_OPTS", "").split():
-    k_, v_ = (int(t) for t in kv.split("="))
-    assert L.load().cfdx_set_option(k_, v_) == 0
+OPTS = [tuple(int(t) for t in kv.split("=")) for kv in os.environ.get("CFD_OPTS", "").split()]
 cfg = ci.CONFIGS["c640"]
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 enc = CFDetrEncoder(cfg, ci.make_weights(cfg, seed=0), max_tasks=B)
+for k_, v_ in OPTS:
+    enc.set_option(k_, v_)
 imgs = bf16_tensor(ci.make_frames(cfg, B), "cuda")
 co = enc.coarse_encode(imgs)
 sel = enc.select_regions(co["scores"], k=[100] * B)

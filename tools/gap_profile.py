@@ -18,14 +18,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--option", action="append", default=[])
 ap.add_argument("--frames", type=int, default=32)
 a = ap.parse_args()
-for kv in a.option:
-    k_, v_ = (int(t) for t in kv.split("="))
-    assert L.load().cfdx_set_option(k_, v_) == 0
+OPTS = [tuple(int(t) for t in kv.split("=")) for kv in a.option]
 cfg = ci.CONFIGS["c640"]
 B = a.frames
 ks = [25 * cfg.n_coarse // 100] * B
 counts = [cfg.n_coarse + (cfg.m ** 2 - 1) * ks[0]] * B
 enc = CFDetrEncoder(cfg, ci.make_weights(cfg, seed=0), max_tasks=B)
+for k_, v_ in OPTS:
+    enc.set_option(k_, v_)
 imgs = bf16_tensor(ci.make_frames(cfg, B), "cuda")
 s = torch.cuda.Stream()
 co, sel, ro = {}, {}, {}

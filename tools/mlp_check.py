@@ -15,7 +15,7 @@ imgs = bf16_tensor(imgs_np, "cuda")
 oc = O.coarse_encode(cfg, w, [imgs_np[1]])[0]
 res = []
 for fused in (1, 0, 1, 0):
-    assert lib.cfdx_set_option(2, fused) == 0
+    enc.set_option(2, fused)
     co = enc.coarse_encode(imgs, want_layers=True)
     torch.cuda.synchronize()
     y = co["layer_out"][:, 1].double().cpu().numpy()
