@@ -785,6 +785,7 @@ def gather_and_check(args, work, full, rank, world, dev):
     protocol: the oracle selects from the GPU's scores; north_star tolerance rel-L2 <= 2e-2,
     max-abs <= 5e-2) and counts the oracle-own-score selection flips."""
     import torch
+    import torch.distributed
     from paper_2505_23317_b200 import shard
     cfg = work.cfg
     Nc, Nf, d = cfg.n_coarse, cfg.n_fine, cfg.d_model
@@ -829,7 +830,7 @@ def gather_and_check(args, work, full, rank, world, dev):
             "tasks": checked, "max_rel_l2": worst_rel, "max_abs": worst_abs,
             "own_score_selection_flips": flips,
             "pass": worst_rel <= 2e-2 and worst_abs <= 5e-2,
-            "gathered_via": "nccl all_gather" if world > 1 else "local"}
+            "gathered_via": f"{torch.distributed.get_backend()} all_gather" if world > 1 else "local"}
 
 
 def main():
