@@ -12,6 +12,25 @@ namespace cfd {
 
 constexpr int ATTN_MAX_T = 4096;  // tasks per persistent attention launch (prefix table in smem)
 
+// Debug-library pipeline trace (-DCFD_TRACE, read by cfdx_attn_trace): clock64() per
+// (CTA < 148, warpgroup w < 4, item it < 2, sub-tile u < 12) at word ((b*4+w)*2+it)*12+u)*8 + ev:
+//   0 softmax: s_full passed   1 S in registers   2 row max done   3 exps done
+//   4 o_full passed (+ O rescale)   5 p_full arrived   6 MMA: QK(u) issued   7 MMA: PV(u) issued
+// (softmax events from warp 0 of the warpgroup, lane 0); word ATTN_TRACE_T0 + b = kernel start.
+constexpr int ATTN_TRACE_T0 = 148 * 4 * 2 * 12 * 8;
+constexpr int ATTN_TRACE_WORDS = ATTN_TRACE_T0 + 148;
+#ifdef CFD_TRACE
+__device__ unsigned long long g_attn_trace[ATTN_TRACE_WORDS];
+#define ATTN_TR(w_, it_, u_, ev_)                                                                  \
+  do {                                                                                            \
+    if ((it_) < 2 && (u_) < 12 && blockIdx.x < 148)                                               \
+      g_attn_trace[(((blockIdx.x * 4 + (w_)) * 2 + (it_)) * 12 + (u_)) * 8 + (ev_)] = clock64();  \
+  } while (0)
+#else
+#define ATTN_TR(w_, it_, u_, ev_) do { } while (0)
+#endif
+
+
 // ---------------------------------------------------------------- packed fp32 helpers
 __device__ __forceinline__ void fma2(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0,
                                      float c1) {

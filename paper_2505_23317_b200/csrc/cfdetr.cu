@@ -29,6 +29,7 @@
 #include "attn_tc.cuh"
 #include "attn_common.cuh"
 #include "attn4_tc.cuh"
+#include "attn7_tc.cuh"
 #include "gemm_tc.cuh"
 #include "misc_kernels.cuh"
 #include "mlp_tc.cuh"
@@ -106,7 +107,8 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
 // copy (set per ctx); the ctx-less debug entry points use g_dbg_opts.  Defaults = the measured
 // best configuration.
 struct Opts {
-  int attn_variant = 4;   // 1: one q-tile per CTA (v1), 4: three q-tiles per CTA (v4)
+  int attn_variant = 4;   // 1: one q-tile per CTA (v1), 4: three q-tiles per CTA (v4), 7: independent
+                          // per-warpgroup items and pipelines (v7)
   int attn_npp = 4;       // v4: polynomial-exp pairs of every 16
   int attn_stagger = 0;   // v4: warpgroup start stagger; -1 / -2 trace modes (debug library)
   int attn_qmajor = 1;    // v4: q-triple-major item order for equal-length batches (option 12)
@@ -123,6 +125,8 @@ struct Opts {
   int balanced_grid = 0;  // fewest CTAs with the same number of rounds (18)
   int keep_x1 = 1;        // fused O-projection: x1 stays in TMEM, MMA2 accumulates onto it (19)
   int preload_x = 0;      // with 19: x loaded into acc2 before MMA_o (20; measured slower)
+  int attn_sleep = 32;    // v7: MMA / producer warp sleep when idle, ns (21: 0, 32, 128)
+  int attn_nwg = 4;       // v7: softmax warpgroups per CTA (22: 3 or 4)
 };
 Opts g_dbg_opts;
 
@@ -315,8 +319,8 @@ bool make_wmap(CUtensorMap* m, const void* w, int N, int K) {
 bool make_amap(CUtensorMap* m, const void* a, int rows, int K) {
   return make_tmap(m, a, K, rows, K, GEMM_BK, GEMM_BM, CU_TENSOR_MAP_SWIZZLE_128B);
 }
-bool make_qkvmap(CUtensorMap* m, const void* qkv, int rows, int d) {
-  return make_tmap(m, qkv, 3 * d, rows, 3 * d, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
+bool make_qkvmap(CUtensorMap* m, const void* qkv, int rows, int d, int box_rows = 128) {
+  return make_tmap(m, qkv, 3 * d, rows, 3 * d, 32, box_rows, CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 // tw1: W1 with 128-row boxes (single-CTA kernel); tw1h: 64-row boxes (CTA-pair kernel)
@@ -384,11 +388,44 @@ cudaError_t launch_attn4_t(const Opts& o, const CUtensorMap& tq, const AttnParam
   return e;
 }
 
-cudaError_t launch_attention(const Opts& o, const CUtensorMap& tq, const AttnParams& p, int max_qtiles, int nh, int T,
-                             cudaStream_t s) {
+template <int NPP, int SLEEP = 32, int NWG = 4>
+cudaError_t launch_attn7_t(const Opts& o, const CUtensorMap& tq64, const AttnParams& p, int items_ub, int nh, int T,
+                           cudaStream_t s) {
+  auto kern = attn7_tc_kernel<NWG, NPP, SLEEP>;
+  constexpr int smem = Attn7Smem<NWG>::TOTAL;
+  if (cudaError_t e = ensure_smem_attr(kern, smem); e != cudaSuccess) return e;
+  const int grid = std::max(1, std::min((items_ub + NWG - 1) / NWG, num_sms(o)));
+  cudaError_t e = launch_ex(kern, dim3(grid), dim3(attn7_threads(NWG)), smem, s, tq64, p, T, nh);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess && getenv("CFD_VERBOSE")) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kern);
+    fprintf(stderr, "attention v7 launch (grid %d, %d threads, %d B smem; kernel: %d regs): %s\n", grid,
+            attn7_threads(NWG), smem, fa.numRegs, cudaGetErrorString(e));
+  }
+  return e;
+}
+
+// tq: qkv map with 128-row boxes (v1, v4); tq64: the same tensor with 64-row boxes (v7)
+cudaError_t launch_attention(const Opts& o, const CUtensorMap& tq, const CUtensorMap& tq64, const AttnParams& p,
+                             int max_qtiles, int nh, int T, cudaStream_t s) {
   probe_begin(PK_ATTN, s);
   cudaError_t e;
-  if (o.attn_variant == 4 && T <= ATTN_MAX_T) {
+  if (o.attn_variant == 7 && T <= ATTN7_MAX_T) {
+    const int items_ub = T * max_qtiles * nh;
+    switch (o.attn_npp) {
+      case 0: e = launch_attn7_t<0>(o, tq64, p, items_ub, nh, T, s); break;
+      case 2: e = launch_attn7_t<2>(o, tq64, p, items_ub, nh, T, s); break;
+      case 6: e = launch_attn7_t<6>(o, tq64, p, items_ub, nh, T, s); break;
+      case 8: e = launch_attn7_t<8>(o, tq64, p, items_ub, nh, T, s); break;
+      default:
+        e = o.attn_nwg == 3       ? launch_attn7_t<4, 32, 3>(o, tq64, p, items_ub, nh, T, s)
+            : o.attn_sleep == 0   ? launch_attn7_t<4, 0>(o, tq64, p, items_ub, nh, T, s)
+            : o.attn_sleep == 128 ? launch_attn7_t<4, 128>(o, tq64, p, items_ub, nh, T, s)
+                                  : launch_attn7_t<4, 32>(o, tq64, p, items_ub, nh, T, s);
+        break;
+    }
+  } else if (o.attn_variant >= 4 && T <= ATTN_MAX_T) {
     const int items_ub = T * ((max_qtiles + ATTN4_NWG - 1) / ATTN4_NWG) * nh;
     switch (o.attn_npp) {
       case 0: e = launch_attn4_t<0>(o, tq, p, items_ub, nh, T, s); break;
@@ -536,9 +573,10 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   const int d = g.d_model, F = g.d_ff;
   const bool fuse_ln = pick_bn(d) == d;  // one GEMM tile spans a whole row
   LayerDev& L = c->layers[l];
-  CUtensorMap ta_h, ta_o, ta_f, tq;
+  CUtensorMap ta_h, ta_o, ta_f, tq, tq64;
   if (!make_amap(&ta_h, w.hbuf, w.rows_cap, d) || !make_amap(&ta_o, w.obuf, w.rows_cap, d) ||
-      !make_amap(&ta_f, w.ff, w.rows_cap, F) || !make_qkvmap(&tq, w.qkv, w.rows_cap, d))
+      !make_amap(&ta_f, w.ff, w.rows_cap, F) || !make_qkvmap(&tq, w.qkv, w.rows_cap, d) ||
+      !make_qkvmap(&tq64, w.qkv, w.rows_cap, d, 64))
     return CFD_E_CUDA;
   if ((l == 0 && !ln1_ready) || !fuse_ln)  // LN1
     CFD_CUDA(launch_layernorm(o, d, x, L.ln1_g, L.ln1_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
@@ -554,7 +592,7 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   ap.stagger = o.attn_stagger;
   ap.uniform_n = o.attn_qmajor ? uniform_n : 0;
   if (o.attn_dyn) ap.work_counter = w.attn_work;  // dynamic item claiming (per-workspace counter)
-  CFD_CUDA(launch_attention(o, tq, ap, max_qtiles, g.n_heads, T, s));
+  CFD_CUDA(launch_attention(o, tq, tq64, ap, max_qtiles, g.n_heads, T, s));
   if (want_lse && scores) {
     ScoreParams sp{};
     sp.n_coarse = c->Nc; sp.n_heads = g.n_heads; sp.d_model = d; sp.lse = w.lse; sp.lse_ld = w.lse_ld;
@@ -709,7 +747,7 @@ cfd_status cfdx_set_option(cfd_ctx* ctx, int32_t key, int32_t value) {
   const int b = value ? 1 : 0;
   switch (key) {
     case 0:
-      if (value != 1 && value != 4) return CFD_E_ARG;
+      if (value != 1 && value != 4 && value != 7) return CFD_E_ARG;
       o.attn_variant = value;
       return CFD_OK;
     case 1:
@@ -737,6 +775,14 @@ cfd_status cfdx_set_option(cfd_ctx* ctx, int32_t key, int32_t value) {
     case 18: o.balanced_grid = b; return CFD_OK;
     case 19: o.keep_x1 = b; return CFD_OK;
     case 20: o.preload_x = b; return CFD_OK;
+    case 21:
+      if (value != 0 && value != 32 && value != 128) return CFD_E_ARG;
+      o.attn_sleep = value;
+      return CFD_OK;
+    case 22:
+      if (value != 3 && value != 4) return CFD_E_ARG;
+      o.attn_nwg = value;
+      return CFD_OK;
   }
   return CFD_E_ARG;
 }
@@ -1259,8 +1305,8 @@ cfd_status cfdx_attention(int32_t T, const int32_t* cu, int32_t max_seqlen, int3
                           int32_t* work_counter, void* stream) {
   if (T <= 0 || !cu || !qkv || !out || max_seqlen <= 0 || rows_cap <= 0 || nh <= 0 || d % nh || d / nh != 32)
     return CFD_E_ARG;
-  CUtensorMap tq;
-  if (!make_qkvmap(&tq, qkv, rows_cap, d)) return CFD_E_CUDA;
+  CUtensorMap tq, tq64;
+  if (!make_qkvmap(&tq, qkv, rows_cap, d) || !make_qkvmap(&tq64, qkv, rows_cap, d, 64)) return CFD_E_CUDA;
   AttnParams ap{};
   ap.cu_seqlens = cu; ap.d_model = d; ap.out = (__nv_bfloat16*)out; ap.lse = lse; ap.lse_ld = lse_ld;
   ap.scale_log2 = 1.4426950408889634f / std::sqrt(32.0f);
@@ -1268,7 +1314,7 @@ cfd_status cfdx_attention(int32_t T, const int32_t* cu, int32_t max_seqlen, int3
   // work_counter: caller-owned zeroed int[2] (dynamic claims, reset by the launch's last CTA)
   // or NULL (static round-robin); no state is shared between calls
   if (g_dbg_opts.attn_dyn) ap.work_counter = work_counter;
-  CFD_CUDA(launch_attention(g_dbg_opts, tq, ap, (max_seqlen + ATTN_BQ - 1) / ATTN_BQ, nh, T, static_cast<cudaStream_t>(stream)));
+  CFD_CUDA(launch_attention(g_dbg_opts, tq, tq64, ap, (max_seqlen + ATTN_BQ - 1) / ATTN_BQ, nh, T, static_cast<cudaStream_t>(stream)));
   return CFD_OK;
 }
 

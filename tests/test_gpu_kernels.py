@@ -143,7 +143,7 @@ def test_attention_wide_logit_range_stays_finite():
     torch.testing.assert_close(lse[:, :rows], rlse[:, :rows], rtol=1e-4, atol=2e-3)
 
 
-@pytest.mark.parametrize("opt", [(16, 0), (0, 1), (1, 0), (1, 8)])
+@pytest.mark.parametrize("opt", [(16, 0), (0, 1), (0, 7), (1, 0), (1, 8)])
 def test_attention_alternative_schedules_match_torch(opt):
     """The non-default attention schedules kept for A/B measurement (static round-robin items,
     the one-tile-per-CTA v1 kernel, all-MUFU and half-polynomial exponentials) against torch on

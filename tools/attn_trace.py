@@ -36,8 +36,20 @@ t0 = a[148 * 4 * 2 * 12 * 8:]
 t = a[:148 * 4 * 2 * 12 * 8].reshape(148, 4, 2, 12, 8)
 names = ["s_full", "S in regs", "max", "exps", "o_full(+resc)", "p_full arr", "MMA QK(u)", "MMA PV(u)"]
 # v5: event 5 = second named barrier passed (P stored); QK/PV are issued by the traced thread itself
+ctl = os.environ.get("CFD_TRACE_CTL")  # v7: slot 3 = warpgroup 0's control thread
 for it in range(2):
     for w in range(4):
+        if ctl and w == 3:
+            ok = t[:, 3, it, 0, 0] > 0
+            ref = t[ok, 0, it, 0, 0][:, None]
+            cn = ["top", "pumped", "kv_full", "s_free", "QK issued", "p_full seen", "PV issued"]
+            print(f"--- item {it}, control thread of warpgroup 0 (cycles since warpgroup 0's s_full of sub-tile 0)")
+            print("  u  " + " ".join(f"{n:>12s}" for n in cn))
+            for u in range(12):
+                if (t[ok, 3, it, u, 0] == 0).all():
+                    break
+                print(f" {u:2d}  " + " ".join(f"{int(np.median(t[ok, 3, it, u, e] - ref[:, 0])):12d}" for e in range(7)))
+            continue
         ok = (t[:, w, it, 0, 0] > 0) & (t[:, w, it, 0, 5] > 0)
         if not ok.any():
             continue

@@ -8,6 +8,7 @@
 //      commit + wait after each group (round-trip latency)
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2505_23317_b200/csrc tools/tc_micro.cu -o tc_micro
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "ptx.cuh"
@@ -181,6 +182,60 @@ __global__ void attn_mma_split(int iters, int mode, unsigned long long* cyc) {
   if (warp == 0) tmem_dealloc<512>(slot);
 }
 
+// cycles per tcgen05.mma (M = 128, K = 16, bf16 -> f32, SW64 operands as in the attention
+// kernel) for N in {32, 64, 128}: SS (A = Q/K tile from smem) or TS (A = P from TMEM)
+template <int N, bool TS>
+__global__ void mma_shape(int iters, unsigned long long* cyc) {
+  extern __shared__ uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 3 * 8192 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (warp == 0) tmem_alloc<512>(&slot);
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const unsigned long long t0 = clock64();
+  if (warp == 0 && lane == 0) {
+    const uint32_t qa = smem_u32(sm), ka = smem_u32(sm + 8192);
+    constexpr uint32_t idesc = make_idesc_bf16(128, N, TS ? 1 : 0);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (TS)
+          mma_ts(slot + 256, slot + k * 8, make_smem_desc(ka + k * 1024, 4096, 512, kLayoutSW64), idesc, 1);
+        else
+          mma_ss(slot + 256, make_smem_desc(qa + (k & 1) * 32, 16, 512, kLayoutSW64),
+                 make_smem_desc(ka + (k & 1) * 32, 16, 512, kLayoutSW64), idesc, 1);
+      }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+  }
+  const unsigned long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(slot);
+}
+
+template <int N, bool TS>
+void run_shape(int grid, unsigned long long* cyc, unsigned long long* h) {
+  const int smem = 3 * 8192 + 1024, iters = 2048;
+  cudaFuncSetAttribute(mma_shape<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mma_shape<N, TS><<<grid, 128, smem>>>(iters, cyc);
+  cudaDeviceSynchronize();
+  cudaMemcpy(h, cyc, sizeof(unsigned long long) * grid, cudaMemcpyDeviceToHost);
+  double c = 0;
+  for (int i = 0; i < grid; ++i) c += h[i];
+  c /= grid;
+  printf("mma shape M=128 N=%3d K=16 %s: %.1f cycles/instr  FLOP/clk/SM=%.0f\n", N, TS ? "TS (A in TMEM)" : "SS",
+         c / (4.0 * iters), 2.0 * 128 * N * 16 * 4 * iters / c);
+}
+
 int main() {
   unsigned long long* cyc;
   uint32_t* sink;
@@ -188,6 +243,13 @@ int main() {
   cudaMalloc(&cyc, sizeof(unsigned long long) * grid * 32);
   cudaMalloc(&sink, 4096);
   unsigned long long h[148 * 32];
+  run_shape<32, false>(grid, cyc, h);
+  run_shape<64, false>(grid, cyc, h);
+  run_shape<128, false>(grid, cyc, h);
+  run_shape<32, true>(grid, cyc, h);
+  run_shape<64, true>(grid, cyc, h);
+  run_shape<128, true>(grid, cyc, h);
+  if (getenv("TC_SHAPES_ONLY")) return 0;
   // 1. TMEM read bandwidth
   for (int nw : {1, 2, 4, 8, 12, 16}) {
     const int iters = 4096;
