@@ -71,14 +71,15 @@ int32_t cfdx_probe_count(int32_t kind);
  * the switch of that context only (each context starts at the defaults); ctx == NULL: the
  * switches the ctx-less debug entry points above use.
  *   key 0  attention kernel: 1 one query tile per CTA (v1), 4 three query tiles / warpgroups
- *          per CTA (v4, default)
- *   key 1  v4: how many of every 16 column pairs are exponentiated by the FMA-pipe polynomial
- *          instead of MUFU (0, 2, 4 default, 6, 8)
+ *          per CTA sharing one K/V stream (v4), 7 independent per-warpgroup items (task, head,
+ *          128-row tile), K/V rings, MMA and producer warps (v7, default)
+ *   key 1  v4 / v7: how many of every 16 column pairs are exponentiated by the FMA-pipe
+ *          polynomial instead of MUFU (0, 2, 4 default, 6, 8)
  *   key 2  fused MLP kernel on (1, default) / off (0)
  *   key 3  TMA-staged residual(+LayerNorm) epilogues on (1, default) / off (0)
  *   key 4  fused MLP as CTA pairs (cta_group::2) on (1) / off (0, default)
- *   key 5  attention v4 warpgroup start stagger in cycles (0 default); -1 / -2 select the
- *          debug library's "quarters" / "MMA warp" attention trace modes
+ *   key 5  attention warpgroup start stagger in cycles (700 default); -1 / -2 select the
+ *          debug library's v4 "quarters" / "MMA warp" attention trace modes
  *   key 7  weight-stationary QKV GEMM on (1, default) / off (0)
  *   key 11 O-projection + residual + LN2 fused into the MLP kernel on (1, default) / off (0)
  *   key 12 attention v4 q-triple-major item order for equal-length (coarse) batches on (1,
@@ -97,6 +98,8 @@ int32_t cfdx_probe_count(int32_t kind);
  *   key 19 fused O-projection keeps x1 = x + o W_o + b_o in TMEM and the MLP's MMA2s
  *          accumulate onto it (1, default) / x1 stored and read back (0)
  *   key 20 with key 19 = 1: x loaded into acc2 while o / W_o stream in (1) / 0 (default)
+ *   key 21 attention v7: control-warp sleep between barrier probes, ns (0, 32 default, 128)
+ *   key 22 attention v7: softmax warpgroups per CTA (3, or 4 default)
  * Other keys / values: CFD_E_ARG. */
 cfd_status cfdx_set_option(cfd_ctx *ctx, int32_t key, int32_t value);
 

@@ -255,6 +255,10 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
       const int w = c - NWG;
       uint64_t* b = bars + w * S::NBAR_WG;
       int g = 0;
+      if (p.stagger > 0 && w > 0) {  // de-phase the warpgroups' pipelines (option 5)
+        const long long t_end = clock64() + (long long)w * p.stagger;
+        while (clock64() < t_end) __nanosleep(64);
+      }
       for (int it = 0;; ++it) {
         const int slot = it & 1;
         if (it >= 2) mbar_poll<SLEEP_NS>(&b[2 + slot], ((it >> 1) - 1) & 1);  // q_empty

@@ -107,10 +107,11 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
 // copy (set per ctx); the ctx-less debug entry points use g_dbg_opts.  Defaults = the measured
 // best configuration.
 struct Opts {
-  int attn_variant = 4;   // 1: one q-tile per CTA (v1), 4: three q-tiles per CTA (v4), 7: independent
-                          // per-warpgroup items and pipelines (v7)
+  int attn_variant = 7;   // 1: one q-tile per CTA (v1), 4: three q-tiles per CTA (v4), 7: independent
+                          // per-warpgroup items and pipelines (v7, default)
   int attn_npp = 4;       // v4: polynomial-exp pairs of every 16
-  int attn_stagger = 0;   // v4: warpgroup start stagger; -1 / -2 trace modes (debug library)
+  int attn_stagger = 700; // v4 / v7: warpgroup start stagger in cycles (v7: 700 measured best:
+                          // 58.2 vs 60.5 us at 700 x 32); -1 / -2 trace modes (debug library)
   int attn_qmajor = 1;    // v4: q-triple-major item order for equal-length batches (option 12)
   int attn_dyn = 1;       // v4: dynamic item claiming through the workspace work counter (16)
   int fused_mlp = 1;      // fused MLP kernel (d == 256) instead of two GEMM launches (2)
