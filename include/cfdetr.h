@@ -138,6 +138,25 @@ cfd_status cfd_batch_refine(cfd_ctx *ctx, int32_t n_tasks, const uint16_t *image
                             float *y, int32_t *cu_seqlens, int32_t *mixed_src, float *layer_out, void *ws,
                             size_t ws_bytes, void *stream);
 
+/* NEXT row f4 — the paper's pad-to-max patch-level batch (§III-B A3 "padding
+ * is applied to equalize them"; :466 [draft]), the baseline the varlen cfd_batch_refine is
+ * measured against.  Every task occupies max_tokens rows: rows [t*max_tokens, t*max_tokens +
+ * N_t) hold its mixed tokens (the same order as cfd_batch_refine), the remaining rows are zero
+ * pad tokens; every layer runs over all T*max_tokens rows, and attention covers all
+ * max_tokens keys of the task with the pad keys masked (exp -> 0; reading R11: unmasked pad
+ * keys would receive softmax weight).  Per task, rows [0, N_t) equal cfd_batch_refine's output
+ * bit for bit.
+ *   max_tokens  >= every N_t = Nc + (m^2-1) k_t and <= Nf (host value; a task with N_t >
+ *             max_tokens sets the device error word, see cfd_check)
+ *   y         [T*max_tokens, d] fp32 out;  cu_seqlens [T+1] out = t*max_tokens;
+ *   kv_len    [T] int32 out = N_t;  mixed_src [T*max_tokens] out (pad rows INT32_MIN)
+ *   layer_out [L, T*max_tokens, d] or NULL;  workspace: cfd_query(ctx, n_tasks).
+ * Errors as cfd_batch_refine; CFD_E_ARG if max_tokens is outside [Nc, Nf]. */
+cfd_status cfd_batch_refine_padded(cfd_ctx *ctx, int32_t n_tasks, const uint16_t *images, const float *x0,
+                                   const int32_t *sel_idx, const int32_t *sel_count, int32_t max_tokens, float *y,
+                                   int32_t *cu_seqlens, int32_t *kv_len, int32_t *mixed_src, float *layer_out,
+                                   void *ws, size_t ws_bytes, void *stream);
+
 /* cfd_batch_refine with T = 1 (y capacity Nf rows, cu_seqlens [2]). */
 cfd_status cfd_refine_encode(cfd_ctx *ctx, const uint16_t *image, const float *x0, const int32_t *sel_idx,
                              const int32_t *sel_count, float *y, int32_t *mixed_src, int32_t *cu_seqlens,

@@ -22,7 +22,7 @@ STATUS = {0: "CFD_OK", -1: "CFD_E_ARG", -2: "CFD_E_SHAPE", -3: "CFD_E_UNSUPPORTE
 
 # public symbols of include/cfdetr.h and include/cfdetr_debug.h
 PUBLIC_SYMBOLS = ["cfd_create", "cfd_destroy", "cfd_query", "cfd_coarse_encode", "cfd_select_regions",
-                  "cfd_refine_encode", "cfd_batch_refine", "cfd_check", "cfd_status_str", "cfd_version",
+                  "cfd_refine_encode", "cfd_batch_refine", "cfd_batch_refine_padded", "cfd_check", "cfd_status_str", "cfd_version",
                   "cfd_hardness", "cfd_box_scores", "cfd_set_decoder", "cfd_decode", "cfd_frames_from_u8"]
 DEBUG_SYMBOLS = ["cfdx_gemm", "cfdx_gemm_resid_ln", "cfdx_attention", "cfdx_layernorm", "cfdx_score", "cfdx_gather",
                  "cfdx_launch_count", "cfdx_mlp_trace", "cfdx_attn_trace", "cfdx_probe_install", "cfdx_probe_count", "cfdx_set_option",
@@ -80,6 +80,7 @@ def load() -> C.CDLL:
         "cfd_select_regions": [P, I32, P, I32, C.POINTER(I32), F32, P, P, P],
         "cfd_refine_encode": [P, P, P, P, P, P, P, P, P, P, SZ, P],
         "cfd_batch_refine": [P, I32, P, P, P, P, C.POINTER(I32), P, P, P, P, P, SZ, P],
+        "cfd_batch_refine_padded": [P, I32, P, P, P, P, I32, P, P, P, P, P, P, SZ, P],
         "cfd_check": [P, P],
         "cfd_hardness": [P, I32, I32, P, F32, F32, P, P],
         "cfd_box_scores": [P, I32, I32, P, P, F32, F32, P, P],

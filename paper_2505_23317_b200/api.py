@@ -166,6 +166,31 @@ class CFDetrEncoder:
             ws.data_ptr(), ws.numel(), _stream(stream)))
         return o
 
+    def batch_refine_padded(self, images: torch.Tensor, x0: torch.Tensor, sel_idx: torch.Tensor,
+                            sel_count: torch.Tensor, max_tokens: int, want_layers: bool = False,
+                            out: Optional[dict] = None, stream=None) -> dict:
+        """The paper's pad-to-max batch (NEXT f4, cfd_batch_refine_padded): every task spans
+        max_tokens rows, pad keys masked -> dict(y [T*max_tokens, d], cu_seqlens, kv_len [T],
+        mixed_src, layer_out)."""
+        T = images.shape[0]
+        rows = T * int(max_tokens)
+        d = self.cfg.d_model
+        o = out if out is not None else {}
+        dev = self.device
+        if "y" not in o:
+            o["y"] = torch.empty(rows, d, dtype=torch.float32, device=dev)
+            o["cu_seqlens"] = torch.empty(T + 1, dtype=torch.int32, device=dev)
+            o["kv_len"] = torch.empty(T, dtype=torch.int32, device=dev)
+            o["mixed_src"] = torch.empty(rows, dtype=torch.int32, device=dev)
+            o["layer_out"] = (torch.empty(self.cfg.n_layers, rows, d, dtype=torch.float32, device=dev)
+                              if want_layers else None)
+        ws = self.workspace(T)
+        L.check("cfd_batch_refine_padded", self.lib.cfd_batch_refine_padded(
+            self.ctx, T, images.data_ptr(), x0.data_ptr(), sel_idx.data_ptr(), sel_count.data_ptr(), int(max_tokens),
+            o["y"].data_ptr(), o["cu_seqlens"].data_ptr(), o["kv_len"].data_ptr(), o["mixed_src"].data_ptr(),
+            _ptr(o["layer_out"]), ws.data_ptr(), ws.numel(), _stream(stream)))
+        return o
+
     def refine_encode(self, image: torch.Tensor, x0: torch.Tensor, sel_idx: torch.Tensor, sel_count: torch.Tensor,
                       want_layers: bool = False, stream=None) -> dict:
         """Single-task refine (image [H, W, 3] or [1, H, W, 3])."""

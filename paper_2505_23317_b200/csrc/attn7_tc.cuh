@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
         decode_item7(order, pre_full, pre_tail, T, nh, n_full, item, t, tile, h, p.cu_seqlens);
         const int N = __ldg(p.cu_seqlens + t + 1) - __ldg(p.cu_seqlens + t);
         const int ns = (N + 63) / 64;
+        const int n_keys = p.kv_len ? __ldg(p.kv_len + t) : N;  // PV covers the unmasked keys only
         const uint32_t qa = smem_u32(smem + S::q_off(w, slot));
         for (int u = 0; u < ns; ++u) {
           const int st = g % ATTN7_ST;
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
           }
           pv_pending = true;
           pv_u = u;
-          pv_ks = (min(64, N - u * 64) + 15) / 16;
+          pv_ks = (max(0, min(64, n_keys - u * 64)) + 15) / 16;
           ++g;
         }
       }
@@ -326,14 +327,24 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
       const int nsub = (N + 63) / 64;
       const int q_valid = N - tile * 128;
       const bool active = quarter * 32 < q_valid;
+      const int n_keys = p.kv_len ? __ldg(p.kv_len + t) : N;  // keys >= n_keys are masked (padded batch)
       float m_run = -INFINITY, l_run = 0.f;
       for (int u = 0; u < nsub; ++u) {
         mbar_wait(s_full, s_cnt & 1);
         ++s_cnt;
         tc_fence_after();
         if (tr) ATTN_TR(wg, it, u, 0);
-        if (active) {
-          const int valid = min(64, N - u * 64);
+        if (active && u * 64 >= n_keys) {
+          // a sub-tile of pad keys only (padded batch): no exponentials, and the MMA warp
+          // issues no PV for it (its k-steps cover the unmasked keys only)
+          tc_fence_before();
+          mbar_arrive(s_free);
+          if (u > 0) {
+            mbar_wait(o_full, o_cnt & 1);
+            ++o_cnt;
+          }
+        } else if (active) {
+          const int valid = min(64, n_keys - u * 64);
           uint32_t sr[64];
           tmem_ld32(s_base, *reinterpret_cast<uint32_t(*)[32]>(sr));
           if (valid > 32) tmem_ld32(s_base + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));

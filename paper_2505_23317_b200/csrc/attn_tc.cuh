@@ -38,6 +38,8 @@ struct AttnParams {
   int* work_counter = nullptr;  // v4: zeroed int; non-null -> items after the first are claimed
                                 // dynamically (atomicAdd) instead of the static round-robin
   int n_q = 0;             // v1 CROSS: queries per task (one 128-row tile shared by every task)
+  const int* kv_len = nullptr;  // v7: [T] valid keys per task (pad-to-max batch: keys >= kv_len[t]
+                                // of the task's cu_seqlens span are masked); nullptr = all
 };
 
 constexpr int ATTN_THREADS = 192;

@@ -568,9 +568,11 @@ Workspace carve(const cfd_ctx* c, int n, void* base) {
 // O-projection epilogue the same way.
 cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const int* m_dev, int rows_grid,
                      const int32_t* cu, int T, int max_qtiles, Workspace& w, bool want_lse, float* scores,
-                     int score_B, cudaStream_t s, int uniform_n = 0, bool ln1_ready = false) {
+                     int score_B, cudaStream_t s, int uniform_n = 0, bool ln1_ready = false,
+                     const int32_t* kv_len = nullptr) {
   const cfd_config& g = c->cfg;
-  const Opts& o = c->opt;
+  Opts o = c->opt;
+  if (kv_len) o.attn_variant = 7;  // key masking (padded batch) is a v7 feature
   const int d = g.d_model, F = g.d_ff;
   const bool fuse_ln = pick_bn(d) == d;  // one GEMM tile spans a whole row
   LayerDev& L = c->layers[l];
@@ -593,6 +595,7 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   ap.stagger = o.attn_stagger;
   ap.uniform_n = o.attn_qmajor ? uniform_n : 0;
   if (o.attn_dyn) ap.work_counter = w.attn_work;  // dynamic item claiming (per-workspace counter)
+  ap.kv_len = kv_len;
   CFD_CUDA(launch_attention(o, tq, tq64, ap, max_qtiles, g.n_heads, T, s));
   if (want_lse && scores) {
     ScoreParams sp{};
@@ -1016,7 +1019,8 @@ cfd_status cfd_select_regions(cfd_ctx* c, int32_t T, const float* scores, cfd_se
 
 static cfd_status launch_gather(cfd_ctx* c, int T, const uint16_t* images, const float* x0, const int32_t* sel_idx,
                                 const int32_t* sel_count, float* X, int32_t* cu, int32_t* msrc, uint16_t* A_f,
-                                int32_t* frow, int32_t* fidx, int32_t* meta, int32_t* attn_work, cudaStream_t s) {
+                                int32_t* frow, int32_t* fidx, int32_t* meta, int32_t* attn_work, cudaStream_t s,
+                                int pad_stride = 0, int32_t* kv_len = nullptr) {
   GatherParams gp{};
   const cfd_config& g = c->cfg;
   gp.T = T; gp.Nc = c->Nc; gp.gc_w = c->gc_w; gp.m = c->m; gp.gf_w = c->gf_w; gp.d = g.d_model;
@@ -1024,6 +1028,7 @@ static cfd_status launch_gather(cfd_ctx* c, int T, const uint16_t* images, const
   gp.images = images; gp.x0 = x0; gp.sel_idx = sel_idx; gp.sel_count = sel_count; gp.X = X; gp.cu_seqlens = cu;
   gp.mixed_src = msrc; gp.A_f = A_f; gp.frow = frow; gp.fidx = fidx; gp.meta = meta; gp.err = c->err;
   gp.zero2 = attn_work;
+  gp.pad_stride = pad_stride; gp.kv_len = kv_len;
   const int G = std::max(1, std::min(32, (c->Nc + 31) / 32));
   const size_t smem = (size_t)2 * c->Nc * sizeof(int32_t);
   probe_begin(PK_GATHER, s);
@@ -1034,9 +1039,34 @@ static cfd_status launch_gather(cfd_ctx* c, int T, const uint16_t* images, const
   return CFD_OK;
 }
 
+static cfd_status batch_refine_impl(cfd_ctx* c, int32_t T, const uint16_t* images, const float* x0,
+                                    const int32_t* sel_idx, const int32_t* sel_count, const int32_t* h_token_counts,
+                                    float* y, int32_t* cu, int32_t* msrc, float* layer_out, void* ws, size_t ws_bytes,
+                                    void* stream, int pad = 0, int32_t* kv_len = nullptr);
+
 cfd_status cfd_batch_refine(cfd_ctx* c, int32_t T, const uint16_t* images, const float* x0, const int32_t* sel_idx,
                             const int32_t* sel_count, const int32_t* h_token_counts, float* y, int32_t* cu,
                             int32_t* msrc, float* layer_out, void* ws, size_t ws_bytes, void* stream) {
+  return batch_refine_impl(c, T, images, x0, sel_idx, sel_count, h_token_counts, y, cu, msrc, layer_out, ws, ws_bytes,
+                           stream);
+}
+
+cfd_status cfd_batch_refine_padded(cfd_ctx* c, int32_t T, const uint16_t* images, const float* x0,
+                                   const int32_t* sel_idx, const int32_t* sel_count, int32_t max_tokens, float* y,
+                                   int32_t* cu, int32_t* kv_len, int32_t* msrc, float* layer_out, void* ws,
+                                   size_t ws_bytes, void* stream) {
+  if (!c) return CFD_E_ARG;
+  if (T == 0) return CFD_OK;
+  if (!kv_len || max_tokens < c->Nc || max_tokens > c->Nf) return CFD_E_ARG;
+  if (T > ATTN7_MAX_T) return CFD_E_UNSUPPORTED;
+  return batch_refine_impl(c, T, images, x0, sel_idx, sel_count, nullptr, y, cu, msrc, layer_out, ws, ws_bytes, stream,
+                           max_tokens, kv_len);
+}
+
+static cfd_status batch_refine_impl(cfd_ctx* c, int32_t T, const uint16_t* images, const float* x0,
+                                    const int32_t* sel_idx, const int32_t* sel_count, const int32_t* h_token_counts,
+                                    float* y, int32_t* cu, int32_t* msrc, float* layer_out, void* ws, size_t ws_bytes,
+                                    void* stream, int pad, int32_t* kv_len) {
   if (!c) return CFD_E_ARG;
   if (T == 0) return CFD_OK;
   if (T < 0 || !images || !x0 || !sel_idx || !sel_count || !y || !cu || !msrc || !ws) return CFD_E_ARG;
@@ -1046,7 +1076,7 @@ cfd_status cfd_batch_refine(cfd_ctx* c, int32_t T, const uint16_t* images, const
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const cfd_config& g = c->cfg;
   const int d = g.d_model;
-  const int cap = T * c->Nf;
+  const int cap = pad > 0 ? T * pad : T * c->Nf;  // rows of y (and of each layer_out slice)
   // host-side sizing hints (grid sizes only; every kernel reads the true counts on device)
   int rows_grid = cap, fine_grid = cap;
   if (h_token_counts) {
@@ -1060,8 +1090,12 @@ cfd_status cfd_batch_refine(cfd_ctx* c, int32_t T, const uint16_t* images, const
     const int m2 = c->m * c->m;
     fine_grid = (m2 > 1) ? (int)((tot - (long long)T * c->Nc) / (m2 - 1) * m2) : 0;
   }
+  if (pad > 0) {  // pad-to-max: every task spans `pad` rows
+    rows_grid = T * pad;
+    fine_grid = (c->m * c->m > 1) ? T * (pad - c->Nc) / (c->m * c->m - 1) * (c->m * c->m) : 0;
+  }
   cfd_status st = launch_gather(c, T, images, x0, sel_idx, sel_count, y, cu, msrc, w.patches, w.frow, w.fidx,
-                                w.meta, w.attn_work, s);
+                                w.meta, w.attn_work, s, pad, kv_len);
   if (st != CFD_OK) return st;
   CUtensorMap ta;
   if (!make_amap(&ta, w.patches, cap + 128, c->Kf)) return CFD_E_CUDA;
@@ -1069,9 +1103,10 @@ cfd_status cfd_batch_refine(cfd_ctx* c, int32_t T, const uint16_t* images, const
   p.M = 0; p.m_dev = w.meta + 1; p.m_cap = cap; p.N = d; p.K = c->Kf; p.bias = c->bf; p.out_f32 = y; p.ld_out = d;
   p.pe = c->pef; p.pe_rows = c->Nf; p.frow = w.frow; p.fidx = w.fidx;
   CFD_CUDA(launch_gemm(c->opt, EPI_EMBED_FINE, ta, c->tm_wf, p, std::max(fine_grid, 1), s, PK_EMBED_F));
-  const int max_qtiles = (c->Nf + ATTN_BQ - 1) / ATTN_BQ;
+  const int max_qtiles = ((pad > 0 ? pad : c->Nf) + ATTN_BQ - 1) / ATTN_BQ;
   for (int l = 0; l < g.n_layers; ++l) {
-    st = run_layer(c, l, y, cap, 0, w.meta, std::max(rows_grid, 1), cu, T, max_qtiles, w, false, nullptr, 0, s);
+    st = run_layer(c, l, y, cap, 0, w.meta, std::max(rows_grid, 1), cu, T, max_qtiles, w, false, nullptr, 0, s, 0,
+                   false, kv_len);
     if (st != CFD_OK) return st;
     if (layer_out)
       CFD_CUDA(cudaMemcpyAsync(layer_out + (size_t)l * cap * d, y, (size_t)cap * d * 4, cudaMemcpyDeviceToDevice, s));

@@ -223,6 +223,9 @@ struct GatherParams {
   int* err;
   int32_t* zero2;                   // [2] or nullptr: zeroed by block (0, 0) (the call's attention
                                     // work counter; every later kernel of the call runs after this one)
+  int pad_stride;                   // > 0: pad-to-max layout (task t at rows t*pad_stride, pad rows
+                                    // zeroed, mixed_src INT32_MIN); 0: packed varlen
+  int32_t* kv_len;                  // pad_stride > 0: [T] out, N_t
 };
 
 // grid = (T, G); block = 256 (8 warps).  Every block of task t rebuilds the task's
@@ -254,14 +257,24 @@ __global__ void gather_kernel(const GatherParams p) {
   if (threadIdx.x == 0) {
     int ksum = 0;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) ksum += s_part[i];
-    const int tb = t * Nc + (m2 - 1) * ksum, fb = m2 * ksum;
+    const int tb = p.pad_stride > 0 ? t * p.pad_stride : t * Nc + (m2 - 1) * ksum, fb = m2 * ksum;
     int k = p.sel_count[t];
     if (k < 0 || k > Nc) { atomicOr(p.err, ERR_SEL_COUNT); k = min(max(k, 0), Nc); }
+    if (p.pad_stride > 0 && Nc + (m2 - 1) * k > p.pad_stride) {  // task longer than the padded length
+      atomicOr(p.err, ERR_SEL_COUNT);
+      k = (p.pad_stride - Nc) / max(m2 - 1, 1);
+    }
     s_tok_base = tb; s_fine_base = fb; s_k = k;
     if (g == 0) {
       if (t == 0) p.cu_seqlens[0] = 0;
-      p.cu_seqlens[t + 1] = tb + Nc + (m2 - 1) * k;
-      if (t == p.T - 1) { p.meta[0] = tb + Nc + (m2 - 1) * k; p.meta[1] = fb + m2 * k; }
+      if (p.pad_stride > 0) {
+        p.cu_seqlens[t + 1] = (t + 1) * p.pad_stride;
+        p.kv_len[t] = Nc + (m2 - 1) * k;
+        if (t == p.T - 1) { p.meta[0] = p.T * p.pad_stride; p.meta[1] = fb + m2 * k; }
+      } else {
+        p.cu_seqlens[t + 1] = tb + Nc + (m2 - 1) * k;
+        if (t == p.T - 1) { p.meta[0] = tb + Nc + (m2 - 1) * k; p.meta[1] = fb + m2 * k; }
+      }
     }
   }
   for (int c = threadIdx.x; c < Nc; c += blockDim.x) pos[c] = 0;  // pos[] holds the selected flag
@@ -302,6 +315,14 @@ __global__ void gather_kernel(const GatherParams p) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int tok_base = s_tok_base, fine_base = s_fine_base;
   const int dvec = p.d / 4;  // float4 per row
+  if (p.pad_stride > 0) {  // pad rows of this task: zero tokens, mixed_src INT32_MIN
+    const int n_t = Nc + (m2 - 1) * k;
+    for (int r = n_t + g * nw + wid; r < p.pad_stride; r += G * nw) {
+      float4* dst = reinterpret_cast<float4*>(p.X + (size_t)(tok_base + r) * p.d);
+      for (int v = lane; v < dvec; v += 32) dst[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (lane == 0) p.mixed_src[tok_base + r] = INT32_MIN;
+    }
+  }
   const int seg_vec = (p.Pf * 3 * 2) / 16;  // 16B vectors per fine pixel-row segment
   const int fvec = p.Pf * seg_vec;           // 16B vectors per fine patch
   // Copies are batched GU 16-byte vectors per lane: all loads of a batch are in flight

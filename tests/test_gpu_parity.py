@@ -342,6 +342,57 @@ def test_fused_oproj_matches_separate_oproj_bitwise():
         assert (a - b).abs().max().item() <= 1e-2
 
 
+@pytest.mark.parametrize("ks,pad", [(list(ci.WORKLOADS["batch6"].ks), 1600), ([0, 37, 100], 720), ([5, 0], 700)])
+def test_padded_batch_equals_varlen_per_task(ks, pad):
+    """NEXT f4: the paper's pad-to-max batch with masked pad keys: each task's
+    rows [0, N_t) equal the varlen cfd_batch_refine output bit for bit (same per-row GEMMs, same
+    attention items; pad keys contribute exp = 0), pad rows are marked in mixed_src, and the
+    real rows match the oracle (task 0 and the last task)."""
+    cfg = ci.CONFIGS["c640"]
+    enc = enc_for("c640")
+    w = ci.make_weights(cfg, seed=0)
+    T = len(ks)
+    imgs_np = ci.make_frames(cfg, T, task0=31)
+    imgs = bf16_tensor(imgs_np, "cuda")
+    co = enc.coarse_encode(imgs)
+    sel = enc.select_regions(co["scores"], k=ks)
+    ro = enc.batch_refine(imgs, co["x0"], sel["sel_idx"], sel["sel_count"], want_layers=True)
+    pr = enc.batch_refine_padded(imgs, co["x0"], sel["sel_idx"], sel["sel_count"], pad, want_layers=True)
+    torch.cuda.synchronize()
+    enc.check()
+    cu = ro["cu_seqlens"].cpu().numpy()
+    assert pr["cu_seqlens"].cpu().tolist() == [t * pad for t in range(T + 1)]
+    assert pr["kv_len"].cpu().tolist() == np.diff(cu).tolist()
+    msrc = pr["mixed_src"].cpu().numpy()
+    for t in range(T):
+        n = int(cu[t + 1] - cu[t])
+        assert torch.equal(pr["y"][t * pad:t * pad + n], ro["y"][cu[t]:cu[t + 1]]), t
+        assert torch.equal(pr["layer_out"][:, t * pad:t * pad + n], ro["layer_out"][:, cu[t]:cu[t + 1]]), t
+        assert np.array_equal(msrc[t * pad:t * pad + n], ro["mixed_src"][cu[t]:cu[t + 1]].cpu().numpy())
+        assert (msrc[t * pad + n:(t + 1) * pad] == np.iinfo(np.int32).min).all()
+    for t in (0, T - 1):
+        oc = O.coarse_encode(cfg, w, [imgs_np[t]])[0]
+        rr = O.refine_encode(cfg, w, imgs_np[t], oc["x0"], O.select_topk(co["scores"][t].cpu().numpy(), ks[t]))
+        n = rr["y"].shape[0]
+        _tol(pr["y"][t * pad:t * pad + n].cpu().numpy(), rr["y"], f"padded task {t}")
+
+
+def test_padded_batch_rejects_short_padding():
+    """A task longer than max_tokens is a device-side input error (cfd_check)."""
+    from paper_2505_23317_b200 import _lib as L
+    cfg = ci.CONFIGS["c640"]
+    enc = enc_for("c640")
+    imgs = bf16_tensor(ci.make_frames(cfg, 2, task0=3), "cuda")
+    co = enc.coarse_encode(imgs)
+    sel = enc.select_regions(co["scores"], k=[100, 200])
+    enc.batch_refine_padded(imgs, co["x0"], sel["sel_idx"], sel["sel_count"], 800)
+    with pytest.raises(L.CfdError) as e:
+        enc.check()
+    assert e.value.status == -6
+    with pytest.raises(L.CfdError):
+        enc.batch_refine_padded(imgs, co["x0"], sel["sel_idx"], sel["sel_count"], 300)  # < Nc: CFD_E_ARG
+
+
 def test_split_factor_m3_the_papers_3x3_to_9x9_example():
     """Split factor m = 3 (a 3x3 coarse grid refined into 9x9 fine patches): 144x144
     frames, Pc = 48, Pf = 16, Nc = 9, Nf = 81; ragged k = (3, 0, 9) against the oracle."""
