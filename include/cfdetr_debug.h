@@ -74,7 +74,7 @@ int32_t cfdx_probe_count(int32_t kind);
  *          per CTA sharing one K/V stream (v4), 7 independent per-warpgroup items (task, head,
  *          128-row tile), K/V rings, MMA and producer warps (v7, default)
  *   key 1  v4 / v7: how many of every 16 column pairs are exponentiated by the FMA-pipe
- *          polynomial instead of MUFU (0, 2, 4 default, 6, 8)
+ *          polynomial instead of MUFU (0, 2 default, 4, 6, 8)
  *   key 2  fused MLP kernel on (1, default) / off (0)
  *   key 3  TMA-staged residual(+LayerNorm) epilogues on (1, default) / off (0)
  *   key 4  fused MLP as CTA pairs (cta_group::2) on (1) / off (0, default)

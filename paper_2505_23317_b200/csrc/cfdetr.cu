@@ -109,7 +109,7 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
 struct Opts {
   int attn_variant = 7;   // 1: one q-tile per CTA (v1), 4: three q-tiles per CTA (v4), 7: independent
                           // per-warpgroup items and pipelines (v7, default)
-  int attn_npp = 4;       // v4: polynomial-exp pairs of every 16
+  int attn_npp = 2;       // v4 / v7: polynomial-exp pairs of every 16 (v7: 2 measured best)
   int attn_stagger = 700; // v4 / v7: warpgroup start stagger in cycles (v7: 700 measured best:
                           // 58.2 vs 60.5 us at 700 x 32); -1 / -2 trace modes (debug library)
   int attn_qmajor = 1;    // v4: q-triple-major item order for equal-length batches (option 12)
@@ -416,14 +416,14 @@ cudaError_t launch_attention(const Opts& o, const CUtensorMap& tq, const CUtenso
     const int items_ub = T * max_qtiles * nh;
     switch (o.attn_npp) {
       case 0: e = launch_attn7_t<0>(o, tq64, p, items_ub, nh, T, s); break;
-      case 2: e = launch_attn7_t<2>(o, tq64, p, items_ub, nh, T, s); break;
       case 6: e = launch_attn7_t<6>(o, tq64, p, items_ub, nh, T, s); break;
       case 8: e = launch_attn7_t<8>(o, tq64, p, items_ub, nh, T, s); break;
+      case 4: e = launch_attn7_t<4>(o, tq64, p, items_ub, nh, T, s); break;
       default:
-        e = o.attn_nwg == 3       ? launch_attn7_t<4, 32, 3>(o, tq64, p, items_ub, nh, T, s)
-            : o.attn_sleep == 0   ? launch_attn7_t<4, 0>(o, tq64, p, items_ub, nh, T, s)
-            : o.attn_sleep == 128 ? launch_attn7_t<4, 128>(o, tq64, p, items_ub, nh, T, s)
-                                  : launch_attn7_t<4, 32>(o, tq64, p, items_ub, nh, T, s);
+        e = o.attn_nwg == 3       ? launch_attn7_t<2, 32, 3>(o, tq64, p, items_ub, nh, T, s)
+            : o.attn_sleep == 0   ? launch_attn7_t<2, 0>(o, tq64, p, items_ub, nh, T, s)
+            : o.attn_sleep == 128 ? launch_attn7_t<2, 128>(o, tq64, p, items_ub, nh, T, s)
+                                  : launch_attn7_t<2, 32>(o, tq64, p, items_ub, nh, T, s);
         break;
     }
   } else if (o.attn_variant >= 4 && T <= ATTN_MAX_T) {
