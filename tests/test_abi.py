@@ -74,6 +74,19 @@ def test_config_validation_without_gpu(lib):
     ctx = C.c_void_p()
     # weights missing -> ARG before any CUDA call
     assert lib.cfd_create(C.byref(cfg), C.byref(w), None, C.byref(ctx)) == -1
+    # geometry checks run before any CUDA call (non-null placeholder weight pointers)
+    layers = (L.cfd_layer_weights * 6)(*[L.cfd_layer_weights(*([1] * 12)) for _ in range(6)])
+    wf = L.cfd_weights(1, 1, 1, 1, 1, 1, layers)
+
+    def create(*g):
+        return lib.cfd_create(C.byref(L.cfd_config(*g)), C.byref(wf), None, C.byref(ctx))
+    # dh = 64 (SURVEY §8(b) lists {32, 64}): rejected -- the kernels are built for 64-byte head rows
+    assert create(640, 640, 32, 16, 256, 4, 6, 1024, 5, 8, 1e-6) == -3
+    assert create(640, 640, 32, 16, 192, 6, 6, 768, 5, 8, 1e-6) == -3     # d not in {64, 128, 256, 512}
+    assert create(640, 600, 32, 16, 256, 8, 6, 1024, 5, 8, 1e-6) == -2    # W % Pc != 0
+    assert create(640, 640, 32, 12, 256, 8, 6, 1024, 5, 8, 1e-6) == -2    # Pc % Pf != 0
+    assert create(640, 640, 32, 16, 256, 8, 6, 1024, 6, 8, 1e-6) == -1    # score_layer >= L
+    assert create(4096, 4096, 32, 16, 64, 2, 1, 256, 0, 8, 1e-6) == -3     # Nc = 16384 > 4096
 
 
 def test_sass_contains_tcgen05_and_tma():

@@ -393,6 +393,40 @@ def test_padded_batch_rejects_short_padding():
         enc.batch_refine_padded(imgs, co["x0"], sel["sel_idx"], sel["sel_count"], 300)  # < Nc: CFD_E_ARG
 
 
+@pytest.mark.parametrize("geom", [
+    (128, 128, 32, 16, 128, 4, 2, 512, 1),    # d = 128 (4 heads): two-GEMM MLP path, fused LN epilogues
+    (128, 128, 32, 16, 512, 16, 1, 2048, 0),  # d = 512 (16 heads): standalone LayerNorms, BN = 256 tiles
+    (1024, 1024, 32, 16, 64, 2, 1, 256, 0),   # Nc = 1024 > 512: select_kernel<1024>, Nf = 4096
+])
+def test_other_accepted_geometries_end_to_end(geom):
+    """Every geometry class validate_cfg accepts (d in {64, 128, 256, 512} with dh = 32, Nc up to
+    4096) runs end to end against the oracle: coarse + refine with ragged k."""
+    cfg = ci.ModelConfig(*geom)
+    w = ci.make_weights(cfg, seed=2)
+    enc = CFDetrEncoder(cfg, w, max_tasks=8)
+    Nc = cfg.n_coarse
+    ks = [Nc // 4, 0, Nc]
+    imgs = ci.make_frames(cfg, len(ks), task0=4)
+    dimg = bf16_tensor(imgs, "cuda")
+    co = enc.coarse_encode(dimg, want_layers=True)
+    sel = enc.select_regions(co["scores"], k=ks)
+    ro = enc.batch_refine(dimg, co["x0"], sel["sel_idx"], sel["sel_count"], want_layers=True)
+    torch.cuda.synchronize()
+    enc.check()
+    cu = ro["cu_seqlens"].cpu().numpy()
+    assert np.diff(cu).tolist() == [Nc + (cfg.m ** 2 - 1) * k for k in ks]
+    for t in (0, 2):
+        oc = O.coarse_encode(cfg, w, [imgs[t]])[0]
+        for l in range(cfg.n_layers):
+            _tol(co["layer_out"][l, t].cpu().numpy(), oc["layers"][l], f"{geom} task {t} coarse layer {l}")
+        sel_o = O.select_topk(co["scores"][t].cpu().numpy(), ks[t])
+        assert np.array_equal(sel["sel_idx"][t, :ks[t]].cpu().numpy(), sel_o)
+        rr = O.refine_encode(cfg, w, imgs[t], oc["x0"], sel_o)
+        for l in range(cfg.n_layers):
+            _tol(ro["layer_out"][l, cu[t]:cu[t + 1]].cpu().numpy(), rr["layers"][l], f"{geom} task {t} refine layer {l}")
+    enc.close()
+
+
 def test_split_factor_m3_the_papers_3x3_to_9x9_example():
     """Split factor m = 3 (a 3x3 coarse grid refined into 9x9 fine patches): 144x144
     frames, Pc = 48, Pf = 16, Nc = 9, Nf = 81; ragged k = (3, 0, 9) against the oracle."""
