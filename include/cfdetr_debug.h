@@ -77,7 +77,8 @@ int32_t cfdx_probe_count(int32_t kind);
  *          polynomial instead of MUFU (0, 2 default, 4, 6, 8)
  *   key 2  fused MLP kernel on (1, default) / off (0)
  *   key 3  TMA-staged residual(+LayerNorm) epilogues on (1, default) / off (0)
- *   key 4  fused MLP as CTA pairs (cta_group::2) on (1) / off (0, default)
+ *   key 4  fused MLP (with the fused O-projection) as CTA pairs (cta_group::2, each SM holding half of
+ *          every weight operand) on (1, default) / off (0)
  *   key 5  attention warpgroup start stagger in cycles (700 default); -1 / -2 select the
  *          debug library's v4 "quarters" / "MMA warp" attention trace modes
  *   key 7  weight-stationary QKV GEMM on (1, default) / off (0)

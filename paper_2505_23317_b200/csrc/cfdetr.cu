@@ -116,7 +116,7 @@ struct Opts {
   int attn_dyn = 1;       // v4: dynamic item claiming through the workspace work counter (16)
   int fused_mlp = 1;      // fused MLP kernel (d == 256) instead of two GEMM launches (2)
   int staged_epi = 1;     // TMA-staged residual + LayerNorm epilogues (3)
-  int mlp_cluster = 0;    // fused MLP as CTA pairs (cta_group::2) (4)
+  int mlp_cluster = 1;    // fused MLP (+ fused O-projection) as CTA pairs (cta_group::2) (4; 52.3 -> 49.2 us)
   int gemm_bres = 1;      // weight-stationary QKV GEMM (7)
   int fuse_oproj = 1;     // O-projection + residual + LN2 inside the fused MLP kernel (11)
   int embed_mode0 = 1;    // patch-embed GEMMs: 1 CTA/SM, 4-stage ring (13)
@@ -335,6 +335,7 @@ cudaError_t launch_mlp(const Opts& o, const CUtensorMap& th, const CUtensorMap& 
     cudaError_t e = ensure_smem_attr(mlp_tc_kernel<256, 1>, smem);
     if (e == cudaSuccess) e = ensure_smem_attr(mlp_tc_kernel<256, 2>, smem);
     if (e == cudaSuccess) e = ensure_smem_attr(mlp_tc_kernel<256, 1, true>, smem);
+    if (e == cudaSuccess) e = ensure_smem_attr(mlp_tc_kernel<256, 2, true>, smem);
     if (e != cudaSuccess) return e;
   }
   const int tiles = (pad_rows(rows_for_grid, p.ln_cap > 0 ? p.ln_cap : rows_for_grid + 256) + 127) / 128;
@@ -358,7 +359,9 @@ cudaError_t launch_mlp(const Opts& o, const CUtensorMap& th, const CUtensorMap& 
     la[0].val.clusterDim.z = 1;
     lc.attrs = la;
     lc.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&lc, mlp_tc_kernel<256, 2>, th, tw1h, tw2, q, mx, ml, th);
+    if (two) q.preload_x = 0;  // not built for the pair kernel
+    cudaError_t e = two ? cudaLaunchKernelEx(&lc, mlp_tc_kernel<256, 2, true>, th, tw1h, tw2, q, mx, ml, *two)
+                        : cudaLaunchKernelEx(&lc, mlp_tc_kernel<256, 2>, th, tw1h, tw2, q, mx, ml, th);
     ++g_launches;
     return e != cudaSuccess ? e : cudaGetLastError();
   }
@@ -604,7 +607,7 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
     CFD_CUDA(launch_score(tq, sp, score_B, s));
   }
   const bool staged_ok = fuse_ln && o.staged_epi && (d % 64 == 0);
-  if (o.fuse_oproj && o.fused_mlp && !o.mlp_cluster && staged_ok && d == 256 && F % 128 == 0) {
+  if (o.fuse_oproj && o.fused_mlp && staged_ok && d == 256 && F % 128 == 0) {
     // O projection + residual + LN2 fused into the MLP kernel (LN2 never leaves the SM)
     CUtensorMap tx, tln;
     if (!make_tmap(&tx, x, d, x_cap, d, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, true) ||

@@ -128,7 +128,6 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
                   const __grid_constant__ CUtensorMap tmW2, const MlpParams p,
                   const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmLN,
                   const __grid_constant__ CUtensorMap tmWo) {
-  static_assert(!OPJ || CL == 1, "the fused O-projection is built for the single-CTA kernel");
   using S = MlpSmem<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
@@ -162,10 +161,13 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   const int n_chunks = p.F / 128;
   constexpr int KB = D / 64;                 // k-blocks of the h tile (= its ring pieces)
   constexpr bool PAIR = (CL == 2);
-  const int slots_per_tile = (OPJ ? 3 * KB : KB) + (PAIR ? 4 : 8) * n_chunks;
-  // OPJ ring offsets of k-block kb within a tile: o piece / first slot of the W_o pair
-  auto opj_o = [](int kb) { return (kb < 2) ? kb : 4 + kb; };          // 0 1 6 7
-  auto opj_w = [](int kb) { return (kb < 2) ? 2 + 2 * kb : 4 + 2 * kb; };  // 2 4 8 10
+  // OPJ ring per tile: single CTA o0 o1 Wo0(2 slots) Wo1(2) o2 o3 Wo2(2) Wo3(2) = 12 slots;
+  // PAIR o0 o1 Wo0 Wo1 o2 o3 Wo2 Wo3 = 8 slots (a W_o k-block slot holds this CTA's 128 output
+  // rows: the pair MMA takes B columns [0, 128) from CTA 0 and [128, 256) from CTA 1)
+  const int slots_per_tile = (OPJ ? (PAIR ? 2 * KB : 3 * KB) : KB) + (PAIR ? 4 : 8) * n_chunks;
+  // OPJ ring offsets of k-block kb within a tile: o piece / (first) slot of W_o
+  auto opj_o = [](int kb) { return PAIR ? ((kb < 2) ? kb : 2 + kb) : ((kb < 2) ? kb : 4 + kb); };   // 0 1 4 5 | 0 1 6 7
+  auto opj_w = [](int kb) { return PAIR ? ((kb < 2) ? 2 + kb : 4 + kb) : ((kb < 2) ? 2 + 2 * kb : 4 + 2 * kb); };
   const int rank = (CL == 2) ? static_cast<int>(cluster_ctarank()) : 0;
   const int t_first = (CL == 2) ? 2 * static_cast<int>(cluster_id_x()) + rank : static_cast<int>(blockIdx.x);
   const int t_step = (CL == 2) ? 2 * static_cast<int>(nclusters_x()) : static_cast<int>(gridDim.x);
@@ -252,7 +254,12 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
       MLP_TILES(tile) {
         MLP_TR(pit, 0);
         ++pit;
-        if constexpr (OPJ) {  // o0 o1 Wo0 Wo1 o2 o3 Wo2 Wo3 (W_o k-block = 2 slots of 128 rows)
+        if constexpr (OPJ && PAIR) {  // o pieces are the pair MMA's A rows: pair loads completing on the leader
+          for (int g2 = 0; g2 < 2; ++g2) {
+            for (int kb = 2 * g2; kb < 2 * g2 + 2; ++kb) load_half(&tmH, kb * 64, tile * 128, 0, 0, 1);
+            for (int kb = 2 * g2; kb < 2 * g2 + 2; ++kb) load_half(&tmWo, kb * 64, 128 * rank, 0, 0, 1);
+          }
+        } else if constexpr (OPJ) {  // o0 o1 Wo0 Wo1 o2 o3 Wo2 Wo3 (W_o k-block = 2 slots of 128 rows)
           for (int g2 = 0; g2 < 2; ++g2) {
             for (int kb = 2 * g2; kb < 2 * g2 + 2; ++kb) load(&tmH, kb * 64, tile * 128);
             for (int kb = 2 * g2; kb < 2 * g2 + 2; ++kb)
@@ -369,19 +376,22 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
             const uint32_t qo = p0 + opj_o(kb), qw = p0 + opj_w(kb);
             const uint32_t a = wait_pos(qo);
             const uint32_t w = wait_pos(qw);
-            wait_pos(qw + 1);
+            if constexpr (!PAIR) wait_pos(qw + 1);
             tc_fence_after();
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_ss(tmem + ACC2, make_smem_desc(a + k * 32, 16, 1024, kLayoutSW128),
-                     make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128), idesc2, p.preload_x || (kb | k) != 0);
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t ad = make_smem_desc(a + k * 32, 16, 1024, kLayoutSW128);
+              const uint64_t bd = make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128);
+              if constexpr (PAIR) mma_ss_2sm(tmem + ACC2, ad, bd, idesc2, (kb | k) != 0);
+              else mma_ss(tmem + ACC2, ad, bd, idesc2, p.preload_x || (kb | k) != 0);
+            }
             commit(&w_empty[qo % MLP_SLOTS]);
             commit(&w_empty[qw % MLP_SLOTS]);
-            commit(&w_empty[(qw + 1) % MLP_SLOTS]);
+            if constexpr (!PAIR) commit(&w_empty[(qw + 1) % MLP_SLOTS]);
           }
           commit(ao_full);
           MLP_TR(it, 41);
-          pos = p0 + 3 * KB;
+          pos = p0 + (PAIR ? 2 * KB : 3 * KB);
         } else {
           pos = static_cast<uint32_t>(it) * slots_per_tile + KB;  // the h pieces belong to the epilogue
         }
@@ -467,17 +477,18 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
           if (lane == 0) mbar_arrive(x_ready);
         }
         if (et == 0) MLP_TR(it, 38);
-        if (p.preload_x)
+        const int a2_cta = PAIR && rank ? 0 : -1;  // PAIR: acc2 releases arrive on the leader
+        if (!PAIR && p.preload_x)
           resid_ln_tma<4, true, true, false, false>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M,
                                                     bo_s, g2_s, b2ln_s, ln_stats, quarter, half, lane, ao_full, it & 1,
-                                                    a2_empty, -1, tmem + lane_off + HT + half * 64);
+                                                    a2_empty, a2_cta, tmem + lane_off + HT + half * 64);
         else if (p.keep_x1)
           resid_ln_tma<4, true, true, true, false>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M,
                                                    bo_s, g2_s, b2ln_s, ln_stats, quarter, half, lane, ao_full, it & 1,
-                                                   a2_empty, -1, tmem + lane_off + HT + half * 64);
+                                                   a2_empty, a2_cta, tmem + lane_off + HT + half * 64);
         else
           resid_ln_tma<4, true, true>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M, bo_s, g2_s,
-                                      b2ln_s, ln_stats, quarter, half, lane, ao_full, it & 1, a2_empty, -1,
+                                      b2ln_s, ln_stats, quarter, half, lane, ao_full, it & 1, a2_empty, a2_cta,
                                       tmem + lane_off + HT + half * 64);
         if (et == 0) MLP_TR(it, 39);
         tmem_wait_st();
@@ -485,7 +496,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         asm volatile("bar.sync 5, 256;" ::: "memory");
         if (et == 0) {
           MLP_TR(it, 2);
-          mbar_arrive(ht_full);
+          arrive_leader(ht_full);
         }
       } else {
       // ---- h tile -> TMEM (A operand of MMA1): piece kb = k-block kb -> columns [32 kb, 32 kb + 32);
@@ -587,11 +598,12 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         if (OPJ && p.keep_x1) {  // acc2 = x1 + MLP(x1): x2 = acc2 + b2, x not read
           if (do_ln)
             resid_ln_tma<4, true, false, false>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M, b2_s,
-                                                lng_s, lnb_s, ln_stats, quarter, half, lane, a2_full, it & 1, a2_empty);
+                                                lng_s, lnb_s, ln_stats, quarter, half, lane, a2_full, it & 1, a2_empty,
+                                                PAIR && rank ? 0 : -1);
           else
             resid_ln_tma<4, false, false, false>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M,
                                                  b2_s, lng_s, lnb_s, ln_stats, quarter, half, lane, a2_full, it & 1,
-                                                 a2_empty);
+                                                 a2_empty, PAIR && rank ? 0 : -1);
         } else if (do_ln)
           resid_ln_tma<4, true>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M, b2_s, lng_s, lnb_s,
                                 ln_stats, quarter, half, lane, a2_full, it & 1, a2_empty, PAIR && rank ? 0 : -1);

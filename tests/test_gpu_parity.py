@@ -274,11 +274,12 @@ def test_staged_epilogues_match_direct_epilogues():
         assert rel < 3e-3, rel
 
 
-def test_mlp_cta_pair_variant_matches_single_cta_bitwise():
+@pytest.mark.parametrize("opj,keep", [(0, 0), (1, 0), (1, 1)])
+def test_mlp_cta_pair_variant_matches_single_cta_bitwise(opj, keep):
     """The CTA-pair fused MLP (cta_group::2 M=256 MMAs, each SM holding half of every weight
     operand; cfdx_set_option(4, 1)) accumulates the same products in the same k order as the
-    single-CTA kernel: outputs agree bit for bit, including an odd tile count (ghost tile in
-    the last pair)."""
+    single-CTA kernel: outputs agree bit for bit, with and without the fused O-projection and
+    x1 kept in TMEM, including an odd tile count (ghost tile in the last pair)."""
     cfg = ci.CONFIGS["c640"]
     enc = CFDetrEncoder(cfg, ci.make_weights(cfg, seed=0), max_tasks=8)
     imgs = bf16_tensor(ci.make_frames(cfg, 3, task0=5), "cuda")
@@ -287,22 +288,18 @@ def test_mlp_cta_pair_variant_matches_single_cta_bitwise():
     sel = enc.select_regions(co["scores"], k=ks)
     x0 = co["x0"].clone()
     outs = []
-    try:
-        # the pair kernel has no fused O-projection; the single-CTA side runs with x1 stored
-        # (option 19 = 0), which is bitwise the separate O-projection (test below)
-        enc.set_option(19, 0)
-        for cl in (0, 1):
-            enc.set_option(4, cl)
-            c2 = enc.coarse_encode(imgs)
-            ro = enc.batch_refine(imgs, x0, sel["sel_idx"], sel["sel_count"])
-            torch.cuda.synchronize()
-            n = int(ro["cu_seqlens"][-1])
-            outs.append((c2["y"].clone(), ro["y"][:n].clone()))
-    finally:
-        enc.set_option(4, 0)
-        enc.set_option(19, 1)
+    enc.set_option(11, opj)
+    enc.set_option(19, keep)
+    for cl in (0, 1):
+        enc.set_option(4, cl)
+        c2 = enc.coarse_encode(imgs, want_layers=True)
+        ro = enc.batch_refine(imgs, x0, sel["sel_idx"], sel["sel_count"], want_layers=True)
+        torch.cuda.synchronize()
+        n = int(ro["cu_seqlens"][-1])
+        outs.append((c2["layer_out"].clone(), c2["scores"].clone(), ro["layer_out"][:, :n].clone()))
     for a, b in zip(outs[0], outs[1]):
         assert torch.equal(a, b)
+    enc.close()
 
 
 def test_fused_oproj_matches_separate_oproj_bitwise():
