@@ -9,8 +9,11 @@ one lane's kernels fill the SMs the other's leave idle in their last wave.  The 
 are checked to equal the single-launch batch bit for bit before timing.
 
 Workloads (BASELINE.json configs):
-  c640     (default) 640x640 frames, Pc 32 / Pf 16, d256/h8/L6, k = 100 (25 %), --frames 32
-           in flight per GPU (weak scaling: every rank its own 32 frames)
+  c640     (default) 640x640 frames, Pc 32 / Pf 16, d256/h8/L6, k = 100 (25 %), --frames 128
+           in flight per GPU as two 64-frame lanes (weak scaling: every rank its own frames);
+           frames/s rises with the frames in flight (32: 24.7k, 64: 29.3k, 128: 33.7k, 256:
+           35.5k on one B200, profiles/r2_frames_sweep.txt) -- per-launch tails shrink
+           as launches carry more tiles; c640b1 is the one-frame latency line
   c640b1   the same model, one frame per step (latency)
   batch6   6 tasks, k = (0, 80, 160, 240, 320, 400): one varlen launch per op
   fine8    8 frames, every region refined (1600 fine tokens each): the dense-attention case
@@ -60,7 +63,7 @@ def parse(argv=None):
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
                     help="multi48 only: strong (48 streams over N GPUs, default) or weak (48 per GPU)")
     ap.add_argument("--mix", default="balanced", choices=["balanced", "s348"], help="multi48 ratio mix")
-    ap.add_argument("--frames", type=int, default=32, help="c640: frames in flight per GPU per step")
+    ap.add_argument("--frames", type=int, default=128, help="c640: frames in flight per GPU per step")
     ap.add_argument("--ratio", type=int, default=25, help="c640: refine percentage per frame")
     ap.add_argument("--streams", type=int, default=None,
                     help="concurrent lanes per GPU (own encoder / stream / CUDA graph each); default 2 for "
