@@ -215,10 +215,13 @@ cudaError_t launch_gemm_t(const Opts& o, const CUtensorMap& ta, const CUtensorMa
   constexpr bool kStgOut = (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_GELU) && MODE != 1;
   constexpr int EW = MODE == 1 ? 4 : 8;
   constexpr int NACC = MODE == 1 ? 1 : 2;
-  constexpr int ST = kImg ? 8 : kBres ? 3 : (MODE == 1 || kTmaEpi) ? 2 : kStgOut ? gemm_stages_stg<BN>() : gemm_stages<BN>();
+  // BRES: 4 A stages (64 KB in flight: the A tiles come from L2 / DRAM at ~1-2 us latency)
+  // with one 2 KB output staging buffer per epilogue warp
+  constexpr int ST = kImg ? 8 : kBres ? 4 : (MODE == 1 || kTmaEpi) ? 2 : kStgOut ? gemm_stages_stg<BN>() : gemm_stages<BN>();
   auto kern = gemm_tc_kernel<BN, ST, EPI, EW, NACC, kBres, kImg>;
   using SM = GemmSmem<BN, ST, NACC, kBres, kImg ? 32 : GEMM_BK>;
-  constexpr int smem = kTmaEpi ? SM::TOTAL_TMA_EPI : kStgOut ? SM::TOTAL_STG_OUT : SM::TOTAL;
+  constexpr int smem = kTmaEpi ? SM::TOTAL_TMA_EPI : (kStgOut && kBres) ? SM::TOTAL_STG_OUT1
+                       : kStgOut ? SM::TOTAL_STG_OUT : SM::TOTAL;
   static_assert(smem <= 232448, "shared memory budget");
   CUtensorMap tout;
   if constexpr (kStgOut) {  // bf16 output [m_cap, N], 32 x 32 boxes

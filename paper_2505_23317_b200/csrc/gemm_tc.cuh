@@ -100,6 +100,7 @@ struct GemmSmem {
   static constexpr int STG_OFF = BAR_OFF + ((BAR_BYTES + PAR_BYTES + 1023) / 1024) * 1024;
   static constexpr int TOTAL_TMA_EPI = 1024 + STG_OFF + GEMM_EPI_WARPS * STG_BYTES;
   static constexpr int TOTAL_STG_OUT = 1024 + STG_OFF + GEMM_EPI_WARPS * 4096;  // bf16 out: 2 x 2 KB per warp
+  static constexpr int TOTAL_STG_OUT1 = 1024 + STG_OFF + GEMM_EPI_WARPS * 2048;  // bf16 out: 1 x 2 KB per warp
   static constexpr uint32_t TMEM_COLS = (NACC * BN <= 32) ? 32 : (NACC * BN <= 64) ? 64 : (NACC * BN <= 128) ? 128
                                         : (NACC * BN <= 256) ? 256 : 512;
 };
@@ -451,8 +452,9 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
 // bf16 output epilogue of one warp (32 rows x CH 32-column chunks) through shared memory:
 // acc + bias (+GELU) -> bf16 -> a 2 KB SW64 buffer (conflict-free 16-byte writes, one row per
 // thread) -> TMA store of the 32 x 32 box.  Two buffers alternate; a buffer is rewritten once
-// the store issued from it two chunks earlier has finished reading.
-template <int CH, int EPI>
+// the store issued from it two chunks earlier has finished reading (SB = 1: one buffer, the
+// previous chunk's store must have finished reading it -- frees shared memory for the ring).
+template <int CH, int EPI, int SB = 2>
 __device__ __forceinline__ void store_bf16_tma(const CUtensorMap& tmO, uint8_t* stg, uint32_t tbase, int row0,
                                                int col_base, const float* bias_s, int lane, uint64_t* tfull_bar,
                                                uint32_t tfull_parity, uint64_t* tempty_bar) {
@@ -477,9 +479,12 @@ __device__ __forceinline__ void store_bf16_tma(const CUtensorMap& tmO, uint8_t* 
       if constexpr (EPI == EPI_BF16_BIAS_GELU) gelu2(x0, x1);
       pk[i] = pack_bf16x2(x0, x1);
     }
-    if (lane == 0) bulk_wait_read1();  // the store that last read this buffer is done reading
+    if (lane == 0) {  // the store that last read this buffer is done reading
+      if constexpr (SB == 2) bulk_wait_read1();
+      else bulk_wait_read0();
+    }
     __syncwarp();
-    uint8_t* buf = stg + (c & 1) * 2048;
+    uint8_t* buf = stg + (SB == 2 ? (c & 1) * 2048 : 0);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
@@ -645,8 +650,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
         resid_ln_tma<CH, true>(la, tmX, tmLN, st, tbase, row0, col_base, M, bias_s, lng_s, lnb_s, ln_stats, quarter,
                                half, lane, &tfull[acc], acc_phase, &tempty[acc]);
       } else if constexpr (kStgOut) {
-        store_bf16_tma<CH, EPI>(tmX, smem + S::STG_OFF + (warp - 2) * 4096, tbase, row0, col_base, bias_s, lane,
-                                &tfull[acc], acc_phase, &tempty[acc]);
+        constexpr int SB = BRES ? 1 : 2;  // BRES: one staging buffer per warp, one more A stage
+        store_bf16_tma<CH, EPI, SB>(tmX, smem + S::STG_OFF + (warp - 2) * 2048 * SB, tbase, row0, col_base, bias_s,
+                                    lane, &tfull[acc], acc_phase, &tempty[acc]);
       } else if constexpr (EPI == EPI_F32_RESID || EPI == EPI_F32_RESID_LN) {
         // Residual epilogue, software-pipelined over the 32-column chunks: the residual
         // row segment of chunk c+1 is loaded while chunk c is added and stored, and chunk
