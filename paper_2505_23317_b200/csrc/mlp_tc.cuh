@@ -137,8 +137,8 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   uint64_t* ht_full = w_empty + MLP_SLOTS;   // h tile copied into TMEM
   uint64_t* a1_full = ht_full + 1;
   uint64_t* a1_empty = a1_full + 1;
-  uint64_t* h_full = a1_empty + 1;           // [2]
-  uint64_t* h_empty = h_full + 2;            // [2]
+  uint64_t* h_full = a1_empty + 1;           // [2 buffers][2 k-blocks]: H[b] k-block kb written
+  uint64_t* h_empty = h_full + 4;            // [2]
   uint64_t* a2_full = h_empty + 2;
   uint64_t* a2_empty = a2_full + 1;
   uint64_t* xbar = a2_empty + 1;             // [8 warps][3] staged-epilogue TMA loads
@@ -183,7 +183,8 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     mbar_init(ht_full, CL);
     mbar_init(a1_full, 1);
     mbar_init(a1_empty, 8 * CL);
-    for (int i = 0; i < 2; ++i) { mbar_init(&h_full[i], 8 * CL); mbar_init(&h_empty[i], 1); }
+    for (int i = 0; i < 4; ++i) mbar_init(&h_full[i], 8 * CL);
+    for (int i = 0; i < 2; ++i) mbar_init(&h_empty[i], 1);
     mbar_init(a2_full, 1);
     mbar_init(a2_empty, 8 * CL);
     for (int i = 0; i < 24; ++i) mbar_init(&xbar[i], 1);
@@ -329,15 +330,18 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
       };
       auto mma2 = [&](int j) {
         const int b = j & 1;
-        mbar_wait(&h_full[b], (h_ph >> b) & 1);
-        h_ph ^= 1u << b;
-        if (j < 8) MLP_TR(it, 12 + j);
-        if (j == 0) {  // acc2 must have been drained by the previous tile's epilogue
-          mbar_wait(a2_empty, (a2_cnt & 1) ^ 1);
-          ++a2_cnt;
-        }
         const uint32_t h_base = smem_u32(smem + S::H_OFF + b * S::H_BYTES);
         for (int kb = 0; kb < 2; ++kb) {
+          // each GELU k-block (64 hidden columns) is signalled separately, so the k-block 0
+          // MMAs run while the epilogue still computes k-block 1
+          mbar_wait(&h_full[2 * b + kb], (h_ph >> b) & 1);
+          if (kb == 0) {
+            if (j < 8) MLP_TR(it, 12 + j);
+            if (j == 0) {  // acc2 must have been drained by the previous tile's epilogue
+              mbar_wait(a2_empty, (a2_cnt & 1) ^ 1);
+              ++a2_cnt;
+            }
+          }
           const uint32_t w = take();  // !PAIR: rows 0-127 of the k-block, rows 128-255 in the next slot
           if constexpr (!PAIR) {
             ++pos;
@@ -356,6 +360,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
           give();
           if constexpr (!PAIR) give();
         }
+        h_ph ^= 1u << b;
         commit(&h_empty[b]);
       };
       MLP_TILES(tile) {
@@ -531,7 +536,10 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         }
       }
       }
-      // ---- hidden chunks: GELU(acc1 + b1) -> bf16 -> H[j&1] (SW128 K-major, k-block = half)
+      // ---- hidden chunks: GELU(acc1 + b1) -> bf16 -> H[j&1] (SW128 K-major).  Warp (quarter,
+      //      half) owns rows 32 quarter.. and columns [32 half, +32) of each 64-column k-block;
+      //      k-block 0 is finished (and signalled) before k-block 1, so MMA2's first half
+      //      overlaps the second half of the GELU.
       for (int j = 0; j < n_chunks; ++j) {
         const int b = j & 1;
         mbar_wait(a1_full, a1_ph);
@@ -539,9 +547,9 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         if (et == 0 && j < 8) MLP_TR(it, 20 + j);
         tc_fence_after();
         uint32_t r0[32], r1[32];
-        const uint32_t ta = tmem + lane_off + ACC1 + half * 64;
-        tmem_ld32(ta, r0);
-        tmem_ld32(ta + 32, r1);
+        const uint32_t ta = tmem + lane_off + ACC1 + half * 32;
+        tmem_ld32(ta, r0);        // k-block 0 columns [32 half, +32)
+        tmem_ld32(ta + 64, r1);   // k-block 1 columns [64 + 32 half, +32)
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
@@ -551,29 +559,33 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
           mbar_wait(&h_empty[b], (h_ph >> b) & 1);
           h_ph ^= 1u << b;
         }
-        uint8_t* hrow = smem + S::H_OFF + b * S::H_BYTES + half * 16384 + r_in_tile * 128;
-        const int col0 = 128 * j + half * 64;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {  // 16-byte chunk q = columns [8q, 8q+8)
-          const uint32_t* r = (q < 4) ? r0 : r1;
-          const int o = (q & 3) * 8;
-          uint32_t pk[4];
-          const float4 bl = *reinterpret_cast<const float4*>(b1_s + col0 + 8 * q);      // smem broadcast
-          const float4 bh = *reinterpret_cast<const float4*>(b1_s + col0 + 8 * q + 4);
-          const float bv[8] = {bl.x, bl.y, bl.z, bl.w, bh.x, bh.y, bh.z, bh.w};
+        for (int kb = 0; kb < 2; ++kb) {
+          const uint32_t* r = kb ? r1 : r0;
+          uint8_t* hrow = smem + S::H_OFF + b * S::H_BYTES + kb * 16384 + r_in_tile * 128;
+          const int col0 = 128 * j + kb * 64 + half * 32;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float a, c;
-            fma2x(a, c, __uint_as_float(r[o + 2 * e]), __uint_as_float(r[o + 2 * e + 1]), 1.f, 1.f, bv[2 * e],
-                  bv[2 * e + 1]);
-            gelu2(a, c);
-            pk[e] = pack_bf16x2(a, c);
+          for (int qq = 0; qq < 4; ++qq) {  // 16-byte chunk q = 4 half + qq: columns [8q, 8q+8) of the k-block
+            const int o = qq * 8;
+            uint32_t pk[4];
+            const float4 bl = *reinterpret_cast<const float4*>(b1_s + col0 + 8 * qq);      // smem broadcast
+            const float4 bh = *reinterpret_cast<const float4*>(b1_s + col0 + 8 * qq + 4);
+            const float bv[8] = {bl.x, bl.y, bl.z, bl.w, bh.x, bh.y, bh.z, bh.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float a, c;
+              fma2x(a, c, __uint_as_float(r[o + 2 * e]), __uint_as_float(r[o + 2 * e + 1]), 1.f, 1.f, bv[2 * e],
+                    bv[2 * e + 1]);
+              gelu2(a, c);
+              pk[e] = pack_bf16x2(a, c);
+            }
+            const int q = 4 * half + qq;
+            *reinterpret_cast<uint4*>(hrow + ((q ^ (r_in_tile & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
-          *reinterpret_cast<uint4*>(hrow + ((q ^ (r_in_tile & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
+          __syncwarp();
+          if (lane == 0) arrive_leader(&h_full[2 * b + kb]);
         }
-        fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
-        __syncwarp();
-        if (lane == 0) arrive_leader(&h_full[b]);
         if (et == 0 && j < 8) MLP_TR(it, 28 + j);
       }
       // the last two H buffers' MMA2 commits (consumed so the phase counts stay in step)
