@@ -101,6 +101,8 @@ int32_t cfdx_probe_count(int32_t kind);
  *   key 20 with key 19 = 1: x loaded into acc2 while o / W_o stream in (1) / 0 (default)
  *   key 21 attention v7: control-warp sleep between barrier probes, ns (0, 32 default, 128)
  *   key 22 attention v7: softmax warpgroups per CTA (3, or 4 default)
+ *   key 23 QKV projection as CTA pairs (cta_group::2, half of each weight column block resident
+ *          per SM, 8 A stages in flight) on (1, default) / off (0: one CTA per column block)
  * Other keys / values: CFD_E_ARG. */
 cfd_status cfdx_set_option(cfd_ctx *ctx, int32_t key, int32_t value);
 

@@ -128,6 +128,7 @@ struct Opts {
   int preload_x = 0;      // with 19: x loaded into acc2 before MMA_o (20; measured slower)
   int attn_sleep = 32;    // v7: MMA / producer warp sleep when idle, ns (21: 0, 32, 128)
   int attn_nwg = 4;       // v7: softmax warpgroups per CTA (22: 3 or 4)
+  int qkv_pair = 1;       // QKV projection as CTA pairs, half of the weights resident per SM (23)
 };
 Opts g_dbg_opts;
 
@@ -241,6 +242,37 @@ cudaError_t launch_gemm_t(const Opts& o, const CUtensorMap& ta, const CUtensorMa
   cudaError_t le = launch_ex(kern, dim3(grid), dim3(64 + 32 * EW), smem, s, ta, tb, p, tx ? *tx : ta, tln ? *tln : ta);
   ++g_launches;
   return le != cudaSuccess ? le : cudaGetLastError();
+}
+
+// QKV projection as CTA pairs (gemm_tc_kernel PAIR): bf16 out + bias, K = 256, N = 3d with
+// BN = 256 column blocks; 2-CTA clusters, (74 / n_tiles) * n_tiles clusters at most.
+cudaError_t launch_qkv_pair(const Opts& o, const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p,
+                            int rows_for_grid, cudaStream_t s) {
+  constexpr int ST = 8;
+  auto kern = gemm_tc_kernel<256, ST, EPI_BF16_BIAS, 8, 2, true, false, true>;
+  using SM = GemmSmem<256, ST, 2, true, GEMM_BK, true>;
+  constexpr int smem = SM::TOTAL_STG_OUT1;
+  static_assert(smem <= 232448, "shared memory budget");
+  if (cudaError_t e = ensure_smem_attr(kern, smem); e != cudaSuccess) return e;
+  CUtensorMap tout;  // bf16 output [m_cap, N], 32 x 32 boxes
+  if (!make_tmap(&tout, p.out_bf16, p.N, p.m_cap, p.N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
+  const int nt = p.N / 256, mt = (rows_for_grid + GEMM_BM - 1) / GEMM_BM;
+  const int pairs_per_col = std::max(1, std::min((mt + 1) / 2, (num_sms(o) / 2) / nt));
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(2 * pairs_per_col * nt);
+  lc.blockDim = dim3(64 + 32 * 8);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeClusterDimension;
+  la[0].val.clusterDim.x = 2;
+  la[0].val.clusterDim.y = 1;
+  la[0].val.clusterDim.z = 1;
+  lc.attrs = la;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, kern, ta, tb_half, p, tout, ta);
+  ++g_launches;
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int EPI>
@@ -493,6 +525,7 @@ struct LayerDev {
   CUtensorMap tm_1c, tm_2c;  // W1 / W2 with 128-row x 64-k boxes (fused MLP ring slots)
   CUtensorMap tm_oc;         // W_o with 128-row x 64-k boxes (fused O-projection + MLP)
   CUtensorMap tm_1h;         // W1 with 64-row x 64-k boxes (CTA-pair fused MLP)
+  CUtensorMap tm_qkv_h;      // W_qkv with 128-row x 64-k boxes (CTA-pair QKV: half a column block per CTA)
 };
 
 struct cfd_ctx {
@@ -593,7 +626,14 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   GemmParams p{};
   p.M = M_static; p.m_dev = m_dev; p.m_cap = w.rows_cap; p.N = 3 * d; p.K = d; p.bias = L.b_qkv;
   p.out_bf16 = w.qkv;
-  CFD_CUDA(launch_gemm(o, EPI_BF16_BIAS, ta_h, L.tm_qkv, p, rows_grid, s, PK_QKV));
+  if (o.qkv_pair && o.gemm_bres && d == 256 && num_sms(o) >= 2 * (3 * d / 256)) {
+    probe_begin(PK_QKV, s);
+    const cudaError_t e = launch_qkv_pair(o, ta_h, L.tm_qkv_h, p, rows_grid, s);
+    probe_end(PK_QKV, s);
+    CFD_CUDA(e);
+  } else {
+    CFD_CUDA(launch_gemm(o, EPI_BF16_BIAS, ta_h, L.tm_qkv, p, rows_grid, s, PK_QKV));
+  }
   // attention
   AttnParams ap{};
   ap.cu_seqlens = cu; ap.d_model = d; ap.out = w.obuf; ap.lse = want_lse ? w.lse : nullptr; ap.lse_ld = w.lse_ld;
@@ -793,6 +833,7 @@ cfd_status cfdx_set_option(cfd_ctx* ctx, int32_t key, int32_t value) {
       if (value != 3 && value != 4) return CFD_E_ARG;
       o.attn_nwg = value;
       return CFD_OK;
+    case 23: o.qkv_pair = b; return CFD_OK;
   }
   return CFD_E_ARG;
 }
@@ -889,7 +930,8 @@ cfd_status cfd_create(const cfd_config* cfg, const cfd_weights* wts, void* strea
         !make_tmap(&ld.tm_1c, ld.w1, d, F, d, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !make_tmap(&ld.tm_2c, ld.w2, F, d, F, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !make_tmap(&ld.tm_1h, ld.w1, d, F, d, GEMM_BK, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_tmap(&ld.tm_oc, ld.wo, d, d, d, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+        !make_tmap(&ld.tm_oc, ld.wo, d, d, d, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap(&ld.tm_qkv_h, ld.wqkv, d, 3 * d, d, GEMM_BK, 128, CU_TENSOR_MAP_SWIZZLE_128B))
       return fail(CFD_E_CUDA);
   }
   *out = c;

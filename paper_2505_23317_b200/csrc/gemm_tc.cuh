@@ -85,10 +85,10 @@ constexpr int GEMM_MAX_LN = 512;   // LayerNorm width for EPI_F32_RESID_LN
 // four 64-wide k-blocks) is loaded into shared memory once and stays there while the CTA
 // streams its row tiles through an A-only ring.  The default streams A and B per k-block.
 constexpr int GEMM_BRES_KB = 4;
-template <int BN, int STAGES, int NACC = 2, bool BRES = false, int BKX = GEMM_BK>
+template <int BN, int STAGES, int NACC = 2, bool BRES = false, int BKX = GEMM_BK, bool PAIR = false>
 struct GemmSmem {
   static constexpr int A_BYTES = GEMM_BM * BKX * 2;
-  static constexpr int B_BYTES = BN * BKX * 2;
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BKX * 2;  // PAIR: this CTA's half of the columns
   static constexpr int STAGE_BYTES = A_BYTES + (BRES ? 0 : B_BYTES);  // TMA bytes per ring stage
   static constexpr int NB = BRES ? GEMM_BRES_KB : STAGES;            // B buffers
   static constexpr int BAR_OFF = STAGES * A_BYTES + NB * B_BYTES;
@@ -457,7 +457,7 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
 template <int CH, int EPI, int SB = 2>
 __device__ __forceinline__ void store_bf16_tma(const CUtensorMap& tmO, uint8_t* stg, uint32_t tbase, int row0,
                                                int col_base, const float* bias_s, int lane, uint64_t* tfull_bar,
-                                               uint32_t tfull_parity, uint64_t* tempty_bar) {
+                                               uint32_t tfull_parity, uint64_t* tempty_bar, int tempty_cta = -1) {
   mbar_wait(tfull_bar, tfull_parity);
   tc_fence_after();
 #pragma unroll 1
@@ -468,7 +468,10 @@ __device__ __forceinline__ void store_bf16_tma(const CUtensorMap& tmO, uint8_t* 
     if (c + 1 == CH) {  // accumulator fully read: hand TMEM back to the MMA warp
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_bar);
+      if (lane == 0) {
+        if (tempty_cta >= 0) mbar_arrive_cluster(tempty_bar, static_cast<uint32_t>(tempty_cta));
+        else mbar_arrive(tempty_bar);
+      }
     }
     const int col0 = col_base + c * 32;
     uint32_t pk[16];
@@ -501,15 +504,23 @@ __device__ __forceinline__ void store_bf16_tma(const CUtensorMap& tmO, uint8_t* 
 // IMG: A tiles are TMA-gathered from the HWC image through a 5-D tensor map (reading R2:
 // patch vector (py, px, ch) = one Pc*3-element pixel segment per patch row), so no im2col
 // buffer is written or read; 32-wide k-blocks in 64-byte (SW64) rows.
-template <int BN, int STAGES, int EPI, int EW, int NACC, bool BRES = false, bool IMG = false>
+// PAIR (BRES bf16 outputs only: the QKV projection): 2-CTA clusters issuing cta_group::2
+// M = 256 MMAs over the pair's two 128-row tiles; each CTA keeps HALF of the column block's
+// weights resident (rows [128 rank, +128) of the BN = 256 block, 64 KB instead of 128 KB), so
+// the freed shared memory holds 8 A stages in flight.  A pieces are pair TMA loads completing
+// on the leader's full barrier; the leader's commits reach both CTAs; both epilogues release
+// the accumulator on the leader's tempty.  Tile walk: the pair takes row-tile pairs
+// (2 i, 2 i + 1); an odd last tile leaves CTA 1 a ghost tile (stores skipped).
+template <int BN, int STAGES, int EPI, int EW, int NACC, bool BRES = false, bool IMG = false, bool PAIR = false>
 __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmParams p, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ CUtensorMap tmLN) {
   static_assert((EW == 8 && NACC == 2) || (EW == 4 && NACC == 1), "supported epilogue configurations");
   static_assert(!IMG || (EPI == EPI_EMBED_COARSE && !BRES), "IMG is the coarse patch embed");
+  static_assert(!PAIR || (BRES && BN == 256 && EW == 8 && EPI == EPI_BF16_BIAS), "PAIR is the QKV projection");
   constexpr int BKX = IMG ? 32 : GEMM_BK;
-  using S = GemmSmem<BN, STAGES, NACC, BRES, BKX>;
+  using S = GemmSmem<BN, STAGES, NACC, BRES, BKX, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
   uint8_t* sA = smem;
@@ -536,27 +547,41 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
   const int n_tiles = p.N / BN;
   const int num_k = p.K / BKX;
   const int rpt = IMG ? p.img_rb * p.img_gw : GEMM_BM;  // rows per tile
-  const int n_fix = BRES ? (int)blockIdx.x % n_tiles : 0;
+  const int rank = PAIR ? static_cast<int>(cluster_ctarank()) : 0;
+  const int cta_id = PAIR ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);  // BRES walk unit
+  const int n_units = PAIR ? static_cast<int>(nclusters_x()) : static_cast<int>(gridDim.x);
+  const int n_fix = BRES ? cta_id % n_tiles : 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < NACC; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], EW); }
+    for (int a = 0; a < NACC; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], EW * (PAIR ? 2 : 1)); }
     for (int i = 0; i < 16; ++i) mbar_init(&xbar[i], 1);
     mbar_init(bres_full, 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<S::TMEM_COLS>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_alloc_2sm<S::TMEM_COLS>(tmem_slot);
+    else tmem_alloc<S::TMEM_COLS>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // peer barriers initialised before any remote arrive / pair load
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if constexpr (BRES) {  // the CTA's weight slice, once
     if (warp == 0 && lane == 0) {
-      mbar_expect_tx(bres_full, GEMM_BRES_KB * S::B_BYTES);
-      for (int kb = 0; kb < GEMM_BRES_KB; ++kb)
-        tma_load_2d(sB + kb * S::B_BYTES, &tmB, bres_full, kb * GEMM_BK, n_fix * BN);
+      if constexpr (PAIR) {  // this CTA's 128 rows of the column block, on the leader's barrier
+        if (rank == 0) mbar_expect_tx(bres_full, 2 * GEMM_BRES_KB * S::B_BYTES);
+        const uint32_t lb = mapa_u32(bres_full, 0);
+        for (int kb = 0; kb < GEMM_BRES_KB; ++kb)
+          tma_load_2d_2sm(sB + kb * S::B_BYTES, &tmB, lb, kb * GEMM_BK, n_fix * BN + 128 * rank);
+      } else {
+        mbar_expect_tx(bres_full, GEMM_BRES_KB * S::B_BYTES);
+        for (int kb = 0; kb < GEMM_BRES_KB; ++kb)
+          tma_load_2d(sB + kb * S::B_BYTES, &tmB, bres_full, kb * GEMM_BK, n_fix * BN);
+      }
     }
   }
   const int M = p.m_dev ? __ldg(p.m_dev) : p.M;
@@ -564,21 +589,27 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
   // RESID_LN also visits the tiles of the pad rows (zeroed in ln_out, x untouched)
   const int m_tiles = ((EPI == EPI_F32_RESID_LN ? pad_rows(M, p.ln_cap) : m_store) + rpt - 1) / rpt;
   const int total = m_tiles * n_tiles;
-  // tile walk: default tile = m_blk * n_tiles + n_blk over all tiles; BRES: the CTA keeps
-  // column block blockIdx % n_tiles and walks row blocks (gridDim is a multiple of n_tiles)
-  const int t_first = BRES ? (int)blockIdx.x / n_tiles : (int)blockIdx.x;
-  const int t_step = BRES ? (int)gridDim.x / n_tiles : (int)gridDim.x;
-  const int t_end = BRES ? ((int)blockIdx.x < t_step * n_tiles ? m_tiles : 0) : total;
+  // tile walk: default tile = m_blk * n_tiles + n_blk over all tiles; BRES: the CTA (PAIR: the
+  // cluster) keeps column block cta_id % n_tiles and walks row blocks (PAIR: row-block pairs;
+  // the unit count is a multiple of n_tiles)
+  const int t_first = BRES ? cta_id / n_tiles : (int)blockIdx.x;
+  const int t_step = BRES ? n_units / n_tiles : (int)gridDim.x;
+  const int m_units = PAIR ? (m_tiles + 1) / 2 : m_tiles;
+  const int t_end = BRES ? (cta_id < t_step * n_tiles ? m_units : 0) : total;
+  auto m_of = [&](int tile) { return BRES ? (PAIR ? 2 * tile + rank : tile) : tile / n_tiles; };
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = t_first; tile < t_end; tile += t_step) {
-        const int m_blk = BRES ? tile : tile / n_tiles, n_blk = BRES ? n_fix : tile % n_tiles;
+        const int m_blk = m_of(tile), n_blk = BRES ? n_fix : tile % n_tiles;
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if constexpr (IMG) {  // rpt rows of 64 B (OOB rows of the last tile are zero-filled)
+          if constexpr (PAIR) {  // this CTA's 128 A rows, completing on the leader's full barrier
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * S::A_BYTES);
+            tma_load_2d_2sm(sA + stage * S::A_BYTES, &tmA, mapa_u32(&full[stage], 0), kb * BKX, m_blk * GEMM_BM);
+          } else if constexpr (IMG) {  // rpt rows of 64 B (OOB rows of the last tile are zero-filled)
             mbar_expect_tx(&full[stage], rpt * 64 + S::B_BYTES);
             tma_load_5d(sA + stage * S::A_BYTES, &tmA, &full[stage], 0, kb % p.img_thirds, 0, kb / p.img_thirds,
                         m_blk * p.img_rb);
@@ -592,8 +623,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(GEMM_BM, BN, 0);
+    if (lane == 0 && rank == 0) {  // PAIR: the leader issues the pair's MMAs
+      constexpr uint32_t idesc = make_idesc_bf16(GEMM_BM * (PAIR ? 2 : 1), BN, 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -614,12 +645,15 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
                                     : make_smem_desc(a0 + k * 32, 16, 1024, kLayoutSW128);
             const uint64_t bd = IMG ? make_smem_desc(b0 + k * 32, 16, 512, kLayoutSW64)
                                     : make_smem_desc(b0 + k * 32, 16, 1024, kLayoutSW128);
-            mma_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            if constexpr (PAIR) mma_ss_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            else mma_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
-          mma_commit(&empty[stage]);
+          if constexpr (PAIR) mma_commit_2sm(&empty[stage], 0x3);
+          else mma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[acc]);
+        if constexpr (PAIR) mma_commit_2sm(&tfull[acc], 0x3);
+        else mma_commit(&tfull[acc]);
         if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -637,9 +671,11 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
     uint32_t acc_phase = 0;
     uint32_t xph = 0;  // bit b: phase of this warp's staging barrier b
     for (int tile = t_first; tile < t_end; tile += t_step) {
-      const int m_blk = BRES ? tile : tile / n_tiles, n_blk = BRES ? n_fix : tile % n_tiles;
-      // IMG: tile-local rows >= rpt are the MMA's padding rows (never stored): pushed past m_store
-      const int row0 = (IMG && quarter * 32 + lane >= rpt) ? (1 << 30) - lane : m_blk * rpt + quarter * 32;
+      const int m_blk = m_of(tile), n_blk = BRES ? n_fix : tile % n_tiles;
+      // IMG: tile-local rows >= rpt are the MMA's padding rows (never stored): pushed past m_store;
+      // PAIR: a ghost tile (m_blk >= m_tiles) likewise
+      const int row0 = ((IMG && quarter * 32 + lane >= rpt) || (PAIR && m_blk >= m_tiles)) ? (1 << 30) - lane
+                                                                                          : m_blk * rpt + quarter * 32;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + half * WCOLS;
       const int col_base = n_blk * BN + half * WCOLS;
       float s1 = 0.f, s2 = 0.f;  // RESID_LN row statistics (lane = row)
@@ -652,7 +688,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
       } else if constexpr (kStgOut) {
         constexpr int SB = BRES ? 1 : 2;  // BRES: one staging buffer per warp, one more A stage
         store_bf16_tma<CH, EPI, SB>(tmX, smem + S::STG_OFF + (warp - 2) * 2048 * SB, tbase, row0, col_base, bias_s,
-                                    lane, &tfull[acc], acc_phase, &tempty[acc]);
+                                    lane, &tfull[acc], acc_phase, &tempty[acc], PAIR && rank ? 0 : -1);
       } else if constexpr (EPI == EPI_F32_RESID || EPI == EPI_F32_RESID_LN) {
         // Residual epilogue, software-pipelined over the 32-column chunks: the residual
         // row segment of chunk c+1 is loaded while chunk c is added and stored, and chunk
@@ -795,9 +831,13 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
     if (warp >= 2 && lane == 0) bulk_wait0();  // staged TMA stores fully written before exit
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // the peer may still arrive on / multicast into this CTA
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc<S::TMEM_COLS>(tmem_base);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_dealloc_2sm<S::TMEM_COLS>(tmem_base);
+    else tmem_dealloc<S::TMEM_COLS>(tmem_base);
+  }
 }
 
 }  // namespace cfd

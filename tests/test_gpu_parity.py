@@ -302,6 +302,31 @@ def test_mlp_cta_pair_variant_matches_single_cta_bitwise(opj, keep):
     enc.close()
 
 
+def test_qkv_cta_pair_matches_single_cta_bitwise():
+    """The CTA-pair QKV projection (cfdx_set_option(23, 1), default: cta_group::2 M = 256 MMAs,
+    half of each weight column block resident per SM) computes the same products in the same k
+    order as the single-CTA weight-stationary GEMM: every layer output and score agrees bit for
+    bit, with an odd row-tile count (ghost tile) in the refine pass."""
+    cfg = ci.CONFIGS["c640"]
+    enc = CFDetrEncoder(cfg, ci.make_weights(cfg, seed=0), max_tasks=8)
+    imgs = bf16_tensor(ci.make_frames(cfg, 3, task0=12), "cuda")
+    ks = [0, 100, 37]
+    co = enc.coarse_encode(imgs)
+    sel = enc.select_regions(co["scores"], k=ks)
+    x0 = co["x0"].clone()
+    outs = []
+    for pair in (0, 1):
+        enc.set_option(23, pair)
+        c2 = enc.coarse_encode(imgs, want_layers=True)
+        ro = enc.batch_refine(imgs, x0, sel["sel_idx"], sel["sel_count"], want_layers=True)
+        torch.cuda.synchronize()
+        n = int(ro["cu_seqlens"][-1])
+        outs.append((c2["layer_out"].clone(), c2["scores"].clone(), ro["layer_out"][:, :n].clone()))
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
+    enc.close()
+
+
 def test_fused_oproj_matches_separate_oproj_bitwise():
     """O-projection + residual + LN2 inside the fused MLP kernel (cfdx_set_option(11, 1),
     default) against the separate O-projection GEMM launch: the same products in the same
