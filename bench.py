@@ -460,10 +460,18 @@ def gpu_arm(args):
     from paper_2505_23317_b200.api import bf16_tensor
 
     rank, world, local = dist_env()
+    # CFD_DIST_BACKEND=gloo (with ranks sharing GPUs: local rank mod device count) exercises the
+    # multi-rank path on a one-GPU box -- timing is then not a scaling measurement
+    backend = os.environ.get("CFD_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    cdev = dev if backend == "nccl" else torch.device("cpu")  # collective tensors
     work = Work(args, rank, world)
     cfg = work.cfg
     work.weights = ci.make_weights(cfg, seed=0)
@@ -535,7 +543,7 @@ def gpu_arm(args):
     step_ms = [starts[i].elapsed_time(ends[i]) for i in range(args.steps)]
     total_ms = sum(step_ms)
     clk = clocks.stop()
-    total_ms_max = shard.max_over_ranks(total_ms, dev)
+    total_ms_max = shard.max_over_ranks(total_ms, cdev)
     value = work.frames_total * args.steps / (total_ms_max / 1e3)
 
     # ---------------------------------------------------------------- per-kernel probes
@@ -615,19 +623,19 @@ def gpu_arm(args):
                      "peak_src": f"MUFU ex2 16/clk/SM x {n_sm} SMs x {sm_mhz:.0f} MHz"}
 
     # ---------------------------------------------------------------- e2e through the public API
-    e2e = None if args.no_e2e else e2e_measure(args, work, lanes, imgs, imgs_np, dev, main, world, u8=True)
+    e2e = None if args.no_e2e else e2e_measure(args, work, lanes, imgs, imgs_np, dev, main, world, u8=True, cdev=cdev)
     if e2e:
         e2e["input"] = "8-bit HWC camera frames, converted on the device (cfd_frames_from_u8, inside the graph)"
         e2e["note"] = ("pinned host frames -> device and packed refined tokens -> host every step, per lane "
                        "double-buffered, uploads and downloads on their own streams overlapped with compute")
     e2e_bf16 = None
     if e2e and work.name == "c640":
-        e2e_bf16 = e2e_measure(args, work, lanes, imgs, imgs_np, dev, main, world, u8=False)
+        e2e_bf16 = e2e_measure(args, work, lanes, imgs, imgs_np, dev, main, world, u8=False, cdev=cdev)
         e2e_bf16["input"] = "bf16 HWC frames (the device-resident value's input), PCIe-bound"
         e2e_bf16["outputs_equal_device_step"] = e2e_bf16.pop("_same", None)
 
     # ---------------------------------------------------------------- outputs gathered over NCCL, checked
-    check = None if args.no_check else gather_and_check(args, work, full, rank, world, dev)
+    check = None if args.no_check else gather_and_check(args, work, full, rank, world, cdev)
     cpu = cpu1 = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         cpu = time_oracle(work, args.cpu_seconds, 64)
@@ -647,7 +655,7 @@ def gpu_arm(args):
                                             "times sum to ~lanes x step time", "probe_sum_in_step_ms":
                                             round(step_sum, 4), "lanes_x_step_ms": round(S * total_ms / args.steps, 4)},
                "step_ms_min": round(min(step_ms), 4), "step_ms_max": round(max(step_ms), 4), "check": check,
-               "dist": {"backend": "nccl" if world > 1 else None, "world_size": world,
+               "dist": {"backend": backend if world > 1 else None, "world_size": world,
                         "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if world > 1 else None,
                         "collectives": "max-over-ranks time, all_gather of sampled task outputs (outside timing)"},
                "impl": "ours", "library": L.load().cfd_version().decode()}
@@ -659,7 +667,7 @@ def gpu_arm(args):
         ln.enc.close()
 
 
-def e2e_measure(args, work, lanes, imgs, imgs_np, dev, main, world, u8):
+def e2e_measure(args, work, lanes, imgs, imgs_np, dev, main, world, u8, cdev=None):
     """Serving loop through the public API: every step uploads its frames from pinned host
     memory (8-bit camera frames converted on the device by cfd_frames_from_u8, or the bf16
     frames) and downloads the packed refined tokens + cu_seqlens to pinned host memory.  Each
@@ -762,7 +770,7 @@ def e2e_measure(args, work, lanes, imgs, imgs_np, dev, main, world, u8):
     run(n_steps_t)
     e_e.record(main)
     torch.cuda.synchronize()
-    e2e_ms = shard.max_over_ranks(e_s.elapsed_time(e_e), dev)
+    e2e_ms = shard.max_over_ranks(e_s.elapsed_time(e_e), cdev if cdev is not None else dev)
     out = {"value": work.frames_total * n_steps_t / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": int(h_all.numel() * h_all.element_size()),
            "d2h_bytes_per_step": int(sum(ln["sets"][0]["h_y"].numel() * 4 + ln["sets"][0]["h_cu"].numel() * 4
@@ -800,8 +808,8 @@ def gather_and_check(args, work, full, rank, world, dev):
     cu = full.ro["cu_seqlens"].cpu().numpy()
     for j, i in enumerate(sample[:n_s]):
         n = int(cu[i + 1] - cu[i])
-        y[j, :n] = full.ro["y"][cu[i]:cu[i + 1]]
-        sc[j] = full.co["scores"][i]
+        y[j, :n] = full.ro["y"][cu[i]:cu[i + 1]].to(dev)
+        sc[j] = full.co["scores"][i].to(dev)
         meta[j] = torch.tensor([work.ids[i], work.ks[i], n])
     ys, scs, metas = shard.gather_outputs(y), shard.gather_outputs(sc), shard.gather_outputs(meta)
     if rank != 0:
@@ -833,7 +841,8 @@ def gather_and_check(args, work, full, rank, world, dev):
             "tasks": checked, "max_rel_l2": worst_rel, "max_abs": worst_abs,
             "own_score_selection_flips": flips,
             "pass": worst_rel <= 2e-2 and worst_abs <= 5e-2,
-            "gathered_via": f"{torch.distributed.get_backend()} all_gather" if world > 1 else "local"}
+            "gathered_via": f"{torch.distributed.get_backend()} all_gather" if world > 1 else "local",
+            "tasks_per_rank_gathered": n_s}
 
 
 def main():
