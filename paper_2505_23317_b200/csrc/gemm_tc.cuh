@@ -273,8 +273,10 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
   if constexpr (LN) {
     // ---- pass A: x_new = x_old + acc + bias -> x (TMA store) and back into the accumulator's
     //      TMEM columns; row statistics.  (The first residual chunks were requested before the
-    //      accumulator was ready.)
-    float s1 = 0.f, s2 = 0.f;
+    //      accumulator was ready.)  The row statistics are shifted sums around the row's first
+    //      value K of this half (s1 = sum (v - K), s2 = sum (v - K)^2), so the variance does not
+    //      cancel catastrophically when |mean| >> std; the halves combine with Chan's formula.
+    float s1 = 0.f, s2 = 0.f, shift = 0.f;
 #pragma unroll 1
     for (int c = 0; c < CH; ++c) {
       const int b = c % NB;
@@ -307,8 +309,10 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
           if (!live) v0 = v1 = v2 = v3 = 0.f;
           if (STOREX) *px = make_float4(v0, v1, v2, v3);
         }
-        s1 += (v0 + v1) + (v2 + v3);
-        s2 += (v0 * v0 + v1 * v1) + (v2 * v2 + v3 * v3);
+        if (q == 0 && c == 0) shift = v0;
+        const float d0 = v0 - shift, d1 = v1 - shift, d2 = v2 - shift, d3 = v3 - shift;
+        s1 += (d0 + d1) + (d2 + d3);
+        s2 += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
         a[4 * q] = __float_as_uint(v0);
         a[4 * q + 1] = __float_as_uint(v1);
         a[4 * q + 2] = __float_as_uint(v2);
@@ -335,15 +339,24 @@ __device__ __forceinline__ void resid_ln_tma(const ResidLnArgs& la, const CUtens
       }
     }
     tmem_wait_st();
-    // ---- statistics of the full row (two warps, one per column half)
+    // ---- statistics of the full row (two warps, one per column half of n_h = n / 2 values):
+    //      per half mean_h = K + s1 / n_h and M2_h = s2 - s1^2 / n_h, then
+    //      mean = (mean_0 + mean_1) / 2, M2 = M2_0 + M2_1 + (mean_0 - mean_1)^2 n_h / 2
     const int r_in_tile = quarter * 32 + lane;
-    stats[half * 128 + r_in_tile] = make_float2(s1, s2);
+    const float n_h = 0.5f * (float)la.n_total;
+    const float mean_h = shift + s1 / n_h;
+    const float m2_h = fmaxf(s2 - s1 * (s1 / n_h), 0.f);
+    stats[half * 128 + r_in_tile] = make_float2(mean_h, m2_h);
     asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
     const float2 o = stats[(half ^ 1) * 128 + r_in_tile];
     asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
-    const float inv_n = 1.f / (float)la.n_total;
-    mean = (s1 + o.x) * inv_n;
-    rstd = rsqrtf(fmaxf((s2 + o.y) * inv_n - mean * mean, 0.f) + la.ln_eps);
+    // both halves combine in the same (half 0, half 1) order, so both warps get identical bits
+    const float2 h0 = half == 0 ? make_float2(mean_h, m2_h) : o;
+    const float2 h1 = half == 0 ? o : make_float2(mean_h, m2_h);
+    const float dm = h0.x - h1.x;
+    mean = 0.5f * (h0.x + h1.x);
+    const float m2 = (h0.y + h1.y) + dm * dm * (0.5f * n_h);
+    rstd = rsqrtf(m2 / (float)la.n_total + la.ln_eps);
     // ---- pass B: LN(x_new) from TMEM -> bf16 (SW64 buffer) -> TMA store
 #pragma unroll 1
     for (int c = 0; c < CH; ++c) {
