@@ -53,7 +53,8 @@ struct Attn7Smem {
   static constexpr int BAR_OFF = NWG * WG_BYTES;
   static constexpr int NBAR_WG = 4 + 2 * ATTN7_ST + 4;             // q_full q_empty [2] | kv [ST] | s p o
   static constexpr int SLOT_OFF = BAR_OFF + NWG * NBAR_WG * 8 + 16;  // + TMEM slot
-  static constexpr int TAB_OFF = SLOT_OFF + NWG * 2 * 4 + 16;
+  static constexpr int SLOT_INTS = 8;  // per published item: item, task, tile, head, seq0, N, n_keys, -
+  static constexpr int TAB_OFF = SLOT_OFF + NWG * 2 * SLOT_INTS * 4 + 16;
   static constexpr int TOTAL = 1024 + TAB_OFF + 3 * (ATTN7_MAX_T + 1) * 4;
   __host__ __device__ static constexpr int q_off(int w, int slot) { return w * WG_BYTES + slot * Q_BYTES; }
   __host__ __device__ static constexpr int k_off(int w, int st) { return w * WG_BYTES + 2 * Q_BYTES + st * SUB_BYTES; }
@@ -110,7 +111,8 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::BAR_OFF + NWG * S::NBAR_WG * 8);
-  volatile int* item_slot = reinterpret_cast<volatile int*>(smem + S::SLOT_OFF);  // [w][2]
+  // [w][slot][SLOT_INTS]: the producer decodes each item once and publishes it with the Q tile
+  volatile int* item_slot = reinterpret_cast<volatile int*>(smem + S::SLOT_OFF);
   int* order = reinterpret_cast<int*>(smem + S::TAB_OFF);
   int* pre_full = order + (ATTN7_MAX_T + 1);
   int* pre_tail = pre_full + (ATTN7_MAX_T + 1);
@@ -199,13 +201,10 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
       for (int it = 0;; ++it) {
         const int slot = it & 1;
         mbar_poll<SLEEP_NS>(&b[slot], (it >> 1) & 1);  // q_full
-        const int item = item_slot[w * 2 + slot];
-        if (item >= total) break;
-        int t, tile, h;
-        decode_item7(order, pre_full, pre_tail, T, nh, n_full, item, t, tile, h, p.cu_seqlens);
-        const int N = __ldg(p.cu_seqlens + t + 1) - __ldg(p.cu_seqlens + t);
-        const int ns = (N + 63) / 64;
-        const int n_keys = p.kv_len ? __ldg(p.kv_len + t) : N;  // PV covers the unmasked keys only
+        const volatile int* is = item_slot + (w * 2 + slot) * S::SLOT_INTS;
+        if (is[0] >= total) break;
+        const int ns = (is[5] + 63) / 64;
+        const int n_keys = is[6];  // PV covers the unmasked keys only
         const uint32_t qa = smem_u32(smem + S::q_off(w, slot));
         for (int u = 0; u < ns; ++u) {
           const int st = g % ATTN7_ST;
@@ -265,7 +264,8 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
         if (it >= 2) mbar_poll<SLEEP_NS>(&b[2 + slot], ((it >> 1) - 1) & 1);  // q_empty
         const int item = (it == 0 || !p.work_counter) ? (int)blockIdx.x + (it * NWG + w) * (int)gridDim.x
                                                        : NWG * (int)gridDim.x + atomicAdd(p.work_counter, 1);
-        item_slot[w * 2 + slot] = item;
+        volatile int* is = item_slot + (w * 2 + slot) * S::SLOT_INTS;
+        is[0] = item;
         if (item >= total) {
           mbar_arrive(&b[slot]);  // sentinel: q_full without bytes
           break;
@@ -273,7 +273,14 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
         int t, tile, h;
         decode_item7(order, pre_full, pre_tail, T, nh, n_full, item, t, tile, h, p.cu_seqlens);
         const int seq0 = __ldg(p.cu_seqlens + t);
-        const int ns = (__ldg(p.cu_seqlens + t + 1) - seq0 + 63) / 64;
+        const int N = __ldg(p.cu_seqlens + t + 1) - seq0;
+        const int ns = (N + 63) / 64;
+        is[1] = t;
+        is[2] = tile;
+        is[3] = h;
+        is[4] = seq0;
+        is[5] = N;
+        is[6] = p.kv_len ? __ldg(p.kv_len + t) : N;
         mbar_expect_tx(&b[slot], S::Q_BYTES);
         tma_load_2d(smem + S::q_off(w, slot), &tmQKV, &b[slot], h * DH, seq0 + tile * 128);
         tma_load_2d(smem + S::q_off(w, slot) + S::SUB_BYTES, &tmQKV, &b[slot], h * DH, seq0 + tile * 128 + 64);
@@ -318,25 +325,32 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
     (void)tr;
     for (int it = 0;; ++it) {
       mbar_wait(&q_full[it & 1], (it >> 1) & 1);
-      const int item = item_slot[wg * 2 + (it & 1)];
-      if (item >= total) break;
-      int t, tile, h;
-      decode_item7(order, pre_full, pre_tail, T, nh, n_full, item, t, tile, h, p.cu_seqlens);
-      const int seq0 = __ldg(p.cu_seqlens + t);
-      const int N = __ldg(p.cu_seqlens + t + 1) - seq0;
+      const volatile int* is = item_slot + (wg * 2 + (it & 1)) * S::SLOT_INTS;
+      if (is[0] >= total) break;
+      const int tile = is[2], h = is[3], seq0 = is[4], N = is[5];
       const int nsub = (N + 63) / 64;
       const int q_valid = N - tile * 128;
       const bool active = quarter * 32 < q_valid;
-      const int n_keys = p.kv_len ? __ldg(p.kv_len + t) : N;  // keys >= n_keys are masked (padded batch)
+      const int n_keys = is[6];  // keys >= n_keys are masked (padded batch)
       float m_run = -INFINITY, l_run = 0.f;
       for (int u = 0; u < nsub; ++u) {
         mbar_wait(s_full, s_cnt & 1);
         ++s_cnt;
         tc_fence_after();
         if (tr) ATTN_TR(wg, it, u, 0);
+        // P(u-1) is published here rather than at the end of sub-tile u-1: the wait for its
+        // TMEM stores overlaps the S(u) load (PV(u-1) is not needed before P(u) is stored)
+        const auto publish_prev_p = [&]() {
+          if (u > 0) {
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(p_full);
+          }
+        };
         if (active && u * 64 >= n_keys) {
           // a sub-tile of pad keys only (padded batch): no exponentials, and the MMA warp
           // issues no PV for it (its k-steps cover the unmasked keys only)
+          publish_prev_p();
           tc_fence_before();
           mbar_arrive(s_free);
           if (u > 0) {
@@ -348,6 +362,7 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
           uint32_t sr[64];
           tmem_ld32(s_base, *reinterpret_cast<uint32_t(*)[32]>(sr));
           if (valid > 32) tmem_ld32(s_base + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+          publish_prev_p();
           tmem_wait_ld();
           if (tr) ATTN_TR(wg, it, u, 1);
           tc_fence_before();
@@ -405,19 +420,20 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
           if (tr) ATTN_TR(wg, it, u, 4);
           tmem_st16(p_addr, *reinterpret_cast<const uint32_t(*)[16]>(sr));
           if (valid > 32) tmem_st16(p_addr + 16, *reinterpret_cast<const uint32_t(*)[16]>(sr + 32));
-          tmem_wait_st();
         } else {
           // padding-only warp of a tail tile: keeps the barrier phases in step
+          publish_prev_p();
           mbar_arrive(s_free);
           if (u > 0) {
             mbar_wait(o_full, o_cnt & 1);
             ++o_cnt;
           }
         }
-        tc_fence_before();
-        mbar_arrive(p_full);
         if (tr) ATTN_TR(wg, it, u, 5);
       }
+      tmem_wait_st();  // the item's last P
+      tc_fence_before();
+      mbar_arrive(p_full);
       mbar_wait(o_full, o_cnt & 1);
       ++o_cnt;
       tc_fence_after();

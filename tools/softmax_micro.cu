@@ -6,12 +6,32 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2505_23317_b200/csrc tools/softmax_micro.cu -o tools/softmax_micro
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include "attn_common.cuh"
 
 using namespace cfd;
 
-template <int NPP, bool SKIPMAX = false>
+// exp_chunk with the bf16 pack by truncation (PRMT of the two high halves) instead of F2FP:
+// tests whether the F2FP conversions compete with MUFU for the XU pipe
+template <int NPP>
+__device__ __forceinline__ void exp_chunk_trunc(uint32_t* sr, float c, float neg, float& sum0, float& sum1) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    float x0, x1, p0, p1;
+    fma2(x0, x1, __uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1]), c, c, neg, neg);
+    if (i >= 16 - NPP) {
+      exp2_poly2(p0, p1, x0, x1);
+    } else {
+      p0 = ex2_approx(x0);
+      p1 = ex2_approx(x1);
+    }
+    add2(sum0, sum1, sum0, sum1, p0, p1);
+    sr[i] = __byte_perm(__float_as_uint(p0), __float_as_uint(p1), 0x7632);
+  }
+}
+
+template <int NPP, bool SKIPMAX = false, bool TRUNC = false>
 __global__ void __launch_bounds__(512, 1) softmax_body(int iters, int nwarps, unsigned long long* cyc, float* sink) {
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -56,8 +76,13 @@ __global__ void __launch_bounds__(512, 1) softmax_body(int iters, int nwarps, un
       if (upd) m_run = m_cand;
       const float neg = -m_run;
       float sum0 = 0.f, sum1 = 0.f, sum2 = 0.f, sum3 = 0.f;
-      exp_chunk<NPP>(sr, c, neg, sum0, sum1);
-      exp_chunk<NPP>(sr + 32, c, neg, sum2, sum3);
+      if (TRUNC) {
+        exp_chunk_trunc<NPP>(sr, c, neg, sum0, sum1);
+        exp_chunk_trunc<NPP>(sr + 32, c, neg, sum2, sum3);
+      } else {
+        exp_chunk<NPP>(sr, c, neg, sum0, sum1);
+        exp_chunk<NPP>(sr + 32, c, neg, sum2, sum3);
+      }
       l_run = l_run * alpha + ((sum0 + sum1) + (sum2 + sum3));
       if (SKIPMAX && __any_sync(0xffffffffu, (sum0 + sum1) + (sum2 + sum3) > 256.f)) m_run += 1e-3f;  // the check
       tmem_st16(tm + 64, *reinterpret_cast<const uint32_t(*)[16]>(sr));
@@ -74,10 +99,10 @@ __global__ void __launch_bounds__(512, 1) softmax_body(int iters, int nwarps, un
   if (warp == 0) tmem_dealloc<512>(slot);
 }
 
-template <int NPP, bool SKIPMAX = false>
+template <int NPP, bool SKIPMAX = false, bool TRUNC = false>
 void run(int nw, unsigned long long* cyc, float* sink) {
   const int grid = 148, iters = 2000;
-  softmax_body<NPP, SKIPMAX><<<grid, 512>>>(iters, nw, cyc, sink);
+  softmax_body<NPP, SKIPMAX, TRUNC><<<grid, 512>>>(iters, nw, cyc, sink);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return; }
   unsigned long long h[148];
@@ -86,22 +111,28 @@ void run(int nw, unsigned long long* cyc, float* sink) {
   for (int i = 0; i < grid; ++i) cy += h[i];
   cy /= grid;
   const double elems = (double)nw * 32 * 64 * iters;
-  printf("softmax body%s NPP=%d warps=%2d (%d per SMSP): %.1f cycles per warp-subtile, %.2f score elements/clk/SM\n",
-         SKIPMAX ? " (no max pass)" : "", NPP, nw, nw / 4, cy / iters, elems / cy);
+  printf("softmax body%s%s NPP=%d warps=%2d (%d per SMSP): %.1f cycles per warp-subtile, %.2f score elements/clk/SM\n",
+         SKIPMAX ? " (no max pass)" : "", TRUNC ? " (PRMT pack)" : "", NPP, nw, nw / 4, cy / iters, elems / cy);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  // optional argument: run only that warp count (for ncu captures of one configuration)
+  const int only = argc > 1 ? atoi(argv[1]) : 0;
   unsigned long long* cyc;
   float* sink;
   cudaMalloc(&cyc, sizeof(unsigned long long) * 148);
   cudaMalloc(&sink, 4096 * 4);
   for (int nw : {4, 8, 12, 16}) {
+    if (only && nw != only) continue;
     run<0>(nw, cyc, sink);
     run<4>(nw, cyc, sink);
     run<6>(nw, cyc, sink);
     run<8>(nw, cyc, sink);
     run<4, true>(nw, cyc, sink);
     run<6, true>(nw, cyc, sink);
+    run<0, false, true>(nw, cyc, sink);
+    run<2, false, true>(nw, cyc, sink);
+    run<4, false, true>(nw, cyc, sink);
   }
   return 0;
 }
