@@ -99,7 +99,9 @@ int32_t cfdx_probe_count(int32_t kind);
  *   key 19 fused O-projection keeps x1 = x + o W_o + b_o in TMEM and the MLP's MMA2s
  *          accumulate onto it (1, default) / x1 stored and read back (0)
  *   key 20 with key 19 = 1: x loaded into acc2 while o / W_o stream in (1) / 0 (default)
- *   key 21 attention v7: control-warp sleep between barrier probes, ns (0, 32 default, 128)
+ *   key 21 attention v7: MMA-warp wait between barrier probes: 0, 8, 32 (default), 128 ns of
+ *          sleep, 1 = try_wait (hardware suspend), 2 = busy test_wait loop
+ *   key 24 attention v7: producer-warp sleep between barrier probes, ns (0..4096, default 256)
  *   key 22 attention v7: softmax warpgroups per CTA (3, or 4 default)
  *   key 23 QKV projection as CTA pairs (cta_group::2, half of each weight column block resident
  *          per SM, 8 A stages in flight) on (1, default) / off (0: one CTA per column block)

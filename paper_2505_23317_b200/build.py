@@ -48,6 +48,8 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False, trace
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     tmp = out + ".tmp"
     extra = (["-DCFD_TRACE"] if trace_only else ["-DCFD_HANG_CHECK", "-DCFD_TRACE"]) if debug else []
+    # extra defines for trace experiments, e.g. CFD_TRACE_DEFS="-DCFD_TRACE_MMA_PRE" (debug library only)
+    extra += os.environ.get("CFD_TRACE_DEFS", "").split() if debug else []
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-shared", "-o", tmp, *srcs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     log = os.path.join(HERE, "build_dbg.log" if debug else "build.log")

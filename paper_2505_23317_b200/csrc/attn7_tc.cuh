@@ -67,9 +67,24 @@ static_assert(Attn7Smem<4>::TOTAL <= 232448, "attn7 shared memory budget");
 
 // Poll an mbarrier phase: test, and sleep ~ns between probes (the control warps share their
 // SMSP with three softmax warps: a busy spin would take their issue slots).
+// Producer-side poll with a run-time sleep: the producer runs up to ATTN7_ST sub-tiles ahead, so
+// it can react slowly, and each probe it makes takes issue slots from the softmax warps that
+// share its SMSP (at 32 ns its kv_empty probes were ~7 % of all issued instructions).
+__device__ __forceinline__ void mbar_poll_slow(uint64_t* bar, uint32_t parity, int ns) {
+  while (!mbar_test(bar, parity)) __nanosleep(ns);
+}
+
+// NS = 1: try_wait (the hardware may suspend the thread until the phase completes);
+// NS = 2: busy test_wait loop
 template <int NS>
 __device__ __forceinline__ void mbar_poll(uint64_t* bar, uint32_t parity) {
-  while (!mbar_test(bar, parity)) __nanosleep(NS);
+  if constexpr (NS == 1) {
+    mbar_wait(bar, parity);
+  } else if constexpr (NS == 2) {
+    mbar_spin(bar, parity);
+  } else {
+    while (!mbar_test(bar, parity)) __nanosleep(NS);
+  }
 }
 
 // Item tables: order[] = tasks in processing order, pre_full[i] = first full-tile item of
@@ -182,13 +197,17 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
     // Registers: the two control warpgroups give theirs up so the softmax warpgroups can
     // hold a 64-column S row in registers (setmaxnreg; 4 * NWG softmax warps at SOFT_REGS).
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(CTRL_REGS));
-    const int c = warp - 4 * NWG;
-    if (c < NWG && lane == 0) {
+    // warp-uniform for the compiler (a shuffle from lane 0), so the MMA warp's descriptor
+    // arithmetic stays in uniform registers
+    const int c = __shfl_sync(0xffffffffu, warp - 4 * NWG, 0);
+    if (c < NWG) {
       // ---------------------------------------------------------- MMA warp of warpgroup w = c
       // One flat sequence over the warpgroup's sub-tiles g (all its items back to back):
       // QK(g) once K(g) is loaded and the softmax has loaded S(g-1) (s_free), then PV(g-1)
       // once P(g-1) is in TMEM (p_full); an item's first QK overlaps the previous item's last
-      // softmax.
+      // softmax.  The whole warp runs the loop (item fields broadcast from lane 0); one elected
+      // lane issues the MMAs and commits (a single-lane loop compiled every tcgen05.mma into a
+      // register -> uniform-register waterfall costing ~150 cycles per instruction).
       const int w = c;
       uint64_t* b = bars + w * S::NBAR_WG;
       uint64_t* s_full = b + 4 + 2 * ATTN7_ST;
@@ -197,41 +216,60 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
       constexpr uint32_t idesc_o = make_idesc_bf16(128, DH, 1);  // O += P_u V_u (V MN-major)
       int g = 0;
       bool pv_pending = false;
-      int pv_ks = 0, pv_u = 0;
+      int pv_ks = 0, pv_u = 0, pv_it = 0;
+      (void)pv_it;
       for (int it = 0;; ++it) {
         const int slot = it & 1;
         mbar_poll<SLEEP_NS>(&b[slot], (it >> 1) & 1);  // q_full
         const volatile int* is = item_slot + (w * 2 + slot) * S::SLOT_INTS;
-        if (is[0] >= total) break;
-        const int ns = (is[5] + 63) / 64;
-        const int n_keys = is[6];  // PV covers the unmasked keys only
+        if (__shfl_sync(0xffffffffu, is[0], 0) >= total) break;
+        const int ns = __shfl_sync(0xffffffffu, (is[5] + 63) / 64, 0);
+        const int n_keys = __shfl_sync(0xffffffffu, is[6], 0);  // PV covers the unmasked keys only
         const uint32_t qa = smem_u32(smem + S::q_off(w, slot));
         for (int u = 0; u < ns; ++u) {
           const int st = g % ATTN7_ST;
           mbar_poll<SLEEP_NS>(&b[4 + st], (g / ATTN7_ST) & 1);           // kv_full
           if (g > 0) mbar_poll<SLEEP_NS>(s_full + 1, (g - 1) & 1);       // s_free
           tc_fence_after();
+#ifdef CFD_TRACE_MMA_PRE
+          ATTN_TR(w, it, u, 6);  // trace experiment: QK(u) about to be issued
+#endif
           const uint32_t ka = smem_u32(smem + S::k_off(w, st));
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < DH / 16; ++k)
-            mma_ss(tw + S::S_COL, make_smem_desc(qa + k * 32, 16, 512, kLayoutSW64),
-                   make_smem_desc(ka + k * 32, 16, 512, kLayoutSW64), idesc_s, k);
-          mma_commit(s_full);
-          ATTN_TR(w, it, u, 6);
-          if (u + 1 == ns) mma_commit(&b[2 + slot]);  // the item's last QK: its Q slot is free
+            for (int k = 0; k < DH / 16; ++k)
+              mma_ss(tw + S::S_COL, make_smem_desc(qa + k * 32, 16, 512, kLayoutSW64),
+                     make_smem_desc(ka + k * 32, 16, 512, kLayoutSW64), idesc_s, k);
+            mma_commit(s_full);
+#ifndef CFD_TRACE_MMA_PRE
+            ATTN_TR(w, it, u, 6);
+#endif
+            if (u + 1 == ns) mma_commit(&b[2 + slot]);  // the item's last QK: its Q slot is free
+          }
+          __syncwarp();
           if (pv_pending) {
             const int sp = (g - 1) % ATTN7_ST;
             mbar_poll<SLEEP_NS>(s_full + 2, (g - 1) & 1);  // p_full
             tc_fence_after();
+#ifdef CFD_TRACE_MMA_PRE
+            ATTN_TR(w, pv_it, pv_u, 7);  // trace experiment: PV about to be issued
+#endif
             const uint32_t va = smem_u32(smem + S::v_off(w, sp));
-            for (int k = 0; k < pv_ks; ++k)
-              mma_ts(tw + S::O_COL, tw + S::P_COL + k * 8, make_smem_desc(va + k * 16 * DH * 2, 4096, 512, kLayoutSW64),
-                     idesc_o, (pv_u | k) != 0);
-            mma_commit(s_full + 3);              // o_full
-            mma_commit(&b[4 + ATTN7_ST + sp]);  // kv_empty
+            if (elect_one()) {
+              for (int k = 0; k < pv_ks; ++k)
+                mma_ts(tw + S::O_COL, tw + S::P_COL + k * 8,
+                       make_smem_desc(va + k * 16 * DH * 2, 4096, 512, kLayoutSW64), idesc_o, (pv_u | k) != 0);
+              mma_commit(s_full + 3);              // o_full
+              mma_commit(&b[4 + ATTN7_ST + sp]);  // kv_empty
+#ifndef CFD_TRACE_MMA_PRE
+              ATTN_TR(w, pv_it, pv_u, 7);
+#endif
+            }
+            __syncwarp();
           }
           pv_pending = true;
           pv_u = u;
+          pv_it = it;
           pv_ks = (max(0, min(64, n_keys - u * 64)) + 15) / 16;
           ++g;
         }
@@ -241,11 +279,14 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
         mbar_poll<SLEEP_NS>(s_full + 2, (g - 1) & 1);
         tc_fence_after();
         const uint32_t va = smem_u32(smem + S::v_off(w, sp));
-        for (int k = 0; k < pv_ks; ++k)
-          mma_ts(tw + S::O_COL, tw + S::P_COL + k * 8, make_smem_desc(va + k * 16 * DH * 2, 4096, 512, kLayoutSW64),
-                 idesc_o, (pv_u | k) != 0);
-        mma_commit(s_full + 3);
-        mma_commit(&b[4 + ATTN7_ST + sp]);
+        if (elect_one()) {
+          for (int k = 0; k < pv_ks; ++k)
+            mma_ts(tw + S::O_COL, tw + S::P_COL + k * 8, make_smem_desc(va + k * 16 * DH * 2, 4096, 512, kLayoutSW64),
+                   idesc_o, (pv_u | k) != 0);
+          mma_commit(s_full + 3);
+          mma_commit(&b[4 + ATTN7_ST + sp]);
+        }
+        __syncwarp();
       }
     } else if (c < 2 * NWG && lane == 0) {
       // ---------------------------------------------------------- producer of warpgroup w
@@ -261,7 +302,7 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
       }
       for (int it = 0;; ++it) {
         const int slot = it & 1;
-        if (it >= 2) mbar_poll<SLEEP_NS>(&b[2 + slot], ((it >> 1) - 1) & 1);  // q_empty
+        if (it >= 2) mbar_poll_slow(&b[2 + slot], ((it >> 1) - 1) & 1, p.producer_sleep);  // q_empty
         const int item = (it == 0 || !p.work_counter) ? (int)blockIdx.x + (it * NWG + w) * (int)gridDim.x
                                                        : NWG * (int)gridDim.x + atomicAdd(p.work_counter, 1);
         volatile int* is = item_slot + (w * 2 + slot) * S::SLOT_INTS;
@@ -286,7 +327,7 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
         tma_load_2d(smem + S::q_off(w, slot) + S::SUB_BYTES, &tmQKV, &b[slot], h * DH, seq0 + tile * 128 + 64);
         for (int u = 0; u < ns; ++u, ++g) {
           const int st = g % ATTN7_ST;
-          if (g >= ATTN7_ST) mbar_poll<SLEEP_NS>(&b[4 + ATTN7_ST + st], ((g / ATTN7_ST) - 1) & 1);  // kv_empty
+          if (g >= ATTN7_ST) mbar_poll_slow(&b[4 + ATTN7_ST + st], ((g / ATTN7_ST) - 1) & 1, p.producer_sleep);  // kv_empty
           mbar_expect_tx(&b[4 + st], 2 * S::SUB_BYTES);
           tma_load_2d(smem + S::k_off(w, st), &tmQKV, &b[4 + st], d + h * DH, seq0 + u * 64);
           tma_load_2d(smem + S::v_off(w, st), &tmQKV, &b[4 + st], 2 * d + h * DH, seq0 + u * 64);
@@ -360,40 +401,79 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
         } else if (active) {
           const int valid = min(64, n_keys - u * 64);
           uint32_t sr[64];
-          tmem_ld32(s_base, *reinterpret_cast<uint32_t(*)[32]>(sr));
-          if (valid > 32) tmem_ld32(s_base + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
-          publish_prev_p();
-          tmem_wait_ld();
-          if (tr) ATTN_TR(wg, it, u, 1);
-          tc_fence_before();
-          mbar_arrive(s_free);  // S may now be overwritten by QK(u+1)
-          if (valid < 64) {
-#pragma unroll
-            for (int i = 0; i < 64; ++i)
-              if (i >= valid) sr[i] = __float_as_uint(-INFINITY);
-          }
-          float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
-#pragma unroll
-          for (int i = 0; i < 64; i += 8) {
-            m0 = fmax3(m0, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
-            m1 = fmax3(m1, __uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3]));
-            m2 = fmax3(m2, __uint_as_float(sr[i + 4]), __uint_as_float(sr[i + 5]));
-            m3 = fmax3(m3, __uint_as_float(sr[i + 6]), __uint_as_float(sr[i + 7]));
-          }
-          const float m_cand = fmax3(m0, m1, fmaxf(m2, m3)) * c;
-          if (tr) ATTN_TR(wg, it, u, 2);
-          // lazy rescale (reading R23): move the reference max only when it grows by > 2^8
-          const bool upd = (m_run == -INFINITY) || (m_cand > m_run + 8.0f);
-          const float alpha = upd ? ((m_run == -INFINITY) ? 0.f : ex2_approx(m_run - m_cand)) : 1.f;
-          if (upd) m_run = m_cand;
-          const float neg = -m_run;
           float sum0 = 0.f, sum1 = 0.f, sum2 = 0.f, sum3 = 0.f;
-          if (valid == 64) {
-            exp_chunk<NPP>(sr, c, neg, sum0, sum1);
-            exp_chunk<NPP>(sr + 32, c, neg, sum2, sum3);
-          } else {
-            exp_chunk<0>(sr, c, neg, sum0, sum1);
-            if (valid > 32) exp_chunk<0>(sr + 32, c, neg, sum2, sum3);
+          float alpha = 1.f;
+          bool upd = false, done = false, published = false;
+          if (u > 0 && valid == 64) {
+            // Speculative fast path: exponentiate against the current reference max m_run (it
+            // moves only when a row max grows by > 2^8, reading R23), so the exps of the first 32
+            // columns run while the second 32 load and the row max is only checked afterwards.
+            // S stays in TMEM (s_free not yet arrived) for the rare warp that must redo.
+            tmem_ld32(s_base, *reinterpret_cast<uint32_t(*)[32]>(sr));
+            publish_prev_p();
+            published = true;
+            tmem_wait_ld();
+            tmem_ld32(s_base + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+            if (tr) ATTN_TR(wg, it, u, 1);
+            float ma = -INFINITY, mb = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              ma = fmax3(ma, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
+              mb = fmax3(mb, __uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3]));
+            }
+            exp_chunk<NPP>(sr, c, -m_run, sum0, sum1);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 32; i < 64; i += 4) {
+              ma = fmax3(ma, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
+              mb = fmax3(mb, __uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3]));
+            }
+            const float m_cand = fmaxf(ma, mb) * c;  // the same row max as the general path
+            if (tr) ATTN_TR(wg, it, u, 2);
+            if (!__any_sync(0xffffffffu, m_cand > m_run + 8.0f)) {
+              exp_chunk<NPP>(sr + 32, c, -m_run, sum2, sum3);
+              tc_fence_before();
+              mbar_arrive(s_free);  // S may now be overwritten by QK(u+1)
+              done = true;
+            } else {
+              sum0 = sum1 = 0.f;
+            }
+          }
+          if (!done) {
+            tmem_ld32(s_base, *reinterpret_cast<uint32_t(*)[32]>(sr));
+            if (valid > 32) tmem_ld32(s_base + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+            if (!published) publish_prev_p();
+            tmem_wait_ld();
+            if (tr) ATTN_TR(wg, it, u, 1);
+            tc_fence_before();
+            mbar_arrive(s_free);  // S may now be overwritten by QK(u+1)
+            if (valid < 64) {
+#pragma unroll
+              for (int i = 0; i < 64; ++i)
+                if (i >= valid) sr[i] = __float_as_uint(-INFINITY);
+            }
+            float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 64; i += 8) {
+              m0 = fmax3(m0, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
+              m1 = fmax3(m1, __uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3]));
+              m2 = fmax3(m2, __uint_as_float(sr[i + 4]), __uint_as_float(sr[i + 5]));
+              m3 = fmax3(m3, __uint_as_float(sr[i + 6]), __uint_as_float(sr[i + 7]));
+            }
+            const float m_cand = fmax3(m0, m1, fmaxf(m2, m3)) * c;
+            if (tr) ATTN_TR(wg, it, u, 2);
+            // lazy rescale (reading R23): move the reference max only when it grows by > 2^8
+            upd = (m_run == -INFINITY) || (m_cand > m_run + 8.0f);
+            alpha = upd ? ((m_run == -INFINITY) ? 0.f : ex2_approx(m_run - m_cand)) : 1.f;
+            if (upd) m_run = m_cand;
+            const float neg = -m_run;
+            if (valid == 64) {
+              exp_chunk<NPP>(sr, c, neg, sum0, sum1);
+              exp_chunk<NPP>(sr + 32, c, neg, sum2, sum3);
+            } else {
+              exp_chunk<0>(sr, c, neg, sum0, sum1);
+              if (valid > 32) exp_chunk<0>(sr + 32, c, neg, sum2, sum3);
+            }
           }
           l_run = l_run * alpha + ((sum0 + sum1) + (sum2 + sum3));
           if (tr) ATTN_TR(wg, it, u, 3);

@@ -40,6 +40,7 @@ struct AttnParams {
   int n_q = 0;             // v1 CROSS: queries per task (one 128-row tile shared by every task)
   const int* kv_len = nullptr;  // v7: [T] valid keys per task (pad-to-max batch: keys >= kv_len[t]
                                 // of the task's cu_seqlens span are masked); nullptr = all
+  int producer_sleep = 256;     // v7: the producer warp's sleep between barrier probes, ns
 };
 
 constexpr int ATTN_THREADS = 192;

@@ -127,6 +127,7 @@ struct Opts {
   int keep_x1 = 1;        // fused O-projection: x1 stays in TMEM, MMA2 accumulates onto it (19)
   int preload_x = 0;      // with 19: x loaded into acc2 before MMA_o (20; measured slower)
   int attn_sleep = 32;    // v7: MMA / producer warp sleep when idle, ns (21: 0, 32, 128)
+  int attn_psleep = 256;  // v7: the producer warp's sleep between barrier probes, ns (24: 0..4096)
   int attn_nwg = 4;       // v7: softmax warpgroups per CTA (22: 3 or 4)
   int qkv_pair = 1;       // QKV projection as CTA pairs, half of the weights resident per SM (23)
 };
@@ -460,6 +461,9 @@ cudaError_t launch_attention(const Opts& o, const CUtensorMap& tq, const CUtenso
       default:
         e = o.attn_nwg == 3       ? launch_attn7_t<2, 32, 3>(o, tq64, p, items_ub, nh, T, s)
             : o.attn_sleep == 0   ? launch_attn7_t<2, 0>(o, tq64, p, items_ub, nh, T, s)
+            : o.attn_sleep == 1   ? launch_attn7_t<2, 1>(o, tq64, p, items_ub, nh, T, s)
+            : o.attn_sleep == 2   ? launch_attn7_t<2, 2>(o, tq64, p, items_ub, nh, T, s)
+            : o.attn_sleep == 8   ? launch_attn7_t<2, 8>(o, tq64, p, items_ub, nh, T, s)
             : o.attn_sleep == 128 ? launch_attn7_t<2, 128>(o, tq64, p, items_ub, nh, T, s)
                                   : launch_attn7_t<2, 32>(o, tq64, p, items_ub, nh, T, s);
         break;
@@ -639,6 +643,7 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   ap.cu_seqlens = cu; ap.d_model = d; ap.out = w.obuf; ap.lse = want_lse ? w.lse : nullptr; ap.lse_ld = w.lse_ld;
   ap.scale_log2 = 1.4426950408889634f / std::sqrt((float)c->dh);
   ap.stagger = o.attn_stagger;
+  ap.producer_sleep = o.attn_psleep;
   ap.uniform_n = o.attn_qmajor ? uniform_n : 0;
   if (o.attn_dyn) ap.work_counter = w.attn_work;  // dynamic item claiming (per-workspace counter)
   ap.kv_len = kv_len;
@@ -826,7 +831,7 @@ cfd_status cfdx_set_option(cfd_ctx* ctx, int32_t key, int32_t value) {
     case 19: o.keep_x1 = b; return CFD_OK;
     case 20: o.preload_x = b; return CFD_OK;
     case 21:
-      if (value != 0 && value != 32 && value != 128) return CFD_E_ARG;
+      if (value != 0 && value != 1 && value != 2 && value != 8 && value != 32 && value != 128) return CFD_E_ARG;
       o.attn_sleep = value;
       return CFD_OK;
     case 22:
@@ -834,6 +839,10 @@ cfd_status cfdx_set_option(cfd_ctx* ctx, int32_t key, int32_t value) {
       o.attn_nwg = value;
       return CFD_OK;
     case 23: o.qkv_pair = b; return CFD_OK;
+    case 24:
+      if (value < 0 || value > 4096) return CFD_E_ARG;
+      o.attn_psleep = value;
+      return CFD_OK;
   }
   return CFD_E_ARG;
 }
@@ -1395,6 +1404,7 @@ cfd_status cfdx_attention(int32_t T, const int32_t* cu, int32_t max_seqlen, int3
   ap.cu_seqlens = cu; ap.d_model = d; ap.out = (__nv_bfloat16*)out; ap.lse = lse; ap.lse_ld = lse_ld;
   ap.scale_log2 = 1.4426950408889634f / std::sqrt(32.0f);
   ap.stagger = g_dbg_opts.attn_stagger;
+  ap.producer_sleep = g_dbg_opts.attn_psleep;
   // work_counter: caller-owned zeroed int[2] (dynamic claims, reset by the launch's last CTA)
   // or NULL (static round-robin); no state is shared between calls
   if (g_dbg_opts.attn_dyn) ap.work_counter = work_counter;

@@ -1,4 +1,5 @@
-"""Time the attention kernel alone at bench shapes (for ncu captures and variant sweeps).
+"""Time the attention kernel alone at bench shapes (for ncu captures and variant sweeps): reps
+back-to-back launches replayed from one CUDA graph, CUDA events around the replay.
 python tools/attn_bench.py --opt 0=4 --opt 1=4 --lens 700x32 --reps 20   (--opt K=V: cfdx_set_option)"""
 import argparse
 import os
@@ -30,16 +31,22 @@ cap = cu_l[-1] + 256
 qkv = torch.randn(cap, 3 * d, device="cuda").to(torch.bfloat16)
 cu = torch.tensor(cu_l, dtype=torch.int32, device="cuda")
 out = torch.zeros(cap, d, device="cuda", dtype=torch.bfloat16)
-s = torch.cuda.current_stream().cuda_stream
 work = torch.zeros(2, dtype=torch.int32, device="cuda")
 run = lambda: lib.cfdx_attention(len(lens), cu.data_ptr(), max(lens), cap, d, nh, qkv.data_ptr(), out.data_ptr(),
-                                 None, 0, work.data_ptr(), s)
+                                 None, 0, work.data_ptr(), torch.cuda.current_stream().cuda_stream)
 for _ in range(3):
     run()
+torch.cuda.synchronize()
+# replay the launches from a CUDA graph: eager ctypes launches are host-bound below ~25 us
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g):
+    for _ in range(a.reps):
+        run()
+g.replay()
+torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-for _ in range(a.reps):
-    run()
+g.replay()
 e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) / a.reps * 1e3

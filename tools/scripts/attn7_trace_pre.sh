@@ -1,0 +1,2 @@
+CFD_TRACE_DEFS="-DCFD_TRACE_MMA_PRE" python -m paper_2505_23317_b200.build --trace --force > /dev/null
+for B in 32; do echo "=== B=$B (MMA events before issue)"; CFD_LIB_DEBUG=1 timeout 120 python tools/attn_trace.py $B; done
