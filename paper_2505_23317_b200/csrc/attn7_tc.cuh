@@ -247,6 +247,11 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
             if (u + 1 == ns) mma_commit(&b[2 + slot]);  // the item's last QK: its Q slot is free
           }
           __syncwarp();
+#ifdef CFD_TRACE_QK_LAT
+          // trace experiment: when QK(u) completes (the warp waits for its own commit)
+          mbar_spin(s_full, g & 1);
+          if (lane == 0) ATTN_TR(w, it, u, 7);
+#endif
           if (pv_pending) {
             const int sp = (g - 1) % ATTN7_ST;
             mbar_poll<SLEEP_NS>(s_full + 2, (g - 1) & 1);  // p_full
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
                        make_smem_desc(va + k * 16 * DH * 2, 4096, 512, kLayoutSW64), idesc_o, (pv_u | k) != 0);
               mma_commit(s_full + 3);              // o_full
               mma_commit(&b[4 + ATTN7_ST + sp]);  // kv_empty
-#ifndef CFD_TRACE_MMA_PRE
+#if !defined(CFD_TRACE_MMA_PRE) && !defined(CFD_TRACE_QK_LAT)
               ATTN_TR(w, pv_it, pv_u, 7);
 #endif
             }

@@ -13,6 +13,8 @@ d = int(sys.argv[4]) if len(sys.argv) > 4 else 256
 nh = d // 32
 lib = L.load()
 assert lib.cfdx_set_option(None, 0, var) == 0 and lib.cfdx_set_option(None, 1, npp) == 0
+for kv in os.environ.get("CFD_OPTS", "").split():  # extra switches, e.g. CFD_OPTS="25=1"
+    assert lib.cfdx_set_option(None, *(int(t) for t in kv.split("="))) == 0, kv
 cu_l = [0]
 for n in lens:
     cu_l.append(cu_l[-1] + n)
