@@ -9,7 +9,10 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcfdetr_dbg.so" if os.environ.get("CFD_LIB_DEBUG") == "1" else "libcfdetr.so")
+# CFD_LIB_DEBUG=1: the debug / trace build; CFD_LIB_VARIANT=name: libcfdetr_<name>.so (A/B timing builds)
+LIB_PATH = os.path.join(HERE, "libcfdetr_dbg.so" if os.environ.get("CFD_LIB_DEBUG") == "1" else
+                        f"libcfdetr_{os.environ['CFD_LIB_VARIANT']}.so" if os.environ.get("CFD_LIB_VARIANT") else
+                        "libcfdetr.so")
 
 P = C.c_void_p
 I32 = C.c_int32

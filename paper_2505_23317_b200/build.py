@@ -64,6 +64,23 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False, trace
     return out
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """A/B timing build: libcfdetr_<name>.so with extra -D defines (release otherwise); load it
+    with CFD_LIB_VARIANT=<name>."""
+    out = os.path.join(HERE, f"libcfdetr_{name}.so")
+    srcs = [os.path.join(CSRC, s) for s in SOURCES]
+    cmd = [nvcc(), *NVCC_FLAGS, *defines, "-shared", "-o", out, *srcs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
+    r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stderr[-8000:])
+        raise RuntimeError(f"nvcc failed for variant {name}")
+    return out
+
+
 if __name__ == "__main__":
+    if "--variant" in sys.argv:  # python build.py --variant NAME -DX=1 ...
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], [a for a in sys.argv[i + 2:] if a.startswith("-D")]))
+        sys.exit(0)
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv,
                 trace_only="--trace" in sys.argv))

@@ -490,12 +490,13 @@ cudaError_t launch_attention(const Opts& o, const CUtensorMap& tq, const CUtenso
   return e;
 }
 
-cudaError_t launch_score(const CUtensorMap& tq, const ScoreParams& p, int B, cudaStream_t s) {
+cudaError_t launch_score(const CUtensorMap& tq, const CUtensorMap& tq32, const ScoreParams& p, int B,
+                         cudaStream_t s) {
   auto kern = score_tc_kernel<32>;
-  constexpr int smem = ScoreSmem<32>::TOTAL;
-  if (cudaError_t e = ensure_smem_attr(kern, smem); e != cudaSuccess) return e;
+  const int smem = ScoreSmem<32>::total(p.n_coarse);
+  if (cudaError_t e = ensure_smem_attr(kern, ScoreSmem<32>::total(4096)); e != cudaSuccess) return e;
   probe_begin(PK_SCORE, s);
-  launch_ex(kern, dim3((p.n_coarse + 127) / 128, B), dim3(SCORE_THREADS), smem, s, tq, p);
+  launch_ex(kern, dim3((p.n_coarse + 127) / 128, B), dim3(SCORE_THREADS), smem, s, tq, tq32, p);
   probe_end(PK_SCORE, s);
   ++g_launches;
   return cudaGetLastError();
@@ -652,7 +653,9 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
     ScoreParams sp{};
     sp.n_coarse = c->Nc; sp.n_heads = g.n_heads; sp.d_model = d; sp.lse = w.lse; sp.lse_ld = w.lse_ld;
     sp.scale_log2 = ap.scale_log2; sp.scores = scores;
-    CFD_CUDA(launch_score(tq, sp, score_B, s));
+    CUtensorMap tq32;
+    if (!make_qkvmap(&tq32, w.qkv, w.rows_cap, d, 32)) return CFD_E_CUDA;
+    CFD_CUDA(launch_score(tq, tq32, sp, score_B, s));
   }
   const bool staged_ok = fuse_ln && o.staged_epi && (d % 64 == 0);
   if (o.fuse_oproj && o.fused_mlp && staged_ok && d == 256 && F % 128 == 0) {
@@ -1423,12 +1426,12 @@ cfd_status cfdx_layernorm(int32_t M, int32_t d, const float* x, const float* g, 
 cfd_status cfdx_score(int32_t B, int32_t Nc, int32_t d, int32_t nh, const uint16_t* qkv, int32_t rows_cap,
                       const float* lse, int32_t lse_ld, float* scores, void* stream) {
   if (B <= 0 || Nc <= 0 || !qkv || !lse || !scores || d / nh != 32) return CFD_E_ARG;
-  CUtensorMap tq;
-  if (!make_qkvmap(&tq, qkv, rows_cap, d)) return CFD_E_CUDA;
+  CUtensorMap tq, tq32;
+  if (!make_qkvmap(&tq, qkv, rows_cap, d) || !make_qkvmap(&tq32, qkv, rows_cap, d, 32)) return CFD_E_CUDA;
   ScoreParams sp{};
   sp.n_coarse = Nc; sp.n_heads = nh; sp.d_model = d; sp.lse = lse; sp.lse_ld = lse_ld;
   sp.scale_log2 = 1.4426950408889634f / std::sqrt(32.0f); sp.scores = scores;
-  CFD_CUDA(launch_score(tq, sp, B, static_cast<cudaStream_t>(stream)));
+  CFD_CUDA(launch_score(tq, tq32, sp, B, static_cast<cudaStream_t>(stream)));
   return CFD_OK;
 }
 
