@@ -35,9 +35,16 @@
 #include "ptx.cuh"
 #include "attn_tc.cuh"
 #include "attn_common.cuh"
+#include "score_tc.cuh"  // named_bar_sync
 
 namespace cfd {
 
+#ifndef CFD_SPLIT_ROWS
+#define CFD_SPLIT_ROWS 32
+#endif
+constexpr int SPLIT_ROWS = CFD_SPLIT_ROWS;  // tail tiles with at most this many real rows are split
+static_assert(SPLIT_ROWS == 32 || SPLIT_ROWS == 64, "split tail: 4 replicas of 32 rows or 2 of 64");
+constexpr int SPLIT_REP = SPLIT_ROWS == 32 ? 4 : 2;  // replicas of a split tail tile over the lane quarters
 constexpr int ATTN7_ST = 4;          // K/V ring stages per warpgroup (64 keys each)
 // NWG softmax warpgroups (3 or 4) + two control warpgroups (an MMA warp and a producer warp
 // per softmax warpgroup, the rest idle)
@@ -55,7 +62,10 @@ struct Attn7Smem {
   static constexpr int SLOT_OFF = BAR_OFF + NWG * NBAR_WG * 8 + 16;  // + TMEM slot
   static constexpr int SLOT_INTS = 8;  // per published item: item, task, tile, head, seq0, N, n_keys, -
   static constexpr int TAB_OFF = SLOT_OFF + NWG * 2 * SLOT_INTS * 4 + 16;
-  static constexpr int TOTAL = 1024 + TAB_OFF + 3 * (ATTN7_MAX_T + 1) * 4;
+  // split tail items: per warpgroup the (m, l) of its 4 x 32 rows and one 32 x 33 fp32 O accumulator
+  static constexpr int MERGE_OFF = TAB_OFF + 3 * (ATTN7_MAX_T + 1) * 4;
+  static constexpr int MERGE_WG_FLOATS = 4 * 32 * 2 + 32 * 33;
+  static constexpr int TOTAL = 1024 + MERGE_OFF + NWG * MERGE_WG_FLOATS * 4;
   __host__ __device__ static constexpr int q_off(int w, int slot) { return w * WG_BYTES + slot * Q_BYTES; }
   __host__ __device__ static constexpr int k_off(int w, int st) { return w * WG_BYTES + 2 * Q_BYTES + st * SUB_BYTES; }
   __host__ __device__ static constexpr int v_off(int w, int st) {
@@ -113,7 +123,8 @@ __device__ __forceinline__ void decode_item7(const int* order, const int* pre_fu
 
 template <int NWG, int NPP, int SLEEP_NS>
 __global__ void __launch_bounds__(attn7_threads(NWG), 1)
-    attn7_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const AttnParams p, const int T, const int nh) {
+    attn7_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmQ32,
+                    const AttnParams p, const int T, const int nh) {
   using S = Attn7Smem<NWG>;
   constexpr int DH = 32;
   constexpr int kMmaWarp = 4 * NWG;  // also allocates TMEM
@@ -326,10 +337,17 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
         is[3] = h;
         is[4] = seq0;
         is[5] = N;
-        is[6] = p.kv_len ? __ldg(p.kv_len + t) : N;
+        const int n_keys = p.kv_len ? __ldg(p.kv_len + t) : N;
+        is[6] = n_keys;
         mbar_expect_tx(&b[slot], S::Q_BYTES);
-        tma_load_2d(smem + S::q_off(w, slot), &tmQKV, &b[slot], h * DH, seq0 + tile * 128);
-        tma_load_2d(smem + S::q_off(w, slot) + S::SUB_BYTES, &tmQKV, &b[slot], h * DH, seq0 + tile * 128 + 64);
+        // the Q tile as four 32-row boxes: slot quarter j takes rows (j mod 4/rep) * 32 of the tile,
+        // i.e. a split tail tile (<= 64 / <= 32 rows) lands rep = 2 / 4 times
+        const int q_real = n_keys - tile * 128;  // real query rows of the tile (the rest: next task / pad)
+        const int nrb = (q_real > 0 && q_real <= SPLIT_ROWS) ? 4 / SPLIT_REP : 4;  // = 4 / rep
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          tma_load_2d(smem + S::q_off(w, slot) + j * (S::SUB_BYTES / 2), &tmQ32, &b[slot], h * DH,
+                      seq0 + tile * 128 + (j % nrb) * 32);
         for (int u = 0; u < ns; ++u, ++g) {
           const int st = g % ATTN7_ST;
           if (g >= ATTN7_ST) mbar_poll_slow(&b[4 + ATTN7_ST + st], ((g / ATTN7_ST) - 1) & 1, p.producer_sleep);  // kv_empty
@@ -376,9 +394,44 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
       const int tile = is[2], h = is[3], seq0 = is[4], N = is[5];
       const int nsub = (N + 63) / 64;
       const int q_valid = N - tile * 128;
-      const bool active = quarter * 32 < q_valid;
+      // split tail tile (<= SPLIT_ROWS real rows): the producer loaded its rows rep times over the lane
+      // quarters; replica rr (quarters rr*(4/rep) + rb) takes key columns [rr*cw, rr*cw + cw) of
+      // every 64-key sub-tile, so all four warps share the tail's exponentials; the replicas'
+      // (m, l, O) are merged at the end of the item
       const int n_keys = is[6];  // keys >= n_keys are masked (padded batch)
+      // split by the real rows (n_keys = N, or kv_len in the padded batch, whose tail tile must take
+      // the same path as the varlen one: rows equal bit for bit)
+      const int q_real = n_keys - tile * 128;
+      const bool split = q_real > 0 && q_real <= SPLIT_ROWS;
+      const bool active = split || quarter * 32 < q_valid;
       float m_run = -INFINITY, l_run = 0.f;
+      if (split) {  // the other replicas' P columns stay zero for the whole item
+        uint32_t z[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) z[i] = 0u;
+        tmem_st16(p_addr, z);
+        tmem_st16(p_addr + 16, z);
+      }
+      // PV(u-1) done: P may be overwritten and O rescaled by alpha (rows whose max moved)
+      const auto wait_o_rescale = [&](bool upd, float alpha) {
+        mbar_wait(o_full, o_cnt & 1);
+        ++o_cnt;
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, upd)) {
+          uint32_t o[32];
+          tmem_ld32(o_addr, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < DH; i += 2) {
+            float a0, a1;
+            fma2(a0, a1, __uint_as_float(o[i]), __uint_as_float(o[i + 1]), alpha, alpha, 0.f, 0.f);
+            o[i] = __float_as_uint(a0);
+            o[i + 1] = __float_as_uint(a1);
+          }
+          tmem_st16(o_addr, *reinterpret_cast<const uint32_t(*)[16]>(o));
+          tmem_st16(o_addr + 16, *reinterpret_cast<const uint32_t(*)[16]>(o + 16));
+        }
+      };
       for (int u = 0; u < nsub; ++u) {
         mbar_wait(s_full, s_cnt & 1);
         ++s_cnt;
@@ -403,6 +456,42 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
             mbar_wait(o_full, o_cnt & 1);
             ++o_cnt;
           }
+        } else if (split) {
+          // split tail tile (all four warps active): this warp's cw key columns of the sub-tile
+          constexpr int rep = SPLIT_REP, cw = 64 / rep;
+          const int rr = quarter / (4 / rep);
+          const int valid = min(64, n_keys - u * 64);
+          const int c0 = rr * cw;
+          uint32_t sr[32];
+          if constexpr (rep == 2) tmem_ld32(s_base + c0, *reinterpret_cast<uint32_t(*)[32]>(sr));
+          else tmem_ld16(s_base + c0, *reinterpret_cast<uint32_t(*)[16]>(sr));
+          publish_prev_p();
+          tmem_wait_ld();
+          tc_fence_before();
+          mbar_arrive(s_free);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i >= cw || c0 + i >= valid) sr[i] = __float_as_uint(-INFINITY);
+          float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            m0 = fmax3(m0, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
+            m1 = fmax3(m1, __uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3]));
+          }
+          const float m_cand = fmaxf(m0, m1) * c;
+          // lazy rescale (R23); a warp may see only masked keys so far (m_cand = m_run = -inf):
+          // it keeps m_run = -inf and exponentiates against 0 (p = 0, no inf - inf)
+          const bool upd = (m_run == -INFINITY) ? (m_cand != -INFINITY) : (m_cand > m_run + 8.0f);
+          const float alpha = upd ? ((m_run == -INFINITY) ? 0.f : ex2_approx(m_run - m_cand)) : 1.f;
+          if (upd) m_run = m_cand;
+          const float neg = (m_run == -INFINITY) ? 0.f : -m_run;
+          float sum0 = 0.f, sum1 = 0.f;
+          if constexpr (rep == 2) exp_chunk<0, 16>(sr, c, neg, sum0, sum1);
+          else exp_chunk<0, 8>(sr, c, neg, sum0, sum1);
+          l_run = l_run * alpha + (sum0 + sum1);
+          if (u > 0) wait_o_rescale(upd, alpha);
+          if constexpr (rep == 2) tmem_st16(p_addr + rr * 16, *reinterpret_cast<const uint32_t(*)[16]>(sr));
+          else tmem_st8(p_addr + rr * 8, *reinterpret_cast<const uint32_t(*)[8]>(sr));
         } else if (active) {
           const int valid = min(64, n_keys - u * 64);
           uint32_t sr[64];
@@ -482,26 +571,7 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
           }
           l_run = l_run * alpha + ((sum0 + sum1) + (sum2 + sum3));
           if (tr) ATTN_TR(wg, it, u, 3);
-          if (u > 0) {
-            // PV(u-1) done: P may be overwritten and O rescaled
-            mbar_wait(o_full, o_cnt & 1);
-            ++o_cnt;
-            tc_fence_after();
-            if (__any_sync(0xffffffffu, upd)) {
-              uint32_t o[32];
-              tmem_ld32(o_addr, o);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < DH; i += 2) {
-                float a0, a1;
-                fma2(a0, a1, __uint_as_float(o[i]), __uint_as_float(o[i + 1]), alpha, alpha, 0.f, 0.f);
-                o[i] = __float_as_uint(a0);
-                o[i + 1] = __float_as_uint(a1);
-              }
-              tmem_st16(o_addr, *reinterpret_cast<const uint32_t(*)[16]>(o));
-              tmem_st16(o_addr + 16, *reinterpret_cast<const uint32_t(*)[16]>(o + 16));
-            }
-          }
+          if (u > 0) wait_o_rescale(upd, alpha);
           if (tr) ATTN_TR(wg, it, u, 4);
           tmem_st16(p_addr, *reinterpret_cast<const uint32_t(*)[16]>(sr));
           if (valid > 32) tmem_st16(p_addr + 16, *reinterpret_cast<const uint32_t(*)[16]>(sr + 32));
@@ -522,7 +592,55 @@ __global__ void __launch_bounds__(attn7_threads(NWG), 1)
       mbar_wait(o_full, o_cnt & 1);
       ++o_cnt;
       tc_fence_after();
-      if (active) {
+      if (split) {
+        constexpr int rep = SPLIT_REP;
+        const int rb = quarter % (4 / rep), rr = quarter / (4 / rep);
+        // merge the replicas of the split tail through shared memory, in a fixed order:
+        // O = sum_j 2^(m_j - M) O_j / sum_j 2^(m_j - M) l_j over the replicas j of a row
+        float* ml = reinterpret_cast<float*>(smem + S::MERGE_OFF) + wg * S::MERGE_WG_FLOATS;  // [4][32][2]
+        float* acc = ml + 4 * 32 * 2;                                                       // [32][33]
+        uint32_t o[32];
+        tmem_ld32(o_addr, o);
+        ml[(quarter * 32 + lane) * 2 + 0] = m_run;
+        ml[(quarter * 32 + lane) * 2 + 1] = l_run;
+        tmem_wait_ld();
+        named_bar_sync(1 + wg, 128);
+        float M = -INFINITY;
+        for (int j = 0; j < rep; ++j) M = fmaxf(M, ml[((j * (4 / rep) + rb) * 32 + lane) * 2]);
+        float L = 0.f;
+        for (int j = 0; j < rep; ++j) {
+          const float mj = ml[((j * (4 / rep) + rb) * 32 + lane) * 2];
+          L += (mj == -INFINITY ? 0.f : ex2_approx(mj - M)) * ml[((j * (4 / rep) + rb) * 32 + lane) * 2 + 1];
+        }
+        const float wgt = (m_run == -INFINITY ? 0.f : ex2_approx(m_run - M)) / L;
+        // the four warps in turn (row block rb, replica rr): first replica writes, the others
+        // add, the last one stores the bf16 rows and the LSE
+        for (int k = 0; k < 4; ++k) {
+          if (k == rb * rep + rr) {
+            float* a = acc + lane * 33;
+            if (rr < rep - 1) {
+#pragma unroll
+              for (int i = 0; i < DH; ++i) a[i] = (rr ? a[i] : 0.f) + __uint_as_float(o[i]) * wgt;
+            } else {
+              const int rrow = rb * 32 + lane;
+              if (rrow < q_valid) {
+                uint32_t ob[DH / 2];
+#pragma unroll
+                for (int i = 0; i < DH / 2; ++i)
+                  ob[i] = pack_bf16x2(a[2 * i] + __uint_as_float(o[2 * i]) * wgt,
+                                      a[2 * i + 1] + __uint_as_float(o[2 * i + 1]) * wgt);
+                const int row = seq0 + tile * 128 + rrow;
+                uint4* dst = reinterpret_cast<uint4*>(p.out + (size_t)row * d + h * DH);
+#pragma unroll
+                for (int i = 0; i < DH / 8; ++i)
+                  dst[i] = make_uint4(ob[4 * i], ob[4 * i + 1], ob[4 * i + 2], ob[4 * i + 3]);
+                if (p.lse) p.lse[(size_t)h * p.lse_ld + row] = (M + __log2f(L)) * 0.69314718055994531f;
+              }
+            }
+          }
+          if (k < 3) named_bar_sync(1 + wg, 128);
+        }
+      } else if (active) {
         uint32_t o[32];
         tmem_ld32(o_addr, o);
         tmem_wait_ld();

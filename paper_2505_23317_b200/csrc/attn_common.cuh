@@ -92,15 +92,15 @@ __device__ __forceinline__ void exp2_poly2_d4(float& y0, float& y1, float x0, fl
   y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
 }
 
-// One 32-column chunk of a score row: p = 2^(s*c - m) for 16 pairs, running pair sums,
-// bf16x2-packed results written to sr[0..15].  Pairs [16-NPP, 16) use the polynomial.
-template <int NPP>
+// One 32-column chunk of a score row: p = 2^(s*c - m) for NPAIR (16) pairs, running pair sums,
+// bf16x2-packed results written to sr[0..NPAIR-1].  Pairs [NPAIR-NPP, NPAIR) use the polynomial.
+template <int NPP, int NPAIR = 16>
 __device__ __forceinline__ void exp_chunk(uint32_t* sr, float c, float neg, float& sum0, float& sum1) {
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
+  for (int i = 0; i < NPAIR; ++i) {
     float x0, x1, p0, p1;
     fma2(x0, x1, __uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1]), c, c, neg, neg);
-    if (i >= 16 - NPP) {
+    if (i >= NPAIR - NPP) {
       exp2_poly2(p0, p1, x0, x1);
     } else {
       p0 = ex2_approx(x0);

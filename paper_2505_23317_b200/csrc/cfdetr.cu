@@ -429,13 +429,14 @@ cudaError_t launch_attn4_t(const Opts& o, const CUtensorMap& tq, const AttnParam
 }
 
 template <int NPP, int SLEEP = 32, int NWG = 4>
-cudaError_t launch_attn7_t(const Opts& o, const CUtensorMap& tq64, const AttnParams& p, int items_ub, int nh, int T,
+cudaError_t launch_attn7_t(const Opts& o, const CUtensorMap& tq64, const CUtensorMap& tq32, const AttnParams& p,
+                           int items_ub, int nh, int T,
                            cudaStream_t s) {
   auto kern = attn7_tc_kernel<NWG, NPP, SLEEP>;
   constexpr int smem = Attn7Smem<NWG>::TOTAL;
   if (cudaError_t e = ensure_smem_attr(kern, smem); e != cudaSuccess) return e;
   const int grid = std::max(1, std::min((items_ub + NWG - 1) / NWG, num_sms(o)));
-  cudaError_t e = launch_ex(kern, dim3(grid), dim3(attn7_threads(NWG)), smem, s, tq64, p, T, nh);
+  cudaError_t e = launch_ex(kern, dim3(grid), dim3(attn7_threads(NWG)), smem, s, tq64, tq32, p, T, nh);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess && getenv("CFD_VERBOSE")) {
     cudaFuncAttributes fa{};
@@ -446,26 +447,27 @@ cudaError_t launch_attn7_t(const Opts& o, const CUtensorMap& tq64, const AttnPar
   return e;
 }
 
-// tq: qkv map with 128-row boxes (v1, v4); tq64: the same tensor with 64-row boxes (v7)
-cudaError_t launch_attention(const Opts& o, const CUtensorMap& tq, const CUtensorMap& tq64, const AttnParams& p,
+// tq: qkv map with 128-row boxes (v1, v4); tq64 / tq32: the same tensor with 64- / 32-row boxes (v7)
+cudaError_t launch_attention(const Opts& o, const CUtensorMap& tq, const CUtensorMap& tq64, const CUtensorMap& tq32,
+                             const AttnParams& p,
                              int max_qtiles, int nh, int T, cudaStream_t s) {
   probe_begin(PK_ATTN, s);
   cudaError_t e;
   if (o.attn_variant == 7 && T <= ATTN7_MAX_T) {
     const int items_ub = T * max_qtiles * nh;
     switch (o.attn_npp) {
-      case 0: e = launch_attn7_t<0>(o, tq64, p, items_ub, nh, T, s); break;
-      case 6: e = launch_attn7_t<6>(o, tq64, p, items_ub, nh, T, s); break;
-      case 8: e = launch_attn7_t<8>(o, tq64, p, items_ub, nh, T, s); break;
-      case 4: e = launch_attn7_t<4>(o, tq64, p, items_ub, nh, T, s); break;
+      case 0: e = launch_attn7_t<0>(o, tq64, tq32, p, items_ub, nh, T, s); break;
+      case 6: e = launch_attn7_t<6>(o, tq64, tq32, p, items_ub, nh, T, s); break;
+      case 8: e = launch_attn7_t<8>(o, tq64, tq32, p, items_ub, nh, T, s); break;
+      case 4: e = launch_attn7_t<4>(o, tq64, tq32, p, items_ub, nh, T, s); break;
       default:
-        e = o.attn_nwg == 3       ? launch_attn7_t<2, 32, 3>(o, tq64, p, items_ub, nh, T, s)
-            : o.attn_sleep == 0   ? launch_attn7_t<2, 0>(o, tq64, p, items_ub, nh, T, s)
-            : o.attn_sleep == 1   ? launch_attn7_t<2, 1>(o, tq64, p, items_ub, nh, T, s)
-            : o.attn_sleep == 2   ? launch_attn7_t<2, 2>(o, tq64, p, items_ub, nh, T, s)
-            : o.attn_sleep == 8   ? launch_attn7_t<2, 8>(o, tq64, p, items_ub, nh, T, s)
-            : o.attn_sleep == 128 ? launch_attn7_t<2, 128>(o, tq64, p, items_ub, nh, T, s)
-                                  : launch_attn7_t<2, 32>(o, tq64, p, items_ub, nh, T, s);
+        e = o.attn_nwg == 3       ? launch_attn7_t<2, 32, 3>(o, tq64, tq32, p, items_ub, nh, T, s)
+            : o.attn_sleep == 0   ? launch_attn7_t<2, 0>(o, tq64, tq32, p, items_ub, nh, T, s)
+            : o.attn_sleep == 1   ? launch_attn7_t<2, 1>(o, tq64, tq32, p, items_ub, nh, T, s)
+            : o.attn_sleep == 2   ? launch_attn7_t<2, 2>(o, tq64, tq32, p, items_ub, nh, T, s)
+            : o.attn_sleep == 8   ? launch_attn7_t<2, 8>(o, tq64, tq32, p, items_ub, nh, T, s)
+            : o.attn_sleep == 128 ? launch_attn7_t<2, 128>(o, tq64, tq32, p, items_ub, nh, T, s)
+                                  : launch_attn7_t<2, 32>(o, tq64, tq32, p, items_ub, nh, T, s);
         break;
     }
   } else if (o.attn_variant >= 4 && T <= ATTN_MAX_T) {
@@ -620,10 +622,10 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   const int d = g.d_model, F = g.d_ff;
   const bool fuse_ln = pick_bn(d) == d;  // one GEMM tile spans a whole row
   LayerDev& L = c->layers[l];
-  CUtensorMap ta_h, ta_o, ta_f, tq, tq64;
+  CUtensorMap ta_h, ta_o, ta_f, tq, tq64, tq32;
   if (!make_amap(&ta_h, w.hbuf, w.rows_cap, d) || !make_amap(&ta_o, w.obuf, w.rows_cap, d) ||
       !make_amap(&ta_f, w.ff, w.rows_cap, F) || !make_qkvmap(&tq, w.qkv, w.rows_cap, d) ||
-      !make_qkvmap(&tq64, w.qkv, w.rows_cap, d, 64))
+      !make_qkvmap(&tq64, w.qkv, w.rows_cap, d, 64) || !make_qkvmap(&tq32, w.qkv, w.rows_cap, d, 32))
     return CFD_E_CUDA;
   if ((l == 0 && !ln1_ready) || !fuse_ln)  // LN1
     CFD_CUDA(launch_layernorm(o, d, x, L.ln1_g, L.ln1_b, w.hbuf, M_static, m_dev, w.rows_cap, g.ln_eps, rows_grid, s));
@@ -648,13 +650,11 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   ap.uniform_n = o.attn_qmajor ? uniform_n : 0;
   if (o.attn_dyn) ap.work_counter = w.attn_work;  // dynamic item claiming (per-workspace counter)
   ap.kv_len = kv_len;
-  CFD_CUDA(launch_attention(o, tq, tq64, ap, max_qtiles, g.n_heads, T, s));
+  CFD_CUDA(launch_attention(o, tq, tq64, tq32, ap, max_qtiles, g.n_heads, T, s));
   if (want_lse && scores) {
     ScoreParams sp{};
     sp.n_coarse = c->Nc; sp.n_heads = g.n_heads; sp.d_model = d; sp.lse = w.lse; sp.lse_ld = w.lse_ld;
     sp.scale_log2 = ap.scale_log2; sp.scores = scores;
-    CUtensorMap tq32;
-    if (!make_qkvmap(&tq32, w.qkv, w.rows_cap, d, 32)) return CFD_E_CUDA;
     CFD_CUDA(launch_score(tq, tq32, sp, score_B, s));
   }
   const bool staged_ok = fuse_ln && o.staged_epi && (d % 64 == 0);
@@ -1164,6 +1164,9 @@ static cfd_status batch_refine_impl(cfd_ctx* c, int32_t T, const uint16_t* image
   p.pe = c->pef; p.pe_rows = c->Nf; p.frow = w.frow; p.fidx = w.fidx;
   CFD_CUDA(launch_gemm(c->opt, EPI_EMBED_FINE, ta, c->tm_wf, p, std::max(fine_grid, 1), s, PK_EMBED_F));
   const int max_qtiles = ((pad > 0 ? pad : c->Nf) + ATTN_BQ - 1) / ATTN_BQ;
+  // padded batch: the attention never writes the pad rows of a split tail tile (rows past the
+  // first 32 of a tile with <= 32 real rows, attn7_tc.cuh), so they stay zero from here
+  if (pad > 0) CFD_CUDA(cudaMemsetAsync(w.obuf, 0, (size_t)w.rows_cap * d * sizeof(__nv_bfloat16), s));
   for (int l = 0; l < g.n_layers; ++l) {
     st = run_layer(c, l, y, cap, 0, w.meta, std::max(rows_grid, 1), cu, T, max_qtiles, w, false, nullptr, 0, s, 0,
                    false, kv_len);
@@ -1401,8 +1404,10 @@ cfd_status cfdx_attention(int32_t T, const int32_t* cu, int32_t max_seqlen, int3
                           int32_t* work_counter, void* stream) {
   if (T <= 0 || !cu || !qkv || !out || max_seqlen <= 0 || rows_cap <= 0 || nh <= 0 || d % nh || d / nh != 32)
     return CFD_E_ARG;
-  CUtensorMap tq, tq64;
-  if (!make_qkvmap(&tq, qkv, rows_cap, d) || !make_qkvmap(&tq64, qkv, rows_cap, d, 64)) return CFD_E_CUDA;
+  CUtensorMap tq, tq64, tq32;
+  if (!make_qkvmap(&tq, qkv, rows_cap, d) || !make_qkvmap(&tq64, qkv, rows_cap, d, 64) ||
+      !make_qkvmap(&tq32, qkv, rows_cap, d, 32))
+    return CFD_E_CUDA;
   AttnParams ap{};
   ap.cu_seqlens = cu; ap.d_model = d; ap.out = (__nv_bfloat16*)out; ap.lse = lse; ap.lse_ld = lse_ld;
   ap.scale_log2 = 1.4426950408889634f / std::sqrt(32.0f);
@@ -1411,7 +1416,7 @@ cfd_status cfdx_attention(int32_t T, const int32_t* cu, int32_t max_seqlen, int3
   // work_counter: caller-owned zeroed int[2] (dynamic claims, reset by the launch's last CTA)
   // or NULL (static round-robin); no state is shared between calls
   if (g_dbg_opts.attn_dyn) ap.work_counter = work_counter;
-  CFD_CUDA(launch_attention(g_dbg_opts, tq, tq64, ap, (max_seqlen + ATTN_BQ - 1) / ATTN_BQ, nh, T, static_cast<cudaStream_t>(stream)));
+  CFD_CUDA(launch_attention(g_dbg_opts, tq, tq64, tq32, ap, (max_seqlen + ATTN_BQ - 1) / ATTN_BQ, nh, T, static_cast<cudaStream_t>(stream)));
   return CFD_OK;
 }
 

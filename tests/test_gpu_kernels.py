@@ -163,6 +163,28 @@ def test_attention_alternative_schedules_match_torch(opt):
     torch.testing.assert_close(lse[:, :rows], rlse[:, :rows], rtol=1e-4, atol=1e-4)
 
 
+def test_attention_split_tail_tiles_match_torch_per_row():
+    """v7 splits a tail tile with <= 32 real rows over the four lane quarters (each replica of the
+    rows takes 16 of every 64 key columns; the replicas' (m, l, O) merged in a fixed order): tails
+    of 1, 2, 16, 31 and 32 rows (and 33, not split) against torch row by row, with a few keys
+    carrying logits far above the rest so that the replicas' maxima differ by far more than the
+    lazy-rescale threshold and the merge weights are far from equal."""
+    d = 256
+    lens = [1, 2, 16, 31, 32, 33, 129, 160, 400]
+    rows = sum(lens)
+    torch.manual_seed(11)
+    qkv = torch.randn(rows + 256, 3 * d, device="cuda")
+    qkv[::37, d:2 * d] *= 6.0  # spiky keys: max logits in some replicas' column ranges only
+    qkv = qkv.to(torch.bfloat16)
+    _, cu_l, out, lse = _run_attn(lens, d, qkv=qkv)
+    ref, rlse = _attn_ref(qkv, cu_l, d, 8)
+    got = out.float()[:rows]
+    assert torch.isfinite(got).all()
+    err = ((got - ref[:rows]).norm(dim=1) / ref[:rows].norm(dim=1).clamp_min(1e-6)).max().item()
+    assert err < 2e-2, err
+    torch.testing.assert_close(lse[:, :rows], rlse[:, :rows], rtol=1e-4, atol=1e-4)
+
+
 def test_attention_dynamic_claims_reset_between_launches():
     """Dynamic item claiming (default): the claim counter is reset by each launch's last CTA,
     so back-to-back launches cover every item again; every item's result is independent of
