@@ -105,6 +105,8 @@ int32_t cfdx_probe_count(int32_t kind);
  *   key 22 attention v7: softmax warpgroups per CTA (3, or 4 default)
  *   key 23 QKV projection as CTA pairs (cta_group::2, half of each weight column block resident
  *          per SM, 8 A stages in flight) on (1, default) / off (0: one CTA per column block)
+ *   key 25 image-sourced coarse patch embed as CTA pairs (cta_group::2, half of W_c per SM,
+ *          12 stages) on (1, default) / off (0: one CTA per row block)
  * Other keys / values: CFD_E_ARG. */
 cfd_status cfdx_set_option(cfd_ctx *ctx, int32_t key, int32_t value);
 

@@ -130,6 +130,7 @@ struct Opts {
   int attn_psleep = 256;  // v7: the producer warp's sleep between barrier probes, ns (24: 0..4096)
   int attn_nwg = 4;       // v7: softmax warpgroups per CTA (22: 3 or 4)
   int qkv_pair = 1;       // QKV projection as CTA pairs, half of the weights resident per SM (23)
+  int embed_pair = 1;     // image-sourced coarse patch embed as CTA pairs, half of W_c per SM (25)
 };
 Opts g_dbg_opts;
 
@@ -243,6 +244,38 @@ cudaError_t launch_gemm_t(const Opts& o, const CUtensorMap& ta, const CUtensorMa
   cudaError_t le = launch_ex(kern, dim3(grid), dim3(64 + 32 * EW), smem, s, ta, tb, p, tx ? *tx : ta, tln ? *tln : ta);
   ++g_launches;
   return le != cudaSuccess ? le : cudaGetLastError();
+}
+
+// Image-sourced coarse patch embed as CTA pairs (gemm_tc_kernel IMG + PAIR): each CTA gathers its
+// own row block of patches and half of every W_c k-block (128 of the 256 columns), the leader issues
+// M = 256 cta_group::2 MMAs, each CTA's epilogue finishes its own rows (PE, x0, layer-0 LN1):
+// per-SM weight ingress halves (W_c is 1.5 MB per row block).
+cudaError_t launch_embed_pair(const Opts& o, const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p,
+                              int rows_for_grid, cudaStream_t s) {
+  constexpr int ST = 12;
+  auto kern = gemm_tc_kernel<256, ST, EPI_EMBED_COARSE, 8, 2, false, true, true>;
+  using SM = GemmSmem<256, ST, 2, false, 32, true>;
+  constexpr int smem = SM::TOTAL;
+  static_assert(smem <= 232448, "shared memory budget");
+  if (cudaError_t e = ensure_smem_attr(kern, smem); e != cudaSuccess) return e;
+  const int rpt = p.img_rb * p.img_gw;
+  const int units = ((rows_for_grid + rpt - 1) / rpt + 1) / 2;  // row-block pairs
+  const int pairs = balanced_grid(o, units, std::max(1, num_sms(o) / 2));
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(2 * pairs);
+  lc.blockDim = dim3(64 + 32 * 8);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeClusterDimension;
+  la[0].val.clusterDim.x = 2;
+  la[0].val.clusterDim.y = 1;
+  la[0].val.clusterDim.z = 1;
+  lc.attrs = la;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, kern, ta, tb_half, p, ta, ta);
+  ++g_launches;
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // QKV projection as CTA pairs (gemm_tc_kernel PAIR): bf16 out + bias, K = 256, N = 3d with
@@ -546,6 +579,7 @@ struct cfd_ctx {
   std::vector<LayerDev> layers;
   CUtensorMap tm_wc, tm_wf;
   CUtensorMap tm_wc32;  // W_c with 32-k x 256-row SW64 boxes (image-sourced coarse embed)
+  CUtensorMap tm_wc32h; // the same with 128-row boxes (CTA-pair embed: half the columns per CTA)
   bool has_wc32 = false;
   // NEXT f3 decoder (cfd_set_decoder): its own device block
   void* dec_block = nullptr;
@@ -842,6 +876,7 @@ cfd_status cfdx_set_option(cfd_ctx* ctx, int32_t key, int32_t value) {
       o.attn_nwg = value;
       return CFD_OK;
     case 23: o.qkv_pair = b; return CFD_OK;
+    case 25: o.embed_pair = b; return CFD_OK;
     case 24:
       if (value < 0 || value > 4096) return CFD_E_ARG;
       o.attn_psleep = value;
@@ -909,7 +944,8 @@ cfd_status cfd_create(const cfd_config* cfg, const cfd_weights* wts, void* strea
       cudaMemsetAsync(c->err, 0, 16, s) != cudaSuccess)
     return fail(CFD_E_CUDA);
   if (!make_wmap(&c->tm_wc, c->wc, d, c->Kc) || !make_wmap(&c->tm_wf, c->wf, d, c->Kf)) return fail(CFD_E_CUDA);
-  c->has_wc32 = d == 256 && make_tmap(&c->tm_wc32, c->wc, c->Kc, d, c->Kc, 32, 256, CU_TENSOR_MAP_SWIZZLE_64B);
+  c->has_wc32 = d == 256 && make_tmap(&c->tm_wc32, c->wc, c->Kc, d, c->Kc, 32, 256, CU_TENSOR_MAP_SWIZZLE_64B) &&
+                make_tmap(&c->tm_wc32h, c->wc, c->Kc, d, c->Kc, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
   c->layers.resize(L);
   for (int l = 0; l < L; ++l) {
     const cfd_layer_weights& hw = wts->h_layers[l];
@@ -1014,7 +1050,9 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
     p.img_thirds = 3 * Pc / 32;
     if (!make_img_map(&ti, images, B, g.img_h, g.img_w, Pc, p.img_rb)) return CFD_E_CUDA;
     probe_begin(PK_EMBED_C, s);
-    cudaError_t e = launch_gemm_t<256, EPI_EMBED_COARSE, 3>(o, ti, c->tm_wc32, p, M, s, nullptr, nullptr);
+    cudaError_t e = o.embed_pair && num_sms(o) >= 2 ? launch_embed_pair(o, ti, c->tm_wc32h, p, M, s)
+                                                    : launch_gemm_t<256, EPI_EMBED_COARSE, 3>(o, ti, c->tm_wc32, p, M, s,
+                                                                                              nullptr, nullptr);
     probe_end(PK_EMBED_C, s);
     CFD_CUDA(e);
   } else {

@@ -531,7 +531,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
                    const __grid_constant__ CUtensorMap tmLN) {
   static_assert((EW == 8 && NACC == 2) || (EW == 4 && NACC == 1), "supported epilogue configurations");
   static_assert(!IMG || (EPI == EPI_EMBED_COARSE && !BRES), "IMG is the coarse patch embed");
-  static_assert(!PAIR || (BRES && BN == 256 && EW == 8 && EPI == EPI_BF16_BIAS), "PAIR is the QKV projection");
+  static_assert(!PAIR || (BN == 256 && EW == 8 &&
+                          ((BRES && EPI == EPI_BF16_BIAS) || (IMG && EPI == EPI_EMBED_COARSE && !BRES))),
+                "PAIR is the QKV projection or the image-sourced coarse patch embed");
   constexpr int BKX = IMG ? 32 : GEMM_BK;
   using S = GemmSmem<BN, STAGES, NACC, BRES, BKX, PAIR>;
   extern __shared__ uint8_t smem_raw[];
@@ -605,11 +607,13 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
   // tile walk: default tile = m_blk * n_tiles + n_blk over all tiles; BRES: the CTA (PAIR: the
   // cluster) keeps column block cta_id % n_tiles and walks row blocks (PAIR: row-block pairs;
   // the unit count is a multiple of n_tiles)
-  const int t_first = BRES ? cta_id / n_tiles : (int)blockIdx.x;
-  const int t_step = BRES ? n_units / n_tiles : (int)gridDim.x;
+  // (PAIR without BRES, the coarse embed: one column block, n_tiles = 1, the same row-pair walk)
+  constexpr bool kUnitWalk = BRES || PAIR;
+  const int t_first = kUnitWalk ? cta_id / n_tiles : (int)blockIdx.x;
+  const int t_step = kUnitWalk ? n_units / n_tiles : (int)gridDim.x;
   const int m_units = PAIR ? (m_tiles + 1) / 2 : m_tiles;
-  const int t_end = BRES ? (cta_id < t_step * n_tiles ? m_units : 0) : total;
-  auto m_of = [&](int tile) { return BRES ? (PAIR ? 2 * tile + rank : tile) : tile / n_tiles; };
+  const int t_end = kUnitWalk ? (cta_id < t_step * n_tiles ? m_units : 0) : total;
+  auto m_of = [&](int tile) { return kUnitWalk ? (PAIR ? 2 * tile + rank : tile) : tile / n_tiles; };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -619,7 +623,13 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
         const int m_blk = m_of(tile), n_blk = BRES ? n_fix : tile % n_tiles;
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if constexpr (PAIR) {  // this CTA's 128 A rows, completing on the leader's full barrier
+          if constexpr (PAIR && IMG) {  // this CTA's rpt A rows + its 128 B columns, on the leader's barrier
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * (rpt * 64 + S::B_BYTES));
+            const uint32_t lb = mapa_u32(&full[stage], 0);
+            tma_load_5d_2sm(sA + stage * S::A_BYTES, &tmA, lb, 0, kb % p.img_thirds, 0, kb / p.img_thirds,
+                            m_blk * p.img_rb);
+            tma_load_2d_2sm(sB + stage * S::B_BYTES, &tmB, lb, kb * BKX, n_blk * BN + 128 * rank);
+          } else if constexpr (PAIR) {  // this CTA's 128 A rows, completing on the leader's full barrier
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * S::A_BYTES);
             tma_load_2d_2sm(sA + stage * S::A_BYTES, &tmA, mapa_u32(&full[stage], 0), kb * BKX, m_blk * GEMM_BM);
           } else if constexpr (IMG) {  // rpt rows of 64 B (OOB rows of the last tile are zero-filled)
@@ -630,7 +640,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
             mbar_expect_tx(&full[stage], S::STAGE_BYTES);
             tma_load_2d(sA + stage * S::A_BYTES, &tmA, &full[stage], kb * BKX, m_blk * GEMM_BM);
           }
-          if constexpr (!BRES) tma_load_2d(sB + stage * S::B_BYTES, &tmB, &full[stage], kb * BKX, n_blk * BN);
+          if constexpr (!BRES && !PAIR) tma_load_2d(sB + stage * S::B_BYTES, &tmB, &full[stage], kb * BKX, n_blk * BN);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -762,7 +772,10 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
         if (c + 2 >= CH) {  // last TMEM read of this accumulator: release it to the MMA warp early
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) {
+            if (PAIR && rank) mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA warp waits
+            else mbar_arrive(&tempty[acc]);
+          }
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {

@@ -213,6 +213,14 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const void* tmap, uin
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_5d_2sm(void* dst, const void* tmap, uint32_t bar_cluster, int c0, int c1,
+                                                int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
 // M = 256 pair MMAs issued by the leader CTA: A rows 0-127 / 128-255 and B columns
 // [0, N/2) / [N/2, N) come from the same smem (or TMEM) address in CTA 0 / CTA 1; D rows
 // 0-127 / 128-255 land in CTA 0's / CTA 1's TMEM at d_tmem.
