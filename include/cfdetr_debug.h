@@ -70,28 +70,25 @@ int32_t cfdx_probe_count(int32_t kind);
 /* Tuning switches for A/B measurement (every combination is parity-checked).  ctx != NULL:
  * the switch of that context only (each context starts at the defaults); ctx == NULL: the
  * switches the ctx-less debug entry points above use.
- *   key 0  attention kernel: 1 one query tile per CTA (v1), 4 three query tiles / warpgroups
- *          per CTA sharing one K/V stream (v4), 7 independent per-warpgroup items (task, head,
- *          128-row tile), K/V rings, MMA and producer warps (v7, default)
- *   key 1  v4 / v7: how many of every 16 column pairs are exponentiated by the FMA-pipe
+ *   key 0  attention kernel: 1 one query tile per CTA (v1; also used above 1024 tasks per launch),
+ *          7 independent per-warpgroup items (task, head, 128-row tile), K/V rings, MMA and
+ *          producer warps (v7, default)
+ *   key 1  v7: how many of every 16 column pairs are exponentiated by the FMA-pipe
  *          polynomial instead of MUFU (0, 2 default, 4, 6, 8)
  *   key 2  fused MLP kernel on (1, default) / off (0)
  *   key 3  TMA-staged residual(+LayerNorm) epilogues on (1, default) / off (0)
  *   key 4  fused MLP (with the fused O-projection) as CTA pairs (cta_group::2, each SM holding half of
  *          every weight operand) on (1, default) / off (0)
- *   key 5  attention warpgroup start stagger in cycles (700 default); -1 / -2 select the
- *          debug library's v4 "quarters" / "MMA warp" attention trace modes
+ *   key 5  attention v7 warpgroup start stagger in cycles (700 default; values <= 0: none)
  *   key 7  weight-stationary QKV GEMM on (1, default) / off (0)
  *   key 11 O-projection + residual + LN2 fused into the MLP kernel on (1, default) / off (0)
- *   key 12 attention v4 q-triple-major item order for equal-length (coarse) batches on (1,
- *          default) / off (0)
  *   key 13 patch-embed GEMMs with one CTA per SM and a 4-stage ring (1, default) instead of
  *          two CTAs per SM with 2 stages (0)
  *   key 14 coarse patch embed gathering its A tiles straight from the image with a 5-D TMA
  *          tensor map (1, default; d = 256, 3Pc % 32 == 0) instead of im2col + GEMM (0)
  *   key 15 layer-0 LN1 of the coarse pass fused into the coarse embed epilogue (1, default)
  *          instead of a standalone LayerNorm launch (0)
- *   key 16 attention v4 dynamic item claiming through the call workspace's work counter (1,
+ *   key 16 attention v7 dynamic item claiming through the call workspace's work counter (1,
  *          default) instead of the static round-robin (0)
  *   key 17 cap on the persistent kernels' grid size (0 = every SM, default)
  *   key 18 balanced persistent grids: the fewest CTAs with the same number of rounds (1) /
@@ -124,8 +121,8 @@ cfd_status cfdx_mlp_trace(uint64_t* dst, int32_t n_words);
 cfd_status cfdx_frames_u8(long long n, const uint8_t* src, const float* scale, const float* shift, uint16_t* dst,
                           void* stream);
 
-/* Debug library only: copies the attention (v4/v5) pipeline trace of the last launch
- * (ATTN_TRACE_WORDS = 148*4*2*12*8 + 148 uint64 clock64 values, layout in attn4_tc.cuh) to
+/* Debug library only: copies the attention (v7) pipeline trace of the last launch
+ * (ATTN_TRACE_WORDS = 148*4*2*12*8 + 148 uint64 clock64 values, layout in attn_common.cuh) to
  * host `dst`.  CFD_E_ARG in the release library or if n_words is too small. */
 cfd_status cfdx_attn_trace(uint64_t* dst, int32_t n_words);
 

@@ -33,8 +33,6 @@ struct AttnParams {
   int lse_ld;
   float scale_log2;        // log2(e) / sqrt(dh)
   int stagger = 0;         // v4: softmax warpgroup w starts w * stagger cycles late (0 = off)
-  int uniform_n = 0;       // > 0: every task has this many tokens (coarse pass) -> v4 walks its
-                           // items q-triple-major (all first triples, then all second ones, ...)
   int* work_counter = nullptr;  // v4: zeroed int; non-null -> items after the first are claimed
                                 // dynamically (atomicAdd) instead of the static round-robin
   int n_q = 0;             // v1 CROSS: queries per task (one 128-row tile shared by every task)

@@ -28,7 +28,6 @@
 #include "../../include/cfdetr_debug.h"
 #include "attn_tc.cuh"
 #include "attn_common.cuh"
-#include "attn4_tc.cuh"
 #include "attn7_tc.cuh"
 #include "gemm_tc.cuh"
 #include "misc_kernels.cuh"
@@ -107,12 +106,11 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
 // copy (set per ctx); the ctx-less debug entry points use g_dbg_opts.  Defaults = the measured
 // best configuration.
 struct Opts {
-  int attn_variant = 7;   // 1: one q-tile per CTA (v1), 4: three q-tiles per CTA (v4), 7: independent
-                          // per-warpgroup items and pipelines (v7, default)
+  int attn_variant = 7;   // 1: one q-tile per CTA (v1; also the fallback above ATTN7_MAX_T tasks),
+                          // 7: independent per-warpgroup items and pipelines (v7, default)
   int attn_npp = 2;       // v4 / v7: polynomial-exp pairs of every 16 (v7: 2 measured best)
   int attn_stagger = 700; // v4 / v7: warpgroup start stagger in cycles (v7: 700 measured best:
                           // 58.2 vs 60.5 us at 700 x 32); -1 / -2 trace modes (debug library)
-  int attn_qmajor = 1;    // v4: q-triple-major item order for equal-length batches (option 12)
   int attn_dyn = 1;       // v4: dynamic item claiming through the workspace work counter (16)
   int fused_mlp = 1;      // fused MLP kernel (d == 256) instead of two GEMM launches (2)
   int staged_epi = 1;     // TMA-staged residual + LayerNorm epilogues (3)
@@ -443,24 +441,6 @@ cudaError_t launch_mlp(const Opts& o, const CUtensorMap& th, const CUtensorMap& 
   return cudaGetLastError();
 }
 
-template <int NPP>
-cudaError_t launch_attn4_t(const Opts& o, const CUtensorMap& tq, const AttnParams& p, int items_ub, int nh, int T,
-                           cudaStream_t s) {
-  auto kern = attn4_tc_kernel<32, 4, NPP>;
-  constexpr int smem = Attn4Smem<32, 4>::TOTAL;
-  if (cudaError_t e = ensure_smem_attr(kern, smem); e != cudaSuccess) return e;
-  const int grid = std::max(1, balanced_grid(o, items_ub, num_sms(o)));
-  cudaError_t e = launch_ex(kern, dim3(grid), dim3(ATTN4_THREADS), smem, s, tq, p, T, nh);
-  if (e == cudaSuccess) e = cudaGetLastError();
-  if (e != cudaSuccess && getenv("CFD_VERBOSE")) {
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, kern);
-    fprintf(stderr, "attention v4 launch (grid %d, %d threads, %d B smem; kernel: %d regs): %s\n", grid,
-            ATTN4_THREADS, smem, fa.numRegs, cudaGetErrorString(e));
-  }
-  return e;
-}
-
 template <int NPP, int SLEEP = 32, int NWG = 4>
 cudaError_t launch_attn7_t(const Opts& o, const CUtensorMap& tq64, const CUtensorMap& tq32, const AttnParams& p,
                            int items_ub, int nh, int T,
@@ -502,15 +482,6 @@ cudaError_t launch_attention(const Opts& o, const CUtensorMap& tq, const CUtenso
             : o.attn_sleep == 128 ? launch_attn7_t<2, 128>(o, tq64, tq32, p, items_ub, nh, T, s)
                                   : launch_attn7_t<2, 32>(o, tq64, tq32, p, items_ub, nh, T, s);
         break;
-    }
-  } else if (o.attn_variant >= 4 && T <= ATTN_MAX_T) {
-    const int items_ub = T * ((max_qtiles + ATTN4_NWG - 1) / ATTN4_NWG) * nh;
-    switch (o.attn_npp) {
-      case 0: e = launch_attn4_t<0>(o, tq, p, items_ub, nh, T, s); break;
-      case 2: e = launch_attn4_t<2>(o, tq, p, items_ub, nh, T, s); break;
-      case 6: e = launch_attn4_t<6>(o, tq, p, items_ub, nh, T, s); break;
-      case 8: e = launch_attn4_t<8>(o, tq, p, items_ub, nh, T, s); break;
-      default: e = launch_attn4_t<4>(o, tq, p, items_ub, nh, T, s); break;
     }
   } else {
     auto kern = attn_tc_kernel<32, 3>;
@@ -648,8 +619,7 @@ Workspace carve(const cfd_ctx* c, int n, void* base) {
 // O-projection epilogue the same way.
 cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const int* m_dev, int rows_grid,
                      const int32_t* cu, int T, int max_qtiles, Workspace& w, bool want_lse, float* scores,
-                     int score_B, cudaStream_t s, int uniform_n = 0, bool ln1_ready = false,
-                     const int32_t* kv_len = nullptr) {
+                     int score_B, cudaStream_t s, bool ln1_ready = false, const int32_t* kv_len = nullptr) {
   const cfd_config& g = c->cfg;
   Opts o = c->opt;
   if (kv_len) o.attn_variant = 7;  // key masking (padded batch) is a v7 feature
@@ -681,7 +651,6 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
   ap.scale_log2 = 1.4426950408889634f / std::sqrt((float)c->dh);
   ap.stagger = o.attn_stagger;
   ap.producer_sleep = o.attn_psleep;
-  ap.uniform_n = o.attn_qmajor ? uniform_n : 0;
   if (o.attn_dyn) ap.work_counter = w.attn_work;  // dynamic item claiming (per-workspace counter)
   ap.kv_len = kv_len;
   CFD_CUDA(launch_attention(o, tq, tq64, tq32, ap, max_qtiles, g.n_heads, T, s));
@@ -839,7 +808,7 @@ cfd_status cfdx_set_option(cfd_ctx* ctx, int32_t key, int32_t value) {
   const int b = value ? 1 : 0;
   switch (key) {
     case 0:
-      if (value != 1 && value != 4 && value != 7) return CFD_E_ARG;
+      if (value != 1 && value != 7) return CFD_E_ARG;
       o.attn_variant = value;
       return CFD_OK;
     case 1:
@@ -855,7 +824,6 @@ cfd_status cfdx_set_option(cfd_ctx* ctx, int32_t key, int32_t value) {
       return CFD_OK;
     case 7: o.gemm_bres = b; return CFD_OK;
     case 11: o.fuse_oproj = b; return CFD_OK;
-    case 12: o.attn_qmajor = b; return CFD_OK;
     case 13: o.embed_mode0 = b; return CFD_OK;
     case 14: o.embed_img = b; return CFD_OK;
     case 15: o.embed_ln = b; return CFD_OK;
@@ -1074,7 +1042,7 @@ cfd_status cfd_coarse_encode(cfd_ctx* c, int32_t B, const uint16_t* images, floa
   for (int l = 0; l < g.n_layers; ++l) {
     const bool sl = (l == g.score_layer);
     cfd_status st =
-        run_layer(c, l, y, M, M, nullptr, M, w.ccu, B, max_qtiles, w, sl && scores, scores, B, s, c->Nc, ln0 && l == 0);
+        run_layer(c, l, y, M, M, nullptr, M, w.ccu, B, max_qtiles, w, sl && scores, scores, B, s, ln0 && l == 0);
     if (st != CFD_OK) return st;
     if (layer_out)
       CFD_CUDA(cudaMemcpyAsync(layer_out + (size_t)l * M * d, y, (size_t)M * d * 4, cudaMemcpyDeviceToDevice, s));
@@ -1206,7 +1174,7 @@ static cfd_status batch_refine_impl(cfd_ctx* c, int32_t T, const uint16_t* image
   // first 32 of a tile with <= 32 real rows, attn7_tc.cuh), so they stay zero from here
   if (pad > 0) CFD_CUDA(cudaMemsetAsync(w.obuf, 0, (size_t)w.rows_cap * d * sizeof(__nv_bfloat16), s));
   for (int l = 0; l < g.n_layers; ++l) {
-    st = run_layer(c, l, y, cap, 0, w.meta, std::max(rows_grid, 1), cu, T, max_qtiles, w, false, nullptr, 0, s, 0,
+    st = run_layer(c, l, y, cap, 0, w.meta, std::max(rows_grid, 1), cu, T, max_qtiles, w, false, nullptr, 0, s,
                    false, kv_len);
     if (st != CFD_OK) return st;
     if (layer_out)

@@ -56,10 +56,10 @@ def test_tuning_option_validation_without_gpu(lib):
     """cfdx_set_option accepts the documented keys/values (cfdetr_debug.h) and rejects others
     (ctx = NULL: the debug entry points' switches)."""
     f = lib.cfdx_set_option
-    assert f(None, 0, 6) == -1 and f(None, 0, 0) == -1 and f(None, 0, 2) == -1
+    assert f(None, 0, 6) == -1 and f(None, 0, 0) == -1 and f(None, 0, 2) == -1 and f(None, 0, 4) == -1
     assert f(None, 1, 3) == -1 and f(None, 1, 10) == -1 and f(None, 1, -2) == -1
     assert f(None, 5, -3) == -1 and f(None, 6, 4) == -1 and f(None, 9, 0) == -1 and f(None, 10, 0) == -1
-    assert f(None, 8, 0) == -1 and f(None, 26, 0) == -1 and f(None, 24, -1) == -1 and f(None, 24, 5000) == -1
+    assert f(None, 8, 0) == -1 and f(None, 12, 0) == -1 and f(None, 26, 0) == -1 and f(None, 24, -1) == -1 and f(None, 24, 5000) == -1
     for key, val in ((0, 1), (1, 8), (2, 0), (3, 0), (4, 0), (5, 300), (7, 0), (11, 0), (19, 0), (20, 0), (17, 74)):
         assert f(None, key, val) == 0
     assert f(None, 21, 5) == -1 and f(None, 22, 2) == -1

@@ -1,6 +1,6 @@
 """Time the attention kernel alone at bench shapes (for ncu captures and variant sweeps): reps
 back-to-back launches replayed from one CUDA graph, CUDA events around the replay.
-python tools/attn_bench.py --opt 0=4 --opt 1=4 --lens 700x32 --reps 20   (--opt K=V: cfdx_set_option)"""
+python tools/attn_bench.py --opt 0=1 --opt 1=4 --lens 700x32 --reps 20   (--opt K=V: cfdx_set_option)"""
 import argparse
 import os
 import sys

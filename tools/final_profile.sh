@@ -11,7 +11,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:mlp_tc_kernel --launch-skip 12 -c 12 \
   -o gpurun_out/final_mlp_full -f python bench.py --steps 2 --warmup 3 --streams 1 --no-cpu-baseline --no-check \
   > gpurun_out/final_mlp_full.log 2>&1
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:attn4_tc_kernel --launch-skip 12 -c 12 \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:attn7_tc_kernel --launch-skip 12 -c 12 \
   -o gpurun_out/final_attn_full -f python bench.py --steps 2 --warmup 3 --streams 1 --no-cpu-baseline --no-check \
   > gpurun_out/final_attn_full.log 2>&1
 for k in mlp attn; do

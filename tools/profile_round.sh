@@ -21,7 +21,7 @@ if [ "$WHAT" != list ]; then
       > "$OUT/full_${TAG}_$name.log" 2>&1
   done <<LIST
 mlp mlp_tc_kernel 20
-attn attn4_tc_kernel 20
+attn attn7_tc_kernel 20
 oproj gemm_tc_kernel<.int.256,..int.2,..int.5 20
 qkv gemm_tc_kernel<.int.256,..int.[34],..int.0 20
 score score_tc_kernel 2
