@@ -67,7 +67,7 @@ def parse(argv=None):
     ap.add_argument("--ratio", type=int, default=25, help="c640: refine percentage per frame")
     ap.add_argument("--streams", type=int, default=None,
                     help="concurrent lanes per GPU (own encoder / stream / CUDA graph each); default 2 for "
-                         "c640 and multi48, 1 otherwise")
+                         "multi48 (its e2e overlaps the lanes' copies), 1 otherwise")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -479,7 +479,10 @@ def gpu_arm(args):
     B = len(work.ids)
     imgs_np = np.stack([ci.make_frame(cfg.img_h, cfg.img_w, ci.frame_seed(t, 0)) for t in work.ids])
     imgs = bf16_tensor(imgs_np, dev)
-    S = args.streams if args.streams is not None else (2 if work.name in ("c640", "multi48") else 1)
+    # lanes: one 128-frame lane beats two 64-frame lanes for c640 since the round-2 kernels
+    # (36.1k vs 35.2k frames/s, e2e 31.5k vs 31.2k; profiles/r2g_streams.txt); multi48 keeps two
+    # (device 22.0k vs 21.6k but e2e 20.1k vs 20.5k with one)
+    S = args.streams if args.streams is not None else (2 if work.name == "multi48" else 1)
     S = max(1, min(S, B))
     main = torch.cuda.Stream(device=dev)
 
