@@ -140,9 +140,11 @@ __device__ __forceinline__ void gelu2(float& a, float& b) {
 // Each epilogue warp owns 32 rows (its TMEM lane quarter) x BN/2 columns of a tile, one
 // row per thread, in 32-column chunks: tcgen05.ld -> + bias (shared-memory broadcast) ->
 // fused op -> 16-byte vector stores of the thread's row segment.
+// s1 / s2: shifted row sums (v - sh) and (v - sh)^2 for the fused LayerNorm, sh = the first value
+// this thread sees (first = true on its first chunk), so |mean| >> std does not cancel.
 template <int EPI>
 __device__ __forceinline__ void direct_chunk(const GemmParams& p, float (&v)[32], int row, int col0, int m_store,
-                                             int M, float& s1, float& s2) {
+                                             int M, float& s1, float& s2, float& sh, bool first) {
   if constexpr (EPI == EPI_BF16_BIAS || EPI == EPI_BF16_BIAS_GELU) {
     if (row >= m_store) return;
     uint32_t pk[16];
@@ -166,8 +168,10 @@ __device__ __forceinline__ void direct_chunk(const GemmParams& p, float (&v)[32]
       x[i].x += v[4 * i + 0]; x[i].y += v[4 * i + 1]; x[i].z += v[4 * i + 2]; x[i].w += v[4 * i + 3];
       dst[i] = x[i];
       if constexpr (EPI == EPI_F32_RESID_LN) {
-        s1 += (x[i].x + x[i].y) + (x[i].z + x[i].w);
-        s2 += (x[i].x * x[i].x + x[i].y * x[i].y) + (x[i].z * x[i].z + x[i].w * x[i].w);
+        if (first && i == 0) sh = x[0].x;
+        const float a = x[i].x - sh, b = x[i].y - sh, c = x[i].z - sh, d = x[i].w - sh;
+        s1 += (a + b) + (c + d);
+        s2 += (a * a + b * b) + (c * c + d * d);
       }
     }
   } else if constexpr (EPI == EPI_EMBED_COARSE) {
@@ -701,7 +705,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
                                                                                           : m_blk * rpt + quarter * 32;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + half * WCOLS;
       const int col_base = n_blk * BN + half * WCOLS;
-      float s1 = 0.f, s2 = 0.f;  // RESID_LN row statistics (lane = row)
+      float s1 = 0.f, s2 = 0.f, sh = 0.f;  // LN row statistics (lane = row): shifted sums around sh
       if constexpr (EPI == EPI_F32_RESID_LN && EW == 8) {
         uint8_t* stg = smem + S::STG_OFF + (warp - 2) * S::STG_BYTES;
         const ResidStage st{stg, 4096, stg + 8192, 2048, xbar + (warp - 2) * 2, &xph};
@@ -753,9 +757,11 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
               x.z += __uint_as_float(r[4 * i + 2]) + bb.z;
               x.w += __uint_as_float(r[4 * i + 3]) + bb.w;
               dst[i] = x;
-              if constexpr (EPI == EPI_F32_RESID_LN) {
-                s1 += (x.x + x.y) + (x.z + x.w);
-                s2 += (x.x * x.x + x.y * x.y) + (x.z * x.z + x.w * x.w);
+              if constexpr (EPI == EPI_F32_RESID_LN) {  // shifted sums around the row's first value
+                if (c == 0 && i == 0) sh = x.x;
+                const float a0 = x.x - sh, a1 = x.y - sh, a2 = x.z - sh, a3 = x.w - sh;
+                s1 += (a0 + a1) + (a2 + a3);
+                s2 += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
               }
             }
           }
@@ -792,7 +798,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
             v[j + 2] = __uint_as_float(r[j + 2]) + bb.z;
             v[j + 3] = __uint_as_float(r[j + 3]) + bb.w;
           }
-          direct_chunk<EPI>(p, v, row, col0, m_store, M, s1, s2);
+          direct_chunk<EPI>(p, v, row, col0, m_store, M, s1, s2, sh, c + q == 0);
         }
       }
       }
@@ -801,17 +807,46 @@ __global__ void __launch_bounds__(64 + 32 * EW, (EW == 4 ? 2 : 1))
       if (((EPI == EPI_F32_RESID_LN && EW != 8) || EPI == EPI_EMBED_COARSE) &&
           (EPI != EPI_EMBED_COARSE || p.ln_g != nullptr)) {
         // row statistics; with EW=8 the two warps sharing these rows exchange halves
-        float2 o = make_float2(0.f, 0.f);
-        if constexpr (EW == 8) {
-          const int r_in_tile = quarter * 32 + lane;
-          ln_stats[half * 128 + r_in_tile] = make_float2(s1, s2);
-          asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
-          o = ln_stats[(half ^ 1) * 128 + r_in_tile];
-          asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+        // RESID_LN: per part (this warp's WCOLS columns) mean_h = sh + s1 / n_h, M2_h = s2 - s1^2 / n_h
+        // from the shifted sums; with EW = 8 the two halves combine with Chan's formula in a fixed
+        // (half 0, half 1) order.  EMBED_COARSE (layer-0 LN1 of the coarse pass) keeps its plain sums
+        // (rows = patch embedding + PE, |mean| ~ std, nothing to cancel): with them the coarse pass and
+        // a k = 0 refine agree bit for bit (test_refine_k0_reproduces_coarse_pass_bitwise), with the
+        // shifted form they did not
+        if constexpr (EPI == EPI_EMBED_COARSE) {
+          float2 o = make_float2(0.f, 0.f);
+          if constexpr (EW == 8) {
+            const int r_in_tile = quarter * 32 + lane;
+            ln_stats[half * 128 + r_in_tile] = make_float2(s1, s2);
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+            o = ln_stats[(half ^ 1) * 128 + r_in_tile];
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+          }
+          const float inv_n = 1.f / (float)p.N;
+          sh = (s1 + o.x) * inv_n;                                                  // mean
+          s1 = rsqrtf(fmaxf((s2 + o.y) * inv_n - sh * sh, 0.f) + p.ln_eps);        // rstd
         }
-        const float inv_n = 1.f / (float)p.N;
-        const float mean = (s1 + o.x) * inv_n;
-        const float rstd = rsqrtf(fmaxf((s2 + o.y) * inv_n - mean * mean, 0.f) + p.ln_eps);
+        const float n_h = (float)WCOLS;
+        const float mean_h = sh + s1 / n_h;
+        const float m2_h = fmaxf(s2 - s1 * (s1 / n_h), 0.f);
+        float mean = mean_h, m2 = m2_h;
+        if constexpr (EW == 8 && EPI != EPI_EMBED_COARSE) {
+          const int r_in_tile = quarter * 32 + lane;
+          ln_stats[half * 128 + r_in_tile] = make_float2(mean_h, m2_h);
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+          const float2 o = ln_stats[(half ^ 1) * 128 + r_in_tile];
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+          const float2 h0 = half == 0 ? make_float2(mean_h, m2_h) : o;
+          const float2 h1 = half == 0 ? o : make_float2(mean_h, m2_h);
+          const float dm = h0.x - h1.x;
+          mean = 0.5f * (h0.x + h1.x);
+          m2 = (h0.y + h1.y) + dm * dm * (0.5f * n_h);
+        }
+        float rstd = rsqrtf(m2 / (float)p.N + p.ln_eps);
+        if constexpr (EPI == EPI_EMBED_COARSE) {
+          mean = sh;
+          rstd = s1;
+        }
         // LN(x) -> bf16 from the x just written (same thread, row = lane)
         const int row = row0 + lane;
         if (row < p.ln_cap) {

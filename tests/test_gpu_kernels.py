@@ -360,13 +360,14 @@ def test_device_side_selection_errors_are_reported(enc_c640):
     enc_c640.check()  # cleared
 
 
-@pytest.mark.parametrize("staged,offset", [(1, 0.0), (0, 0.0), (1, 3000.0)])
+@pytest.mark.parametrize("staged,offset", [(1, 0.0), (0, 0.0), (1, 3000.0), (0, 3000.0)])
 @pytest.mark.parametrize("M,N,K", [(16, 64, 64), (80, 64, 256), (128, 256, 256), (300, 256, 1024), (1000, 256, 256),
                                    (22400, 256, 256)])
 def test_gemm_residual_layernorm_epilogue(M, N, K, staged, offset):
     """x += A W^T + b and LN(x) -> bf16 with zeroed pad rows, against torch fp32.  offset = 3000:
-    rows whose mean is ~3000x their spread (the staged epilogue's shifted sums keep the variance
-    exact where E[x^2] - mean^2 would cancel to noise)."""
+    rows whose mean is ~3000x their spread (both the staged and the direct epilogue — the latter
+    shared with the coarse embed's fused LN1 — use shifted sums combined with Chan's formula, so the
+    variance stays exact where E[x^2] - mean^2 would cancel to noise)."""
     g = torch.Generator(device="cuda").manual_seed(M + N + K + staged)
     A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
     W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
