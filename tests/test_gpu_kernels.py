@@ -227,7 +227,10 @@ def test_layernorm_matches_torch_fp32(M, d):
     torch.testing.assert_close(y.float(), ref.to(torch.bfloat16).float(), rtol=1e-2, atol=2e-2)
 
 
-@pytest.mark.parametrize("B,Nc,d", [(1, 16, 64), (3, 400, 256), (2, 130, 256)])
+# last key tile of 16 / 16 / 2 / 100 / 52 keys (replicated 4x / 4x / 4x / 1x / 2x over the lane
+# quarters) and Nc = 1024 (full tiles only)
+@pytest.mark.parametrize("B,Nc,d", [(1, 16, 64), (3, 400, 256), (2, 130, 256), (2, 100, 256), (2, 180, 256),
+                                    (1, 1024, 256)])
 def test_score_matches_torch_fp32_and_is_a_distribution(B, Nc, d):
     nh = d // 32
     cap = B * Nc + 256
