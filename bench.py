@@ -724,7 +724,11 @@ def e2e_measure(args, work, lanes, imgs, imgs_np, dev, main, world, u8, cdev=Non
                              up=torch.cuda.Event(), done=torch.cuda.Event(), down=torch.cuda.Event()))
         ls.append(dict(h_in=h_in, sets=sets, s=s_l, n_out=n_out_l, copy_s=torch.cuda.Stream(device=dev),
                        down_s=torch.cuda.Stream(device=dev)))
-    n_steps_t = max(8, args.steps)
+    # at least 40 timed steps: the loop's fill (first upload) and drain (last download) are not
+    # overlapped with compute, which a continuously running serving loop does not pay per step
+    # (c640, 128 frames: 10 steps 31.4k, 40 steps 33.6k, 80 steps 33.6k frames/s;
+    # profiles/r2h_e2e_window.txt)
+    n_steps_t = max(40, args.steps)
 
     def run(n_steps):
         fork = torch.cuda.Event()
