@@ -326,9 +326,14 @@ __global__ void gather_kernel(const GatherParams p) {
   const int seg_vec = (p.Pf * 3 * 2) / 16;  // 16B vectors per fine pixel-row segment
   const int fvec = p.Pf * seg_vec;           // 16B vectors per fine patch
   // Copies are batched GU 16-byte vectors per lane: all loads of a batch are in flight
-  // before its stores (the copy is latency-bound: one load-store pair at a time per lane
-  // left most of the HBM bandwidth idle).
-  constexpr int GU = 8;
+  // before its stores (one load-store pair at a time per lane left most of the HBM bandwidth
+  // idle).  GU = 2 measured best at 128 c640 frames (GU 1 / 2 / 4 / 8 / 16: 78 / 68 / 71 / 88 /
+  // 145 us, profiles/r2h_gather_gu.txt): larger batches cost more registers than their loads
+  // in flight buy.
+#ifndef CFD_GATHER_GU
+#define CFD_GATHER_GU 2
+#endif
+  constexpr int GU = CFD_GATHER_GU;
   for (int c = g * nw + wid; c < Nc; c += G * nw) {
     const int off = c + (m2 - 1) * pre[c];
     const int pc = pre[c];  // rank among selected cells when pos[c] != 0
