@@ -250,7 +250,7 @@ cudaError_t launch_gemm_t(const Opts& o, const CUtensorMap& ta, const CUtensorMa
 // per-SM weight ingress halves (W_c is 1.5 MB per row block).
 cudaError_t launch_embed_pair(const Opts& o, const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p,
                               int rows_for_grid, cudaStream_t s) {
-  constexpr int ST = 12;
+  constexpr int ST = 8;  // 8 / 12 / 6 stages: 135.7 / 139.0 / 139.9 us per 128 frames
   auto kern = gemm_tc_kernel<256, ST, EPI_EMBED_COARSE, 8, 2, false, true, true>;
   using SM = GemmSmem<256, ST, 2, false, 32, true>;
   constexpr int smem = SM::TOTAL;
