@@ -78,7 +78,7 @@ int32_t cfdx_probe_count(int32_t kind);
  *   key 2  fused MLP kernel on (1, default) / off (0)
  *   key 3  TMA-staged residual(+LayerNorm) epilogues on (1, default) / off (0)
  *   key 4  fused MLP (with the fused O-projection) as CTA pairs (cta_group::2, each SM holding half of
- *          every weight operand) on (1, default) / off (0)
+ *          every weight operand) on (1, default) / off (0); with key 11 = 0 the single-CTA kernel runs
  *   key 5  attention v7 warpgroup start stagger in cycles (700 default; values <= 0: none)
  *   key 7  weight-stationary QKV GEMM on (1, default) / off (0)
  *   key 11 O-projection + residual + LN2 fused into the MLP kernel on (1, default) / off (0)
@@ -95,7 +95,6 @@ int32_t cfdx_probe_count(int32_t kind);
  *          min(units, SMs) (0, default)
  *   key 19 fused O-projection keeps x1 = x + o W_o + b_o in TMEM and the MLP's MMA2s
  *          accumulate onto it (1, default) / x1 stored and read back (0)
- *   key 20 with key 19 = 1: x loaded into acc2 while o / W_o stream in (1) / 0 (default)
  *   key 21 attention v7: MMA-warp wait between barrier probes: 0, 8, 32 (default), 128 ns of
  *          sleep, 1 = try_wait (hardware suspend), 2 = busy test_wait loop
  *   key 24 attention v7: producer-warp sleep between barrier probes, ns (0..4096, default 256)

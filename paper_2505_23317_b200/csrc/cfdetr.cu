@@ -123,7 +123,6 @@ struct Opts {
   int sm_cap = 0;         // cap on the persistent grids (0 = all SMs) (17)
   int balanced_grid = 0;  // fewest CTAs with the same number of rounds (18)
   int keep_x1 = 1;        // fused O-projection: x1 stays in TMEM, MMA2 accumulates onto it (19)
-  int preload_x = 0;      // with 19: x loaded into acc2 before MMA_o (20; measured slower)
   int attn_sleep = 32;    // v7: MMA / producer warp sleep when idle, ns (21: 0, 32, 128)
   int attn_psleep = 256;  // v7: the producer warp's sleep between barrier probes, ns (24: 0..4096)
   int attn_nwg = 4;       // v7: softmax warpgroups per CTA (22: 3 or 4)
@@ -410,8 +409,10 @@ cudaError_t launch_mlp(const Opts& o, const CUtensorMap& th, const CUtensorMap& 
   q.staged = (tx != nullptr && (tln != nullptr || p.ln_g == nullptr)) ? 1 : 0;
   const CUtensorMap& mx = tx ? *tx : th;
   const CUtensorMap& ml = tln ? *tln : th;
-  if (o.mlp_cluster && num_sms(o) >= 2) {
-    // CTA pairs (cta_group::2 MMAs, each SM holding half of every weight operand)
+  // CTA pairs (cta_group::2 MMAs, each SM holding half of every weight operand) with the fused
+  // O-projection only: without it (option 11 = 0) the pair kernel hung with >= 5 tiles per pair
+  // (128 c640 frames) and the single-CTA kernel runs
+  if (o.mlp_cluster && two && num_sms(o) >= 2) {
     const int pairs = (tiles + 1) / 2;
     const int clusters = std::max(1, std::min(pairs, num_sms(o) / 2));
     cudaLaunchConfig_t lc = {};
@@ -426,7 +427,6 @@ cudaError_t launch_mlp(const Opts& o, const CUtensorMap& th, const CUtensorMap& 
     la[0].val.clusterDim.z = 1;
     lc.attrs = la;
     lc.numAttrs = 1;
-    if (two) q.preload_x = 0;  // not built for the pair kernel
     cudaError_t e = two ? cudaLaunchKernelEx(&lc, mlp_tc_kernel<256, 2, true>, th, tw1h, tw2, q, mx, ml, *two)
                         : cudaLaunchKernelEx(&lc, mlp_tc_kernel<256, 2>, th, tw1h, tw2, q, mx, ml, th);
     ++g_launches;
@@ -670,7 +670,6 @@ cfd_status run_layer(cfd_ctx* c, int l, float* x, int x_cap, int M_static, const
     MlpParams mp{};
     mp.M = M_static; mp.m_dev = m_dev; mp.F = F; mp.b1 = L.b_1; mp.b2 = L.b_2; mp.x = x; mp.ln_eps = g.ln_eps;
     mp.bo = L.b_o; mp.ln2_g = L.ln2_g; mp.ln2_b = L.ln2_b; mp.keep_x1 = o.keep_x1;
-    mp.preload_x = o.keep_x1 && o.preload_x;
     mp.ln_cap = w.rows_cap;
     if (l + 1 < g.n_layers) {
       const LayerDev& Ln = c->layers[l + 1];
@@ -834,7 +833,6 @@ cfd_status cfdx_set_option(cfd_ctx* ctx, int32_t key, int32_t value) {
       return CFD_OK;
     case 18: o.balanced_grid = b; return CFD_OK;
     case 19: o.keep_x1 = b; return CFD_OK;
-    case 20: o.preload_x = b; return CFD_OK;
     case 21:
       if (value != 0 && value != 1 && value != 2 && value != 8 && value != 32 && value != 128) return CFD_E_ARG;
       o.attn_sleep = value;

@@ -63,9 +63,6 @@ struct MlpParams {
   // MLP's MMA2s then accumulate onto it and the final epilogue computes x2 = acc2 + b2 without
   // reading x (saves the x1 store + reload: 2 x 128 KB per tile)
   int keep_x1;
-  // OPJ + keep_x1 only: the epilogue warps load x into acc2's TMEM columns while o / W_o
-  // stream in, MMA_o accumulates onto it, and the residual pass is acc2 + b_o (no x wait)
-  int preload_x;
 };
 
 constexpr int MLP_THREADS = 320;  // TMA warp, MMA warp, 8 epilogue warps
@@ -143,8 +140,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   uint64_t* a2_empty = a2_full + 1;
   uint64_t* xbar = a2_empty + 1;             // [8 warps][3] staged-epilogue TMA loads
   uint64_t* ao_full = xbar + 24;             // OPJ: acc_o = o . W_o^T complete
-  uint64_t* x_ready = ao_full + 1;           // OPJ preload_x: x tile in acc2 (8 epilogue warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_ready + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ao_full + 1);
   float2* ln_stats = reinterpret_cast<float2*>(smem + S::STATS_OFF);
   float* b1_s = reinterpret_cast<float*>(smem + S::PAR_OFF);
   float* b2_s = b1_s + GEMM_MAX_N;
@@ -189,7 +185,6 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
     mbar_init(a2_empty, 8 * CL);
     for (int i = 0; i < 24; ++i) mbar_init(&xbar[i], 1);
     mbar_init(ao_full, 1);
-    mbar_init(x_ready, 8);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -370,7 +365,6 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
           const uint32_t p0 = static_cast<uint32_t>(it) * slots_per_tile;
           mbar_wait(a2_empty, (a2_cnt & 1) ^ 1);  // previous tile's final epilogue drained acc2
           ++a2_cnt;
-          if (p.preload_x) mbar_wait(x_ready, it & 1);  // acc2 = x: MMA_o accumulates onto it
           auto wait_pos = [&](uint32_t q) {
             mbar_wait(&w_full[q % MLP_SLOTS], (q / MLP_SLOTS) & 1);
             return smem_u32(smem + S::W_OFF + (q % MLP_SLOTS) * S::SLOT_BYTES);
@@ -388,7 +382,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
               const uint64_t ad = make_smem_desc(a + k * 32, 16, 1024, kLayoutSW128);
               const uint64_t bd = make_smem_desc(w + k * 32, 16, 1024, kLayoutSW128);
               if constexpr (PAIR) mma_ss_2sm(tmem + ACC2, ad, bd, idesc2, (kb | k) != 0);
-              else mma_ss(tmem + ACC2, ad, bd, idesc2, p.preload_x || (kb | k) != 0);
+              else mma_ss(tmem + ACC2, ad, bd, idesc2, (kb | k) != 0);
             }
             commit(&w_empty[qo % MLP_SLOTS]);
             commit(&w_empty[qw % MLP_SLOTS]);
@@ -440,54 +434,9 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         const ResidStage st{hslice, S::H_BYTES, nullptr, 0, xbar + 3 * e, &xph, nullptr};
         const ResidLnArgs la{D, p.ln_cap, p.ln_eps};
         const uint32_t tb = tmem + lane_off + ACC2 + half * 128;
-        if (p.preload_x) {
-          // x tile -> acc2 TMEM columns (this warp: 32 rows x 128 columns, 4 TMA chunks through
-          // the 3 staging buffers), then x_ready: MMA_o accumulates onto x
-          const int row0 = tile * 128 + quarter * 32;
-          auto xbuf = [&](int b) { return b == 2 ? st.xb3 : st.xb + b * st.xb_stride; };
-          auto xload = [&](int c, int b) {
-            if (lane == 0) {
-              mbar_expect_tx(&st.bar[b], 4096);
-              tma_load_2d(xbuf(b), &tmX, &st.bar[b], half * 128 + c * 32, row0);
-            }
-          };
-          xload(0, 0);
-          xload(1, 1);
-          xload(2, 2);
-#pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            const int b = c % 3;
-            mbar_wait(&st.bar[b], (xph >> b) & 1);
-            xph ^= 1u << b;
-            uint32_t a[32];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float4 x = *reinterpret_cast<const float4*>(xbuf(b) + lane * 128 + ((q ^ (lane & 7)) << 4));
-              a[4 * q] = __float_as_uint(x.x);
-              a[4 * q + 1] = __float_as_uint(x.y);
-              a[4 * q + 2] = __float_as_uint(x.z);
-              a[4 * q + 3] = __float_as_uint(x.w);
-            }
-            tmem_st16(tb + c * 32, *reinterpret_cast<const uint32_t(*)[16]>(a));
-            tmem_st16(tb + c * 32 + 16, *reinterpret_cast<const uint32_t(*)[16]>(a + 16));
-            if (c == 0) {
-              fence_proxy_async();  // generic reads of buffer 0 before the TMA overwrite
-              __syncwarp();
-              xload(3, 0);
-            }
-          }
-          tmem_wait_st();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(x_ready);
-        }
         if (et == 0) MLP_TR(it, 38);
         const int a2_cta = PAIR && rank ? 0 : -1;  // PAIR: acc2 releases arrive on the leader
-        if (!PAIR && p.preload_x)
-          resid_ln_tma<4, true, true, false, false>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M,
-                                                    bo_s, g2_s, b2ln_s, ln_stats, quarter, half, lane, ao_full, it & 1,
-                                                    a2_empty, a2_cta, tmem + lane_off + HT + half * 64);
-        else if (p.keep_x1)
+        if (p.keep_x1)
           resid_ln_tma<4, true, true, true, false>(la, tmX, tmLN, st, tb, tile * 128 + quarter * 32, half * 128, M,
                                                    bo_s, g2_s, b2ln_s, ln_stats, quarter, half, lane, ao_full, it & 1,
                                                    a2_empty, a2_cta, tmem + lane_off + HT + half * 64);

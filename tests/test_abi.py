@@ -59,12 +59,12 @@ def test_tuning_option_validation_without_gpu(lib):
     assert f(None, 0, 6) == -1 and f(None, 0, 0) == -1 and f(None, 0, 2) == -1 and f(None, 0, 4) == -1
     assert f(None, 1, 3) == -1 and f(None, 1, 10) == -1 and f(None, 1, -2) == -1
     assert f(None, 5, -3) == -1 and f(None, 6, 4) == -1 and f(None, 9, 0) == -1 and f(None, 10, 0) == -1
-    assert f(None, 8, 0) == -1 and f(None, 12, 0) == -1 and f(None, 26, 0) == -1 and f(None, 24, -1) == -1 and f(None, 24, 5000) == -1
-    for key, val in ((0, 1), (1, 8), (2, 0), (3, 0), (4, 0), (5, 300), (7, 0), (11, 0), (19, 0), (20, 0), (17, 74)):
+    assert f(None, 8, 0) == -1 and f(None, 12, 0) == -1 and f(None, 20, 0) == -1 and f(None, 26, 0) == -1 and f(None, 24, -1) == -1 and f(None, 24, 5000) == -1
+    for key, val in ((0, 1), (1, 8), (2, 0), (3, 0), (4, 0), (5, 300), (7, 0), (11, 0), (19, 0), (17, 74)):
         assert f(None, key, val) == 0
     assert f(None, 21, 5) == -1 and f(None, 22, 2) == -1
     assert f(None, 24, 1024) == 0 and f(None, 24, 256) == 0
-    for key, val in ((0, 7), (1, 2), (2, 1), (3, 1), (4, 1), (5, 700), (7, 1), (11, 1), (19, 1), (20, 0), (17, 0),
+    for key, val in ((0, 7), (1, 2), (2, 1), (3, 1), (4, 1), (5, 700), (7, 1), (11, 1), (19, 1), (17, 0),
                      (21, 32), (22, 4), (23, 1), (25, 1)):
         assert f(None, key, val) == 0  # restore the defaults
 

@@ -274,12 +274,13 @@ def test_staged_epilogues_match_direct_epilogues():
         assert rel < 3e-3, rel
 
 
-@pytest.mark.parametrize("opj,keep", [(0, 0), (1, 0), (1, 1)])
+@pytest.mark.parametrize("opj,keep", [(1, 0), (1, 1)])
 def test_mlp_cta_pair_variant_matches_single_cta_bitwise(opj, keep):
     """The CTA-pair fused MLP (cta_group::2 M=256 MMAs, each SM holding half of every weight
     operand; cfdx_set_option(4, 1)) accumulates the same products in the same k order as the
-    single-CTA kernel: outputs agree bit for bit, with and without the fused O-projection and
-    x1 kept in TMEM, including an odd tile count (ghost tile in the last pair)."""
+    single-CTA kernel: outputs agree bit for bit, with and without x1 kept in TMEM, including an
+    odd tile count (ghost tile in the last pair).  (Without the fused O-projection the library
+    runs the single-CTA kernel.)"""
     cfg = ci.CONFIGS["c640"]
     enc = CFDetrEncoder(cfg, ci.make_weights(cfg, seed=0), max_tasks=8)
     imgs = bf16_tensor(ci.make_frames(cfg, 3, task0=5), "cuda")
